@@ -1,0 +1,256 @@
+/*
+ * photon.h -- C ABI of the B200-native Photon federated-round path.
+ *
+ * Drop-in boundary for the reference library `fedsim::core`
+ * (/root/reference/proj/core).  Every entry point names the reference
+ * interface it replaces (file:line).  Plain pointers and sizes only: host
+ * buffers are f64 in the reference's canonical flat parameter order
+ * (ParamVector::flatten, param_vector.cpp:154-159); device state is owned by
+ * opaque handles.  Errors: every call returns a photon status code and fills
+ * an optional photon_err; codes map 1:1 onto fedsim/errors.h:9-72, so an
+ * adapter can rethrow the matching fedsim:: exception.
+ */
+#ifndef PHOTON_H
+#define PHOTON_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PHOTON_ABI_VERSION 1
+
+/* status codes (fedsim/errors.h) */
+enum {
+  PHOTON_OK = 0,
+  PHOTON_ERR_CONFIG = 1,        /* ConfigError */
+  PHOTON_ERR_CAPACITY = 2,      /* CapacityError */
+  PHOTON_ERR_SHAPE = 3,         /* ShapeError */
+  PHOTON_ERR_INDEX = 4,         /* IndexError */
+  PHOTON_ERR_USAGE = 5,         /* UsageError */
+  PHOTON_ERR_LOOKUP = 6,        /* LookupError */
+  PHOTON_ERR_NUMERIC = 7,       /* NumericError */
+  PHOTON_ERR_DIVERGENCE = 8,    /* DivergenceError{round,client,step} */
+  PHOTON_ERR_IO = 9,            /* IoError */
+  PHOTON_ERR_INTEGRITY = 10,    /* IntegrityError */
+  PHOTON_ERR_ROUND_FAILURE = 11,/* RoundFailureError */
+  PHOTON_ERR_CUDA = 20,         /* device failure (no reference equivalent) */
+  PHOTON_ERR_NCCL = 21
+};
+
+/* arithmetic of the client step */
+enum {
+  PHOTON_PREC_F32 = 0,  /* fp32 storage + fp32 SIMT contractions (parity mode) */
+  PHOTON_PREC_BF16 = 1  /* fp32 master/moments, bf16 operands on tcgen05, fp32 accumulate */
+};
+
+typedef struct {
+  int32_t code;
+  uint64_t round, client, step; /* DivergenceError fields (errors.h:45-52) */
+  char msg[256];
+} photon_err;
+
+/* ModelConfig, model.h:12-25 */
+typedef struct {
+  uint64_t n_blocks, d_model, n_heads, expansion_ratio, vocab_size, seq_len;
+} photon_model_cfg;
+
+/* LrSchedule, optim.h:13-21 */
+typedef struct {
+  double eta_max;
+  uint64_t warmup_steps, decay_steps;
+  double alpha;
+} photon_lr_schedule;
+
+/* AdamWConfig, optim.h:25-33 */
+typedef struct {
+  double beta1, beta2, eps, weight_decay, clip_norm;
+} photon_adamw_cfg;
+
+/* LocalTrainConfig, client.h:66-76 (+ PostProcessPolicy client.h:58-62) */
+typedef struct {
+  photon_model_cfg model;
+  photon_adamw_cfg adamw;
+  photon_lr_schedule schedule;
+  int32_t opt;            /* 0 AdamW, 1 SGD (ClientOptKind) */
+  double sgd_clip_norm;
+  uint64_t local_steps;   /* tau */
+  uint64_t batch_size;    /* B */
+  double throughput_bps;  /* nu (simulated seconds per step = 1/nu) */
+  int32_t post_kind;      /* 0 identity, 1 clip update norm */
+  double post_threshold;
+} photon_train_cfg;
+
+/* ServerOptConfig, optim.h:54-63 */
+typedef struct {
+  int32_t kind;           /* 0 FedAvg, 1 FedMomentum */
+  double eta, momentum;
+  int32_t nesterov;
+} photon_server_cfg;
+
+/* FederationConfig, aggregator.h:18-26 */
+typedef struct {
+  uint64_t population;        /* P */
+  uint64_t clients_per_round; /* K */
+  uint64_t rounds;            /* T */
+  int32_t topology;           /* 0 ps, 1 ar, 2 rar (cost_model.h Topology) */
+  uint64_t seed;
+} photon_fed_cfg;
+
+/* StepMetric, client.h:78-82 */
+typedef struct {
+  double loss;
+  uint64_t tokens;
+  double sim_seconds;
+} photon_step_metric;
+
+/* RoundRecord, aggregator.h:38-53 (simulated-cost fields omitted: cost model is
+ * out of scope) + measured device time of the round on this rank. */
+typedef struct {
+  uint64_t round;
+  uint64_t n_sampled;
+  uint64_t sampled_ids[64];   /* first min(K,64) sampled ids, ascending */
+  double mean_client_loss, min_client_loss, max_client_loss;
+  double local_ms;            /* device time: first client step -> last client step */
+  double aggregate_ms;        /* device time: exchange + fused mean/outer update + gather */
+  double round_ms;            /* device time of the whole round on this rank */
+  uint64_t tokens;            /* tokens trained on this rank this round */
+} photon_round_record;
+
+typedef struct photon_ctx photon_ctx;       /* one GPU: device state of one client slot */
+typedef struct photon_plan photon_plan;     /* ShardPlan (data.h:33-62), host */
+typedef struct photon_runner photon_runner; /* FederationRunner (aggregator.h:70-102) */
+
+int photon_abi_version(void);
+const char* photon_status_name(int code);
+
+/* ---- host: determinism primitives (bit-exact ports) ------------------------ */
+uint64_t photon_mix64(uint64_t x);                                 /* rng.h:14-19 */
+uint64_t photon_stream_seed(uint64_t global_seed, uint64_t client); /* data.cpp:201-203 */
+int photon_sample_clients(uint64_t population, uint64_t k, uint64_t seed, uint64_t round,
+                          uint64_t* out_ids, photon_err* err);     /* aggregator.cpp:25-41 */
+int photon_lr_at(const photon_lr_schedule* s, uint64_t step, double* out,
+                 photon_err* err);                                 /* optim.cpp:16-27 */
+
+/* ---- host: model layout + init ---------------------------------------------- */
+uint64_t photon_param_count(const photon_model_cfg* m);            /* model.cpp:21-26 */
+uint64_t photon_layout_size(const photon_model_cfg* m);            /* model.cpp:32-61 */
+int photon_layout_entry(const photon_model_cfg* m, uint64_t i, uint64_t* offset,
+                        uint64_t* rows, uint64_t* cols, char* name, int name_cap);
+int photon_init_params(const photon_model_cfg* m, uint64_t seed, double* out,
+                       photon_err* err);                           /* model.cpp:72-96 */
+
+/* ---- host: data (data.cpp) ---------------------------------------------------- */
+int photon_generate_corpus(const char* style, uint64_t length, uint64_t seed, uint32_t vocab,
+                           uint16_t* out, photon_err* err);        /* data.cpp:44-71 */
+int photon_plan_iid(const uint16_t* tokens, uint64_t n_tokens, uint64_t n_shards,
+                    uint64_t seq_len, uint64_t seed, photon_plan** out,
+                    photon_err* err);                              /* data.cpp:137-164 */
+int photon_plan_by_source(const uint16_t* const* corpora, const uint64_t* lens,
+                          uint64_t n_sources, uint64_t clients_per_source, uint64_t seq_len,
+                          photon_plan** out, photon_err* err);     /* data.cpp:166-199 */
+void photon_plan_free(photon_plan* p);
+uint64_t photon_plan_n_clients(const photon_plan* p);
+uint64_t photon_plan_client_blocks(const photon_plan* p, uint64_t client);
+/* BatchStream::next, data.cpp:231-253: batch rows from cursor; advances cursor */
+int photon_stream_next(const photon_plan* p, uint64_t client, uint64_t batch_size,
+                       uint64_t seed, uint64_t* cursor, int32_t* inputs, int32_t* targets,
+                       photon_err* err);
+
+/* ---- device context ------------------------------------------------------------ */
+/* One GPU's client engine for `model` at `precision`, activations sized for
+ * max_batch rows of model->seq_len tokens. */
+int photon_ctx_create(int device, const photon_model_cfg* model, int precision,
+                      uint64_t max_batch, photon_ctx** out, photon_err* err);
+void photon_ctx_destroy(photon_ctx* ctx);
+/* ms of device time of the last call that ran kernels on this ctx */
+double photon_ctx_last_ms(const photon_ctx* ctx);
+
+/* TransformerModel::forward_loss + backward + collect_grads (model.cpp:98-174):
+ * params/grads f64 host, canonical order; grads may be NULL (forward only). */
+int photon_forward_backward(photon_ctx* ctx, const double* params, const int32_t* inputs,
+                            const int32_t* targets, uint64_t batch, uint64_t seq,
+                            double* loss, double* grads, photon_err* err);
+
+/* eval_perplexity (model.cpp:176-192): n_batches batches of batch_sizes[i] rows */
+int photon_eval_perplexity(photon_ctx* ctx, const double* params, const int32_t* inputs,
+                           const int32_t* targets, uint64_t n_batches,
+                           const uint64_t* batch_sizes, uint64_t seq, double* ppl,
+                           photon_err* err);
+
+/* run_local_round (client.cpp:125-158 / client.h:97-99): tau local steps from
+ * theta_in with fresh optimizer state; inputs/targets hold the tau batches the
+ * client's BatchStream yields ([tau][B][S] int32, from photon_stream_next).
+ * Non-finite loss -> PHOTON_ERR_DIVERGENCE with (round, client, step). */
+int photon_client_round(photon_ctx* ctx, const photon_train_cfg* cfg, const double* theta_in,
+                        const int32_t* inputs, const int32_t* targets, uint64_t round,
+                        uint64_t client, uint64_t step_base, double* theta_out,
+                        photon_step_metric* metrics, photon_err* err);
+
+/* ---- aggregation + outer optimizer, f64, bit-exact vs the reference ------------- */
+/* ParamVector::mean (param_vector.cpp:127-152), anchored, ascending order */
+int photon_mean(photon_ctx* ctx, const double* const* models, uint64_t k, uint64_t n,
+                double* out, photon_err* err);
+/* ParamVector::sub (param_vector.cpp:120-125) */
+int photon_sub(photon_ctx* ctx, const double* a, const double* b, uint64_t n, double* out,
+               photon_err* err);
+/* server_step (optim.cpp:124-159); velocity updated in place */
+int photon_server_step(photon_ctx* ctx, const photon_server_cfg* cfg, const double* theta,
+                       const double* delta, const double* mean, double* velocity, uint64_t n,
+                       double* theta_out, photon_err* err);
+/* fused mean -> pseudo-gradient -> outer step (aggregator.cpp:177-179) */
+int photon_aggregate(photon_ctx* ctx, const double* const* models, uint64_t k, uint64_t n,
+                     const double* theta, double* velocity, const photon_server_cfg* cfg,
+                     double* theta_out, photon_err* err);
+/* adamw_step / sgd_step (optim.cpp:61-103) on f64 host buffers, bit-exact */
+int photon_adamw_step(photon_ctx* ctx, double* params, const double* grads, double* m,
+                      double* v, uint64_t n, uint64_t* step_count,
+                      const photon_adamw_cfg* cfg, double lr, photon_err* err);
+int photon_sgd_step(photon_ctx* ctx, double* params, const double* grads, uint64_t n,
+                    double lr, double clip_norm, photon_err* err);
+
+/* fp32 device-resident fused aggregation over device pointers (the fast path):
+ * models[k] -> theta (in/out) and velocity (in/out); returns device ms. */
+int photon_aggregate_device_f32(photon_ctx* ctx, const float* const* d_models, uint64_t k,
+                                uint64_t n, float* d_theta, float* d_velocity,
+                                const photon_server_cfg* cfg, double* ms, photon_err* err);
+
+/* ---- test / benchmark hooks ------------------------------------------------------- */
+/* One contraction of the client step on device pointers: impl 0 = SIMT,
+ * 1 = tcgen05; dtypes 0 f32 / 1 bf16; epi as gemm.cuh (0 store, 1 accum,
+ * 2 bias, 3 resid+bias, 4 gelu+bias, 5 gelu backward).  Runs `iters` times
+ * on an internal stream; *ms = mean device time per launch. */
+int photon_debug_gemm(int impl, int M, int N, int K, const void* A, int64_t lda, int a_kmajor,
+                      const void* B, int64_t ldb, int b_kmajor, int ab_dtype, void* C,
+                      int64_t ldc, int c_dtype, int epi, const float* bias, const float* resid,
+                      void* aux, int iters, double* ms, photon_err* err);
+
+/* ---- federated round runner (FederationRunner, aggregator.h:70-102) ------------ */
+/* Device-resident: theta_t, velocity and client state live in HBM.  With
+ * world > 1 each rank runs the sampled clients with slot % world == rank and
+ * the round boundary exchanges parameter shards over NCCL (nccl_id: 128-byte
+ * ncclUniqueId from rank 0; NULL when world == 1). */
+int photon_runner_create(photon_ctx* ctx, const photon_fed_cfg* fed,
+                         const photon_train_cfg* train, const photon_server_cfg* server,
+                         const photon_plan* plan, const double* theta0, int rank, int world,
+                         const uint8_t* nccl_id, photon_runner** out, photon_err* err);
+void photon_runner_destroy(photon_runner* r);
+int photon_nccl_unique_id(uint8_t* out128, photon_err* err);
+/* simulated dropouts (RunnerOptions::dropouts, aggregator.h:59-61) */
+int photon_runner_add_dropout(photon_runner* r, uint64_t round, uint64_t client);
+int photon_runner_run_round(photon_runner* r, photon_round_record* rec, photon_err* err);
+uint64_t photon_runner_next_round(const photon_runner* r);
+int photon_runner_theta(photon_runner* r, double* out, photon_err* err);
+int photon_runner_velocity(photon_runner* r, double* out, photon_err* err);
+uint64_t photon_runner_cursor(const photon_runner* r, uint64_t client);
+/* FederationRunner::restore (aggregator.cpp:78-91) */
+int photon_runner_restore(photon_runner* r, const double* theta, const double* velocity,
+                          uint64_t next_round, const uint64_t* cursors, uint64_t n_cursors,
+                          photon_err* err);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

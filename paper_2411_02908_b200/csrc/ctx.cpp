@@ -1,0 +1,162 @@
+// ctx.cpp -- device context and the device-resident client update.
+#include "ctx.hpp"
+
+#include <cmath>
+
+#include "kernels.cuh"
+
+namespace photon {
+
+void RoundBatches::prepare(int tau_, int B_, int S_, int V) {
+  tau = tau_;
+  B = B_;
+  S = S_;
+  const size_t M = (size_t)B * S;
+  tokens.reserve(tau * M);
+  targets.reserve(tau * M);
+  csr_off.reserve((size_t)tau * (V + 1));
+  csr_rows.reserve(tau * M);
+  inv_count.assign(tau, 0.f);
+}
+
+void RoundBatches::finalize(int V) {
+  const int M = B * S;
+  for (int i = 0; i < tau; ++i) {
+    const int32_t* tk = tokens.ptr + (size_t)i * M;
+    for (int m = 0; m < M; ++m)
+      if (tk[m] < 0 || tk[m] >= V)
+        throw Error(PHOTON_ERR_INDEX, "gather_rows: index " + std::to_string(tk[m]) +
+                                          " out of range [0," + std::to_string(V) + ")");
+    build_token_csr(tk, M, V, csr_off.ptr + (size_t)i * (V + 1), csr_rows.ptr + (size_t)i * M);
+    const int32_t* tg = targets.ptr + (size_t)i * M;
+    int count = 0;
+    for (int m = 0; m < M; ++m) {
+      if (tg[m] >= V) throw Error(PHOTON_ERR_INDEX, "cross_entropy: target out of vocab");
+      count += tg[m] >= 0;
+    }
+    if (count == 0) throw Error(PHOTON_ERR_USAGE, "cross_entropy: no target tokens");
+    inv_count[i] = (float)(1.0 / (double)count);
+  }
+}
+
+Ctx::Ctx(int dev, const photon_model_cfg& m, int prec, uint64_t mb)
+    : device(dev), cfg(m), precision(prec), max_batch(mb) {
+  validate_model(m);
+  PH_CUDA(cudaSetDevice(dev));
+  PH_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  PH_CUDA(cudaEventCreate(&ev0));
+  PH_CUDA(cudaEventCreate(&ev1));
+  eng = Engine::create(m, prec, mb, stream);
+  h_flag.reserve(4);
+}
+
+Ctx::~Ctx() {
+  eng.reset();
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+void Ctx::begin_timing() { PH_CUDA(cudaEventRecord(ev0, stream)); }
+
+double Ctx::end_timing() {
+  PH_CUDA(cudaEventRecord(ev1, stream));
+  PH_CUDA(cudaEventSynchronize(ev1));
+  float ms = 0.f;
+  PH_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+  last_ms = ms;
+  return ms;
+}
+
+void Ctx::upload(const RoundBatches& rb) {
+  const size_t M = (size_t)rb.B * rb.S, V = cfg.vocab_size;
+  d_tokens.reserve(rb.tau * M);
+  d_targets.reserve(rb.tau * M);
+  d_csr_off.reserve(rb.tau * (V + 1));
+  d_csr_rows.reserve(rb.tau * M);
+  PH_CUDA(cudaMemcpyAsync(d_tokens.ptr, rb.tokens.ptr, rb.tau * M * 4, cudaMemcpyHostToDevice, stream));
+  PH_CUDA(cudaMemcpyAsync(d_targets.ptr, rb.targets.ptr, rb.tau * M * 4, cudaMemcpyHostToDevice, stream));
+  PH_CUDA(cudaMemcpyAsync(d_csr_off.ptr, rb.csr_off.ptr, rb.tau * (V + 1) * 4, cudaMemcpyHostToDevice, stream));
+  PH_CUDA(cudaMemcpyAsync(d_csr_rows.ptr, rb.csr_rows.ptr, rb.tau * M * 4, cudaMemcpyHostToDevice, stream));
+}
+
+// optim.cpp:20-35, 105-113 validation of the client hyper-parameters
+void check_train_cfg(const photon_train_cfg& t) {
+  validate_model(t.model);
+  const auto& a = t.adamw;
+  if (a.beta1 < 0.0 || a.beta1 >= 1.0 || a.beta2 < 0.0 || a.beta2 >= 1.0)
+    throw Error(PHOTON_ERR_CONFIG, "adamw: betas must be in [0,1)");
+  if (!(a.eps > 0.0)) throw Error(PHOTON_ERR_CONFIG, "adamw: eps must be > 0");
+  if (a.weight_decay < 0.0) throw Error(PHOTON_ERR_CONFIG, "adamw: weight_decay must be >= 0");
+  if (t.opt != 0 && t.opt != 1) throw Error(PHOTON_ERR_CONFIG, "unknown client optimizer");
+  if (t.batch_size == 0) throw Error(PHOTON_ERR_CONFIG, "stream: batch_size must be >= 1");
+  if (t.post_kind == 1 && !(t.post_threshold > 0.0))
+    throw Error(PHOTON_ERR_CONFIG, "clip post-process needs a positive threshold");
+  (void)lr_at(t.schedule, 0);  // validates the schedule
+}
+
+// run_local_round (client.cpp:125-158) on the device: theta copy, fresh AdamW
+// state, tau x {forward, backward, clip, AdamW/SGD}, post-process.  Losses are
+// read back once at the end; the first non-finite loss (DivergenceError) or
+// non-finite gradient norm (NumericError) is reported with its step, in the
+// order the reference would have raised them.
+LocalResult Ctx::local_round(const photon_train_cfg& t, const RoundBatches& rb,
+                             const float* d_theta_in, float* d_theta_out, uint64_t step_base) {
+  Engine& e = *eng;
+  const uint64_t P = e.P;
+  const int tau = rb.tau;
+  d_losses.reserve(std::max(tau, 1));
+  h_losses.reserve(std::max(tau, 1));
+  if (d_theta_in != e.master)
+    PH_CUDA(cudaMemcpyAsync(e.master, d_theta_in, P * 4, cudaMemcpyDeviceToDevice, stream));
+  e.refresh_shadow();
+  PH_CUDA(cudaMemsetAsync(e.mom, 0, P * 4, stream));
+  PH_CUDA(cudaMemsetAsync(e.vel2, 0, P * 4, stream));
+  PH_CUDA(cudaMemsetAsync(e.bad_step, 0, sizeof(int), stream));
+  const size_t M = (size_t)rb.B * rb.S, V = cfg.vocab_size;
+  const double b1 = t.adamw.beta1, b2 = t.adamw.beta2;
+  for (int i = 0; i < tau; ++i) {
+    StepBatch sb;
+    sb.tokens = d_tokens.ptr + i * M;
+    sb.targets = d_targets.ptr + i * M;
+    sb.csr_off = d_csr_off.ptr + i * (V + 1);
+    sb.csr_rows = d_csr_rows.ptr + i * M;
+    sb.B = rb.B;
+    sb.S = rb.S;
+    sb.inv_count = rb.inv_count[i];
+    e.forward_backward(sb, d_losses.ptr + i, true);
+    const double lr = lr_at(t.schedule, step_base + i);
+    if (t.opt == 0) {
+      const double stepc = (double)(i + 1);  // fresh state each round: step_count = i+1
+      e.adamw(t.adamw.clip_norm, lr, b1, b2, 1.0 - std::pow(b1, stepc), 1.0 - std::pow(b2, stepc),
+              t.adamw.eps, t.adamw.weight_decay, i);
+    } else {
+      e.sgd(t.sgd_clip_norm, lr, i);
+    }
+  }
+  if (t.post_kind == 1)
+    k::clip_update_f32(d_theta_in, e.master, P, t.post_threshold, e.red_part, stream);
+  if (d_theta_out != e.master)
+    PH_CUDA(cudaMemcpyAsync(d_theta_out, e.master, P * 4, cudaMemcpyDeviceToDevice, stream));
+  PH_CUDA(cudaMemcpyAsync(h_losses.ptr, d_losses.ptr, tau * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  PH_CUDA(cudaMemcpyAsync(h_flag.ptr, e.bad_step, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  PH_CUDA(cudaStreamSynchronize(stream));
+  LocalResult r;
+  r.losses.assign(h_losses.ptr, h_losses.ptr + tau);
+  const int bad = h_flag.ptr[0];  // 1-based step of the first non-finite grad norm
+  for (int i = 0; i < tau; ++i) {
+    if (!std::isfinite(r.losses[i])) {
+      r.error = PHOTON_ERR_DIVERGENCE;
+      r.error_step = i;
+      break;
+    }
+    if (bad == i + 1) {
+      r.error = PHOTON_ERR_NUMERIC;
+      r.error_step = i;
+      break;
+    }
+  }
+  return r;
+}
+
+}  // namespace photon

@@ -1,0 +1,97 @@
+// ctx.hpp -- photon_ctx: one GPU's engine plus the per-round device buffers,
+// and the device-resident client update (run_local_round, client.cpp:125-158).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "engine.cuh"
+
+namespace photon {
+
+template <typename U>
+struct DevBuf {
+  U* ptr = nullptr;
+  size_t n = 0;
+  void reserve(size_t want) {
+    if (want <= n) return;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    n = 0;
+    PH_CUDA(cudaMalloc(&ptr, want * sizeof(U)));
+    n = want;
+  }
+  ~DevBuf() {
+    if (ptr) cudaFree(ptr);
+  }
+};
+
+template <typename U>
+struct PinnedBuf {
+  U* ptr = nullptr;
+  size_t n = 0;
+  void reserve(size_t want) {
+    if (want <= n) return;
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    n = 0;
+    PH_CUDA(cudaMallocHost(&ptr, want * sizeof(U)));
+    n = want;
+  }
+  ~PinnedBuf() {
+    if (ptr) cudaFreeHost(ptr);
+  }
+};
+
+// The tau batches of one client round, staged on the host.
+struct RoundBatches {
+  int tau = 0, B = 0, S = 0;
+  PinnedBuf<int32_t> tokens, targets, csr_off, csr_rows;  // [tau][...]
+  std::vector<float> inv_count;                            // [tau]
+  void prepare(int tau_, int B_, int S_, int V);           // sizes pinned buffers
+  void finalize(int V);                                    // CSR + counts from tokens/targets
+};
+
+struct LocalResult {
+  std::vector<double> losses;  // tau
+  int error = PHOTON_OK;
+  uint64_t error_step = 0;
+};
+
+struct Ctx {
+  int device = 0;
+  photon_model_cfg cfg{};
+  int precision = 0;
+  uint64_t max_batch = 0;
+  cudaStream_t stream = nullptr;
+  std::unique_ptr<Engine> eng;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double last_ms = 0.0;
+
+  // device copies of the current round's batches
+  DevBuf<int32_t> d_tokens, d_targets, d_csr_off, d_csr_rows;
+  DevBuf<double> d_losses;
+  PinnedBuf<double> h_losses;
+  PinnedBuf<int> h_flag;
+  // generic scratch
+  DevBuf<double> d_f64a, d_f64b, d_f64c, d_f64d;
+  DevBuf<float> d_f32a, d_f32b;
+  DevBuf<const void*> d_ptrs;
+
+  Ctx(int dev, const photon_model_cfg& m, int prec, uint64_t mb);
+  ~Ctx();
+
+  void begin_timing();
+  double end_timing();  // syncs, returns ms since begin_timing
+
+  // H2D of a staged round (async on stream)
+  void upload(const RoundBatches& rb);
+  // tau local steps from d_theta_in (fp32 device) into d_theta_out (may equal
+  // engine master); returns per-step losses and the first failure.
+  LocalResult local_round(const photon_train_cfg& cfg, const RoundBatches& rb,
+                          const float* d_theta_in, float* d_theta_out, uint64_t step_base);
+};
+
+void check_train_cfg(const photon_train_cfg& t);
+
+}  // namespace photon

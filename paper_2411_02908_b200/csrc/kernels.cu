@@ -1,0 +1,580 @@
+// kernels.cu -- embedding, layer norm, bias-gradient column sums, fused
+// softmax cross-entropy and the SIMT attention path of the client step.
+// Citations: /root/reference/proj/core/src/tensor.cpp.
+#include "kernels.cuh"
+
+namespace photon {
+namespace k {
+
+// ============================================================================
+// Embedding: x[m] = tok[tokens[m]] + pos[m % S]   (model.cpp:140-141)
+// ============================================================================
+__global__ void embed_fwd_kernel(const int32_t* __restrict__ tokens, const float* __restrict__ tok,
+                                 const float* __restrict__ pos, float* __restrict__ x, int M,
+                                 int S, int d) {
+  const int warps = blockDim.x / 32, lane = threadIdx.x & 31;
+  for (int m = blockIdx.x * warps + threadIdx.x / 32; m < M; m += gridDim.x * warps) {
+    const float* te = tok + (size_t)tokens[m] * d;
+    const float* pe = pos + (size_t)(m % S) * d;
+    float* xo = x + (size_t)m * d;
+    if ((d & 3) == 0) {
+      for (int j = lane * 4; j < d; j += 128) {
+        const float4 a = *reinterpret_cast<const float4*>(te + j);
+        const float4 b = *reinterpret_cast<const float4*>(pe + j);
+        *reinterpret_cast<float4*>(xo + j) = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+      }
+    } else {
+      for (int j = lane; j < d; j += 32) xo[j] = te[j] + pe[j];
+    }
+  }
+}
+
+void embed_fwd(const int32_t* tokens, const float* tok, const float* pos, float* x, int M, int S,
+               int d, cudaStream_t st) {
+  const int blocks = std::min<int>(cdiv(M, 8), kNumSMs * 16);
+  embed_fwd_kernel<<<blocks, 256, 0, st>>>(tokens, tok, pos, x, M, S, d);
+  PH_LAUNCH_CHECK();
+}
+
+// gather_rows backward (tensor.cpp:305-318): duplicates accumulate in ascending
+// row order.  One warp per vocab row walks that token's rows (CSR sorted by
+// row), so the sum order is fixed and no atomics are needed.
+__global__ void embed_bwd_tok_kernel(const float* __restrict__ dx, const int32_t* __restrict__ off,
+                                     const int32_t* __restrict__ rows, float* __restrict__ dtok,
+                                     int V, int d) {
+  const int warps = blockDim.x / 32, lane = threadIdx.x & 31;
+  for (int v = blockIdx.x * warps + threadIdx.x / 32; v < V; v += gridDim.x * warps) {
+    const int b = off[v], e = off[v + 1];
+    float* out = dtok + (size_t)v * d;
+    for (int j = lane; j < d; j += 32) {
+      float acc = 0.f;
+      for (int r = b; r < e; ++r) acc += dx[(size_t)rows[r] * d + j];
+      out[j] = acc;
+    }
+  }
+}
+__global__ void embed_bwd_pos_kernel(const float* __restrict__ dx, float* __restrict__ dpos,
+                                     int M, int S, int d) {
+  const size_t total = (size_t)S * d;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int s = (int)(i / d), j = (int)(i % d);
+    float acc = 0.f;
+    for (int m = s; m < M; m += S) acc += dx[(size_t)m * d + j];
+    dpos[i] = acc;
+  }
+}
+
+void embed_bwd(const float* dx, const int32_t* csr_off, const int32_t* csr_rows, float* dtok,
+               float* dpos, int V, int M, int S, int d, cudaStream_t st) {
+  embed_bwd_tok_kernel<<<std::min<int>(cdiv(V, 8), kNumSMs * 16), 256, 0, st>>>(
+      dx, csr_off, csr_rows, dtok, V, d);
+  PH_LAUNCH_CHECK();
+  embed_bwd_pos_kernel<<<std::min<int>(cdiv((uint64_t)S * d, 256), kNumSMs * 8), 256, 0, st>>>(
+      dx, dpos, M, S, d);
+  PH_LAUNCH_CHECK();
+}
+
+// ============================================================================
+// LayerNorm forward: two-pass mean / biased variance, eps 1e-5 (tensor.cpp:336-357)
+// One warp per row; fp32 statistics.
+// ============================================================================
+template <typename T>
+__global__ void ln_fwd_kernel(const float* __restrict__ x, const float* __restrict__ gain,
+                              const float* __restrict__ bias, T* __restrict__ y,
+                              float* __restrict__ mean_out, float* __restrict__ rstd_out, int M,
+                              int d) {
+  const int warps = blockDim.x / 32, lane = threadIdx.x & 31;
+  const float inv_d = 1.0f / (float)d;
+  for (int m = blockIdx.x * warps + threadIdx.x / 32; m < M; m += gridDim.x * warps) {
+    const float* xr = x + (size_t)m * d;
+    float s = 0.f;
+    for (int j = lane; j < d; j += 32) s += xr[j];
+    const float mean = warp_sum(s) * inv_d;
+    float v = 0.f;
+    for (int j = lane; j < d; j += 32) {
+      const float t = xr[j] - mean;
+      v += t * t;
+    }
+    const float rstd = rsqrtf(warp_sum(v) * inv_d + 1e-5f);
+    T* yr = y + (size_t)m * d;
+    for (int j = lane; j < d; j += 32) yr[j] = from_f<T>(gain[j] * ((xr[j] - mean) * rstd) + bias[j]);
+    if (lane == 0) {
+      mean_out[m] = mean;
+      rstd_out[m] = rstd;
+    }
+  }
+}
+
+template <typename T>
+void ln_fwd(const float* x, const float* gain, const float* bias, T* y, float* mean, float* rstd,
+            int M, int d, cudaStream_t st) {
+  ln_fwd_kernel<T><<<std::min<int>(cdiv(M, 8), kNumSMs * 16), 256, 0, st>>>(x, gain, bias, y,
+                                                                            mean, rstd, M, d);
+  PH_LAUNCH_CHECK();
+}
+
+// LayerNorm backward (tensor.cpp:370-392):
+//   dx = rstd * (dxh - mean(dxh) - xhat * mean(dxh * xhat)),  dxh = dy * gain
+// plus dgain = sum dy*xhat, dbias = sum dy over rows (per-block partials).
+constexpr int kLnBwdBlocks = kNumSMs * 2;
+constexpr int kLnBwdWarps = 8;
+int ln_bwd_parts() { return kLnBwdBlocks; }
+
+template <typename T>
+__global__ void __launch_bounds__(kLnBwdWarps * 32)
+ln_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ x,
+              const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
+              const float* __restrict__ gain, const float* __restrict__ dres,
+              float* __restrict__ dx_out, T* __restrict__ dx_T, float* __restrict__ part, int M,
+              int d) {
+  extern __shared__ float sm[];  // [warps][2][d]
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  float* my = sm + (size_t)warp * 2 * d;
+  for (int j = lane; j < 2 * d; j += 32) my[j] = 0.f;
+  const float inv_d = 1.0f / (float)d;
+  for (int m = blockIdx.x * kLnBwdWarps + warp; m < M; m += gridDim.x * kLnBwdWarps) {
+    const float* dyr = dy + (size_t)m * d;
+    const float* xr = x + (size_t)m * d;
+    const float mean = mean_in[m], rstd = rstd_in[m];
+    float s1 = 0.f, s2 = 0.f;
+    for (int j = lane; j < d; j += 32) {
+      const float xh = (xr[j] - mean) * rstd;
+      const float g = dyr[j];
+      const float dxh = g * gain[j];
+      s1 += dxh;
+      s2 += dxh * xh;
+      my[j] += g * xh;
+      my[d + j] += g;
+    }
+    s1 = warp_sum(s1) * inv_d;
+    s2 = warp_sum(s2) * inv_d;
+    float* out = dx_out + (size_t)m * d;
+    const float* rr = dres ? dres + (size_t)m * d : nullptr;
+    T* outT = dx_T ? dx_T + (size_t)m * d : nullptr;
+    for (int j = lane; j < d; j += 32) {
+      const float xh = (xr[j] - mean) * rstd;
+      float g = rstd * (dyr[j] * gain[j] - s1 - xh * s2);
+      if (rr) g += rr[j];
+      out[j] = g;
+      if (outT) outT[j] = from_f<T>(g);
+    }
+  }
+  __syncthreads();
+  // reduce warps -> block partial
+  for (int j = threadIdx.x; j < 2 * d; j += blockDim.x) {
+    float acc = 0.f;
+    for (int w = 0; w < kLnBwdWarps; ++w) acc += sm[(size_t)w * 2 * d + j];
+    part[(size_t)blockIdx.x * 2 * d + j] = acc;
+  }
+}
+
+// out[j] = sum_p part[p*stride + j]  (fixed order)
+__global__ void colreduce_kernel(const float* __restrict__ part, int nparts, int n, int stride,
+                                 float* __restrict__ out) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int p = 0; p < nparts; ++p) acc += part[(size_t)p * stride + j];
+    out[j] = acc;
+  }
+}
+
+template <typename T>
+void ln_bwd(const float* dy, const float* x, const float* mean, const float* rstd,
+            const float* gain, const float* dres, float* dx_out, T* dx_T, float* part,
+            float* dgain, float* dbias, int M, int d, cudaStream_t st) {
+  const size_t smem = (size_t)kLnBwdWarps * 2 * d * sizeof(float);
+  if (smem > 48 * 1024)
+    PH_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+  ln_bwd_kernel<T><<<kLnBwdBlocks, kLnBwdWarps * 32, smem, st>>>(dy, x, mean, rstd, gain, dres,
+                                                                 dx_out, dx_T, part, M, d);
+  PH_LAUNCH_CHECK();
+  colreduce_kernel<<<cdiv(d, 256), 256, 0, st>>>(part, kLnBwdBlocks, d, 2 * d, dgain);
+  PH_LAUNCH_CHECK();
+  colreduce_kernel<<<cdiv(d, 256), 256, 0, st>>>(part + d, kLnBwdBlocks, d, 2 * d, dbias);
+  PH_LAUNCH_CHECK();
+}
+
+// ============================================================================
+// Column sums for bias gradients: two passes, fixed order (deterministic).
+// ============================================================================
+static int colsum_chunks(int M, int N) {
+  const int colblocks = (int)cdiv(N, 256);
+  int r = std::max(1, (kNumSMs * 4) / colblocks);
+  return std::min(r, std::max(1, M / 16));
+}
+size_t colsum_part_floats(int M, int N) { return (size_t)colsum_chunks(M, N) * N; }
+
+template <typename T>
+__global__ void colsum_part_kernel(const T* __restrict__ x, int M, int N, int rows_per,
+                                   float* __restrict__ part) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  const int r0 = blockIdx.y * rows_per, r1 = min(M, r0 + rows_per);
+  float acc = 0.f;
+  for (int r = r0; r < r1; ++r) acc += to_f<T>(x[(size_t)r * N + j]);
+  part[(size_t)blockIdx.y * N + j] = acc;
+}
+
+template <typename T>
+void colsum(const T* x, int M, int N, float* part, float* out, cudaStream_t st) {
+  const int chunks = colsum_chunks(M, N);
+  const int rows_per = (int)cdiv(M, chunks);
+  colsum_part_kernel<T><<<dim3(cdiv(N, 256), chunks), 256, 0, st>>>(x, M, N, rows_per, part);
+  PH_LAUNCH_CHECK();
+  colreduce_kernel<<<cdiv(N, 256), 256, 0, st>>>(part, chunks, N, N, out);
+  PH_LAUNCH_CHECK();
+}
+
+// ============================================================================
+// Softmax cross-entropy, fused forward + backward, one CTA per row.
+// loss_row = log(sum exp(l - max)) + max - l[t]      (tensor.cpp:569-582)
+// dl = (softmax - onehot(t)) / count                   (tensor.cpp:590-600)
+// ============================================================================
+template <typename T>
+__global__ void __launch_bounds__(512) ce_kernel(T* __restrict__ logits,
+                                                 const int32_t* __restrict__ targets, int V,
+                                                 float inv_count, double* __restrict__ rowloss,
+                                                 int write_grad) {
+  __shared__ float red_m[16], red_s[16];
+  const int row = blockIdx.x;
+  T* l = logits + (size_t)row * V;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  float m = -INFINITY, s = 0.f;
+  int bad = 0;  // NaN / +inf logit: the reference's loss is NaN (tensor.cpp:569-582)
+  for (int j = tid; j < V; j += blockDim.x) {
+    const float v = to_f<T>(l[j]);
+    bad |= !(v < INFINITY);
+    if (v > m) {
+      s = s * __expf(m - v) + 1.f;
+      m = v;
+    } else {
+      s += __expf(v - m);
+    }
+  }
+  // warp combine (max, sum)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+    const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    const float mm = fmaxf(m, m2);
+    s = (m == -INFINITY ? 0.f : s * __expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mm));
+    m = mm;
+  }
+  if (lane == 0) {
+    red_m[warp] = m;
+    red_s[warp] = s;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    m = lane < nw ? red_m[lane] : -INFINITY;
+    s = lane < nw ? red_s[lane] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+      const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+      const float mm = fmaxf(m, m2);
+      s = (m == -INFINITY ? 0.f : s * __expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mm));
+      m = mm;
+    }
+    if (lane == 0) {
+      red_m[0] = m;
+      red_s[0] = s;
+    }
+  }
+  bad = __syncthreads_or(bad);
+  m = red_m[0];
+  s = red_s[0];
+  const int t = targets[row];
+  if (tid == 0) {
+    rowloss[row] = t < 0 ? 0.0
+                   : bad ? (double)NAN
+                         : (double)logf(s) + (double)m - (double)to_f<T>(l[t]);
+  }
+  if (!write_grad) return;
+  __syncthreads();  // everyone has read l[t] before it is overwritten
+  const float inv_s = 1.f / s;
+  const float g = t >= 0 ? inv_count : 0.f;
+  for (int j = tid; j < V; j += blockDim.x) {
+    const float p = __expf(to_f<T>(l[j]) - m) * inv_s;
+    l[j] = from_f<T>(g * (p - (j == t ? 1.f : 0.f)));
+  }
+}
+
+template <typename T>
+void ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count, double* rowloss,
+                bool write_grad, cudaStream_t st) {
+  ce_kernel<T><<<M, 512, 0, st>>>(logits, targets, V, inv_count, rowloss, write_grad ? 1 : 0);
+  PH_LAUNCH_CHECK();
+}
+
+__global__ void sum_scaled_kernel(const double* __restrict__ x, int n, double scale,
+                                  double* __restrict__ out) {
+  __shared__ double sm[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += x[i];
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+    acc = warp_sum(acc);
+    if (threadIdx.x == 0) *out = acc * scale;
+  }
+}
+
+void sum_scaled(const double* x, int n, double scale, double* out, cudaStream_t st) {
+  sum_scaled_kernel<<<1, 1024, 0, st>>>(x, n, scale, out);
+  PH_LAUNCH_CHECK();
+}
+
+// ============================================================================
+// SIMT causal attention (parity path, any head dim).  One warp per query row
+// (forward, dQ) or key row (dK, dV); lanes split the head dim.  Matches the
+// reference's masking j <= i and scale-before-max (tensor.cpp:455-483).
+// ============================================================================
+constexpr int kMaxDhPerLane = 8;  // head dim <= 256
+
+template <typename T>
+__global__ void attn_fwd_simt_kernel(const T* __restrict__ q, const T* __restrict__ k,
+                                     const T* __restrict__ v, T* __restrict__ o,
+                                     float* __restrict__ lse, int B, int S, int H, int d) {
+  const int dh = d / H, lane = threadIdx.x & 31;
+  const int warps = blockDim.x / 32;
+  const int row = blockIdx.x * warps + threadIdx.x / 32;  // (b, h, i) flattened as ((b*H+h)*S+i)
+  if (row >= B * H * S) return;
+  const int i = row % S, bh = row / S, h = bh % H, b = bh / H;
+  const float scale = rsqrtf((float)dh);
+  float qr[kMaxDhPerLane], acc[kMaxDhPerLane];
+  const size_t qoff = ((size_t)(b * S + i)) * d + h * dh;
+#pragma unroll
+  for (int c = 0; c < kMaxDhPerLane; ++c) {
+    const int col = lane + 32 * c;
+    qr[c] = col < dh ? to_f<T>(q[qoff + col]) : 0.f;
+    acc[c] = 0.f;
+  }
+  float mrun = -INFINITY, lrun = 0.f;
+  for (int j = 0; j <= i; ++j) {
+    const size_t koff = ((size_t)(b * S + j)) * d + h * dh;
+    float part = 0.f;
+#pragma unroll
+    for (int c = 0; c < kMaxDhPerLane; ++c) {
+      const int col = lane + 32 * c;
+      if (col < dh) part += qr[c] * to_f<T>(k[koff + col]);
+    }
+    const float sc = warp_sum(part) * scale;
+    const float mnew = fmaxf(mrun, sc);
+    const float corr = __expf(mrun - mnew);
+    const float p = __expf(sc - mnew);
+    lrun = lrun * corr + p;
+#pragma unroll
+    for (int c = 0; c < kMaxDhPerLane; ++c) {
+      const int col = lane + 32 * c;
+      if (col < dh) acc[c] = acc[c] * corr + p * to_f<T>(v[koff + col]);
+    }
+    mrun = mnew;
+  }
+  const float inv = 1.f / lrun;
+#pragma unroll
+  for (int c = 0; c < kMaxDhPerLane; ++c) {
+    const int col = lane + 32 * c;
+    if (col < dh) o[qoff + col] = from_f<T>(acc[c] * inv);
+  }
+  if (lane == 0) lse[row] = mrun + logf(lrun);
+}
+
+// D[row] = dO_i . O_i
+template <typename T>
+__global__ void attn_bwd_dot_kernel(const T* __restrict__ o, const T* __restrict__ dO,
+                                    float* __restrict__ Dvec, int B, int S, int H, int d) {
+  const int dh = d / H, lane = threadIdx.x & 31, warps = blockDim.x / 32;
+  const int row = blockIdx.x * warps + threadIdx.x / 32;
+  if (row >= B * H * S) return;
+  const int i = row % S, bh = row / S, h = bh % H, b = bh / H;
+  const size_t off = ((size_t)(b * S + i)) * d + h * dh;
+  float acc = 0.f;
+  for (int c = lane; c < dh; c += 32) acc += to_f<T>(o[off + c]) * to_f<T>(dO[off + c]);
+  acc = warp_sum(acc);
+  if (lane == 0) Dvec[row] = acc;
+}
+
+template <typename T>
+__global__ void attn_bwd_dq_kernel(const T* __restrict__ q, const T* __restrict__ k,
+                                   const T* __restrict__ v, const T* __restrict__ dO,
+                                   const float* __restrict__ lse, const float* __restrict__ Dvec,
+                                   T* __restrict__ dq, int B, int S, int H, int d) {
+  const int dh = d / H, lane = threadIdx.x & 31, warps = blockDim.x / 32;
+  const int row = blockIdx.x * warps + threadIdx.x / 32;
+  if (row >= B * H * S) return;
+  const int i = row % S, bh = row / S, h = bh % H, b = bh / H;
+  const float scale = rsqrtf((float)dh);
+  const size_t qoff = ((size_t)(b * S + i)) * d + h * dh;
+  float qr[kMaxDhPerLane], dor[kMaxDhPerLane], acc[kMaxDhPerLane];
+#pragma unroll
+  for (int c = 0; c < kMaxDhPerLane; ++c) {
+    const int col = lane + 32 * c;
+    qr[c] = col < dh ? to_f<T>(q[qoff + col]) : 0.f;
+    dor[c] = col < dh ? to_f<T>(dO[qoff + col]) : 0.f;
+    acc[c] = 0.f;
+  }
+  const float L = lse[row], D = Dvec[row];
+  for (int j = 0; j <= i; ++j) {
+    const size_t koff = ((size_t)(b * S + j)) * d + h * dh;
+    float ps = 0.f, pd = 0.f;
+#pragma unroll
+    for (int c = 0; c < kMaxDhPerLane; ++c) {
+      const int col = lane + 32 * c;
+      if (col < dh) {
+        ps += qr[c] * to_f<T>(k[koff + col]);
+        pd += dor[c] * to_f<T>(v[koff + col]);
+      }
+    }
+    const float s = warp_sum(ps) * scale;
+    const float dp = warp_sum(pd);
+    const float p = __expf(s - L);
+    const float ds = p * (dp - D) * scale;
+#pragma unroll
+    for (int c = 0; c < kMaxDhPerLane; ++c) {
+      const int col = lane + 32 * c;
+      if (col < dh) acc[c] += ds * to_f<T>(k[koff + col]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kMaxDhPerLane; ++c) {
+    const int col = lane + 32 * c;
+    if (col < dh) dq[qoff + col] = from_f<T>(acc[c]);
+  }
+}
+
+template <typename T>
+__global__ void attn_bwd_dkdv_kernel(const T* __restrict__ q, const T* __restrict__ k,
+                                     const T* __restrict__ v, const T* __restrict__ dO,
+                                     const float* __restrict__ lse,
+                                     const float* __restrict__ Dvec, T* __restrict__ dk,
+                                     T* __restrict__ dv, int B, int S, int H, int d) {
+  const int dh = d / H, lane = threadIdx.x & 31, warps = blockDim.x / 32;
+  const int row = blockIdx.x * warps + threadIdx.x / 32;  // key row
+  if (row >= B * H * S) return;
+  const int j = row % S, bh = row / S, h = bh % H, b = bh / H;
+  const float scale = rsqrtf((float)dh);
+  const size_t koff = ((size_t)(b * S + j)) * d + h * dh;
+  float kr[kMaxDhPerLane], vr[kMaxDhPerLane], ak[kMaxDhPerLane], av[kMaxDhPerLane];
+#pragma unroll
+  for (int c = 0; c < kMaxDhPerLane; ++c) {
+    const int col = lane + 32 * c;
+    kr[c] = col < dh ? to_f<T>(k[koff + col]) : 0.f;
+    vr[c] = col < dh ? to_f<T>(v[koff + col]) : 0.f;
+    ak[c] = 0.f;
+    av[c] = 0.f;
+  }
+  for (int i = j; i < S; ++i) {
+    const size_t qoff = ((size_t)(b * S + i)) * d + h * dh;
+    const int qrow = bh * S + i;
+    float ps = 0.f, pd = 0.f;
+#pragma unroll
+    for (int c = 0; c < kMaxDhPerLane; ++c) {
+      const int col = lane + 32 * c;
+      if (col < dh) {
+        ps += to_f<T>(q[qoff + col]) * kr[c];
+        pd += to_f<T>(dO[qoff + col]) * vr[c];
+      }
+    }
+    const float s = warp_sum(ps) * scale;
+    const float dp = warp_sum(pd);
+    const float p = __expf(s - lse[qrow]);
+    const float ds = p * (dp - Dvec[qrow]) * scale;
+#pragma unroll
+    for (int c = 0; c < kMaxDhPerLane; ++c) {
+      const int col = lane + 32 * c;
+      if (col < dh) {
+        av[c] += p * to_f<T>(dO[qoff + col]);
+        ak[c] += ds * to_f<T>(q[qoff + col]);
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kMaxDhPerLane; ++c) {
+    const int col = lane + 32 * c;
+    if (col < dh) {
+      dk[koff + col] = from_f<T>(ak[c]);
+      dv[koff + col] = from_f<T>(av[c]);
+    }
+  }
+}
+
+template <typename T>
+void attn_fwd_simt(const T* q, const T* k, const T* v, T* o, float* lse, int B, int S, int H,
+                   int d, cudaStream_t st) {
+  if (d / H > 32 * kMaxDhPerLane) throw Error(PHOTON_ERR_CONFIG, "attention: head dim > 256");
+  const int rows = B * H * S;
+  attn_fwd_simt_kernel<T><<<cdiv(rows, 4), 128, 0, st>>>(q, k, v, o, lse, B, S, H, d);
+  PH_LAUNCH_CHECK();
+}
+
+template <typename T>
+void attn_bwd_simt(const T* q, const T* k, const T* v, const T* o, const T* dO, const float* lse,
+                   float* Dvec, T* dq, T* dk, T* dv, int B, int S, int H, int d, cudaStream_t st) {
+  const int rows = B * H * S;
+  attn_bwd_dot_kernel<T><<<cdiv(rows, 4), 128, 0, st>>>(o, dO, Dvec, B, S, H, d);
+  PH_LAUNCH_CHECK();
+  attn_bwd_dq_kernel<T><<<cdiv(rows, 4), 128, 0, st>>>(q, k, v, dO, lse, Dvec, dq, B, S, H, d);
+  PH_LAUNCH_CHECK();
+  attn_bwd_dkdv_kernel<T><<<cdiv(rows, 4), 128, 0, st>>>(q, k, v, dO, lse, Dvec, dk, dv, B, S, H,
+                                                         d);
+  PH_LAUNCH_CHECK();
+}
+
+// ============================================================================
+// casts
+// ============================================================================
+__global__ void f64_to_f32_kernel(const double* __restrict__ in, float* __restrict__ out,
+                                  uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = (float)in[i];
+}
+__global__ void f32_to_f64_kernel(const float* __restrict__ in, double* __restrict__ out,
+                                  uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = (double)in[i];
+}
+__global__ void f32_to_bf16_kernel(const float* __restrict__ in, bf16* __restrict__ out,
+                                   uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = __float2bfloat16_rn(in[i]);
+}
+void f64_to_f32(const double* in, float* out, uint64_t n, cudaStream_t st) {
+  f64_to_f32_kernel<<<std::min<unsigned>(cdiv(n, 256), kNumSMs * 8), 256, 0, st>>>(in, out, n);
+  PH_LAUNCH_CHECK();
+}
+void f32_to_f64(const float* in, double* out, uint64_t n, cudaStream_t st) {
+  f32_to_f64_kernel<<<std::min<unsigned>(cdiv(n, 256), kNumSMs * 8), 256, 0, st>>>(in, out, n);
+  PH_LAUNCH_CHECK();
+}
+void f32_to_bf16(const float* in, bf16* out, uint64_t n, cudaStream_t st) {
+  f32_to_bf16_kernel<<<std::min<unsigned>(cdiv(n, 256), kNumSMs * 8), 256, 0, st>>>(in, out, n);
+  PH_LAUNCH_CHECK();
+}
+
+// ---- instantiations ----------------------------------------------------------
+#define INST(T)                                                                                 \
+  template void ln_fwd<T>(const float*, const float*, const float*, T*, float*, float*, int, int, \
+                          cudaStream_t);                                                        \
+  template void ln_bwd<T>(const float*, const float*, const float*, const float*, const float*,   \
+                          const float*, float*, T*, float*, float*, float*, int, int,            \
+                          cudaStream_t);                                                        \
+  template void colsum<T>(const T*, int, int, float*, float*, cudaStream_t);                    \
+  template void ce_fwd_bwd<T>(T*, const int32_t*, int, int, float, double*, bool, cudaStream_t); \
+  template void attn_fwd_simt<T>(const T*, const T*, const T*, T*, float*, int, int, int, int,    \
+                                 cudaStream_t);                                                 \
+  template void attn_bwd_simt<T>(const T*, const T*, const T*, const T*, const T*, const float*,  \
+                                 float*, T*, T*, T*, int, int, int, int, cudaStream_t);
+INST(float)
+INST(bf16)
+#undef INST
+
+}  // namespace k
+}  // namespace photon

@@ -1,0 +1,95 @@
+// kernels.cuh -- launch wrappers for the non-GEMM kernels of the client step,
+// the optimizer and the aggregation.  Reference citations are in kernels.cu /
+// optim.cu next to each kernel.
+#pragma once
+
+#include "common.cuh"
+
+namespace photon {
+namespace k {
+
+// ---- embedding (gather_rows + add, tensor.cpp:209-223, 290-320) ------------
+void embed_fwd(const int32_t* tokens, const float* tok, const float* pos, float* x, int M, int S,
+               int d, cudaStream_t st);
+// deterministic scatter-add: rows sorted by token (CSR), ascending row order
+void embed_bwd(const float* dx, const int32_t* csr_off, const int32_t* csr_rows, float* dtok,
+               float* dpos, int V, int M, int S, int d, cudaStream_t st);
+
+// ---- layer norm (tensor.cpp:322-394) ---------------------------------------
+template <typename T>
+void ln_fwd(const float* x, const float* gain, const float* bias, T* y, float* mean, float* rstd,
+            int M, int d, cudaStream_t st);
+// dx_out = dres + LN'(dy); dx_T = bf16/f32 copy (optional); gain/bias grads
+// written to dgain/dbias via per-block partials in `part` (>= ln_bwd_parts()*2*d floats)
+template <typename T>
+void ln_bwd(const float* dy, const float* x, const float* mean, const float* rstd,
+            const float* gain, const float* dres, float* dx_out, T* dx_T, float* part,
+            float* dgain, float* dbias, int M, int d, cudaStream_t st);
+int ln_bwd_parts();
+
+// ---- column sums (add_bias backward, tensor.cpp:279-285) -------------------
+template <typename T>
+void colsum(const T* x, int M, int N, float* part, float* out, cudaStream_t st);
+size_t colsum_part_floats(int M, int N);
+
+// ---- softmax cross-entropy fwd+bwd (tensor.cpp:544-603) --------------------
+// logits [M,V] overwritten with dlogits = (softmax - onehot) * inv_count;
+// rowloss[m] = logsumexp - logit[target] (0 for target < 0)
+template <typename T>
+void ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count,
+                double* rowloss, bool write_grad, cudaStream_t st);
+// out = inv_count * sum(rowloss) (fixed-order tree)
+void sum_scaled(const double* x, int n, double scale, double* out, cudaStream_t st);
+
+// ---- causal attention (tensor.cpp:436-542), SIMT fp32 math ------------------
+template <typename T>
+void attn_fwd_simt(const T* q, const T* k, const T* v, T* o, float* lse, int B, int S, int H,
+                   int d, cudaStream_t st);
+template <typename T>
+void attn_bwd_simt(const T* q, const T* k, const T* v, const T* o, const T* dO, const float* lse,
+                   float* Dvec, T* dq, T* dk, T* dv, int B, int S, int H, int d, cudaStream_t st);
+
+// ---- casts -------------------------------------------------------------------
+void f64_to_f32(const double* in, float* out, uint64_t n, cudaStream_t st);
+void f32_to_f64(const float* in, double* out, uint64_t n, cudaStream_t st);
+void f32_to_bf16(const float* in, bf16* out, uint64_t n, cudaStream_t st);
+
+// ---- optimizer (optim.cu, compiled without FMA contraction) ---------------------
+// global-norm clip (optim.cpp:50-57): parts -> norm, cf; bad[0] set to step+1
+// on a non-finite norm (first one wins)
+void sumsq_parts(const float* g, uint64_t n, double* part, cudaStream_t st);
+int sumsq_nparts();
+void clip_finalize(const double* part, double clip, double* norm_out, float* cf_out,
+                   int* bad_step, int step, cudaStream_t st);
+// AdamW (optim.cpp:61-90) in f64 arithmetic over fp32 storage
+void adamw_f32(float* p, const float* g, float* m, float* v, bf16* shadow, uint64_t n,
+               const float* cf, double lr, double b1, double b2, double bc1, double bc2,
+               double eps, double wd, cudaStream_t st);
+void sgd_f32(float* p, const float* g, bf16* shadow, uint64_t n, const float* cf, double lr,
+             cudaStream_t st);
+// exact f64 variants for the f64 C-ABI (bit-exact vs the reference)
+void sumsq_sequential_f64(const double* g, uint64_t n, double* out, cudaStream_t st);
+void adamw_f64(double* p, const double* g, double* m, double* v, uint64_t n, const double* norm,
+               double clip, double lr, double b1, double b2, double bc1, double bc2, double eps,
+               double wd, cudaStream_t st);
+void sgd_f64(double* p, const double* g, uint64_t n, const double* norm, double clip, double lr,
+             cudaStream_t st);
+
+// ---- aggregation (param_vector.cpp:120-152, optim.cpp:124-159) -----------------
+// kind: 0 FedAvg, 1 momentum.  models: device array of k device pointers.
+template <typename T>
+void aggregate(const T* const* models, int k, uint64_t n, T* theta, T* velocity, int kind,
+               double eta, double mu, int nesterov, cudaStream_t st);
+template <typename T>
+void mean_only(const T* const* models, int k, uint64_t n, T* out, cudaStream_t st);
+template <typename T>
+void sub_only(const T* a, const T* b, uint64_t n, T* out, cudaStream_t st);
+template <typename T>
+void server_step_only(const T* theta, const T* delta, const T* mean, T* velocity, T* out,
+                      uint64_t n, int kind, double eta, double mu, int nesterov, cudaStream_t st);
+// post_process clip (client.cpp:96-110): out = ref + min(1, thr/|k-ref|) (k - ref)
+void clip_update_f32(const float* ref, float* theta_k, uint64_t n, double threshold,
+                     double* part, cudaStream_t st);
+
+}  // namespace k
+}  // namespace photon

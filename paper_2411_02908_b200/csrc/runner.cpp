@@ -1,0 +1,270 @@
+// runner.cpp -- FederationRunner::run_round (aggregator.cpp:93-220) on B200s.
+//
+// Each rank runs the sampled clients whose slot % world == rank, each from the
+// replicated theta_t.  The round boundary is the only communication:
+//   1. every rank scatters 1/world shards of its client models to the shard
+//      owners (ncclSend/ncclRecv in ascending slot order -> the owner holds its
+//      shard of every surviving model in canonical ascending client order);
+//   2. the owner runs the fused anchored-mean -> pseudo-gradient -> outer
+//      update kernel on its shard (theta_t and velocity shards stay resident);
+//   3. ncclAllGather rebuilds theta_{t+1} on every rank.
+// Per-GPU wire bytes = 2 (G-1)/G * P * 4, the ring all-reduce volume; the
+// arithmetic is bit-identical to the single-GPU path for any world size.
+#include "runner.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <cstring>
+
+#include "kernels.cuh"
+
+namespace photon {
+
+#define PH_NCCL(call)                                                                    \
+  do {                                                                                   \
+    ncclResult_t r_ = (call);                                                            \
+    if (r_ != ncclSuccess)                                                               \
+      throw Error(PHOTON_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_));  \
+  } while (0)
+
+// optim.cpp:105-113
+void validate_server(const photon_server_cfg& s) {
+  if (!(s.eta > 0.0)) throw Error(PHOTON_ERR_CONFIG, "server opt: eta must be > 0");
+  if (s.momentum < 0.0 || s.momentum >= 1.0)
+    throw Error(PHOTON_ERR_CONFIG, "server opt: momentum must be in [0,1)");
+  if (s.kind != 0 && s.kind != 1) throw Error(PHOTON_ERR_CONFIG, "server opt: unknown kind");
+  if (s.kind == 0 && (s.eta != 1.0 || s.momentum != 0.0))
+    throw Error(PHOTON_ERR_CONFIG, "server opt: fedavg is eta=1, momentum=0 by definition");
+}
+
+Runner::Runner(Ctx* c, const photon_fed_cfg& f, const photon_train_cfg& t,
+               const photon_server_cfg& s, const Plan* p, const double* theta0, int rk, int ws,
+               const uint8_t* nccl_id)
+    : ctx(c), fed(f), train(t), server(s), plan(p), rank(rk), world(ws) {
+  // FederationConfig::validate (aggregator.cpp:16-23) + runner guards (:50-71)
+  if (f.population < 1) throw Error(PHOTON_ERR_CONFIG, "federation: population must be >= 1");
+  if (f.clients_per_round < 1 || f.clients_per_round > f.population)
+    throw Error(PHOTON_ERR_CONFIG, "federation: need 1 <= K <= P");
+  if (f.rounds < 1) throw Error(PHOTON_ERR_CONFIG, "federation: rounds must be >= 1");
+  if (!p) throw Error(PHOTON_ERR_USAGE, "runner: null shard plan");
+  if (p->blocks.size() < f.population)
+    throw Error(PHOTON_ERR_CONFIG, "shard plan covers " + std::to_string(p->blocks.size()) +
+                                       " clients, federation needs " +
+                                       std::to_string(f.population));
+  if (p->seq_len != t.model.seq_len)
+    throw Error(PHOTON_ERR_USAGE, "stream: seq_len does not match the plan's block size");
+  if (std::memcmp(&t.model, &c->cfg, sizeof(photon_model_cfg)) != 0)
+    throw Error(PHOTON_ERR_CONFIG, "runner: train model differs from the context's model");
+  if (t.batch_size > c->max_batch)
+    throw Error(PHOTON_ERR_CONFIG, "runner: batch_size exceeds the context's max_batch");
+  if (ws < 1 || rk < 0 || rk >= ws) throw Error(PHOTON_ERR_USAGE, "runner: bad rank/world");
+  check_train_cfg(t);
+  validate_server(s);
+  P = c->eng->P;
+  shard = ((P + ws - 1) / ws + 3) / 4 * 4;
+  Ppad = shard * ws;
+  cursors.assign(f.population, 0);
+  PH_CUDA(cudaSetDevice(c->device));
+  d_theta.reserve(Ppad);
+  d_vel.reserve(Ppad);
+  PH_CUDA(cudaMemsetAsync(d_theta.ptr, 0, Ppad * 4, c->stream));
+  PH_CUDA(cudaMemsetAsync(d_vel.ptr, 0, Ppad * 4, c->stream));
+  c->d_f64a.reserve(P);
+  PH_CUDA(cudaMemcpyAsync(c->d_f64a.ptr, theta0, P * 8, cudaMemcpyHostToDevice, c->stream));
+  k::f64_to_f32(c->d_f64a.ptr, d_theta.ptr, P, c->stream);
+  h_stats.reserve(4 * f.clients_per_round + 4);
+  d_stats.reserve(4 * f.clients_per_round + 4);
+  PH_CUDA(cudaEventCreate(&ev_a));
+  PH_CUDA(cudaEventCreate(&ev_b));
+  PH_CUDA(cudaEventCreate(&ev_c));
+  if (ws > 1) {
+    if (!nccl_id) throw Error(PHOTON_ERR_USAGE, "runner: world > 1 needs an NCCL unique id");
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    PH_NCCL(ncclCommInitRank(&comm, ws, id, rk));
+  }
+  PH_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+Runner::~Runner() {
+  if (comm) ncclCommDestroy(comm);
+  if (ev_a) cudaEventDestroy(ev_a);
+  if (ev_b) cudaEventDestroy(ev_b);
+  if (ev_c) cudaEventDestroy(ev_c);
+}
+
+void Runner::run_round(photon_round_record* rec) {
+  if (next_round >= fed.rounds) throw Error(PHOTON_ERR_USAGE, "run_round called after the final round");
+  PH_CUDA(cudaSetDevice(ctx->device));
+  const uint64_t round = next_round;
+  const auto sampled = sample_clients(fed.population, fed.clients_per_round, fed.seed, round);
+  const int K = (int)sampled.size();
+  const int tau = (int)train.local_steps, B = (int)train.batch_size, S = (int)plan->seq_len;
+  const int V = (int)train.model.vocab_size;
+  const uint64_t step_base = round * train.local_steps;
+  cudaStream_t st = ctx->stream;
+
+  std::vector<int> mine;
+  for (int si = 0; si < K; ++si)
+    if (si % world == rank) mine.push_back(si);
+  if (d_models.n < mine.size() * Ppad) {
+    d_models.reserve(mine.size() * Ppad);
+    PH_CUDA(cudaMemsetAsync(d_models.ptr, 0, d_models.n * 4, st));
+  }
+
+  // stats layout: [0,K) mean loss, [K,2K) error code, [2K,3K) error step
+  std::fill(h_stats.ptr, h_stats.ptr + 3 * K, 0.0);
+  PH_CUDA(cudaEventRecord(ev_a, st));
+  for (size_t j = 0; j < mine.size(); ++j) {
+    const int si = mine[j];
+    const uint64_t client = sampled[si];
+    // BatchStream(plan, client, B, S, stream_seed(seed, client), cursor) x tau
+    batches.prepare(tau, B, S, V);
+    const uint64_t seed = derive(fed.seed, kPurposeStream, client);
+    for (int i = 0; i < tau; ++i)
+      stream_rows(*plan, client, seed, cursors[client] + (uint64_t)i * B, B,
+                  batches.tokens.ptr + (size_t)i * B * S, batches.targets.ptr + (size_t)i * B * S);
+    batches.finalize(V);
+    ctx->upload(batches);
+    LocalResult r = ctx->local_round(train, batches, d_theta.ptr, d_models.ptr + j * Ppad, step_base);
+    double acc = 0.0;
+    for (double l : r.losses) acc += l;
+    h_stats.ptr[si] = tau ? acc / tau : 0.0;  // ClientResult::mean_loss (client.cpp:112-117)
+    if (r.error) {
+      h_stats.ptr[K + si] = r.error;
+      h_stats.ptr[2 * K + si] = (double)r.error_step;
+      break;
+    }
+  }
+  PH_CUDA(cudaEventRecord(ev_b, st));
+  if (world > 1) {
+    PH_CUDA(cudaMemcpyAsync(d_stats.ptr, h_stats.ptr, 3 * K * 8, cudaMemcpyHostToDevice, st));
+    PH_NCCL(ncclAllReduce(d_stats.ptr, d_stats.ptr, 3 * K, ncclDouble, ncclSum, comm, st));
+    PH_CUDA(cudaMemcpyAsync(h_stats.ptr, d_stats.ptr, 3 * K * 8, cudaMemcpyDeviceToHost, st));
+    PH_CUDA(cudaStreamSynchronize(st));
+  }
+  // errors surface in ascending client order (aggregator.cpp:141-144)
+  for (int si = 0; si < K; ++si) {
+    const int code = (int)h_stats.ptr[K + si];
+    if (code) {
+      Error e(code, code == PHOTON_ERR_DIVERGENCE
+                        ? "client " + std::to_string(sampled[si]) + " diverged at round " +
+                              std::to_string(round) + ", step " +
+                              std::to_string((uint64_t)h_stats.ptr[2 * K + si])
+                        : "gradient norm is not finite");
+      e.round = round;
+      e.client = sampled[si];
+      e.step = (uint64_t)h_stats.ptr[2 * K + si];
+      throw e;
+    }
+  }
+  // a dropped client trains and advances its cursor but never reports
+  std::vector<int> surv;
+  for (int si = 0; si < K; ++si) {
+    cursors[sampled[si]] += (uint64_t)tau * B;
+    if (!dropouts.count({round, sampled[si]})) surv.push_back(si);
+  }
+  if (surv.empty())
+    throw Error(PHOTON_ERR_ROUND_FAILURE, "round " + std::to_string(round) + ": no surviving clients");
+  if ((int)surv.size() < K && fed.topology == 2)
+    throw Error(PHOTON_ERR_ROUND_FAILURE,
+                "round " + std::to_string(round) + ": ring all-reduce cannot tolerate dropouts");
+
+  // ---- round boundary: mean -> pseudo-gradient -> outer step ----
+  const int n = (int)surv.size();
+  std::vector<const float*> ptrs(n);
+  if (world == 1) {
+    for (int r = 0; r < n; ++r) ptrs[r] = d_models.ptr + (size_t)(surv[r] / world) * Ppad;
+  } else {
+    d_recv.reserve((size_t)n * shard);
+    PH_NCCL(ncclGroupStart());
+    for (int r = 0; r < n; ++r) {
+      const int si = surv[r], owner = si % world;
+      if (owner == rank) {
+        const float* model = d_models.ptr + (size_t)(si / world) * Ppad;
+        for (int q = 0; q < world; ++q)
+          PH_NCCL(ncclSend(model + (size_t)q * shard, shard, ncclFloat, q, comm, st));
+      }
+      PH_NCCL(ncclRecv(d_recv.ptr + (size_t)r * shard, shard, ncclFloat, owner, comm, st));
+    }
+    PH_NCCL(ncclGroupEnd());
+    for (int r = 0; r < n; ++r) ptrs[r] = d_recv.ptr + (size_t)r * shard;
+  }
+  d_model_ptrs.reserve(n);
+  PH_CUDA(cudaMemcpyAsync(d_model_ptrs.ptr, ptrs.data(), n * sizeof(float*), cudaMemcpyHostToDevice, st));
+  const uint64_t off = world == 1 ? 0 : (uint64_t)rank * shard;
+  const uint64_t len = world == 1 ? P : shard;
+  k::aggregate<float>(d_model_ptrs.ptr, n, len, d_theta.ptr + off, d_vel.ptr + off, server.kind,
+                      server.eta, server.momentum, server.nesterov, st);
+  if (world > 1)
+    PH_NCCL(ncclAllGather(d_theta.ptr + off, d_theta.ptr, shard, ncclFloat, comm, st));
+  PH_CUDA(cudaEventRecord(ev_c, st));
+  PH_CUDA(cudaEventSynchronize(ev_c));
+
+  if (rec) {
+    std::memset(rec, 0, sizeof(*rec));
+    rec->round = round;
+    rec->n_sampled = K;
+    for (int si = 0; si < K && si < 64; ++si) rec->sampled_ids[si] = sampled[si];
+    double acc = 0.0, lo = std::numeric_limits<double>::infinity(), hi = -lo;
+    for (int si : surv) {
+      const double l = h_stats.ptr[si];
+      acc += l;
+      lo = std::min(lo, l);
+      hi = std::max(hi, l);
+    }
+    rec->mean_client_loss = acc / (double)n;
+    rec->min_client_loss = lo;
+    rec->max_client_loss = hi;
+    float ms = 0.f;
+    PH_CUDA(cudaEventElapsedTime(&ms, ev_a, ev_b));
+    rec->local_ms = ms;
+    PH_CUDA(cudaEventElapsedTime(&ms, ev_b, ev_c));
+    rec->aggregate_ms = ms;
+    PH_CUDA(cudaEventElapsedTime(&ms, ev_a, ev_c));
+    rec->round_ms = ms;
+    rec->tokens = (uint64_t)mine.size() * tau * B * S;
+  }
+  next_round = round + 1;
+}
+
+void Runner::theta_f64(double* out) {
+  PH_CUDA(cudaSetDevice(ctx->device));
+  ctx->d_f64a.reserve(P);
+  k::f32_to_f64(d_theta.ptr, ctx->d_f64a.ptr, P, ctx->stream);
+  PH_CUDA(cudaMemcpyAsync(out, ctx->d_f64a.ptr, P * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  PH_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void Runner::velocity_f64(double* out) {
+  PH_CUDA(cudaSetDevice(ctx->device));
+  const float* src = d_vel.ptr;
+  if (world > 1) {
+    ctx->d_f32a.reserve(Ppad);
+    PH_NCCL(ncclAllGather(d_vel.ptr + (size_t)rank * shard, ctx->d_f32a.ptr, shard, ncclFloat,
+                          comm, ctx->stream));
+    src = ctx->d_f32a.ptr;
+  }
+  ctx->d_f64a.reserve(P);
+  k::f32_to_f64(src, ctx->d_f64a.ptr, P, ctx->stream);
+  PH_CUDA(cudaMemcpyAsync(out, ctx->d_f64a.ptr, P * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  PH_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// FederationRunner::restore (aggregator.cpp:78-91)
+void Runner::restore(const double* theta, const double* velocity, uint64_t nr,
+                     const uint64_t* cur, uint64_t n) {
+  if (n != cursors.size()) throw Error(PHOTON_ERR_USAGE, "restore: cursor vector has wrong length");
+  PH_CUDA(cudaSetDevice(ctx->device));
+  ctx->d_f64a.reserve(P);
+  PH_CUDA(cudaMemcpyAsync(ctx->d_f64a.ptr, theta, P * 8, cudaMemcpyHostToDevice, ctx->stream));
+  k::f64_to_f32(ctx->d_f64a.ptr, d_theta.ptr, P, ctx->stream);
+  PH_CUDA(cudaMemcpyAsync(ctx->d_f64a.ptr, velocity, P * 8, cudaMemcpyHostToDevice, ctx->stream));
+  k::f64_to_f32(ctx->d_f64a.ptr, d_vel.ptr, P, ctx->stream);
+  PH_CUDA(cudaStreamSynchronize(ctx->stream));
+  next_round = nr;
+  cursors.assign(cur, cur + n);
+}
+
+}  // namespace photon

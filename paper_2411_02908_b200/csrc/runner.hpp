@@ -1,0 +1,52 @@
+// runner.hpp -- device-resident FederationRunner (aggregator.h:70-102) with a
+// sharded, NCCL-backed round boundary across ranks.
+#pragma once
+
+#include <nccl.h>
+
+#include <set>
+#include <utility>
+#include <vector>
+
+#include "ctx.hpp"
+
+namespace photon {
+
+struct Runner {
+  Ctx* ctx;
+  photon_fed_cfg fed;
+  photon_train_cfg train;
+  photon_server_cfg server;
+  const Plan* plan;
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+
+  uint64_t P = 0, shard = 0, Ppad = 0;
+  uint64_t next_round = 0;
+  std::vector<uint64_t> cursors;
+  std::set<std::pair<uint64_t, uint64_t>> dropouts;
+
+  DevBuf<float> d_theta;     // [Ppad] theta_t (replicated)
+  DevBuf<float> d_vel;       // [Ppad] outer velocity (this rank's shard is authoritative)
+  DevBuf<float> d_models;    // [slots_local][Ppad] client results on this rank
+  DevBuf<float> d_recv;      // [K][shard] exchanged shards
+  DevBuf<const float*> d_model_ptrs;
+  DevBuf<double> d_stats;    // [2K] loss stats / error exchange
+  PinnedBuf<double> h_stats;
+  RoundBatches batches;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;
+
+  Runner(Ctx* c, const photon_fed_cfg& f, const photon_train_cfg& t, const photon_server_cfg& s,
+         const Plan* p, const double* theta0, int rank, int world, const uint8_t* nccl_id);
+  ~Runner();
+
+  void run_round(photon_round_record* rec);
+  void theta_f64(double* out);
+  void velocity_f64(double* out);
+  void restore(const double* theta, const double* velocity, uint64_t next_round,
+               const uint64_t* cursors, uint64_t n);
+};
+
+void validate_server(const photon_server_cfg& s);
+
+}  // namespace photon
