@@ -117,6 +117,9 @@ typedef struct {
   double aggregate_ms;        /* device time: exchange + fused mean/outer update + gather */
   double round_ms;            /* device time of the whole round on this rank */
   uint64_t tokens;            /* tokens trained on this rank this round */
+  double host_ms;             /* host batch staging (BatchStream x tau) + H2D issue */
+  uint64_t h2d_bytes;         /* inputs copied host->device this round on this rank */
+  uint64_t d2h_bytes;         /* results read back device->host this round */
 } photon_round_record;
 
 typedef struct photon_ctx photon_ctx;       /* one GPU: device state of one client slot */
@@ -226,6 +229,21 @@ int photon_debug_gemm(int impl, int M, int N, int K, const void* A, int64_t lda,
                       const void* B, int64_t ldb, int b_kmajor, int ab_dtype, void* C,
                       int64_t ldc, int c_dtype, int epi, const float* bias, const float* resid,
                       void* aux, int iters, double* ms, photon_err* err);
+
+/* Causal attention on device pointers (bf16 q,k,v,o,dO,dq,dk,dv as [B*S, d]
+ * with head h in columns [h*dh,(h+1)*dh); lse, scratch fp32 [B*H*S]):
+ * impl 0 = SIMT, 1 = tensor core.  dO == NULL: forward only.  *ms = device
+ * time of the call. */
+int photon_debug_attention(int impl, int B, int S, int H, int d, const void* q, const void* k,
+                           const void* v, void* o, float* lse, const void* dO, float* scratch,
+                           void* dq, void* dk, void* dv, double* ms, photon_err* err);
+
+/* Per-kernel-class device timing of the client step (CUDA events around each
+ * launch; adds overhead, for profiling rounds only).  times[8] = {gemm_ms,
+ * attn_ms, other_ms, gemm_flops, attn_flops, gemm_launches, attn_launches,
+ * launches}, accumulated since the last reset (set_timing resets). */
+int photon_ctx_set_timing(photon_ctx* ctx, int on);
+int photon_ctx_kernel_times(photon_ctx* ctx, double* times8);
 
 /* ---- federated round runner (FederationRunner, aggregator.h:70-102) ------------ */
 /* Device-resident: theta_t, velocity and client state live in HBM.  With

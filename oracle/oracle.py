@@ -527,6 +527,16 @@ class Reference:
                                        _p(secs, C.c_double)), "ref_run_rounds")
         return out, vel, losses, secs
 
+    def train_sample(self, cfg: ModelCfg, t: TrainCfg, batch: int, seq: int, steps: int,
+                     threads: int):
+        """(wall seconds, last loss) of `threads` reference clients x `steps` steps."""
+        secs, loss = C.c_double(), C.c_double()
+        _check(self.lib.ref_train_sample(cfg.as_array(), t.as_doubles(), C.c_uint64(batch),
+                                         C.c_uint64(seq), C.c_uint64(steps),
+                                         C.c_uint64(threads), C.byref(secs), C.byref(loss)),
+               "ref_train_sample")
+        return secs.value, loss.value
+
     def run_experiment_fed(self, cfg: ModelCfg, t: TrainCfg, s: ServerCfg, corpus_tokens,
                            population, rounds, seed, model_seed, data_seed, eval_sequences,
                            eval_batch, out_dir: str):

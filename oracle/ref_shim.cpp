@@ -11,6 +11,7 @@
 #include <exception>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "fedsim/aggregator.h"
@@ -279,6 +280,52 @@ int ref_run_experiment_fed(const uint64_t* m, const double* t, const double* s,
         f.eval_batch = eval_batch;
         RunOutcome o = run_experiment(f, out_dir); ppl_out[0] = o.initial_ppl;
         ppl_out[1] = o.final_ppl)
+}
+
+// Bounded CPU sample of the reference client step (client.cpp:135-154):
+// `threads` independent clients, each `steps` x {forward_loss, backward,
+// collect_grads, lr_at, adamw_step} on [batch, seq] token blocks drawn from the
+// reference's own corpus generator.  Wall seconds of the step loop only.
+int ref_train_sample(const uint64_t* m, const double* t, uint64_t batch, uint64_t seq,
+                     uint64_t steps, uint64_t threads, double* seconds_out, double* loss_out) {
+  GUARD(LocalTrainConfig c = tcfg(m, t); TransformerModel model(c.model);
+        const ParamVector theta0 = model.init_params(1);
+        std::vector<double> losses(threads, 0.0);
+        std::vector<std::exception_ptr> errs(threads);
+        auto body = [&](uint64_t w) {
+          try {
+            Corpus corp = generate_corpus("web", steps * batch * (seq + 1) + 1, 7 + w,
+                                          (uint32_t)c.model.vocab_size);
+            ParamVector theta = theta0.clone();
+            AdamWState opt = AdamWState::fresh(c.adamw, theta);
+            for (uint64_t i = 0; i < steps; ++i) {
+              Batch b;
+              b.batch_size = batch;
+              b.seq_len = seq;
+              for (uint64_t r = 0; r < batch; ++r)
+                for (uint64_t q = 0; q < seq; ++q) {
+                  const std::size_t o = (i * batch + r) * (seq + 1) + q;
+                  b.inputs.push_back(corp.tokens[o]);
+                  b.targets.push_back(corp.tokens[o + 1]);
+                }
+              ForwardResult fwd = model.forward_loss(theta, b);
+              losses[w] = fwd.loss.item();
+              backward(fwd.loss);
+              ParamVector grads = model.collect_grads(fwd);
+              adamw_step(theta, grads, opt, lr_at(c.schedule, i));
+            }
+          } catch (...) {
+            errs[w] = std::current_exception();
+          }
+        };
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> pool;
+        for (uint64_t w = 0; w < threads; ++w) pool.emplace_back(body, w);
+        for (auto& th : pool) th.join();
+        const auto t1 = std::chrono::steady_clock::now();
+        for (auto& e : errs) if (e) std::rethrow_exception(e);
+        *seconds_out = std::chrono::duration<double>(t1 - t0).count();
+        if (loss_out) *loss_out = losses[0])
 }
 
 }  // extern "C"

@@ -56,7 +56,8 @@ class photon_step_metric(C.Structure):
 class photon_round_record(C.Structure):
     _fields_ = [("round", u64), ("n_sampled", u64), ("sampled_ids", u64 * 64),
                 ("mean_client_loss", dbl), ("min_client_loss", dbl), ("max_client_loss", dbl),
-                ("local_ms", dbl), ("aggregate_ms", dbl), ("round_ms", dbl), ("tokens", u64)]
+                ("local_ms", dbl), ("aggregate_ms", dbl), ("round_ms", dbl), ("tokens", u64),
+                ("host_ms", dbl), ("h2d_bytes", u64), ("d2h_bytes", u64)]
 
 
 _SIGS = {
@@ -107,6 +108,12 @@ _SIGS = {
                                 C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p,
                                 C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                                 C.c_int, P(dbl), P(photon_err)]),
+    "photon_debug_attention": (i32, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     P(dbl), P(photon_err)]),
+    "photon_ctx_set_timing": (i32, [C.c_void_p, C.c_int]),
+    "photon_ctx_kernel_times": (i32, [C.c_void_p, P(dbl)]),
     "photon_nccl_unique_id": (i32, [P(u8), P(photon_err)]),
     "photon_runner_create": (i32, [C.c_void_p, P(photon_fed_cfg), P(photon_train_cfg),
                                    P(photon_server_cfg), C.c_void_p, P(dbl), C.c_int, C.c_int,

@@ -202,7 +202,8 @@ int photon_forward_backward(photon_ctx* ctx, const double* params, const int32_t
     Engine& e = *c.eng;
     c.d_losses.reserve(1);
     c.begin_timing();
-    StepBatch sb{c.d_tokens.ptr, c.d_targets.ptr, c.d_csr_off.ptr, c.d_csr_rows.ptr,
+    const DeviceBatches& db = c.dev_batches;
+    StepBatch sb{db.tokens.ptr, db.targets.ptr, db.csr_off.ptr, db.csr_rows.ptr,
                  (int)B, (int)S, rb.inv_count[0]};
     e.forward_backward(sb, c.d_losses.ptr, grads != nullptr);
     c.end_timing();
@@ -235,7 +236,8 @@ int photon_eval_perplexity(photon_ctx* ctx, const double* params, const int32_t*
       uint64_t valid = 0;
       for (uint64_t i = 0; i < bsz[b] * S; ++i) valid += tg[i] >= 0;
       stage_single(c, rb, in, tg, bsz[b], S);
-      StepBatch sb{c.d_tokens.ptr, c.d_targets.ptr, c.d_csr_off.ptr, c.d_csr_rows.ptr,
+      const DeviceBatches& db = c.dev_batches;
+      StepBatch sb{db.tokens.ptr, db.targets.ptr, db.csr_off.ptr, db.csr_rows.ptr,
                    (int)bsz[b], (int)S, rb.inv_count[0]};
       c.eng->forward_backward(sb, c.d_losses.ptr, false);
       double loss = 0.0;
@@ -274,7 +276,7 @@ int photon_client_round(photon_ctx* ctx, const photon_train_cfg* cfg, const doub
     c.d_f32b.reserve(e.P);
     PH_CUDA(cudaMemcpyAsync(c.d_f64a.ptr, theta_in, e.P * 8, cudaMemcpyHostToDevice, c.stream));
     k::f64_to_f32(c.d_f64a.ptr, c.d_f32b.ptr, e.P, c.stream);
-    LocalResult r = c.local_round(*cfg, rb, c.d_f32b.ptr, e.master, step_base);
+    LocalResult r = c.local_round(*cfg, c.d_f32b.ptr, e.master, step_base);
     if (r.error) {
       Error ex(r.error, r.error == PHOTON_ERR_DIVERGENCE
                             ? "client " + std::to_string(client) + " diverged at round " +
@@ -507,6 +509,60 @@ int photon_debug_gemm(int impl, int M, int N, int K, const void* A, int64_t lda,
     cudaEventDestroy(e1);
     cudaStreamDestroy(st);
   });
+}
+
+int photon_debug_attention(int impl, int B, int S, int H, int d, const void* q, const void* k,
+                           const void* v, void* o, float* lse, const void* dO, float* scratch,
+                           void* dq, void* dk, void* dv, double* ms, photon_err* err) {
+  return guarded(err, [&] {
+    cudaStream_t st;
+    cudaEvent_t e0, e1;
+    PH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    PH_CUDA(cudaEventCreate(&e0));
+    PH_CUDA(cudaEventCreate(&e1));
+    auto Q = static_cast<const bf16*>(q), K = static_cast<const bf16*>(k),
+         Vv = static_cast<const bf16*>(v);
+    PH_CUDA(cudaEventRecord(e0, st));
+    if (!dO) {
+      if (impl == 1) k::attn_fwd_mma(Q, K, Vv, static_cast<bf16*>(o), lse, B, S, H, d, st);
+      else k::attn_fwd_simt<bf16>(Q, K, Vv, static_cast<bf16*>(o), lse, B, S, H, d, st);
+    } else {
+      auto O = static_cast<const bf16*>(o), DO = static_cast<const bf16*>(dO);
+      if (impl == 1)
+        k::attn_bwd_mma(Q, K, Vv, O, DO, lse, scratch, static_cast<bf16*>(dq),
+                        static_cast<bf16*>(dk), static_cast<bf16*>(dv), B, S, H, d, st);
+      else
+        k::attn_bwd_simt<bf16>(Q, K, Vv, O, DO, lse, scratch, static_cast<bf16*>(dq),
+                               static_cast<bf16*>(dk), static_cast<bf16*>(dv), B, S, H, d, st);
+    }
+    PH_CUDA(cudaEventRecord(e1, st));
+    PH_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    PH_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    if (ms) *ms = t;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(st);
+  });
+}
+
+int photon_ctx_set_timing(photon_ctx* ctx, int on) {
+  ctx->c.eng->timing = on != 0;
+  ctx->c.eng->times = KernelTimes{};
+  return PHOTON_OK;
+}
+
+int photon_ctx_kernel_times(photon_ctx* ctx, double* t) {
+  const KernelTimes& k = ctx->c.eng->times;
+  t[0] = k.gemm_ms;
+  t[1] = k.attn_ms;
+  t[2] = k.other_ms + k.optim_ms;
+  t[3] = k.gemm_flops;
+  t[4] = k.attn_flops;
+  t[5] = k.gemm_launches;
+  t[6] = k.attn_launches;
+  t[7] = k.launches;
+  return PHOTON_OK;
 }
 
 // ---- runner ------------------------------------------------------------------------------

@@ -68,17 +68,24 @@ double Ctx::end_timing() {
   return ms;
 }
 
-void Ctx::upload(const RoundBatches& rb) {
-  const size_t M = (size_t)rb.B * rb.S, V = cfg.vocab_size;
-  d_tokens.reserve(rb.tau * M);
-  d_targets.reserve(rb.tau * M);
-  d_csr_off.reserve(rb.tau * (V + 1));
-  d_csr_rows.reserve(rb.tau * M);
-  PH_CUDA(cudaMemcpyAsync(d_tokens.ptr, rb.tokens.ptr, rb.tau * M * 4, cudaMemcpyHostToDevice, stream));
-  PH_CUDA(cudaMemcpyAsync(d_targets.ptr, rb.targets.ptr, rb.tau * M * 4, cudaMemcpyHostToDevice, stream));
-  PH_CUDA(cudaMemcpyAsync(d_csr_off.ptr, rb.csr_off.ptr, rb.tau * (V + 1) * 4, cudaMemcpyHostToDevice, stream));
-  PH_CUDA(cudaMemcpyAsync(d_csr_rows.ptr, rb.csr_rows.ptr, rb.tau * M * 4, cudaMemcpyHostToDevice, stream));
+void DeviceBatches::upload(const RoundBatches& rb, int V, cudaStream_t st) {
+  const size_t M = (size_t)rb.B * rb.S;
+  tau = rb.tau;
+  B = rb.B;
+  S = rb.S;
+  inv_count = rb.inv_count;
+  tokens.reserve(rb.tau * M);
+  targets.reserve(rb.tau * M);
+  csr_off.reserve(rb.tau * (size_t)(V + 1));
+  csr_rows.reserve(rb.tau * M);
+  PH_CUDA(cudaMemcpyAsync(tokens.ptr, rb.tokens.ptr, rb.tau * M * 4, cudaMemcpyHostToDevice, st));
+  PH_CUDA(cudaMemcpyAsync(targets.ptr, rb.targets.ptr, rb.tau * M * 4, cudaMemcpyHostToDevice, st));
+  PH_CUDA(cudaMemcpyAsync(csr_off.ptr, rb.csr_off.ptr, rb.tau * (size_t)(V + 1) * 4,
+                          cudaMemcpyHostToDevice, st));
+  PH_CUDA(cudaMemcpyAsync(csr_rows.ptr, rb.csr_rows.ptr, rb.tau * M * 4, cudaMemcpyHostToDevice, st));
 }
+
+void Ctx::upload(const RoundBatches& rb) { dev_batches.upload(rb, (int)cfg.vocab_size, stream); }
 
 // optim.cpp:20-35, 105-113 validation of the client hyper-parameters
 void check_train_cfg(const photon_train_cfg& t) {
@@ -96,35 +103,31 @@ void check_train_cfg(const photon_train_cfg& t) {
 }
 
 // run_local_round (client.cpp:125-158) on the device: theta copy, fresh AdamW
-// state, tau x {forward, backward, clip, AdamW/SGD}, post-process.  Losses are
-// read back once at the end; the first non-finite loss (DivergenceError) or
-// non-finite gradient norm (NumericError) is reported with its step, in the
-// order the reference would have raised them.
-LocalResult Ctx::local_round(const photon_train_cfg& t, const RoundBatches& rb,
-                             const float* d_theta_in, float* d_theta_out, uint64_t step_base) {
+// state, tau x {forward, backward, clip, AdamW/SGD}, post-process.  Losses stay
+// on the device until the caller reads them once per round.
+void Ctx::launch_local_round(const photon_train_cfg& t, const DeviceBatches& db,
+                             const float* d_theta_in, float* d_theta_out, uint64_t step_base,
+                             double* d_loss, int* d_flag) {
   Engine& e = *eng;
   const uint64_t P = e.P;
-  const int tau = rb.tau;
-  d_losses.reserve(std::max(tau, 1));
-  h_losses.reserve(std::max(tau, 1));
   if (d_theta_in != e.master)
     PH_CUDA(cudaMemcpyAsync(e.master, d_theta_in, P * 4, cudaMemcpyDeviceToDevice, stream));
   e.refresh_shadow();
   PH_CUDA(cudaMemsetAsync(e.mom, 0, P * 4, stream));
   PH_CUDA(cudaMemsetAsync(e.vel2, 0, P * 4, stream));
   PH_CUDA(cudaMemsetAsync(e.bad_step, 0, sizeof(int), stream));
-  const size_t M = (size_t)rb.B * rb.S, V = cfg.vocab_size;
+  const size_t M = (size_t)db.B * db.S, V = cfg.vocab_size;
   const double b1 = t.adamw.beta1, b2 = t.adamw.beta2;
-  for (int i = 0; i < tau; ++i) {
+  for (int i = 0; i < db.tau; ++i) {
     StepBatch sb;
-    sb.tokens = d_tokens.ptr + i * M;
-    sb.targets = d_targets.ptr + i * M;
-    sb.csr_off = d_csr_off.ptr + i * (V + 1);
-    sb.csr_rows = d_csr_rows.ptr + i * M;
-    sb.B = rb.B;
-    sb.S = rb.S;
-    sb.inv_count = rb.inv_count[i];
-    e.forward_backward(sb, d_losses.ptr + i, true);
+    sb.tokens = db.tokens.ptr + i * M;
+    sb.targets = db.targets.ptr + i * M;
+    sb.csr_off = db.csr_off.ptr + i * (V + 1);
+    sb.csr_rows = db.csr_rows.ptr + i * M;
+    sb.B = db.B;
+    sb.S = db.S;
+    sb.inv_count = db.inv_count[i];
+    e.forward_backward(sb, d_loss + i, true);
     const double lr = lr_at(t.schedule, step_base + i);
     if (t.opt == 0) {
       const double stepc = (double)(i + 1);  // fresh state each round: step_count = i+1
@@ -138,12 +141,12 @@ LocalResult Ctx::local_round(const photon_train_cfg& t, const RoundBatches& rb,
     k::clip_update_f32(d_theta_in, e.master, P, t.post_threshold, e.red_part, stream);
   if (d_theta_out != e.master)
     PH_CUDA(cudaMemcpyAsync(d_theta_out, e.master, P * 4, cudaMemcpyDeviceToDevice, stream));
-  PH_CUDA(cudaMemcpyAsync(h_losses.ptr, d_losses.ptr, tau * sizeof(double), cudaMemcpyDeviceToHost, stream));
-  PH_CUDA(cudaMemcpyAsync(h_flag.ptr, e.bad_step, sizeof(int), cudaMemcpyDeviceToHost, stream));
-  PH_CUDA(cudaStreamSynchronize(stream));
+  PH_CUDA(cudaMemcpyAsync(d_flag, e.bad_step, sizeof(int), cudaMemcpyDeviceToDevice, stream));
+}
+
+LocalResult classify(const double* losses, int tau, int bad) {
   LocalResult r;
-  r.losses.assign(h_losses.ptr, h_losses.ptr + tau);
-  const int bad = h_flag.ptr[0];  // 1-based step of the first non-finite grad norm
+  r.losses.assign(losses, losses + tau);
   for (int i = 0; i < tau; ++i) {
     if (!std::isfinite(r.losses[i])) {
       r.error = PHOTON_ERR_DIVERGENCE;
@@ -157,6 +160,19 @@ LocalResult Ctx::local_round(const photon_train_cfg& t, const RoundBatches& rb,
     }
   }
   return r;
+}
+
+LocalResult Ctx::local_round(const photon_train_cfg& t, const float* d_theta_in,
+                             float* d_theta_out, uint64_t step_base) {
+  const int tau = dev_batches.tau;
+  d_losses.reserve(std::max(tau, 1));
+  h_losses.reserve(std::max(tau, 1));
+  d_flags.reserve(1);
+  launch_local_round(t, dev_batches, d_theta_in, d_theta_out, step_base, d_losses.ptr, d_flags.ptr);
+  PH_CUDA(cudaMemcpyAsync(h_losses.ptr, d_losses.ptr, tau * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  PH_CUDA(cudaMemcpyAsync(h_flag.ptr, d_flags.ptr, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  PH_CUDA(cudaStreamSynchronize(stream));
+  return classify(h_losses.ptr, tau, h_flag.ptr[0]);
 }
 
 }  // namespace photon

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <memory>
+#include <utility>
 #include <vector>
 
 #include "engine.cuh"
@@ -13,6 +14,18 @@ template <typename U>
 struct DevBuf {
   U* ptr = nullptr;
   size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), n(o.n) {
+    o.ptr = nullptr;
+    o.n = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    std::swap(ptr, o.ptr);
+    std::swap(n, o.n);
+    return *this;
+  }
   void reserve(size_t want) {
     if (want <= n) return;
     if (ptr) cudaFree(ptr);
@@ -30,6 +43,18 @@ template <typename U>
 struct PinnedBuf {
   U* ptr = nullptr;
   size_t n = 0;
+  PinnedBuf() = default;
+  PinnedBuf(const PinnedBuf&) = delete;
+  PinnedBuf& operator=(const PinnedBuf&) = delete;
+  PinnedBuf(PinnedBuf&& o) noexcept : ptr(o.ptr), n(o.n) {
+    o.ptr = nullptr;
+    o.n = 0;
+  }
+  PinnedBuf& operator=(PinnedBuf&& o) noexcept {
+    std::swap(ptr, o.ptr);
+    std::swap(n, o.n);
+    return *this;
+  }
   void reserve(size_t want) {
     if (want <= n) return;
     if (ptr) cudaFreeHost(ptr);
@@ -52,6 +77,14 @@ struct RoundBatches {
   void finalize(int V);                                    // CSR + counts from tokens/targets
 };
 
+// A staged round's batches on the device.
+struct DeviceBatches {
+  DevBuf<int32_t> tokens, targets, csr_off, csr_rows;
+  std::vector<float> inv_count;
+  int tau = 0, B = 0, S = 0;
+  void upload(const RoundBatches& rb, int V, cudaStream_t st);
+};
+
 struct LocalResult {
   std::vector<double> losses;  // tau
   int error = PHOTON_OK;
@@ -68,10 +101,11 @@ struct Ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
 
-  // device copies of the current round's batches
-  DevBuf<int32_t> d_tokens, d_targets, d_csr_off, d_csr_rows;
+  // device copies of the current call's batches (C-ABI single-client path)
+  DeviceBatches dev_batches;
   DevBuf<double> d_losses;
   PinnedBuf<double> h_losses;
+  DevBuf<int> d_flags;
   PinnedBuf<int> h_flag;
   // generic scratch
   DevBuf<double> d_f64a, d_f64b, d_f64c, d_f64d;
@@ -84,14 +118,21 @@ struct Ctx {
   void begin_timing();
   double end_timing();  // syncs, returns ms since begin_timing
 
-  // H2D of a staged round (async on stream)
+  // H2D of a staged round (async on stream) into dev_batches
   void upload(const RoundBatches& rb);
-  // tau local steps from d_theta_in (fp32 device) into d_theta_out (may equal
-  // engine master); returns per-step losses and the first failure.
-  LocalResult local_round(const photon_train_cfg& cfg, const RoundBatches& rb,
-                          const float* d_theta_in, float* d_theta_out, uint64_t step_base);
+  // Enqueue tau local steps from d_theta_in (fp32 device) into d_theta_out (may
+  // equal engine master): per-step losses -> d_loss[0..tau), first bad-norm
+  // step (1-based, 0 = none) -> *d_flag.  Asynchronous.
+  void launch_local_round(const photon_train_cfg& cfg, const DeviceBatches& db,
+                          const float* d_theta_in, float* d_theta_out, uint64_t step_base,
+                          double* d_loss, int* d_flag);
+  // Synchronous convenience over dev_batches: launch, read back, classify.
+  LocalResult local_round(const photon_train_cfg& cfg, const float* d_theta_in,
+                          float* d_theta_out, uint64_t step_base);
 };
 
 void check_train_cfg(const photon_train_cfg& t);
+// First failure in step order (DivergenceError before the same step's NumericError).
+LocalResult classify(const double* losses, int tau, int bad_step);
 
 }  // namespace photon

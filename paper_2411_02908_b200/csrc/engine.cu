@@ -29,12 +29,14 @@ Engine::Engine(const photon_model_cfg& c, int prec, uint64_t mb, cudaStream_t st
 
 void Engine::adamw(double clip, double lr, double b1, double b2, double bc1, double bc2,
                    double eps, double wd, int step) {
+  if (timing) times.launches += 3;
   k::sumsq_parts(grads, P, red_part, stream);
   k::clip_finalize(red_part, clip, norm, cf, bad_step, step, stream);
   k::adamw_f32(master, grads, mom, vel2, shadow, P, cf, lr, b1, b2, bc1, bc2, eps, wd, stream);
 }
 
 void Engine::sgd(double clip, double lr, int step) {
+  if (timing) times.launches += 3;
   k::sumsq_parts(grads, P, red_part, stream);
   k::clip_finalize(red_part, clip, norm, cf, bad_step, step, stream);
   k::sgd_f32(master, grads, shadow, P, cf, lr, stream);
@@ -60,6 +62,7 @@ class EngineT final : public Engine {
     Smax_ = c.seq_len;
     Mmax_ = mb * Smax_;
     if (const char* e = std::getenv("PHOTON_GEMM")) gemm_mode = std::string(e) == "simt" ? 0 : 1;
+    if (const char* e = std::getenv("PHOTON_ATTN")) attn_mode = std::string(e) == "simt" ? 0 : 1;
     allocate();
   }
   ~EngineT() override {
@@ -201,6 +204,29 @@ class EngineT final : public Engine {
     ev_next_ = 0;
   }
 
+  bool use_mma_attn() const {
+    return sizeof(T) == 2 && attn_mode == 1 && k::attn_mma_supported((int)(d_ / H_));
+  }
+  void attn_fwd(const T* q, const T* k, const T* v, T* o, float* lse, int B, int S, int H, int d) {
+    if constexpr (sizeof(T) == 2) {
+      if (use_mma_attn()) {
+        k::attn_fwd_mma(q, k, v, o, lse, B, S, H, d, stream);
+        return;
+      }
+    }
+    k::attn_fwd_simt<T>(q, k, v, o, lse, B, S, H, d, stream);
+  }
+  void attn_bwd(const T* q, const T* k, const T* v, const T* o, const T* dO, const float* lse,
+                int B, int S, int H, int d) {
+    if constexpr (sizeof(T) == 2) {
+      if (use_mma_attn()) {
+        k::attn_bwd_mma(q, k, v, o, dO, lse, Dvec_, dq_, dk_, dv_, B, S, H, d, stream);
+        return;
+      }
+    }
+    k::attn_bwd_simt<T>(q, k, v, o, dO, lse, Dvec_, dq_, dk_, dv_, B, S, H, d, stream);
+  }
+
   void mm(int M, int N, int K, const void* A, int64_t lda, bool ak, const void* B, int64_t ldb,
           bool bk, void* C, int64_t ldc, DT cdt, Epi epi, const float* bias = nullptr,
           const float* resid = nullptr, void* aux = nullptr) {
@@ -252,7 +278,7 @@ void EngineT<T>::forward_backward(const StepBatch& bt, double* loss_dev, bool ba
     mm(M, d, d, h, d, true, W(o.wv), d, false, v, d, TT, Epi::Bias, Pm(o.bv));
     {
       Scope sc(this, 1, attn_fwd_flops);
-      k::attn_fwd_simt<T>(q, kk, v, ao, lse_ + (size_t)l * B * H * S, B, S, H, d, stream);
+      attn_fwd(q, kk, v, ao, lse_ + (size_t)l * B * H * S, B, S, H, d);
     }
     mm(M, d, d, ao, d, true, W(o.wo), d, false, xm, d, DT::F32, Epi::ResidBias, Pm(o.bo), x);
     {
@@ -330,8 +356,7 @@ void EngineT<T>::forward_backward(const StepBatch& bt, double* loss_dev, bool ba
     mm(d, d, M, ao, d, false, dxT_, d, false, G(o.wo), d, DT::F32, Epi::Store);
     {
       Scope sc(this, 1, 2.5 * attn_fwd_flops);
-      k::attn_bwd_simt<T>(q, kk, v, ao, dO_, lse_ + (size_t)l * B * H * S, Dvec_, dq_, dk_, dv_, B,
-                          S, H, d, stream);
+      attn_bwd(q, kk, v, ao, dO_, lse_ + (size_t)l * B * H * S, B, S, H, d);
     }
     // q,k,v = h W{q,k,v} + b{q,k,v}; LN1's output grad sums v, k, q in that order
     {

@@ -54,6 +54,7 @@ class Engine {
   bool timing = false;
   KernelTimes times;
   int gemm_mode = 1;  // 1: tcgen05 for bf16 operands, 0: SIMT everywhere
+  int attn_mode = 1;  // 1: tensor-core attention for bf16, 0: SIMT
 
   // master -> shadow (bf16 mode)
   virtual void refresh_shadow() = 0;

@@ -49,6 +49,14 @@ template <typename T>
 void attn_bwd_simt(const T* q, const T* k, const T* v, const T* o, const T* dO, const float* lse,
                    float* Dvec, T* dq, T* dk, T* dv, int B, int S, int H, int d, cudaStream_t st);
 
+// ---- causal attention on tensor cores (bf16, mma.sync m16n8k16), attn_mma.cu ----
+bool attn_mma_supported(int dh);
+void attn_fwd_mma(const bf16* q, const bf16* k, const bf16* v, bf16* o, float* lse, int B, int S,
+                  int H, int d, cudaStream_t st);
+void attn_bwd_mma(const bf16* q, const bf16* k, const bf16* v, const bf16* o, const bf16* dO,
+                  const float* lse, float* Dvec, bf16* dq, bf16* dk, bf16* dv, int B, int S, int H,
+                  int d, cudaStream_t st);
+
 // ---- casts -------------------------------------------------------------------
 void f64_to_f32(const double* in, float* out, uint64_t n, cudaStream_t st);
 void f32_to_f64(const float* in, double* out, uint64_t n, cudaStream_t st);

@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <limits>
+#include <chrono>
 #include <cstring>
 
 #include "kernels.cuh"
@@ -113,31 +114,57 @@ void Runner::run_round(photon_round_record* rec) {
     PH_CUDA(cudaMemsetAsync(d_models.ptr, 0, d_models.n * 4, st));
   }
 
-  // stats layout: [0,K) mean loss, [K,2K) error code, [2K,3K) error step
-  std::fill(h_stats.ptr, h_stats.ptr + 3 * K, 0.0);
-  PH_CUDA(cudaEventRecord(ev_a, st));
+  // ---- host: stage every local client's tau batches (BatchStream x tau) and H2D
+  const auto t_host0 = std::chrono::steady_clock::now();
+  if (host_batches.size() < mine.size()) {
+    host_batches.resize(mine.size());
+    dev_batches.resize(mine.size());
+  }
   for (size_t j = 0; j < mine.size(); ++j) {
-    const int si = mine[j];
-    const uint64_t client = sampled[si];
-    // BatchStream(plan, client, B, S, stream_seed(seed, client), cursor) x tau
-    batches.prepare(tau, B, S, V);
+    const uint64_t client = sampled[mine[j]];
+    RoundBatches& hb = host_batches[j];
+    hb.prepare(tau, B, S, V);
     const uint64_t seed = derive(fed.seed, kPurposeStream, client);
     for (int i = 0; i < tau; ++i)
       stream_rows(*plan, client, seed, cursors[client] + (uint64_t)i * B, B,
-                  batches.tokens.ptr + (size_t)i * B * S, batches.targets.ptr + (size_t)i * B * S);
-    batches.finalize(V);
-    ctx->upload(batches);
-    LocalResult r = ctx->local_round(train, batches, d_theta.ptr, d_models.ptr + j * Ppad, step_base);
+                  hb.tokens.ptr + (size_t)i * B * S, hb.targets.ptr + (size_t)i * B * S);
+    hb.finalize(V);
+    dev_batches[j].upload(hb, V, st);
+  }
+  const double host_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
+
+  // ---- device: the local phase, inputs resident in HBM
+  const size_t nm = std::max<size_t>(mine.size(), 1);
+  d_loss.reserve(nm * std::max(tau, 1));
+  d_flag.reserve(nm);
+  h_loss.reserve(nm * std::max(tau, 1));
+  h_flag.reserve(nm);
+  PH_CUDA(cudaEventRecord(ev_a, st));
+  for (size_t j = 0; j < mine.size(); ++j)
+    ctx->launch_local_round(train, dev_batches[j], d_theta.ptr, d_models.ptr + j * Ppad, step_base,
+                            d_loss.ptr + j * tau, d_flag.ptr + j);
+  PH_CUDA(cudaEventRecord(ev_b, st));
+  if (!mine.empty()) {
+    PH_CUDA(cudaMemcpyAsync(h_loss.ptr, d_loss.ptr, mine.size() * tau * sizeof(double),
+                            cudaMemcpyDeviceToHost, st));
+    PH_CUDA(cudaMemcpyAsync(h_flag.ptr, d_flag.ptr, mine.size() * sizeof(int),
+                            cudaMemcpyDeviceToHost, st));
+  }
+  PH_CUDA(cudaStreamSynchronize(st));
+  // stats layout: [0,K) mean loss, [K,2K) error code, [2K,3K) error step
+  std::fill(h_stats.ptr, h_stats.ptr + 3 * K, 0.0);
+  for (size_t j = 0; j < mine.size(); ++j) {
+    const int si = mine[j];
+    LocalResult lr = classify(h_loss.ptr + j * tau, tau, h_flag.ptr[j]);
     double acc = 0.0;
-    for (double l : r.losses) acc += l;
+    for (double l : lr.losses) acc += l;
     h_stats.ptr[si] = tau ? acc / tau : 0.0;  // ClientResult::mean_loss (client.cpp:112-117)
-    if (r.error) {
-      h_stats.ptr[K + si] = r.error;
-      h_stats.ptr[2 * K + si] = (double)r.error_step;
-      break;
+    if (lr.error) {
+      h_stats.ptr[K + si] = lr.error;
+      h_stats.ptr[2 * K + si] = (double)lr.error_step;
     }
   }
-  PH_CUDA(cudaEventRecord(ev_b, st));
   if (world > 1) {
     PH_CUDA(cudaMemcpyAsync(d_stats.ptr, h_stats.ptr, 3 * K * 8, cudaMemcpyHostToDevice, st));
     PH_NCCL(ncclAllReduce(d_stats.ptr, d_stats.ptr, 3 * K, ncclDouble, ncclSum, comm, st));
@@ -201,6 +228,7 @@ void Runner::run_round(photon_round_record* rec) {
     PH_NCCL(ncclAllGather(d_theta.ptr + off, d_theta.ptr, shard, ncclFloat, comm, st));
   PH_CUDA(cudaEventRecord(ev_c, st));
   PH_CUDA(cudaEventSynchronize(ev_c));
+  (void)host_ms;
 
   if (rec) {
     std::memset(rec, 0, sizeof(*rec));
@@ -225,6 +253,11 @@ void Runner::run_round(photon_round_record* rec) {
     PH_CUDA(cudaEventElapsedTime(&ms, ev_a, ev_c));
     rec->round_ms = ms;
     rec->tokens = (uint64_t)mine.size() * tau * B * S;
+    rec->host_ms = host_ms;
+    rec->h2d_bytes = 0;
+    for (size_t j = 0; j < mine.size(); ++j)
+      rec->h2d_bytes += (uint64_t)tau * ((uint64_t)B * S * 3 + V + 1) * 4;
+    rec->d2h_bytes = (uint64_t)mine.size() * (tau * sizeof(double) + sizeof(int));
   }
   next_round = round + 1;
 }

@@ -33,7 +33,12 @@ struct Runner {
   DevBuf<const float*> d_model_ptrs;
   DevBuf<double> d_stats;    // [2K] loss stats / error exchange
   PinnedBuf<double> h_stats;
-  RoundBatches batches;
+  std::vector<RoundBatches> host_batches;   // per local slot (pinned)
+  std::vector<DeviceBatches> dev_batches;   // per local slot
+  DevBuf<double> d_loss;
+  DevBuf<int> d_flag;
+  PinnedBuf<double> h_loss;
+  PinnedBuf<int> h_flag;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;
 
   Runner(Ctx* c, const photon_fed_cfg& f, const photon_train_cfg& t, const photon_server_cfg& s,

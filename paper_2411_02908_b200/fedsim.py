@@ -271,6 +271,9 @@ class RoundRecord:
     aggregate_ms: float
     round_ms: float
     tokens: int
+    host_ms: float = 0.0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
 
 
 # ---------------------------------------------------------------------------
@@ -717,7 +720,8 @@ class FederationRunner:
         k = int(rec.n_sampled)
         return RoundRecord(int(rec.round), [int(x) for x in rec.sampled_ids[:min(k, 64)]],
                            rec.mean_client_loss, rec.min_client_loss, rec.max_client_loss,
-                           rec.local_ms, rec.aggregate_ms, rec.round_ms, int(rec.tokens))
+                           rec.local_ms, rec.aggregate_ms, rec.round_ms, int(rec.tokens),
+                           rec.host_ms, int(rec.h2d_bytes), int(rec.d2h_bytes))
 
     def done(self) -> bool:
         return self.next_round() >= self.fed.rounds

@@ -1,0 +1,70 @@
+"""Fused causal attention (tensor-core and SIMT paths) vs a plain PyTorch fp32
+reference of the same op (tensor.cpp:436-542 semantics: scale before the max,
+keys j <= i).  bf16 inputs/outputs, fp32 math: outputs within 2e-2 of the
+output scale, lse within 1e-3 absolute."""
+import ctypes as C
+import math
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _ref(q, k, v, dO, H):
+    B, S, d = q.shape
+    dh = d // H
+    qf, kf, vf = (x.float().view(B, S, H, dh).transpose(1, 2).requires_grad_(True)
+                  for x in (q, k, v))
+    s = qf @ kf.transpose(-1, -2) / math.sqrt(dh)
+    mask = torch.ones(S, S, device=q.device, dtype=torch.bool).triu(1)
+    s = s.masked_fill(mask, float("-inf"))
+    lse = torch.logsumexp(s, dim=-1)
+    p = torch.softmax(s, dim=-1)
+    o = p @ vf
+    o.backward(dO.float().view(B, S, H, dh).transpose(1, 2))
+    back = lambda t: t.transpose(1, 2).reshape(B, S, d)  # noqa: E731
+    return back(o.detach()), lse.detach().reshape(B * H * S), back(qf.grad), back(kf.grad), \
+        back(vf.grad)
+
+
+def _run(impl, B, S, H, d, seed=0):
+    from paper_2411_02908_b200 import _capi as A
+
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    mk = lambda: (torch.randn(B, S, d, device="cuda", generator=g)).bfloat16()  # noqa: E731
+    q, k, v, dO = mk(), mk(), mk(), mk()
+    o = torch.empty_like(q)
+    lse = torch.empty(B * H * S, device="cuda")
+    scratch = torch.empty(B * H * S, device="cuda")
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
+    err = A.photon_err()
+    ms_f, ms_b = C.c_double(), C.c_double()
+    rc = A.lib().photon_debug_attention(impl, B, S, H, d, q.data_ptr(), k.data_ptr(),
+                                        v.data_ptr(), o.data_ptr(), lse.data_ptr(), None, None,
+                                        None, None, None, C.byref(ms_f), C.byref(err))
+    assert rc == 0, err.msg
+    rc = A.lib().photon_debug_attention(impl, B, S, H, d, q.data_ptr(), k.data_ptr(),
+                                        v.data_ptr(), o.data_ptr(), lse.data_ptr(), dO.data_ptr(),
+                                        scratch.data_ptr(), dq.data_ptr(), dk.data_ptr(),
+                                        dv.data_ptr(), C.byref(ms_b), C.byref(err))
+    assert rc == 0, err.msg
+    torch.cuda.synchronize()
+    o_r, lse_r, dq_r, dk_r, dv_r = _ref(q, k, v, dO, H)
+    for name, got, want in (("o", o, o_r), ("dq", dq, dq_r), ("dk", dk, dk_r), ("dv", dv, dv_r)):
+        rel = (got.float() - want).abs().max().item() / (want.abs().max().item() + 1e-6)
+        assert rel <= 2e-2, (name, impl, B, S, H, d, rel)
+    assert (lse - lse_r).abs().max().item() <= 1e-3
+    return ms_f.value, ms_b.value
+
+
+@pytest.mark.parametrize("impl", [1, 0])
+@pytest.mark.parametrize("B,S,H,d", [(2, 16, 2, 32), (2, 32, 2, 64), (1, 128, 2, 128),
+                                     (1, 200, 3, 192), (2, 256, 4, 512)])
+def test_attention_small(impl, B, S, H, d):
+    _run(impl, B, S, H, d)
+
+
+def test_attention_photon125m_head_shape():
+    # dh = 64, S = 2048 (the 125M shape), tensor-core path
+    _run(1, 2, 2048, 2, 128)
