@@ -138,6 +138,17 @@ def lib():
     """The loaded libphoton.so.  Raises if it was never built: no fallback."""
     global _lib
     if _lib is None:
+        # NCCL is bound at runtime (nccl_api.hpp): point it at torch's bundled
+        # copy so a later `import torch` finds the same libnccl.so.2 loaded.
+        if "PHOTON_NCCL_LIB" not in os.environ:
+            import glob
+            import sysconfig
+
+            for sp in {sysconfig.get_paths()["purelib"], sysconfig.get_paths()["platlib"]}:
+                hits = glob.glob(os.path.join(sp, "nvidia", "nccl", "lib", "libnccl.so.2"))
+                if hits:
+                    os.environ["PHOTON_NCCL_LIB"] = hits[0]
+                    break
         if not os.path.exists(LIB_PATH):
             raise ImportError(
                 f"{LIB_PATH} is missing: run `python -m paper_2411_02908_b200.build` "

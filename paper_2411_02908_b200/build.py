@@ -77,7 +77,7 @@ def build(verbose: bool = False, clean: bool = False) -> str:
                 print(log)
     if _needs(LIB, objs):
         cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + [
-            "-lcudart", "-lcuda", "-lnccl", f"-L{CUDA}/lib64", f"-L{CUDA}/lib64/stubs",
+            "-lcudart", "-lcuda", "-ldl", f"-L{CUDA}/lib64", f"-L{CUDA}/lib64/stubs",
             "-Xlinker", f"-rpath={CUDA}/lib64"]
         out = subprocess.run(cmd, capture_output=True, text=True)
         if out.returncode != 0:

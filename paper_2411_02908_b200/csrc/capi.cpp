@@ -7,6 +7,7 @@
 
 #include "gemm.cuh"
 #include "kernels.cuh"
+#include "nccl_api.hpp"
 #include "runner.hpp"
 
 struct photon_plan {
@@ -569,7 +570,7 @@ int photon_ctx_kernel_times(photon_ctx* ctx, double* t) {
 int photon_nccl_unique_id(uint8_t* out, photon_err* err) {
   return guarded(err, [&] {
     ncclUniqueId id;
-    if (ncclGetUniqueId(&id) != ncclSuccess) throw Error(PHOTON_ERR_NCCL, "ncclGetUniqueId failed");
+    if (nccl().GetUniqueId(&id) != ncclSuccess) throw Error(PHOTON_ERR_NCCL, "ncclGetUniqueId failed");
     static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
     std::memcpy(out, &id, 128);
   });

@@ -19,6 +19,7 @@
 #include <cstring>
 
 #include "kernels.cuh"
+#include "nccl_api.hpp"
 
 namespace photon {
 
@@ -26,7 +27,7 @@ namespace photon {
   do {                                                                                   \
     ncclResult_t r_ = (call);                                                            \
     if (r_ != ncclSuccess)                                                               \
-      throw Error(PHOTON_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_));  \
+      throw Error(PHOTON_ERR_NCCL, std::string(#call) + ": " + nccl().GetErrorString(r_)); \
   } while (0)
 
 // optim.cpp:105-113
@@ -83,13 +84,13 @@ Runner::Runner(Ctx* c, const photon_fed_cfg& f, const photon_train_cfg& t,
     if (!nccl_id) throw Error(PHOTON_ERR_USAGE, "runner: world > 1 needs an NCCL unique id");
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof(id));
-    PH_NCCL(ncclCommInitRank(&comm, ws, id, rk));
+    PH_NCCL(nccl().CommInitRank(&comm, ws, id, rk));
   }
   PH_CUDA(cudaStreamSynchronize(c->stream));
 }
 
 Runner::~Runner() {
-  if (comm) ncclCommDestroy(comm);
+  if (comm) nccl().CommDestroy(comm);
   if (ev_a) cudaEventDestroy(ev_a);
   if (ev_b) cudaEventDestroy(ev_b);
   if (ev_c) cudaEventDestroy(ev_c);
@@ -167,7 +168,7 @@ void Runner::run_round(photon_round_record* rec) {
   }
   if (world > 1) {
     PH_CUDA(cudaMemcpyAsync(d_stats.ptr, h_stats.ptr, 3 * K * 8, cudaMemcpyHostToDevice, st));
-    PH_NCCL(ncclAllReduce(d_stats.ptr, d_stats.ptr, 3 * K, ncclDouble, ncclSum, comm, st));
+    PH_NCCL(nccl().AllReduce(d_stats.ptr, d_stats.ptr, 3 * K, ncclDouble, ncclSum, comm, st));
     PH_CUDA(cudaMemcpyAsync(h_stats.ptr, d_stats.ptr, 3 * K * 8, cudaMemcpyDeviceToHost, st));
     PH_CUDA(cudaStreamSynchronize(st));
   }
@@ -205,17 +206,17 @@ void Runner::run_round(photon_round_record* rec) {
     for (int r = 0; r < n; ++r) ptrs[r] = d_models.ptr + (size_t)(surv[r] / world) * Ppad;
   } else {
     d_recv.reserve((size_t)n * shard);
-    PH_NCCL(ncclGroupStart());
+    PH_NCCL(nccl().GroupStart());
     for (int r = 0; r < n; ++r) {
       const int si = surv[r], owner = si % world;
       if (owner == rank) {
         const float* model = d_models.ptr + (size_t)(si / world) * Ppad;
         for (int q = 0; q < world; ++q)
-          PH_NCCL(ncclSend(model + (size_t)q * shard, shard, ncclFloat, q, comm, st));
+          PH_NCCL(nccl().Send(model + (size_t)q * shard, shard, ncclFloat, q, comm, st));
       }
-      PH_NCCL(ncclRecv(d_recv.ptr + (size_t)r * shard, shard, ncclFloat, owner, comm, st));
+      PH_NCCL(nccl().Recv(d_recv.ptr + (size_t)r * shard, shard, ncclFloat, owner, comm, st));
     }
-    PH_NCCL(ncclGroupEnd());
+    PH_NCCL(nccl().GroupEnd());
     for (int r = 0; r < n; ++r) ptrs[r] = d_recv.ptr + (size_t)r * shard;
   }
   d_model_ptrs.reserve(n);
@@ -225,7 +226,7 @@ void Runner::run_round(photon_round_record* rec) {
   k::aggregate<float>(d_model_ptrs.ptr, n, len, d_theta.ptr + off, d_vel.ptr + off, server.kind,
                       server.eta, server.momentum, server.nesterov, st);
   if (world > 1)
-    PH_NCCL(ncclAllGather(d_theta.ptr + off, d_theta.ptr, shard, ncclFloat, comm, st));
+    PH_NCCL(nccl().AllGather(d_theta.ptr + off, d_theta.ptr, shard, ncclFloat, comm, st));
   PH_CUDA(cudaEventRecord(ev_c, st));
   PH_CUDA(cudaEventSynchronize(ev_c));
   (void)host_ms;
@@ -275,7 +276,7 @@ void Runner::velocity_f64(double* out) {
   const float* src = d_vel.ptr;
   if (world > 1) {
     ctx->d_f32a.reserve(Ppad);
-    PH_NCCL(ncclAllGather(d_vel.ptr + (size_t)rank * shard, ctx->d_f32a.ptr, shard, ncclFloat,
+    PH_NCCL(nccl().AllGather(d_vel.ptr + (size_t)rank * shard, ctx->d_f32a.ptr, shard, ncclFloat,
                           comm, ctx->stream));
     src = ctx->d_f32a.ptr;
   }
