@@ -2,12 +2,15 @@
 //
 // bf16 operands, fp32 accumulation in tensor memory, fused epilogues
 // (gemm.cuh).  One CTA per SM, persistent over (tile, k-split) work units:
-//   warp 0      TMA producer: 128B-swizzled A/B tiles into a STAGES-deep ring
+//   warp 0      TMA producer: 128B-swizzled A/B k-blocks into a STAGES-deep ring
 //   warp 1      MMA issuer: one elected thread issues tcgen05.mma (M=128,
 //               N=BN, K=16) into one of two TMEM accumulators
-//   warps 2..5  epilogue: tcgen05.ld accumulator rows -> registers -> fused
-//               bias / residual / GELU -> global, overlapped with the next
-//               tile's main loop through the second accumulator
+//   warps 2..5  epilogue, one per TMEM lane quarter: tcgen05.ld 32x32 chunks,
+//               fused bias / residual / GELU math in registers, st.shared into
+//               a staging box and one TMA store per chunk; per-element inputs
+//               (residual, GELU pre-activation, accumulate target) arrive by
+//               TMA one chunk ahead.  The second accumulator lets the epilogue
+//               of tile i overlap the main loop of tile i+1.
 // Operands may be K-major or MN-major (the three layouts of tensor.cpp:152-207
 // on canonical [in,out] weights); both are legal UMMA smem layouts, so no
 // transposes are materialised.  Small-tile GEMMs with a long contraction
@@ -25,20 +28,17 @@ namespace photon {
 namespace {
 
 constexpr int BM = 128, BK = 64;
-constexpr int kThreads = 192;
-constexpr int kSmemBudget = 196608;  // operand ring bytes
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kEpiBytesPerWarp = 16384;  // out[2] 4 KB + in[2] 4 KB
+constexpr int kRingBudget = 232448 - kEpiWarps * kEpiBytesPerWarp - 2048;
 
 struct TcParams {
   int M, N, K;
   int num_m, num_n, splits, kb_total, kb_per_split, units;
   int epi;     // Epi
   int c_bf16;  // output dtype
-  void* C;
-  int64_t ldc;
   const float* bias;
-  const float* resid;
-  void* aux;
-  float* ws;  // split-K partials [splits][M][N]
 };
 
 // ---- PTX wrappers -------------------------------------------------------------
@@ -73,6 +73,49 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(su32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
       : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0,
+                                             int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(su32(src)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0,
+                                             int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(su32(src)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
+                                       uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
 }
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -121,82 +164,28 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uin
   return d;
 }
 
-// ---- epilogue -------------------------------------------------------------------
-__device__ __forceinline__ void store_vals(const TcParams& p, int row, int col0, const float* v,
-                                           int n) {
-  // v[0..n) -> columns [col0, col0+n) of row, applying p.epi
-  const int64_t o = (int64_t)row * p.ldc + col0;
-  const bool vec = (n == 32) && ((p.ldc & 7) == 0) && ((col0 & 7) == 0);
-  const Epi epi = static_cast<Epi>(p.epi);
-  float r[32];
-  switch (epi) {
-    case Epi::Store:
-#pragma unroll
-      for (int i = 0; i < 32; ++i) r[i] = v[i];
-      break;
-    case Epi::Accum:
-      for (int i = 0; i < n; ++i) r[i] = static_cast<float*>(p.C)[o + i] + v[i];
-      break;
-    case Epi::Bias:
-      for (int i = 0; i < n; ++i) r[i] = v[i] + p.bias[col0 + i];
-      break;
-    case Epi::ResidBias:
-      for (int i = 0; i < n; ++i) r[i] = p.resid[o + i] + (v[i] + p.bias[col0 + i]);
-      break;
-    case Epi::GeluBias: {
-      bf16* aux = static_cast<bf16*>(p.aux);
-      for (int i = 0; i < n; ++i) {
-        const float pre = v[i] + p.bias[col0 + i];
-        aux[o + i] = __float2bfloat16_rn(pre);
-        r[i] = gelu_f(pre);
-      }
-      break;
-    }
-    case Epi::GeluBwd: {
-      const bf16* aux = static_cast<const bf16*>(p.aux);
-      for (int i = 0; i < n; ++i) r[i] = v[i] * gelu_grad_f(__bfloat162float(aux[o + i]));
-      break;
-    }
-  }
-  if (p.c_bf16) {
-    bf16* C = static_cast<bf16*>(p.C) + o;
-    if (vec) {
-#pragma unroll
-      for (int i = 0; i < 32; i += 8) {
-        uint4 pk;
-        __nv_bfloat162 t0 = __floats2bfloat162_rn(r[i], r[i + 1]);
-        __nv_bfloat162 t1 = __floats2bfloat162_rn(r[i + 2], r[i + 3]);
-        __nv_bfloat162 t2 = __floats2bfloat162_rn(r[i + 4], r[i + 5]);
-        __nv_bfloat162 t3 = __floats2bfloat162_rn(r[i + 6], r[i + 7]);
-        pk.x = *reinterpret_cast<uint32_t*>(&t0);
-        pk.y = *reinterpret_cast<uint32_t*>(&t1);
-        pk.z = *reinterpret_cast<uint32_t*>(&t2);
-        pk.w = *reinterpret_cast<uint32_t*>(&t3);
-        *reinterpret_cast<uint4*>(C + i) = pk;
-      }
-    } else {
-      for (int i = 0; i < n; ++i) C[i] = __float2bfloat16_rn(r[i]);
-    }
-  } else {
-    float* C = static_cast<float*>(p.C) + o;
-    if (vec && ((p.ldc & 3) == 0)) {
-#pragma unroll
-      for (int i = 0; i < 32; i += 4)
-        *reinterpret_cast<float4*>(C + i) = make_float4(r[i], r[i + 1], r[i + 2], r[i + 3]);
-    } else {
-      for (int i = 0; i < n; ++i) C[i] = r[i];
-    }
-  }
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&t);
 }
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+// Epilogue tensor maps (row-major [M][N] boxes of 32 rows x 32 cols).
+struct EpiMaps {
+  CUtensorMap C;    // output (or split-K workspace, 3D [splits][M][N])
+  CUtensorMap aux;  // GELU pre-activation (bf16): stored by GeluBias, loaded by GeluBwd
+  CUtensorMap in;   // fp32 residual (ResidBias) or C itself (Accum)
+};
 
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const TcParams p) {
+                   const __grid_constant__ EpiMaps em, const TcParams p) {
   constexpr int A_BYTES = BM * BK * 2;
   constexpr int B_BYTES = BN * BK * 2;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  constexpr int STAGES = kSmemBudget / STAGE_BYTES;
+  constexpr int STAGES = kRingBudget / STAGE_BYTES;
   constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulators
   // instruction descriptor: D f32, A/B bf16, majors, N, M = 128
   constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
@@ -206,13 +195,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint8_t* epi_buf = smem + STAGES * STAGE_BYTES;  // [kEpiWarps][out0 out1 in0 in1] x 4 KB
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_buf + kEpiWarps * kEpiBytesPerWarp);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* inbar = tempty + 2;  // [kEpiWarps][2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(inbar + 2 * kEpiWarps);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const Epi epi = static_cast<Epi>(p.epi);
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -220,8 +212,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], kEpiWarps);
     }
+    for (int i = 0; i < 2 * kEpiWarps; ++i) mbar_init(&inbar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -247,16 +240,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m0 = (tile % p.num_m) * BM, n0 = (tile / p.num_m) * BN;
         const int kb0 = split * p.kb_per_split;
         const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+        // MN-major 64-wide boxes lying wholly past M / N are skipped: their
+        // smem is stale but only feeds accumulator rows/cols never stored.
+        const int a_boxes = A_MN ? min(BM / 64, (p.M - m0 + 63) / 64) : 1;
+        const int b_boxes = B_MN ? min(BN / 64, (p.N - n0 + 63) / 64) : 1;
+        const uint32_t tx = (A_MN ? a_boxes * 8192 : A_BYTES) + (B_MN ? b_boxes * 8192 : B_BYTES);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
-          // MN-major 64-wide boxes lying wholly past M / N are skipped: their
-          // smem is stale but only feeds accumulator rows/cols never stored.
-          const int a_boxes = A_MN ? min(BM / 64, (p.M - m0 + 63) / 64) : 1;
-          const int b_boxes = B_MN ? min(BN / 64, (p.N - n0 + 63) / 64) : 1;
-          mbar_expect_tx(&full[stage], (A_MN ? a_boxes * 8192 : A_BYTES) +
-                                           (B_MN ? b_boxes * 8192 : B_BYTES));
+          mbar_expect_tx(&full[stage], tx);
           const int k0 = kb * BK;
           if (!A_MN) {
             tma_load_2d(sa, &tmA, &full[stage], k0, m0);
@@ -317,35 +310,125 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ================= epilogue (warps 2..5) =================
+    const int ew = warp - 2;
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    uint8_t* wbuf = epi_buf + ew * kEpiBytesPerWarp;
+    uint64_t* ibar = inbar + 2 * ew;
+    uint32_t in_phase[2] = {0, 0};
+    const bool splitk = p.splits > 1;
+    const bool need_in = !splitk && (epi == Epi::ResidBias || epi == Epi::Accum || epi == Epi::GeluBwd);
+    const bool in_bf16 = epi == Epi::GeluBwd;
+    const uint32_t in_bytes = in_bf16 ? 2048 : 4096;
+    const CUtensorMap* in_map = in_bf16 ? &em.aux : &em.in;
+    const bool out_bf16 = !splitk && p.c_bf16;
+    int ob = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       const int tile = u / p.splits, split = u % p.splits;
       const int m0 = (tile % p.num_m) * BM, n0 = (tile / p.num_m) * BN;
+      const int row0 = m0 + q * 32;
+      const bool rows_live = row0 < p.M;
+      const int nchunks = min(BN / 32, (p.N - n0 + 31) / 32);
+      if (need_in && rows_live && lane == 0) {  // first input chunk, overlapped with the main loop
+        mbar_expect_tx(&ibar[0], in_bytes);
+        tma_load_2d(wbuf + 8192, in_map, &ibar[0], n0, row0);
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = m0 + q * 32 + lane;
       const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
+      if (rows_live) {
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        float v[32];
-        tmem_ld32(taddr + c0, v);
-        const int col0 = n0 + c0;
-        if (row < p.M && col0 < p.N) {
-          const int n = min(32, p.N - col0);
-          if (p.splits > 1) {
-            float* w = p.ws + ((int64_t)split * p.M + row) * p.N + col0;
-            if (n == 32 && (p.N & 3) == 0) {
-#pragma unroll
-              for (int i = 0; i < 32; i += 4)
-                *reinterpret_cast<float4*>(w + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-            } else {
-              for (int i = 0; i < n; ++i) w[i] = v[i];
-            }
-          } else {
-            store_vals(p, row, col0, v, n);
+        for (int c = 0; c < nchunks; ++c) {
+          const int col0 = n0 + c * 32;
+          const int ib = c & 1;
+          if (need_in && c + 1 < nchunks && lane == 0) {
+            mbar_expect_tx(&ibar[ib ^ 1], in_bytes);
+            tma_load_2d(wbuf + 8192 + (ib ^ 1) * 4096, in_map, &ibar[ib ^ 1], col0 + 32, row0);
           }
+          float v[32];
+          tmem_ld32(taddr + c * 32, v);  // v[j] = acc[row0 + lane][col0 + j]
+          if (!splitk && (epi == Epi::Bias || epi == Epi::ResidBias || epi == Epi::GeluBias)) {
+            if (col0 + 32 <= p.N) {
+              const float4* b4 = reinterpret_cast<const float4*>(p.bias + col0);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float4 b = b4[j];
+                v[4 * j] += b.x;
+                v[4 * j + 1] += b.y;
+                v[4 * j + 2] += b.z;
+                v[4 * j + 3] += b.w;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] += col0 + j < p.N ? p.bias[col0 + j] : 0.f;
+            }
+          }
+          if (need_in) {
+            mbar_wait(&ibar[ib], in_phase[ib]);
+            in_phase[ib] ^= 1;
+            const uint32_t ia = su32(wbuf + 8192 + ib * 4096);
+            if (in_bf16) {  // GeluBwd: v *= gelu'(pre)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const uint4 w = lds128(ia + lane * 64 + j * 16);
+                const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  v[8 * j + 2 * e] *= gelu_grad_f(bf_lo(ww[e]));
+                  v[8 * j + 2 * e + 1] *= gelu_grad_f(bf_hi(ww[e]));
+                }
+              }
+            } else {  // ResidBias: resid + (acc + bias);  Accum: C + acc
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const uint4 w = lds128(ia + lane * 128 + j * 16);
+                v[4 * j] += __uint_as_float(w.x);
+                v[4 * j + 1] += __uint_as_float(w.y);
+                v[4 * j + 2] += __uint_as_float(w.z);
+                v[4 * j + 3] += __uint_as_float(w.w);
+              }
+            }
+          }
+          // stage the chunk; the store that last used this buffer must have read it
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+          const uint32_t oa = su32(wbuf + ob * 4096);
+          if (epi == Epi::GeluBias && !splitk) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {  // pre-activation -> aux box (second 2 KB)
+              sts128(oa + 2048 + lane * 64 + j * 16, pack2(v[8 * j], v[8 * j + 1]),
+                     pack2(v[8 * j + 2], v[8 * j + 3]), pack2(v[8 * j + 4], v[8 * j + 5]),
+                     pack2(v[8 * j + 6], v[8 * j + 7]));
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
+          }
+          if (out_bf16) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              sts128(oa + lane * 64 + j * 16, pack2(v[8 * j], v[8 * j + 1]),
+                     pack2(v[8 * j + 2], v[8 * j + 3]), pack2(v[8 * j + 4], v[8 * j + 5]),
+                     pack2(v[8 * j + 6], v[8 * j + 7]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              sts128(oa + lane * 128 + j * 16, __float_as_uint(v[4 * j]),
+                     __float_as_uint(v[4 * j + 1]), __float_as_uint(v[4 * j + 2]),
+                     __float_as_uint(v[4 * j + 3]));
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (splitk) {
+              tma_store_3d(&em.C, wbuf + ob * 4096, col0, row0, split);
+            } else {
+              tma_store_2d(&em.C, wbuf + ob * 4096, col0, row0);
+              if (epi == Epi::GeluBias) tma_store_2d(&em.aux, wbuf + ob * 4096 + 2048, col0, row0);
+            }
+            bulk_commit();
+          }
+          ob ^= 1;
         }
       }
       tc_fence_before();
@@ -356,6 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -366,17 +450,41 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// split-K: out = epi(sum_s ws[s]) in fixed order
-__global__ void splitk_reduce_kernel(const TcParams p) {
-  const int64_t total = (int64_t)p.M * p.N;
+// split-K: out = epi(sum_s ws[s]) in fixed order (ws[s] is [M][N] fp32)
+struct ReduceArgs {
+  int M, N, splits, epi, c_bf16;
+  int64_t ldc;
+  const float* ws;
+  void* C;
+  const float* bias;
+  const float* resid;
+  void* aux;
+};
+__global__ void splitk_reduce_kernel(const ReduceArgs r) {
+  const int64_t total = (int64_t)r.M * r.N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     float acc = 0.f;
-    for (int s = 0; s < p.splits; ++s) acc += p.ws[s * total + i];
-    const int row = (int)(i / p.N), col = (int)(i % p.N);
-    float v[32];
-    v[0] = acc;
-    store_vals(p, row, col, v, 1);
+    for (int s = 0; s < r.splits; ++s) acc += r.ws[s * total + i];
+    const int row = (int)(i / r.N), col = (int)(i % r.N);
+    const int64_t o = (int64_t)row * r.ldc + col;
+    const float b = r.bias ? r.bias[col] : 0.f;
+    float out;
+    switch (static_cast<Epi>(r.epi)) {
+      case Epi::Store: out = acc; break;
+      case Epi::Accum: out = static_cast<const float*>(r.C)[o] + acc; break;
+      case Epi::Bias: out = acc + b; break;
+      case Epi::ResidBias: out = r.resid[o] + (acc + b); break;
+      case Epi::GeluBias:
+        static_cast<bf16*>(r.aux)[o] = __float2bfloat16_rn(acc + b);
+        out = gelu_f(acc + b);
+        break;
+      default:
+        out = acc * gelu_grad_f(__bfloat162float(static_cast<const bf16*>(r.aux)[o]));
+        break;
+    }
+    if (r.c_bf16) static_cast<bf16*>(r.C)[o] = __float2bfloat16_rn(out);
+    else static_cast<float*>(r.C)[o] = out;
   }
 }
 
@@ -396,37 +504,51 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 2D bf16 tensor [outer][inner] (inner contiguous, row stride ld elements),
-// box {64, box_outer}, 128B swizzle, zero fill out of bounds.
-CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer, int64_t ld,
-                     uint32_t box_outer) {
+CUtensorMap encode(CUtensorMapDataType dt, int rank, const void* base, const cuuint64_t* dims,
+                   const cuuint64_t* strides, const cuuint32_t* box, CUtensorMapSwizzle sw) {
   CUtensorMap m;
-  cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-  cuuint32_t box[2] = {64, box_outer};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
-                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, dt, rank, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     throw Error(PHOTON_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return m;
 }
 
+// operand: 2D bf16 [outer][inner] (row stride ld), box {64, box_outer}, 128B swizzle
+CUtensorMap operand_map(const void* base, uint64_t inner, uint64_t outer, int64_t ld,
+                        uint32_t box_outer) {
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {64, box_outer};
+  return encode(CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box,
+                CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+// epilogue tile: row-major [M][N] (row stride ld), box {32 cols, 32 rows}, no swizzle
+CUtensorMap epi_map(const void* base, bool bf, uint64_t N, uint64_t M, int64_t ld) {
+  cuuint64_t dims[2] = {N, M};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * (bf ? 2 : 4)};
+  cuuint32_t box[2] = {32, 32};
+  return encode(bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base,
+                dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
 template <int BN, bool A_MN, bool B_MN>
-void launch(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, int grid,
-            cudaStream_t st) {
+void launch(const CUtensorMap& a, const CUtensorMap& b, const EpiMaps& em, const TcParams& p,
+            int grid, cudaStream_t st) {
   constexpr int STAGE_BYTES = (BM + BN) * BK * 2;
-  constexpr int STAGES = kSmemBudget / STAGE_BYTES;
-  constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  constexpr int STAGES = kRingBudget / STAGE_BYTES;
+  static_assert(STAGES >= 3, "operand ring too shallow");
+  constexpr int SMEM = STAGES * STAGE_BYTES + kEpiWarps * kEpiBytesPerWarp + 1024 + 512;
   auto kern = gemm_tc_kernel<BN, A_MN, B_MN>;
   static bool configured = false;
   if (!configured) {
     PH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
     configured = true;
   }
-  kern<<<grid, kThreads, SMEM, st>>>(a, b, p);
+  kern<<<grid, kThreads, SMEM, st>>>(a, b, em, p);
   PH_LAUNCH_CHECK();
 }
 
@@ -448,15 +570,23 @@ float* workspace(size_t n) {
   return g_ws.ptr;
 }
 
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 }  // namespace
 
 bool gemm_tc_supported(const GemmArgs& g) {
   if (g.ab != DT::BF16) return false;
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return false;
   if ((g.lda & 7) || (g.ldb & 7)) return false;  // TMA: 16-byte row strides
-  if ((reinterpret_cast<uintptr_t>(g.A) & 15) || (reinterpret_cast<uintptr_t>(g.B) & 15))
+  if (!aligned16(g.A) || !aligned16(g.B) || !aligned16(g.C)) return false;
+  if ((g.ldc * (g.c == DT::BF16 ? 2 : 4)) & 15) return false;
+  if ((g.epi == Epi::GeluBias || g.epi == Epi::GeluBwd) && (g.c != DT::BF16 || !aligned16(g.aux)))
     return false;
-  if ((g.epi == Epi::GeluBias || g.epi == Epi::GeluBwd) && g.c != DT::BF16) return false;
+  if (g.epi == Epi::ResidBias && (g.c != DT::F32 || !aligned16(g.resid))) return false;
+  if (g.epi == Epi::Accum && g.c != DT::F32) return false;
+  if ((g.epi == Epi::Bias || g.epi == Epi::ResidBias || g.epi == Epi::GeluBias) &&
+      (!g.bias || !aligned16(g.bias)))
+    return false;
   return true;
 }
 
@@ -482,34 +612,46 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
   p.units = tiles * p.splits;
   p.epi = static_cast<int>(g.epi);
   p.c_bf16 = g.c == DT::BF16;
-  p.C = g.C;
-  p.ldc = g.ldc;
   p.bias = g.bias;
-  p.resid = g.resid;
-  p.aux = g.aux;
-  if (p.splits > 1) p.ws = workspace((size_t)p.splits * g.M * g.N);
+
+  EpiMaps em{};
+  float* ws = nullptr;
+  if (p.splits > 1) {
+    ws = workspace((size_t)p.splits * g.M * g.N);
+    cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.M, (cuuint64_t)p.splits};
+    cuuint64_t strides[2] = {(cuuint64_t)g.N * 4, (cuuint64_t)g.N * g.M * 4};
+    cuuint32_t box[3] = {32, 32, 1};
+    em.C = encode(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ws, dims, strides, box,
+                  CU_TENSOR_MAP_SWIZZLE_NONE);
+  } else {
+    em.C = epi_map(g.C, g.c == DT::BF16, g.N, g.M, g.ldc);
+    if (g.epi == Epi::GeluBias || g.epi == Epi::GeluBwd) em.aux = epi_map(g.aux, true, g.N, g.M, g.ldc);
+    if (g.epi == Epi::ResidBias) em.in = epi_map(g.resid, false, g.N, g.M, g.ldc);
+    if (g.epi == Epi::Accum) em.in = epi_map(g.C, false, g.N, g.M, g.ldc);
+  }
 
   // A(i,k): K-major -> [M][K] rows; MN-major -> [K][M] rows
-  const CUtensorMap ta = g.a_kmajor ? make_map(g.A, g.K, g.M, g.lda, BM)
-                                    : make_map(g.A, g.M, g.K, g.lda, 64);
+  const CUtensorMap ta = g.a_kmajor ? operand_map(g.A, g.K, g.M, g.lda, BM)
+                                    : operand_map(g.A, g.M, g.K, g.lda, 64);
   // B(k,j): K-major -> [N][K] rows; N-major -> [K][N] rows
-  const CUtensorMap tb = g.b_kmajor ? make_map(g.B, g.K, g.N, g.ldb, BN)
-                                    : make_map(g.B, g.N, g.K, g.ldb, 64);
+  const CUtensorMap tb = g.b_kmajor ? operand_map(g.B, g.K, g.N, g.ldb, BN)
+                                    : operand_map(g.B, g.N, g.K, g.ldb, 64);
   const int grid = std::min(p.units, kNumSMs);
   const bool amn = !g.a_kmajor, bmn = !g.b_kmajor;
   if (BN == 128) {
-    if (!amn && !bmn) launch<128, false, false>(ta, tb, p, grid, st);
-    else if (!amn && bmn) launch<128, false, true>(ta, tb, p, grid, st);
-    else if (amn && !bmn) launch<128, true, false>(ta, tb, p, grid, st);
-    else launch<128, true, true>(ta, tb, p, grid, st);
+    if (!amn && !bmn) launch<128, false, false>(ta, tb, em, p, grid, st);
+    else if (!amn && bmn) launch<128, false, true>(ta, tb, em, p, grid, st);
+    else if (amn && !bmn) launch<128, true, false>(ta, tb, em, p, grid, st);
+    else launch<128, true, true>(ta, tb, em, p, grid, st);
   } else {
-    if (!amn && !bmn) launch<256, false, false>(ta, tb, p, grid, st);
-    else if (!amn && bmn) launch<256, false, true>(ta, tb, p, grid, st);
-    else if (amn && !bmn) launch<256, true, false>(ta, tb, p, grid, st);
-    else launch<256, true, true>(ta, tb, p, grid, st);
+    if (!amn && !bmn) launch<256, false, false>(ta, tb, em, p, grid, st);
+    else if (!amn && bmn) launch<256, false, true>(ta, tb, em, p, grid, st);
+    else if (amn && !bmn) launch<256, true, false>(ta, tb, em, p, grid, st);
+    else launch<256, true, true>(ta, tb, em, p, grid, st);
   }
   if (p.splits > 1) {
-    splitk_reduce_kernel<<<kNumSMs * 4, 256, 0, st>>>(p);
+    ReduceArgs r{g.M, g.N, p.splits, p.epi, p.c_bf16, g.ldc, ws, g.C, g.bias, g.resid, g.aux};
+    splitk_reduce_kernel<<<kNumSMs * 4, 256, 0, st>>>(r);
     PH_LAUNCH_CHECK();
   }
   return true;
