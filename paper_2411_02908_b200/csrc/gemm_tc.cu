@@ -5,7 +5,7 @@
 //   warp 0      TMA producer: 128B-swizzled A/B k-blocks into a STAGES-deep ring
 //   warp 1      MMA issuer: one elected thread issues tcgen05.mma (M=128,
 //               N=BN, K=16) into one of two TMEM accumulators
-//   warps 2..5  epilogue, one per TMEM lane quarter: tcgen05.ld 32x32 chunks,
+//   warps 2..9  epilogue, two per TMEM lane quarter: tcgen05.ld 32x32 chunks,
 //               fused bias / residual / GELU math in registers, st.shared into
 //               a staging box and one TMA store per chunk; per-element inputs
 //               (residual, GELU pre-activation, accumulate target) arrive by
@@ -28,9 +28,9 @@ namespace photon {
 namespace {
 
 constexpr int BM = 128, BK = 64;
-constexpr int kEpiWarps = 4;
+constexpr int kEpiWarps = 8;  // two per TMEM lane quarter, alternating 32-column chunks
 constexpr int kThreads = 64 + 32 * kEpiWarps;
-constexpr int kEpiBytesPerWarp = 16384;  // out[2] 4 KB + in[2] 4 KB
+constexpr int kEpiBytesPerWarp = 8192;  // out 4 KB + in 4 KB
 constexpr int kRingBudget = 232448 - kEpiWarps * kEpiBytesPerWarp - 2048;
 
 struct TcParams {
@@ -89,6 +89,12 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
           reinterpret_cast<uint64_t>(map)),
       "r"(su32(src)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
 }
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -195,13 +201,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* epi_buf = smem + STAGES * STAGE_BYTES;  // [kEpiWarps][out0 out1 in0 in1] x 4 KB
+  uint8_t* epi_buf = smem + STAGES * STAGE_BYTES;  // [kEpiWarps][out in] x 4 KB
   uint64_t* full = reinterpret_cast<uint64_t*>(epi_buf + kEpiWarps * kEpiBytesPerWarp);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* inbar = tempty + 2;  // [kEpiWarps][2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(inbar + 2 * kEpiWarps);
+  uint64_t* inbar = tempty + 2;  // [kEpiWarps]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(inbar + kEpiWarps);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const Epi epi = static_cast<Epi>(p.epi);
@@ -214,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], kEpiWarps);
     }
-    for (int i = 0; i < 2 * kEpiWarps; ++i) mbar_init(&inbar[i], 1);
+    for (int i = 0; i < kEpiWarps; ++i) mbar_init(&inbar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -309,19 +315,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ================= epilogue (warps 2..5) =================
+    // ================= epilogue (warps 2..9) =================
     const int ew = warp - 2;
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
-    uint8_t* wbuf = epi_buf + ew * kEpiBytesPerWarp;
-    uint64_t* ibar = inbar + 2 * ew;
-    uint32_t in_phase[2] = {0, 0};
+    const int q = warp & 3;     // TMEM lane quarter this warp may access
+    const int sub = ew >> 2;    // this warp takes chunks c = sub, sub + 2, ...
+    uint8_t* obuf = epi_buf + ew * kEpiBytesPerWarp;
+    uint8_t* ibuf = obuf + 4096;
+    uint64_t* ibar = inbar + ew;
+    uint32_t in_phase = 0;
     const bool splitk = p.splits > 1;
     const bool need_in = !splitk && (epi == Epi::ResidBias || epi == Epi::Accum || epi == Epi::GeluBwd);
     const bool in_bf16 = epi == Epi::GeluBwd;
     const uint32_t in_bytes = in_bf16 ? 2048 : 4096;
     const CUtensorMap* in_map = in_bf16 ? &em.aux : &em.in;
     const bool out_bf16 = !splitk && p.c_bf16;
-    int ob = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
@@ -330,22 +337,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row0 = m0 + q * 32;
       const bool rows_live = row0 < p.M;
       const int nchunks = min(BN / 32, (p.N - n0 + 31) / 32);
-      if (need_in && rows_live && lane == 0) {  // first input chunk, overlapped with the main loop
-        mbar_expect_tx(&ibar[0], in_bytes);
-        tma_load_2d(wbuf + 8192, in_map, &ibar[0], n0, row0);
+      if (need_in && rows_live && sub < nchunks && lane == 0) {  // overlaps the main loop
+        mbar_expect_tx(ibar, in_bytes);
+        tma_load_2d(ibuf, in_map, ibar, n0 + 32 * sub, row0);
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
       if (rows_live) {
 #pragma unroll 1
-        for (int c = 0; c < nchunks; ++c) {
+        for (int c = sub; c < nchunks; c += 2) {
           const int col0 = n0 + c * 32;
-          const int ib = c & 1;
-          if (need_in && c + 1 < nchunks && lane == 0) {
-            mbar_expect_tx(&ibar[ib ^ 1], in_bytes);
-            tma_load_2d(wbuf + 8192 + (ib ^ 1) * 4096, in_map, &ibar[ib ^ 1], col0 + 32, row0);
-          }
           float v[32];
           tmem_ld32(taddr + c * 32, v);  // v[j] = acc[row0 + lane][col0 + j]
           if (!splitk && (epi == Epi::Bias || epi == Epi::ResidBias || epi == Epi::GeluBias)) {
@@ -365,35 +367,51 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           if (need_in) {
-            mbar_wait(&ibar[ib], in_phase[ib]);
-            in_phase[ib] ^= 1;
-            const uint32_t ia = su32(wbuf + 8192 + ib * 4096);
+            mbar_wait(ibar, in_phase);
+            in_phase ^= 1;
+            const uint32_t ia = su32(ibuf);
             if (in_bf16) {  // GeluBwd: v *= gelu'(pre)
+              uint32_t w[16];
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
-                const uint4 w = lds128(ia + lane * 64 + j * 16);
-                const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+                const uint4 t = lds128(ia + lane * 64 + j * 16);
+                w[4 * j] = t.x;
+                w[4 * j + 1] = t.y;
+                w[4 * j + 2] = t.z;
+                w[4 * j + 3] = t.w;
+              }
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  v[8 * j + 2 * e] *= gelu_grad_f(bf_lo(ww[e]));
-                  v[8 * j + 2 * e + 1] *= gelu_grad_f(bf_hi(ww[e]));
-                }
+              for (int e = 0; e < 16; ++e) {
+                v[2 * e] *= gelu_grad_f(bf_lo(w[e]));
+                v[2 * e + 1] *= gelu_grad_f(bf_hi(w[e]));
+              }
+              // the shared loads are consumed (values used) before the async
+              // proxy may overwrite the buffer
+              __syncwarp();
+              if (lane == 0 && c + 2 < nchunks) {
+                mbar_expect_tx(ibar, in_bytes);
+                tma_load_2d(ibuf, in_map, ibar, col0 + 64, row0);
               }
             } else {  // ResidBias: resid + (acc + bias);  Accum: C + acc
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                const uint4 w = lds128(ia + lane * 128 + j * 16);
-                v[4 * j] += __uint_as_float(w.x);
-                v[4 * j + 1] += __uint_as_float(w.y);
-                v[4 * j + 2] += __uint_as_float(w.z);
-                v[4 * j + 3] += __uint_as_float(w.w);
+                const uint4 t = lds128(ia + lane * 128 + j * 16);
+                v[4 * j] += __uint_as_float(t.x);
+                v[4 * j + 1] += __uint_as_float(t.y);
+                v[4 * j + 2] += __uint_as_float(t.z);
+                v[4 * j + 3] += __uint_as_float(t.w);
+              }
+              __syncwarp();
+              if (lane == 0 && c + 2 < nchunks) {
+                mbar_expect_tx(ibar, in_bytes);
+                tma_load_2d(ibuf, in_map, ibar, col0 + 64, row0);
               }
             }
           }
-          // stage the chunk; the store that last used this buffer must have read it
-          if (lane == 0) bulk_wait_read<1>();
+          // stage the chunk once the previous store from this buffer has read it
+          if (lane == 0) bulk_wait_read<0>();
           __syncwarp();
-          const uint32_t oa = su32(wbuf + ob * 4096);
+          const uint32_t oa = su32(obuf);
           if (epi == Epi::GeluBias && !splitk) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {  // pre-activation -> aux box (second 2 KB)
@@ -421,14 +439,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) {
             if (splitk) {
-              tma_store_3d(&em.C, wbuf + ob * 4096, col0, row0, split);
+              tma_store_3d(&em.C, obuf, col0, row0, split);
             } else {
-              tma_store_2d(&em.C, wbuf + ob * 4096, col0, row0);
-              if (epi == Epi::GeluBias) tma_store_2d(&em.aux, wbuf + ob * 4096 + 2048, col0, row0);
+              tma_store_2d(&em.C, obuf, col0, row0);
+              if (epi == Epi::GeluBias) tma_store_2d(&em.aux, obuf + 2048, col0, row0);
             }
             bulk_commit();
           }
-          ob ^= 1;
         }
       }
       tc_fence_before();

@@ -197,31 +197,65 @@ void ln_bwd(const float* dy, const float* x, const float* mean, const float* rst
 }
 
 // ============================================================================
-// Column sums for bias gradients: two passes, fixed order (deterministic).
+// Column sums for bias gradients (add_bias backward, tensor.cpp:279-285).
+// Pass 1: CTA (column strip, row chunk); each lane owns VEC consecutive columns
+// (16-byte loads), the 8 warps of a CTA interleave rows, 4 rows in flight per
+// lane; warps are reduced in smem in a fixed order.  Pass 2: fixed-order sum
+// over row chunks.  Deterministic; reads the matrix once at HBM speed.
 // ============================================================================
-static int colsum_chunks(int M, int N) {
-  const int colblocks = (int)cdiv(N, 256);
-  int r = std::max(1, (kNumSMs * 4) / colblocks);
-  return std::min(r, std::max(1, M / 16));
-}
+constexpr int kColRows = 1024;  // rows per chunk
+static int colsum_chunks(int M, int /*N*/) { return (M + kColRows - 1) / kColRows; }
 size_t colsum_part_floats(int M, int N) { return (size_t)colsum_chunks(M, N) * N; }
 
 template <typename T>
-__global__ void colsum_part_kernel(const T* __restrict__ x, int M, int N, int rows_per,
-                                   float* __restrict__ part) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= N) return;
-  const int r0 = blockIdx.y * rows_per, r1 = min(M, r0 + rows_per);
-  float acc = 0.f;
-  for (int r = r0; r < r1; ++r) acc += to_f<T>(x[(size_t)r * N + j]);
-  part[(size_t)blockIdx.y * N + j] = acc;
+__global__ void __launch_bounds__(256) colsum_part_kernel(const T* __restrict__ x, int M, int N,
+                                                          float* __restrict__ part) {
+  constexpr int VEC = 16 / sizeof(T);  // columns per lane
+  constexpr int STRIP = 32 * VEC;      // columns per CTA
+  __shared__ float red[8][STRIP];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int c0 = blockIdx.x * STRIP + lane * VEC;
+  const int r0 = blockIdx.y * kColRows, r1 = min(M, r0 + kColRows);
+  float acc[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) acc[e] = 0.f;
+  const bool full = c0 + VEC <= N && (N % VEC) == 0;
+  for (int r = r0 + warp; r < r1; r += 8 * 4) {
+    T buf[4][VEC];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int rr = r + 8 * u;
+      if (rr < r1 && full) {
+        *reinterpret_cast<uint4*>(buf[u]) = *reinterpret_cast<const uint4*>(x + (size_t)rr * N + c0);
+      } else {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e)
+          buf[u][e] = (rr < r1 && c0 + e < N) ? x[(size_t)rr * N + c0 + e] : from_f<T>(0.f);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) acc[e] += to_f<T>(buf[u][e]);
+  }
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) red[warp][lane * VEC + e] = acc[e];
+  __syncthreads();
+  for (int j = threadIdx.x; j < STRIP; j += blockDim.x) {
+    const int c = blockIdx.x * STRIP + j;
+    if (c >= N) continue;
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += red[w][j];
+    part[(size_t)blockIdx.y * N + c] = s;
+  }
 }
 
 template <typename T>
 void colsum(const T* x, int M, int N, float* part, float* out, cudaStream_t st) {
+  constexpr int STRIP = 32 * (16 / sizeof(T));
   const int chunks = colsum_chunks(M, N);
-  const int rows_per = (int)cdiv(M, chunks);
-  colsum_part_kernel<T><<<dim3(cdiv(N, 256), chunks), 256, 0, st>>>(x, M, N, rows_per, part);
+  colsum_part_kernel<T><<<dim3(cdiv(N, STRIP), chunks), 256, 0, st>>>(x, M, N, part);
   PH_LAUNCH_CHECK();
   colreduce_kernel<<<cdiv(N, 256), 256, 0, st>>>(part, chunks, N, N, out);
   PH_LAUNCH_CHECK();
