@@ -1,0 +1,41 @@
+"""Run 3 rounds of a K=4 federation at world = WORLD_SIZE; rank 0 saves theta."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+from paper_2411_02908_b200 import fedsim as F  # noqa: E402
+
+out, server = sys.argv[1], sys.argv[2]
+world = int(os.environ.get("WORLD_SIZE", "1"))
+rank = int(os.environ.get("RANK", "0"))
+local = int(os.environ.get("LOCAL_RANK", "0"))
+nccl_id = None
+if world > 1:
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    obj = [F.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    nccl_id = obj[0]
+cfg = F.ModelConfig(1, 32, 2, 4, 64, 16)
+plan = F.partition_iid(F.generate_corpus("web", 60000, 7, 64), 6, 16, 7)
+theta0 = F.TransformerModel(cfg).init_params(1)
+local_cfg = F.LocalTrainConfig(model=cfg, schedule=F.LrSchedule(2e-3, 16, 160, 0.1),
+                               local_steps=4, batch_size=4)
+srv = F.ServerOptConfig() if server == "fedavg" else F.diloco_server_opt()
+runner = F.FederationRunner(F.FederationConfig(6, 4, 3, F.Topology.kRingAllReduce, 42), local_cfg,
+                            srv, plan, theta0, device=local, precision="f32", rank=rank,
+                            world=world, nccl_id=nccl_id)
+for _ in range(3):
+    runner.run_round()
+theta = runner.theta()
+vel = runner.velocity()
+if rank == 0:
+    np.save(out, np.concatenate([theta, vel]))
+if world > 1:
+    dist.barrier()
+    dist.destroy_process_group()
