@@ -336,9 +336,113 @@ __global__ void __launch_bounds__(512) ce_kernel(T* __restrict__ logits,
   }
 }
 
+// bf16 rows up to kCeRegChunks*8*256 wide stay in registers: one HBM read and
+// one write per logit.
+constexpr int kCeThreads = 256, kCeRegChunks = 26;  // V <= 53248
+__global__ void __launch_bounds__(kCeThreads) ce_reg_kernel(bf16* __restrict__ logits,
+                                                            const int32_t* __restrict__ targets,
+                                                            int V, float inv_count,
+                                                            double* __restrict__ rowloss,
+                                                            int write_grad) {
+  __shared__ float red[kCeThreads / 32];
+  __shared__ float bcast;
+  const int row = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  bf16* l = logits + (size_t)row * V;
+  const int nvec = V / 8;  // V % 8 == 0 (checked by the launcher)
+  uint4 x[kCeRegChunks];
+  float m = -INFINITY;
+  int bad = 0;
+#pragma unroll
+  for (int c = 0; c < kCeRegChunks; ++c) {
+    const int i = tid + c * kCeThreads;
+    if (i < nvec) {
+      x[c] = reinterpret_cast<const uint4*>(l)[i];
+      const uint32_t w[4] = {x[c].x, x[c].y, x[c].z, x[c].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float a = __uint_as_float(w[e] << 16), b = __uint_as_float(w[e] & 0xffff0000u);
+        bad |= !(a < INFINITY) | !(b < INFINITY);
+        m = fmaxf(m, fmaxf(a, b));
+      }
+    }
+  }
+  m = warp_max(m);
+  if (lane == 0) red[warp] = m;
+  __syncthreads();
+  if (tid < 32) {
+    float t = tid < kCeThreads / 32 ? red[tid] : -INFINITY;
+    t = warp_max(t);
+    if (tid == 0) bcast = t;
+  }
+  __syncthreads();
+  m = bcast;
+  const float ml2 = m * 1.4426950408889634f;
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < kCeRegChunks; ++c) {
+    const int i = tid + c * kCeThreads;
+    if (i < nvec) {
+      const uint32_t w[4] = {x[c].x, x[c].y, x[c].z, x[c].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        s += exp2f(fmaf(__uint_as_float(w[e] << 16), 1.4426950408889634f, -ml2));
+        s += exp2f(fmaf(__uint_as_float(w[e] & 0xffff0000u), 1.4426950408889634f, -ml2));
+      }
+    }
+  }
+  s = warp_sum(s);
+  __syncthreads();
+  if (lane == 0) red[warp] = s;
+  bad = __syncthreads_or(bad);
+  if (tid < 32) {
+    float t = tid < kCeThreads / 32 ? red[tid] : 0.f;
+    t = warp_sum(t);
+    if (tid == 0) bcast = t;
+  }
+  __syncthreads();
+  s = bcast;
+  const int t = targets[row];
+  if (tid == 0)
+    rowloss[row] = t < 0 ? 0.0
+                   : bad ? (double)NAN
+                         : (double)logf(s) + (double)m - (double)__bfloat162float(l[t]);
+  if (!write_grad) return;
+  __syncthreads();  // l[t] read before it is overwritten
+  const float g = t >= 0 ? inv_count : 0.f;
+  const float gs = g / s;
+#pragma unroll
+  for (int c = 0; c < kCeRegChunks; ++c) {
+    const int i = tid + c * kCeThreads;
+    if (i < nvec) {
+      const uint32_t w[4] = {x[c].x, x[c].y, x[c].z, x[c].w};
+      uint32_t o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = i * 8 + 2 * e;
+        float a = gs * exp2f(fmaf(__uint_as_float(w[e] << 16), 1.4426950408889634f, -ml2));
+        float b = gs * exp2f(fmaf(__uint_as_float(w[e] & 0xffff0000u), 1.4426950408889634f, -ml2));
+        if (j == t) a -= g;
+        if (j + 1 == t) b -= g;
+        const __nv_bfloat162 p = __floats2bfloat162_rn(a, b);
+        o[e] = *reinterpret_cast<const uint32_t*>(&p);
+      }
+      reinterpret_cast<uint4*>(l)[i] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
 template <typename T>
 void ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count, double* rowloss,
                 bool write_grad, cudaStream_t st) {
+  if constexpr (sizeof(T) == 2) {
+    if (V % 8 == 0 && V <= kCeRegChunks * 8 * kCeThreads &&
+        (reinterpret_cast<uintptr_t>(logits) & 15) == 0) {
+      ce_reg_kernel<<<M, kCeThreads, 0, st>>>(logits, targets, V, inv_count, rowloss,
+                                              write_grad ? 1 : 0);
+      PH_LAUNCH_CHECK();
+      return;
+    }
+  }
   ce_kernel<T><<<M, 512, 0, st>>>(logits, targets, V, inv_count, rowloss, write_grad ? 1 : 0);
   PH_LAUNCH_CHECK();
 }
