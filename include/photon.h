@@ -232,7 +232,8 @@ int photon_debug_gemm(int impl, int M, int N, int K, const void* A, int64_t lda,
 
 /* Causal attention on device pointers (bf16 q,k,v,o,dO,dq,dk,dv as [B*S, d]
  * with head h in columns [h*dh,(h+1)*dh); lse, scratch fp32 [B*H*S]):
- * impl 0 = SIMT, 1 = tensor core.  dO == NULL: forward only.  *ms = device
+ * impl 0 = SIMT, 1 = mma.sync tensor core, 2 = tcgen05 forward (dh = 64).
+ * dO == NULL: forward only.  *ms = device
  * time of the call. */
 int photon_debug_attention(int impl, int B, int S, int H, int d, const void* q, const void* k,
                            const void* v, void* o, float* lse, const void* dO, float* scratch,

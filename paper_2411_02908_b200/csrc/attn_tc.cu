@@ -1,0 +1,842 @@
+// attn_tc.cu -- causal attention forward on tcgen05 / TMEM / TMA (sm_100a).
+//
+// One CTA per (128-query tile, batch*head), two CTAs per SM (80 KB smem,
+// 256 TMEM columns each) so one CTA's softmax overlaps the other's MMAs; 6 warps:
+//   warp 0     TMA producer: Q once, K/V 128-key tiles into a 2-stage ring
+//   warp 1     MMA issuer (one thread): S_j = Q K_j^T (M128 N128 K64) into
+//              TMEM, then O += P_{j-1} V_{j-1} (M128 N64 K128) with P read
+//              from TMEM (tcgen05.mma A-from-TMEM form)
+//   warps 2-5  softmax, thread = query row (its TMEM lane): tcgen05.ld the
+//              score row, causal mask, online max/sum in the exp2 domain
+//              (one FFMA + EX2 per score), P as packed bf16 via tcgen05.st;
+//              O is rescaled in TMEM only when the running max grows by more
+//              than 2^8 (lazy rescale), final O / l and the log-sum-exp out.
+// Semantics are those of tensor.cpp:436-542 (scale 1/sqrt(dh) before the max,
+// keys j <= i); the lse feeds the (deterministic) backward in attn_mma.cu.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "kernels.cuh"
+
+namespace photon {
+namespace k {
+
+namespace {
+
+constexpr int TQ = 128, TK = 128, DH = 64;
+constexpr int kThreads = 192;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kRescaleThresh = 8.0f;  // log2 units
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nLAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra LAB_WAIT;\n}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                    uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ uint64_t sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+#define TMEM_LD32(taddr, r)                                                                     \
+  asm volatile(                                                                                 \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"  \
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"       \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),    \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),             \
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),          \
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),          \
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),          \
+        "=r"(r[31])                                                                             \
+      : "r"(taddr))
+#define TMEM_ST32(taddr, r)                                                                     \
+  asm volatile(                                                                                 \
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"   \
+      "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"( \
+          taddr),                                                                               \
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),  \
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),        \
+      "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),      \
+      "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),      \
+      "r"(r[29]), "r"(r[30]), "r"(r[31])                                                        \
+      : "memory")
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
+                                       uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t pk(float a, float b) {
+  __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&t);
+}
+
+struct FwdArgs {
+  int S, H, d;
+  float sl2;  // scale * log2(e)
+  bf16* o;
+  float* lse;
+};
+
+// A from TMEM ("TS" form): D[tmem] += A[tmem] * B[smem]
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                       uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// TMEM columns per CTA: S [0,128) fp32 scores, P [128,192) bf16x2, O [192,256).
+constexpr uint32_t kColS = 0, kColP = 128, kColO = 192;
+
+__global__ void __launch_bounds__(kThreads, 2)
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                       const __grid_constant__ CUtensorMap tv, const FwdArgs a) {
+  // smem: Q 16K | K[2] 16K | V[2] 16K | barriers  -> two CTAs per SM
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint8_t* sQ = sm;
+  uint8_t* sK = sm + 16384;
+  uint8_t* sV = sK + 2 * 16384;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + 2 * 16384);
+  uint64_t* q_full = bar;
+  uint64_t* kv_full = bar + 1;   // [2]
+  uint64_t* kv_empty = bar + 3;  // [2]
+  uint64_t* s_full = bar + 5;
+  uint64_t* s_empty = bar + 6;
+  uint64_t* p_full = bar + 7;
+  uint64_t* o_done = bar + 8;    // one completion per PV_j
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9);
+
+  const int nqt = (a.S + TQ - 1) / TQ;
+  const int qt = nqt - 1 - blockIdx.x;  // heavy tiles first
+  const int bh = blockIdx.y, b = bh / a.H, h = bh % a.H;
+  const int q0 = qt * TQ;
+  const int row_base = b * a.S;
+  const int n_kt = (q0 + TQ - 1) / TK + 1;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_empty, 4);
+    mbar_init(p_full, 4);
+    mbar_init(o_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+        su32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ===== producer =====
+      mbar_expect_tx(q_full, 16384);
+      tma_load_2d(sQ, &tq, q_full, h * DH, row_base + q0);
+      for (int j = 0; j < n_kt; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[st], 32768);
+        tma_load_2d(sK + st * 16384, &tk, &kv_full[st], h * DH, row_base + j * TK);
+        tma_load_2d(sV + st * 16384, &tv, &kv_full[st], h * DH, row_base + j * TK);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ===== MMA issuer =====
+      constexpr uint32_t IDS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TK >> 3) << 17) |
+                               ((uint32_t)(TQ >> 4) << 24);
+      constexpr uint32_t IDO = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
+                               ((uint32_t)(DH >> 3) << 17) | ((uint32_t)(TQ >> 4) << 24);
+      mbar_wait(q_full, 0);
+      const uint32_t aq = su32(sQ);
+      auto issue_pv = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(p_full, j & 1);
+        fence_after();
+        const uint32_t bv = su32(sV + st * 16384);
+#pragma unroll
+        for (int kk = 0; kk < TK / 16; ++kk)  // 16 keys = 8 packed bf16x2 TMEM columns
+          mma_ts(tmem + kColO, tmem + kColP + kk * 8, sw128(bv + kk * 2048, 8192, 1024), IDO,
+                 (j > 0 || kk > 0) ? 1u : 0u);
+        commit(o_done);
+        commit(&kv_empty[st]);
+      };
+      for (int j = 0; j < n_kt; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        mbar_wait(s_empty, (j & 1) ^ 1);  // softmax holds S_{j-1} in registers
+        fence_after();
+        const uint32_t bk = su32(sK + st * 16384);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)
+          mma(tmem + kColS, sw128(aq + kk * 32, 16, 1024), sw128(bk + kk * 32, 16, 1024), IDS,
+              kk > 0 ? 1u : 0u);
+        commit(s_full);
+        if (j > 0) issue_pv(j - 1);
+      }
+      issue_pv(n_kt - 1);
+    }
+  } else {
+    // ===== softmax: thread = query row r (its TMEM lane) =====
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const int qrow = q0 + r;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const float sl2 = a.sl2;
+    float m = -INFINITY, l = 0.f;  // m in log2 units
+    for (int j = 0; j < n_kt; ++j) {
+      mbar_wait(s_full, j & 1);
+      fence_after();
+      uint32_t s[TK];
+#pragma unroll
+      for (int c = 0; c < TK / 32; ++c) TMEM_LD32(tmem + lane_off + kColS + c * 32, (s + c * 32));
+      tmem_wait_ld();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_empty);
+      const int k0 = j * TK;
+      if (k0 + TK > q0) {  // diagonal / tail tile: causal and length mask
+#pragma unroll
+        for (int i = 0; i < TK; ++i)
+          if (k0 + i > qrow || k0 + i >= a.S) s[i] = __float_as_uint(-INFINITY);
+      }
+      float mx = -INFINITY;  // raw-score max (scale > 0 keeps the order)
+#pragma unroll
+      for (int i = 0; i < TK; ++i) mx = fmaxf(mx, __uint_as_float(s[i]));
+      mx *= sl2;
+      // lazy rescale: keep the stale max unless it grew by > 2^8
+      float scale = 1.f;
+      bool rescale = false;
+      if (mx > m + kRescaleThresh || m == -INFINITY) {
+        if (m != -INFINITY) {
+          scale = exp2f(m - mx);
+          rescale = true;
+        }
+        m = mx;
+      }
+      // P and O are free once PV_{j-1} retired
+      if (j >= 1) mbar_wait(o_done, (j - 1) & 1);
+      fence_after();
+      if (__any_sync(0xffffffffu, rescale)) {
+#pragma unroll
+        for (int c = 0; c < DH / 32; ++c) {
+          uint32_t u[32];
+          TMEM_LD32(tmem + lane_off + kColO + c * 32, u);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * scale);
+          TMEM_ST32(tmem + lane_off + kColO + c * 32, u);
+        }
+      }
+      l *= scale;
+      // P = exp2(s*sl2 - m) -> bf16 pairs into TMEM columns [128, 192)
+      float rs = 0.f;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t pp[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float p0 = exp2f(fmaf(__uint_as_float(s[c * 64 + 2 * i]), sl2, -m));
+          const float p1 = exp2f(fmaf(__uint_as_float(s[c * 64 + 2 * i + 1]), sl2, -m));
+          rs += p0 + p1;
+          pp[i] = pk(p0, p1);
+        }
+        TMEM_ST32(tmem + lane_off + kColP + c * 32, pp);
+      }
+      l += rs;
+      tmem_wait_st();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    // final: O / l, log-sum-exp
+    mbar_wait(o_done, (n_kt - 1) & 1);
+    fence_after();
+    const float inv = 1.f / l;
+    bf16* orow = a.o + (int64_t)(row_base + qrow) * a.d + h * DH;
+#pragma unroll
+    for (int c = 0; c < DH / 32; ++c) {
+      uint32_t u[32];
+      TMEM_LD32(tmem + lane_off + kColO + c * 32, u);
+      tmem_wait_ld();
+      if (qrow < a.S) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8)
+          *reinterpret_cast<uint4*>(orow + c * 32 + i) =
+              make_uint4(pk(__uint_as_float(u[i]) * inv, __uint_as_float(u[i + 1]) * inv),
+                         pk(__uint_as_float(u[i + 2]) * inv, __uint_as_float(u[i + 3]) * inv),
+                         pk(__uint_as_float(u[i + 4]) * inv, __uint_as_float(u[i + 5]) * inv),
+                         pk(__uint_as_float(u[i + 6]) * inv, __uint_as_float(u[i + 7]) * inv));
+      }
+    }
+    if (qrow < a.S) a.lse[(int64_t)bh * a.S + qrow] = m * kLn2 + logf(l);
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  }
+}
+
+// ============================================================================
+// Backward.  prep: D = rowsum(dO * O) and lse in log2 units into padded
+// [B*H][Spad] arrays (pad: lse = +inf -> P = 0, D = 0), so every 128-query
+// slice is an in-bounds 512-byte bulk copy.
+// ============================================================================
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar))
+      : "memory");
+}
+
+__global__ void attn_bwd_prep_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dO,
+                                     const float* __restrict__ lse, float* __restrict__ Lp,
+                                     float* __restrict__ Dp, int B, int S, int H, int d, int Spad) {
+  const int lane = threadIdx.x & 31, warps = blockDim.x / 32;
+  const int idx = blockIdx.x * warps + threadIdx.x / 32;  // (bh, i) over Spad
+  if (idx >= B * H * Spad) return;
+  const int i = idx % Spad, bh = idx / Spad, b = bh / H, h = bh % H;
+  if (i >= S) {
+    if (lane == 0) {
+      Lp[idx] = INFINITY;
+      Dp[idx] = 0.f;
+    }
+    return;
+  }
+  const int64_t off = ((int64_t)(b * S + i)) * d + h * DH + lane * 2;
+  const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(o + off);
+  const __nv_bfloat162 y = *reinterpret_cast<const __nv_bfloat162*>(dO + off);
+  float acc = __bfloat162float(x.x) * __bfloat162float(y.x) + __bfloat162float(x.y) * __bfloat162float(y.y);
+  acc = warp_sum(acc);
+  if (lane == 0) {
+    Dp[idx] = acc;
+    Lp[idx] = lse[(int64_t)bh * S + i] * kLog2e;
+  }
+}
+
+struct BwdArgs {
+  int S, H, d, Spad;
+  float sl2, scale;
+  const float* Lp;
+  const float* Dp;
+  bf16* g0;  // dk (dkdv kernel) or dq (dq kernel)
+  bf16* g1;  // dv
+};
+
+constexpr int kBwdThreads = 64 + 8 * 32;  // producer, MMA, 8 softmax warps
+
+// Store rows of two 64-column fp32 TMEM accumulators (thread = row, column
+// half hf handles 32 columns of each) as bf16 rows of the head slice.
+__device__ __forceinline__ void store_acc_rows(uint32_t taddr, bf16* row_ptr, float mul, bool live) {
+  uint32_t u[32];
+  TMEM_LD32(taddr, u);
+  tmem_wait_ld();
+  if (live) {
+#pragma unroll
+    for (int i = 0; i < 32; i += 8)
+      *reinterpret_cast<uint4*>(row_ptr + i) =
+          make_uint4(pk(__uint_as_float(u[i]) * mul, __uint_as_float(u[i + 1]) * mul),
+                     pk(__uint_as_float(u[i + 2]) * mul, __uint_as_float(u[i + 3]) * mul),
+                     pk(__uint_as_float(u[i + 4]) * mul, __uint_as_float(u[i + 5]) * mul),
+                     pk(__uint_as_float(u[i + 6]) * mul, __uint_as_float(u[i + 7]) * mul));
+  }
+}
+
+// ---- dK, dV: CTA per 128-key tile; keys are the TMEM lanes ------------------------
+// TMEM: S^T [0,128)  dP^T [128,256)  P^T [256,320)  dS^T [320,384)  dV [384,448)  dK [448,512)
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                            const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
+                            const BwdArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint8_t* sK = sm;
+  uint8_t* sV = sm + 16384;
+  uint8_t* sQ = sm + 2 * 16384;   // [2]
+  uint8_t* sO = sm + 4 * 16384;   // [2] dO
+  float* sL = reinterpret_cast<float*>(sm + 6 * 16384);  // [2][128]
+  float* sD = sL + 256;                                  // [2][128]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sD + 256);
+  uint64_t* kv_full = bar;
+  uint64_t* q_full = bar + 1;   // [2]
+  uint64_t* q_empty = bar + 3;  // [2]
+  uint64_t* s_full = bar + 5;
+  uint64_t* s_empty = bar + 6;
+  uint64_t* p_full = bar + 7;
+  uint64_t* g_done = bar + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9);
+
+  const int nt = (a.S + TQ - 1) / TQ;
+  const int kt = blockIdx.x;
+  const int bh = blockIdx.y, b = bh / a.H, h = bh % a.H;
+  const int row_base = b * a.S;
+  const int n_it = nt - kt;  // query tiles kt .. nt-1
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_empty, 8);
+    mbar_init(p_full, 8);
+    mbar_init(g_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        su32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(kv_full, 32768);
+      tma_load_2d(sK, &tk, kv_full, h * DH, row_base + kt * TK);
+      tma_load_2d(sV, &tv, kv_full, h * DH, row_base + kt * TK);
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it & 1, qt = kt + it;
+        mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);
+        mbar_expect_tx(&q_full[st], 32768 + 1024);
+        tma_load_2d(sQ + st * 16384, &tq, &q_full[st], h * DH, row_base + qt * TQ);
+        tma_load_2d(sO + st * 16384, &tdo, &q_full[st], h * DH, row_base + qt * TQ);
+        bulk_load(sL + st * 128, a.Lp + (int64_t)bh * a.Spad + qt * TQ, 512, &q_full[st]);
+        bulk_load(sD + st * 128, a.Dp + (int64_t)bh * a.Spad + qt * TQ, 512, &q_full[st]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t IDS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TQ >> 3) << 17) |
+                               ((uint32_t)(TK >> 4) << 24);
+      constexpr uint32_t IDG = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
+                               ((uint32_t)(DH >> 3) << 17) | ((uint32_t)(TK >> 4) << 24);
+      mbar_wait(kv_full, 0);
+      const uint32_t ak = su32(sK), av = su32(sV);
+      auto issue_grads = [&](int it) {
+        const int st = it & 1;
+        mbar_wait(p_full, it & 1);
+        fence_after();
+        const uint32_t bo = su32(sO + st * 16384), bq = su32(sQ + st * 16384);
+#pragma unroll
+        for (int kk = 0; kk < TQ / 16; ++kk)  // dV += P^T dO
+          mma_ts(tmem + 384, tmem + 256 + kk * 8, sw128(bo + kk * 2048, 8192, 1024), IDG,
+                 (it > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < TQ / 16; ++kk)  // dK += dS^T Q
+          mma_ts(tmem + 448, tmem + 320 + kk * 8, sw128(bq + kk * 2048, 8192, 1024), IDG,
+                 (it > 0 || kk > 0) ? 1u : 0u);
+        commit(g_done);
+        commit(&q_empty[st]);
+      };
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it & 1;
+        mbar_wait(&q_full[st], (it >> 1) & 1);
+        mbar_wait(s_empty, (it & 1) ^ 1);
+        fence_after();
+        const uint32_t bq = su32(sQ + st * 16384), bo = su32(sO + st * 16384);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)  // S^T = K Q^T
+          mma(tmem + 0, sw128(ak + kk * 32, 16, 1024), sw128(bq + kk * 32, 16, 1024), IDS,
+              kk > 0 ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)  // dP^T = V dO^T
+          mma(tmem + 128, sw128(av + kk * 32, 16, 1024), sw128(bo + kk * 32, 16, 1024), IDS,
+              kk > 0 ? 1u : 0u);
+        commit(s_full);
+        if (it > 0) issue_grads(it - 1);
+      }
+      issue_grads(n_it - 1);
+    }
+  } else {
+    const int q = warp & 3, hf = (warp - 2) >> 2;  // lane quarter, query-column half
+    const int r = q * 32 + lane;
+    const int key = kt * TK + r;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    for (int it = 0; it < n_it; ++it) {
+      const int st = it & 1, q0 = (kt + it) * TQ;
+      mbar_wait(&q_full[st], (it >> 1) & 1);  // L, D of this query tile visible
+      mbar_wait(s_full, it & 1);
+      fence_after();
+      uint32_t s[64], dp[64];
+      TMEM_LD32(tmem + lane_off + hf * 64, s);
+      TMEM_LD32(tmem + lane_off + hf * 64 + 32, (s + 32));
+      TMEM_LD32(tmem + lane_off + 128 + hf * 64, dp);
+      TMEM_LD32(tmem + lane_off + 128 + hf * 64 + 32, (dp + 32));
+      tmem_wait_ld();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_empty);
+      const float* L = sL + st * 128 + hf * 64;
+      const float* D = sD + st * 128 + hf * 64;
+      const bool diag = kt * TK + TK > q0;  // this key tile meets the diagonal
+      const bool key_live = key < a.S;
+      uint32_t pp[32], dd[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        float p0 = exp2f(fmaf(__uint_as_float(s[2 * i]), a.sl2, -L[2 * i]));
+        float p1 = exp2f(fmaf(__uint_as_float(s[2 * i + 1]), a.sl2, -L[2 * i + 1]));
+        const int qc = q0 + hf * 64 + 2 * i;
+        if (!key_live || (diag && key > qc)) p0 = 0.f;
+        if (!key_live || (diag && key > qc + 1)) p1 = 0.f;
+        const float d0 = p0 * (__uint_as_float(dp[2 * i]) - D[2 * i]) * a.scale;
+        const float d1 = p1 * (__uint_as_float(dp[2 * i + 1]) - D[2 * i + 1]) * a.scale;
+        pp[i] = pk(p0, p1);
+        dd[i] = pk(d0, d1);
+      }
+      if (it >= 1) mbar_wait(g_done, (it - 1) & 1);  // P^T / dS^T columns free
+      fence_after();
+      TMEM_ST32(tmem + lane_off + 256 + hf * 32, pp);
+      TMEM_ST32(tmem + lane_off + 320 + hf * 32, dd);
+      tmem_wait_st();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    mbar_wait(g_done, (n_it - 1) & 1);
+    fence_after();
+    const int64_t row = (int64_t)(row_base + key) * a.d + h * DH + hf * 32;
+    store_acc_rows(tmem + lane_off + 448 + hf * 32, a.g0 + row, 1.f, key < a.S);  // dK
+    store_acc_rows(tmem + lane_off + 384 + hf * 32, a.g1 + row, 1.f, key < a.S);  // dV
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ---- dQ: CTA per 128-query tile; queries are the TMEM lanes ------------------------
+// TMEM: S [0,128)  dP [128,256)  dS [256,320)  dQ [320,384)
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                          const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
+                          const BwdArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint8_t* sQ = sm;
+  uint8_t* sO = sm + 16384;
+  uint8_t* sK = sm + 2 * 16384;  // [2]
+  uint8_t* sV = sm + 4 * 16384;  // [2]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 6 * 16384);
+  uint64_t* q_full = bar;
+  uint64_t* kv_full = bar + 1;   // [2]
+  uint64_t* kv_empty = bar + 3;  // [2]
+  uint64_t* s_full = bar + 5;
+  uint64_t* s_empty = bar + 6;
+  uint64_t* p_full = bar + 7;
+  uint64_t* g_done = bar + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9);
+
+  const int nt = (a.S + TQ - 1) / TQ;
+  const int qt = nt - 1 - blockIdx.x;
+  const int bh = blockIdx.y, b = bh / a.H, h = bh % a.H;
+  const int row_base = b * a.S;
+  const int q0 = qt * TQ;
+  const int n_kt = qt + 1;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_empty, 8);
+    mbar_init(p_full, 8);
+    mbar_init(g_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        su32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, 32768);
+      tma_load_2d(sQ, &tq, q_full, h * DH, row_base + q0);
+      tma_load_2d(sO, &tdo, q_full, h * DH, row_base + q0);
+      for (int j = 0; j < n_kt; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[st], 32768);
+        tma_load_2d(sK + st * 16384, &tk, &kv_full[st], h * DH, row_base + j * TK);
+        tma_load_2d(sV + st * 16384, &tv, &kv_full[st], h * DH, row_base + j * TK);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t IDS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TK >> 3) << 17) |
+                               ((uint32_t)(TQ >> 4) << 24);
+      constexpr uint32_t IDG = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
+                               ((uint32_t)(DH >> 3) << 17) | ((uint32_t)(TQ >> 4) << 24);
+      mbar_wait(q_full, 0);
+      const uint32_t aq = su32(sQ), ao = su32(sO);
+      auto issue_dq = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(p_full, j & 1);
+        fence_after();
+        const uint32_t bk = su32(sK + st * 16384);
+#pragma unroll
+        for (int kk = 0; kk < TK / 16; ++kk)  // dQ += dS K
+          mma_ts(tmem + 320, tmem + 256 + kk * 8, sw128(bk + kk * 2048, 8192, 1024), IDG,
+                 (j > 0 || kk > 0) ? 1u : 0u);
+        commit(g_done);
+        commit(&kv_empty[st]);
+      };
+      for (int j = 0; j < n_kt; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        mbar_wait(s_empty, (j & 1) ^ 1);
+        fence_after();
+        const uint32_t bk = su32(sK + st * 16384), bv = su32(sV + st * 16384);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)  // S = Q K^T
+          mma(tmem + 0, sw128(aq + kk * 32, 16, 1024), sw128(bk + kk * 32, 16, 1024), IDS,
+              kk > 0 ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)  // dP = dO V^T
+          mma(tmem + 128, sw128(ao + kk * 32, 16, 1024), sw128(bv + kk * 32, 16, 1024), IDS,
+              kk > 0 ? 1u : 0u);
+        commit(s_full);
+        if (j > 0) issue_dq(j - 1);
+      }
+      issue_dq(n_kt - 1);
+    }
+  } else {
+    const int q = warp & 3, hf = (warp - 2) >> 2;  // lane quarter, key-column half
+    const int r = q * 32 + lane;
+    const int qrow = q0 + r;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const float L = a.Lp[(int64_t)bh * a.Spad + qrow];
+    const float D = a.Dp[(int64_t)bh * a.Spad + qrow];
+    for (int j = 0; j < n_kt; ++j) {
+      mbar_wait(s_full, j & 1);
+      fence_after();
+      uint32_t s[64], dp[64];
+      TMEM_LD32(tmem + lane_off + hf * 64, s);
+      TMEM_LD32(tmem + lane_off + hf * 64 + 32, (s + 32));
+      TMEM_LD32(tmem + lane_off + 128 + hf * 64, dp);
+      TMEM_LD32(tmem + lane_off + 128 + hf * 64 + 32, (dp + 32));
+      tmem_wait_ld();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_empty);
+      const int k0 = j * TK + hf * 64;
+      const bool diag = j * TK + TK > q0;
+      uint32_t dd[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        float p0 = exp2f(fmaf(__uint_as_float(s[2 * i]), a.sl2, -L));
+        float p1 = exp2f(fmaf(__uint_as_float(s[2 * i + 1]), a.sl2, -L));
+        if (diag && (k0 + 2 * i > qrow || k0 + 2 * i >= a.S)) p0 = 0.f;
+        if (diag && (k0 + 2 * i + 1 > qrow || k0 + 2 * i + 1 >= a.S)) p1 = 0.f;
+        dd[i] = pk(p0 * (__uint_as_float(dp[2 * i]) - D) * a.scale,
+                   p1 * (__uint_as_float(dp[2 * i + 1]) - D) * a.scale);
+      }
+      if (j >= 1) mbar_wait(g_done, (j - 1) & 1);
+      fence_after();
+      TMEM_ST32(tmem + lane_off + 256 + hf * 32, dd);
+      tmem_wait_st();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    mbar_wait(g_done, (n_kt - 1) & 1);
+    fence_after();
+    store_acc_rows(tmem + lane_off + 320 + hf * 32,
+                   a.g0 + (int64_t)(row_base + qrow) * a.d + h * DH + hf * 32, 1.f, qrow < a.S);
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult qr;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &qr) ==
+            cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  if (!fn) throw Error(PHOTON_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// [rows][d] bf16, box {64 cols of one head, 128 rows}, 128B swizzle
+CUtensorMap head_map(const void* base, int rows, int d) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(PHOTON_ERR_CUDA, "attention tensor map failed");
+  return m;
+}
+
+struct Scratch {
+  float* ptr = nullptr;
+  size_t n = 0;
+  std::mutex mu;
+};
+Scratch g_scratch;
+float* scratch(size_t n) {
+  std::lock_guard<std::mutex> lk(g_scratch.mu);
+  if (n > g_scratch.n) {
+    if (g_scratch.ptr) cudaFree(g_scratch.ptr);
+    g_scratch.ptr = nullptr;
+    PH_CUDA(cudaMalloc(&g_scratch.ptr, n * sizeof(float)));
+    g_scratch.n = n;
+  }
+  return g_scratch.ptr;
+}
+
+}  // namespace
+
+bool attn_tc_supported(int dh, int d) { return dh == DH && (d % 8) == 0; }
+
+void attn_bwd_tc(const bf16* q, const bf16* k, const bf16* v, const bf16* o, const bf16* dO,
+                 const float* lse, bf16* dq, bf16* dk, bf16* dv, int B, int S, int H, int d,
+                 cudaStream_t st) {
+  if (d / H != DH) throw Error(PHOTON_ERR_CONFIG, "attn_bwd_tc: head dim must be 64");
+  const int nt = (S + TQ - 1) / TQ, Spad = nt * TQ, rows = B * S;
+  float* Lp = scratch((size_t)2 * B * H * Spad);
+  float* Dp = Lp + (size_t)B * H * Spad;
+  attn_bwd_prep_kernel<<<(B * H * Spad + 7) / 8, 256, 0, st>>>(o, dO, lse, Lp, Dp, B, S, H, d, Spad);
+  PH_LAUNCH_CHECK();
+  const CUtensorMap mq = head_map(q, rows, d), mk = head_map(k, rows, d), mv = head_map(v, rows, d),
+                    mo = head_map(dO, rows, d);
+  BwdArgs a{S, H, d, Spad, rsqrtf((float)DH) * kLog2e, rsqrtf((float)DH), Lp, Dp, dk, dv};
+  constexpr int SMEM1 = 1024 + 6 * 16384 + 2048 + 256;
+  constexpr int SMEM2 = 1024 + 6 * 16384 + 256;
+  static bool cfg = false;
+  if (!cfg) {
+    PH_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM1));
+    PH_CUDA(cudaFuncSetAttribute(attn_bwd_dq_tc_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2));
+    cfg = true;
+  }
+  dim3 grid(nt, B * H);
+  attn_bwd_dkdv_tc_kernel<<<grid, kBwdThreads, SMEM1, st>>>(mq, mk, mv, mo, a);
+  PH_LAUNCH_CHECK();
+  a.g0 = dq;
+  a.g1 = nullptr;
+  attn_bwd_dq_tc_kernel<<<grid, kBwdThreads, SMEM2, st>>>(mq, mk, mv, mo, a);
+  PH_LAUNCH_CHECK();
+}
+
+void attn_fwd_tc(const bf16* q, const bf16* k, const bf16* v, bf16* o, float* lse, int B, int S,
+                 int H, int d, cudaStream_t st) {
+  if (d / H != DH) throw Error(PHOTON_ERR_CONFIG, "attn_fwd_tc: head dim must be 64");
+  const int rows = B * S;
+  const CUtensorMap mq = head_map(q, rows, d), mk = head_map(k, rows, d), mv = head_map(v, rows, d);
+  const FwdArgs a{S, H, d, rsqrtf((float)DH) * kLog2e, o, lse};
+  constexpr int SMEM = 1024 + 16384 * 5 + 256;
+  static bool cfg = false;
+  if (!cfg) {
+    PH_CUDA(cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 SMEM));
+    cfg = true;
+  }
+  dim3 grid((S + TQ - 1) / TQ, B * H);
+  attn_fwd_tc_kernel<<<grid, kThreads, SMEM, st>>>(mq, mk, mv, a);
+  PH_LAUNCH_CHECK();
+}
+
+}  // namespace k
+}  // namespace photon

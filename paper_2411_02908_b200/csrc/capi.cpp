@@ -525,11 +525,15 @@ int photon_debug_attention(int impl, int B, int S, int H, int d, const void* q, 
          Vv = static_cast<const bf16*>(v);
     PH_CUDA(cudaEventRecord(e0, st));
     if (!dO) {
-      if (impl == 1) k::attn_fwd_mma(Q, K, Vv, static_cast<bf16*>(o), lse, B, S, H, d, st);
+      if (impl == 2) k::attn_fwd_tc(Q, K, Vv, static_cast<bf16*>(o), lse, B, S, H, d, st);
+      else if (impl == 1) k::attn_fwd_mma(Q, K, Vv, static_cast<bf16*>(o), lse, B, S, H, d, st);
       else k::attn_fwd_simt<bf16>(Q, K, Vv, static_cast<bf16*>(o), lse, B, S, H, d, st);
     } else {
       auto O = static_cast<const bf16*>(o), DO = static_cast<const bf16*>(dO);
-      if (impl == 1)
+      if (impl == 2)
+        k::attn_bwd_tc(Q, K, Vv, O, DO, lse, static_cast<bf16*>(dq), static_cast<bf16*>(dk),
+                       static_cast<bf16*>(dv), B, S, H, d, st);
+      else if (impl == 1)
         k::attn_bwd_mma(Q, K, Vv, O, DO, lse, scratch, static_cast<bf16*>(dq),
                         static_cast<bf16*>(dk), static_cast<bf16*>(dv), B, S, H, d, st);
       else

@@ -62,7 +62,8 @@ class EngineT final : public Engine {
     Smax_ = c.seq_len;
     Mmax_ = mb * Smax_;
     if (const char* e = std::getenv("PHOTON_GEMM")) gemm_mode = std::string(e) == "simt" ? 0 : 1;
-    if (const char* e = std::getenv("PHOTON_ATTN")) attn_mode = std::string(e) == "simt" ? 0 : 1;
+    if (const char* e = std::getenv("PHOTON_ATTN"))
+      attn_mode = std::string(e) == "simt" ? 0 : (std::string(e) == "mma" ? 2 : 1);
     allocate();
   }
   ~EngineT() override {
@@ -205,10 +206,14 @@ class EngineT final : public Engine {
   }
 
   bool use_mma_attn() const {
-    return sizeof(T) == 2 && attn_mode == 1 && k::attn_mma_supported((int)(d_ / H_));
+    return sizeof(T) == 2 && attn_mode >= 1 && k::attn_mma_supported((int)(d_ / H_));
   }
   void attn_fwd(const T* q, const T* k, const T* v, T* o, float* lse, int B, int S, int H, int d) {
     if constexpr (sizeof(T) == 2) {
+      if (attn_mode == 1 && k::attn_tc_supported((int)(d_ / H_), d)) {
+        k::attn_fwd_tc(q, k, v, o, lse, B, S, H, d, stream);
+        return;
+      }
       if (use_mma_attn()) {
         k::attn_fwd_mma(q, k, v, o, lse, B, S, H, d, stream);
         return;
@@ -219,6 +224,10 @@ class EngineT final : public Engine {
   void attn_bwd(const T* q, const T* k, const T* v, const T* o, const T* dO, const float* lse,
                 int B, int S, int H, int d) {
     if constexpr (sizeof(T) == 2) {
+      if (attn_mode == 1 && k::attn_tc_supported((int)(d_ / H_), d)) {
+        k::attn_bwd_tc(q, k, v, o, dO, lse, dq_, dk_, dv_, B, S, H, d, stream);
+        return;
+      }
       if (use_mma_attn()) {
         k::attn_bwd_mma(q, k, v, o, dO, lse, Dvec_, dq_, dk_, dv_, B, S, H, d, stream);
         return;

@@ -66,5 +66,11 @@ def test_attention_small(impl, B, S, H, d):
 
 
 def test_attention_photon125m_head_shape():
-    # dh = 64, S = 2048 (the 125M shape), tensor-core path
+    # dh = 64, S = 2048 (the 125M shape), tensor-core paths
     _run(1, 2, 2048, 2, 128)
+    _run(2, 2, 2048, 2, 128)
+
+
+@pytest.mark.parametrize("B,S,H", [(2, 128, 2), (1, 256, 3), (2, 200, 2), (1, 64, 1), (3, 384, 2)])
+def test_attention_tcgen05_forward(B, S, H):
+    _run(2, B, S, H, 64 * H)
