@@ -373,7 +373,7 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--tau", type=int, default=int(os.environ.get("PHOTON_BENCH_TAU", "16")))
+    ap.add_argument("--tau", type=int, default=int(os.environ.get("PHOTON_BENCH_TAU", "64")))
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--precision", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--agg-k", type=int, default=8)
