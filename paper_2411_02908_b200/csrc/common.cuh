@@ -68,4 +68,31 @@ __device__ __forceinline__ float gelu_grad_f(float x) {
   return cdf + x * pdf;
 }
 
+// Fast exact-erf GELU for bf16 epilogues: Phi(x) from Abramowitz & Stegun
+// 7.1.26 (|erf error| <= 1.5e-7) sharing one exp(-x^2/2) with phi(x).
+__device__ __forceinline__ void phi_Phi(float x, float& Phi, float& phi) {
+  const float z = fabsf(x) * 0.70710678118654752440f;
+  float t;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f, z, 1.0f)));
+  const float e = __expf(-0.5f * x * x);  // = exp(-z^2)
+  float poly = fmaf(1.061405429f, t, -1.453152027f);
+  poly = fmaf(poly, t, 1.421413741f);
+  poly = fmaf(poly, t, -0.284496736f);
+  poly = fmaf(poly, t, 0.254829592f);
+  const float erf_abs = 1.0f - poly * t * e;
+  const float erf_x = copysignf(erf_abs, x);
+  Phi = 0.5f * (1.0f + erf_x);
+  phi = 0.39894228040143267794f * e;
+}
+__device__ __forceinline__ float gelu_fast(float x) {
+  float Phi, phi;
+  phi_Phi(x, Phi, phi);
+  return x * Phi;
+}
+__device__ __forceinline__ float gelu_grad_fast(float x) {
+  float Phi, phi;
+  phi_Phi(x, Phi, phi);
+  return fmaf(x, phi, Phi);
+}
+
 }  // namespace photon

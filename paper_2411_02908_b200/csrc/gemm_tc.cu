@@ -19,6 +19,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "gemm.cuh"
@@ -36,6 +37,7 @@ constexpr int kRingBudget = 232448 - kEpiWarps * kEpiBytesPerWarp - 2048;
 struct TcParams {
   int M, N, K;
   int num_m, num_n, splits, kb_total, kb_per_split, units;
+  int group_m;  // raster: bands of group_m M-tiles, N-tiles swept inside a band
   int epi;     // Epi
   int c_bf16;  // output dtype
   const float* bias;
@@ -177,6 +179,28 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
 
+// Grouped raster: the tiles in flight share a band of group_m row tiles of A
+// (L2-resident) and sweep N inside it, so A streams from HBM about once.
+__device__ __forceinline__ void tile_coords(const TcParams& p, int tile, int bn, int& m0, int& n0) {
+  const int per_group = p.group_m * p.num_n;
+  const int g = tile / per_group;
+  const int first_m = g * p.group_m;
+  const int gsz = min(p.group_m, p.num_m - first_m);
+  const int r = tile - g * per_group;
+  m0 = (first_m + r % gsz) * BM;
+  n0 = (r / gsz) * bn;
+}
+
+// Staging offsets of 16-byte column chunk j of row `lane` in a TMA box of 32
+// rows: bf16 rows are 64 B (SWIZZLE_64B), fp32 rows 128 B (SWIZZLE_128B);
+// the XOR spreads the 32 lanes over all banks.
+__device__ __forceinline__ uint32_t sw64_off(int lane, int j) {
+  return lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4);
+}
+__device__ __forceinline__ uint32_t sw128_off(int lane, int j) {
+  return lane * 128 + ((j ^ (lane & 7)) << 4);
+}
+
 // Epilogue tensor maps (row-major [M][N] boxes of 32 rows x 32 cols).
 struct EpiMaps {
   CUtensorMap C;    // output (or split-K workspace, 3D [splits][M][N])
@@ -243,7 +267,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
         const int tile = u / p.splits, split = u % p.splits;
-        const int m0 = (tile % p.num_m) * BM, n0 = (tile / p.num_m) * BN;
+        int m0, n0;
+        tile_coords(p, tile, BN, m0, n0);
         const int kb0 = split * p.kb_per_split;
         const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
         // MN-major 64-wide boxes lying wholly past M / N are skipped: their
@@ -333,7 +358,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       const int tile = u / p.splits, split = u % p.splits;
-      const int m0 = (tile % p.num_m) * BM, n0 = (tile / p.num_m) * BN;
+      int m0, n0;
+      tile_coords(p, tile, BN, m0, n0);
       const int row0 = m0 + q * 32;
       const bool rows_live = row0 < p.M;
       const int nchunks = min(BN / 32, (p.N - n0 + 31) / 32);
@@ -374,7 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               uint32_t w[16];
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
-                const uint4 t = lds128(ia + lane * 64 + j * 16);
+                const uint4 t = lds128(ia + sw64_off(lane, j));
                 w[4 * j] = t.x;
                 w[4 * j + 1] = t.y;
                 w[4 * j + 2] = t.z;
@@ -382,8 +408,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
 #pragma unroll
               for (int e = 0; e < 16; ++e) {
-                v[2 * e] *= gelu_grad_f(bf_lo(w[e]));
-                v[2 * e + 1] *= gelu_grad_f(bf_hi(w[e]));
+                v[2 * e] *= gelu_grad_fast(bf_lo(w[e]));
+                v[2 * e + 1] *= gelu_grad_fast(bf_hi(w[e]));
               }
               // the shared loads are consumed (values used) before the async
               // proxy may overwrite the buffer
@@ -395,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else {  // ResidBias: resid + (acc + bias);  Accum: C + acc
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                const uint4 t = lds128(ia + lane * 128 + j * 16);
+                const uint4 t = lds128(ia + sw128_off(lane, j));
                 v[4 * j] += __uint_as_float(t.x);
                 v[4 * j + 1] += __uint_as_float(t.y);
                 v[4 * j + 2] += __uint_as_float(t.z);
@@ -415,23 +441,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (epi == Epi::GeluBias && !splitk) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {  // pre-activation -> aux box (second 2 KB)
-              sts128(oa + 2048 + lane * 64 + j * 16, pack2(v[8 * j], v[8 * j + 1]),
+              sts128(oa + 2048 + sw64_off(lane, j), pack2(v[8 * j], v[8 * j + 1]),
                      pack2(v[8 * j + 2], v[8 * j + 3]), pack2(v[8 * j + 4], v[8 * j + 5]),
                      pack2(v[8 * j + 6], v[8 * j + 7]));
             }
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
+            for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
           }
           if (out_bf16) {
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-              sts128(oa + lane * 64 + j * 16, pack2(v[8 * j], v[8 * j + 1]),
+              sts128(oa + sw64_off(lane, j), pack2(v[8 * j], v[8 * j + 1]),
                      pack2(v[8 * j + 2], v[8 * j + 3]), pack2(v[8 * j + 4], v[8 * j + 5]),
                      pack2(v[8 * j + 6], v[8 * j + 7]));
           } else {
 #pragma unroll
             for (int j = 0; j < 8; ++j)
-              sts128(oa + lane * 128 + j * 16, __float_as_uint(v[4 * j]),
+              sts128(oa + sw128_off(lane, j), __float_as_uint(v[4 * j]),
                      __float_as_uint(v[4 * j + 1]), __float_as_uint(v[4 * j + 2]),
                      __float_as_uint(v[4 * j + 3]));
           }
@@ -543,13 +569,14 @@ CUtensorMap operand_map(const void* base, uint64_t inner, uint64_t outer, int64_
                 CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-// epilogue tile: row-major [M][N] (row stride ld), box {32 cols, 32 rows}, no swizzle
+// epilogue tile: row-major [M][N] (row stride ld), box {32 cols, 32 rows},
+// swizzled to match sw64_off / sw128_off
 CUtensorMap epi_map(const void* base, bool bf, uint64_t N, uint64_t M, int64_t ld) {
   cuuint64_t dims[2] = {N, M};
   cuuint64_t strides[1] = {(cuuint64_t)ld * (bf ? 2 : 4)};
   cuuint32_t box[2] = {32, 32};
   return encode(bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base,
-                dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+                dims, strides, box, bf ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 template <int BN, bool A_MN, bool B_MN>
@@ -627,6 +654,13 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
   p.kb_per_split = (p.kb_total + splits - 1) / splits;
   p.splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
   p.units = tiles * p.splits;
+  static const int group_env = [] {
+    const char* e = std::getenv("PHOTON_GEMM_GROUP");
+    return e ? std::atoi(e) : -1;
+  }();
+  // measured on the 125M shapes: bands of 8 row tiles, 32 for very wide N
+  const int group = group_env >= 0 ? group_env : (p.num_n >= 64 ? 32 : 8);
+  p.group_m = std::max(1, std::min(group > 0 ? group : p.num_m, p.num_m));
   p.epi = static_cast<int>(g.epi);
   p.c_bf16 = g.c == DT::BF16;
   p.bias = g.bias;
@@ -639,7 +673,7 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
     cuuint64_t strides[2] = {(cuuint64_t)g.N * 4, (cuuint64_t)g.N * g.M * 4};
     cuuint32_t box[3] = {32, 32, 1};
     em.C = encode(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ws, dims, strides, box,
-                  CU_TENSOR_MAP_SWIZZLE_NONE);
+                  CU_TENSOR_MAP_SWIZZLE_128B);
   } else {
     em.C = epi_map(g.C, g.c == DT::BF16, g.N, g.M, g.ldc);
     if (g.epi == Epi::GeluBias || g.epi == Epi::GeluBwd) em.aux = epi_map(g.aux, true, g.N, g.M, g.ldc);
