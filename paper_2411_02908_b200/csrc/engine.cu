@@ -112,7 +112,9 @@ class EngineT final : public Engine {
     const uint64_t M = Mmax_, d = d_, L = L_, hid = hid_;
     const uint64_t rows_bhs = max_batch * H_ * Smax_;
     size_t part_floats = std::max<size_t>((size_t)k::ln_bwd_parts() * 2 * d,
-                                          k::colsum_part_floats((int)M, (int)std::max(V_, hid)));
+                                          std::max({k::colsum_part_floats((int)M, (int)V_),
+                                                    k::colsum_part_floats((int)M, (int)hid),
+                                                    k::colsum_part_floats((int)M, (int)d)}));
     auto plan = [&](char* p) {
       char* s = p;
       master = carve<float>(p, P);

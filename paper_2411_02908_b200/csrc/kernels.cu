@@ -2,6 +2,7 @@
 // softmax cross-entropy and the SIMT attention path of the client step.
 // Citations: /root/reference/proj/core/src/tensor.cpp.
 #include "kernels.cuh"
+#include "sm100.cuh"
 
 namespace photon {
 namespace k {
@@ -106,11 +107,76 @@ __global__ void ln_fwd_kernel(const float* __restrict__ x, const float* __restri
   }
 }
 
+// Register-resident variant for d = 128 * NV: each lane holds NV float4 of the
+// row (16-byte coalesced loads), so x is read from HBM exactly once.
+__device__ __forceinline__ void store4(float* p, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+__device__ __forceinline__ void store4(bf16* p, float a, float b, float c, float d) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&lo);
+  u.y = *reinterpret_cast<uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(p) = u;
+}
+
+template <typename T, int NV>
+__global__ void __launch_bounds__(256) ln_fwd_vec_kernel(const float* __restrict__ x,
+                                                         const float* __restrict__ gain,
+                                                         const float* __restrict__ bias,
+                                                         T* __restrict__ y,
+                                                         float* __restrict__ mean_out,
+                                                         float* __restrict__ rstd_out, int M) {
+  constexpr int D = NV * 128;
+  const int lane = threadIdx.x & 31;
+  const float inv_d = 1.0f / (float)D;
+  for (int m = blockIdx.x * 8 + (threadIdx.x >> 5); m < M; m += gridDim.x * 8) {
+    const float4* xr = reinterpret_cast<const float4*>(x + (size_t)m * D);
+    float4 v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = xr[lane + 32 * i];
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) s += ((v[i].x + v[i].y) + v[i].z) + v[i].w;
+    const float mean = warp_sum(s) * inv_d;
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const float a = v[i].x - mean, b = v[i].y - mean, cc = v[i].z - mean, e = v[i].w - mean;
+      q += ((a * a + b * b) + cc * cc) + e * e;
+    }
+    const float rstd = rsqrtf(warp_sum(q) * inv_d + 1e-5f);
+    T* yr = y + (size_t)m * D;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c4 = lane + 32 * i;
+      const float4 g = reinterpret_cast<const float4*>(gain)[c4];
+      const float4 b = reinterpret_cast<const float4*>(bias)[c4];
+      store4(yr + 4 * c4, g.x * ((v[i].x - mean) * rstd) + b.x, g.y * ((v[i].y - mean) * rstd) + b.y,
+             g.z * ((v[i].z - mean) * rstd) + b.z, g.w * ((v[i].w - mean) * rstd) + b.w);
+    }
+    if (lane == 0) {
+      mean_out[m] = mean;
+      rstd_out[m] = rstd;
+    }
+  }
+}
+
 template <typename T>
 void ln_fwd(const float* x, const float* gain, const float* bias, T* y, float* mean, float* rstd,
             int M, int d, cudaStream_t st) {
-  ln_fwd_kernel<T><<<std::min<int>(cdiv(M, 8), kNumSMs * 16), 256, 0, st>>>(x, gain, bias, y,
-                                                                            mean, rstd, M, d);
+  const int grid = std::min<int>(cdiv(M, 8), kNumSMs * 8);
+  switch (d) {
+#define PH_LNF(NV)                                                                       \
+  case NV * 128:                                                                         \
+    ln_fwd_vec_kernel<T, NV><<<grid, 256, 0, st>>>(x, gain, bias, y, mean, rstd, M);      \
+    break;
+    PH_LNF(1) PH_LNF(2) PH_LNF(3) PH_LNF(4) PH_LNF(5) PH_LNF(6) PH_LNF(8)
+#undef PH_LNF
+    default:
+      ln_fwd_kernel<T><<<std::min<int>(cdiv(M, 8), kNumSMs * 16), 256, 0, st>>>(x, gain, bias, y,
+                                                                                mean, rstd, M, d);
+  }
   PH_LAUNCH_CHECK();
 }
 
@@ -125,9 +191,8 @@ template <typename T>
 __global__ void __launch_bounds__(kLnBwdWarps * 32)
 ln_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ x,
               const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
-              const float* __restrict__ gain, const float* __restrict__ dres,
-              float* __restrict__ dx_out, T* __restrict__ dx_T, float* __restrict__ part, int M,
-              int d) {
+              const float* __restrict__ gain, const float* dres, float* dx_out,
+              T* __restrict__ dx_T, float* __restrict__ part, int M, int d) {
   extern __shared__ float sm[];  // [warps][2][d]
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   float* my = sm + (size_t)warp * 2 * d;
@@ -169,13 +234,123 @@ ln_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ x,
   }
 }
 
-// out[j] = sum_p part[p*stride + j]  (fixed order)
-__global__ void colreduce_kernel(const float* __restrict__ part, int nparts, int n, int stride,
-                                 float* __restrict__ out) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+// out[j] = sum_p part[p*stride + j] for j < n, with columns j >= split going to
+// out1[j - split].  Fixed order: slice s of 8 sums parts p = s (mod 8) in
+// ascending p, then the 8 slices are added in ascending s.  32 columns per CTA.
+__global__ void __launch_bounds__(256) colreduce_kernel(const float* __restrict__ part, int nparts,
+                                                        int n, int stride, float* __restrict__ out,
+                                                        int split, float* __restrict__ out1) {
+  __shared__ float red[8][33];
+  const int cl = threadIdx.x & 31, s = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + cl;
+  float acc = 0.f;
+  if (j < n) {
+    int p = s;
+    for (; p + 24 < nparts; p += 32) {  // four independent loads in flight
+      const float a = part[(size_t)p * stride + j], b = part[(size_t)(p + 8) * stride + j];
+      const float c2 = part[(size_t)(p + 16) * stride + j], d2 = part[(size_t)(p + 24) * stride + j];
+      acc = (((acc + a) + b) + c2) + d2;
+    }
+    for (; p < nparts; p += 8) acc += part[(size_t)p * stride + j];
+  }
+  red[s][cl] = acc;
+  __syncthreads();
+  if (s == 0 && j < n) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w][cl];
+    if (j < split) out[j] = t;
+    else out1[j - split] = t;
+  }
+}
+static void colreduce(const float* part, int nparts, int n, int stride, float* out, int split,
+                      float* out1, cudaStream_t st) {
+  colreduce_kernel<<<cdiv(n, 32), 256, 0, st>>>(part, nparts, n, stride, out, split, out1);
+  PH_LAUNCH_CHECK();
+}
+
+// Register-resident variant for d = 128 * NV: one warp per row, x and dy read
+// once as float4, dgain/dbias accumulated per lane (each lane owns fixed
+// columns) and reduced over the block's warps in a fixed order at the end.
+// dres may alias dx_out (in-place residual accumulation), so neither is restrict.
+template <typename T, int NV>
+__global__ void __launch_bounds__(256, 2)
+ln_bwd_vec_kernel(const float* __restrict__ dy, const float* __restrict__ x,
+                  const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
+                  const float* __restrict__ gain, const float* dres, float* dx_out,
+                  T* __restrict__ dx_T, float* __restrict__ part, int M) {
+  constexpr int D = NV * 128;
+  __shared__ float4 gs[D / 4];
+  __shared__ float red[kLnBwdWarps][D];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = threadIdx.x; j < D / 4; j += blockDim.x) gs[j] = reinterpret_cast<const float4*>(gain)[j];
+  __syncthreads();
+  const float inv_d = 1.0f / (float)D;
+  float4 ag[NV], ab[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) ag[i] = ab[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int m = blockIdx.x * kLnBwdWarps + warp; m < M; m += gridDim.x * kLnBwdWarps) {
+    const float4* xr = reinterpret_cast<const float4*>(x + (size_t)m * D);
+    const float4* gr = reinterpret_cast<const float4*>(dy + (size_t)m * D);
+    float4 xv[NV], gv[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      xv[i] = xr[lane + 32 * i];
+      gv[i] = gr[lane + 32 * i];
+    }
+    const float mean = mean_in[m], rstd = rstd_in[m];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const float4 gg = gs[lane + 32 * i];
+#define PH_LNB_ACC(c)                                 \
+  {                                                   \
+    const float xh = (xv[i].c - mean) * rstd;         \
+    const float dxh = gv[i].c * gg.c;                 \
+    s1 += dxh;                                        \
+    s2 += dxh * xh;                                   \
+    ag[i].c += gv[i].c * xh;                          \
+    ab[i].c += gv[i].c;                               \
+  }
+      PH_LNB_ACC(x) PH_LNB_ACC(y) PH_LNB_ACC(z) PH_LNB_ACC(w)
+#undef PH_LNB_ACC
+    }
+    s1 = warp_sum(s1) * inv_d;
+    s2 = warp_sum(s2) * inv_d;
+    float* out = dx_out + (size_t)m * D;
+    const float* rr = dres ? dres + (size_t)m * D : nullptr;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c4 = lane + 32 * i;
+      const float4 gg = gs[c4];
+      float4 r = rr ? reinterpret_cast<const float4*>(rr)[c4] : make_float4(0.f, 0.f, 0.f, 0.f);
+      r.x += rstd * (gv[i].x * gg.x - s1 - ((xv[i].x - mean) * rstd) * s2);
+      r.y += rstd * (gv[i].y * gg.y - s1 - ((xv[i].y - mean) * rstd) * s2);
+      r.z += rstd * (gv[i].z * gg.z - s1 - ((xv[i].z - mean) * rstd) * s2);
+      r.w += rstd * (gv[i].w * gg.w - s1 - ((xv[i].w - mean) * rstd) * s2);
+      reinterpret_cast<float4*>(out)[c4] = r;
+      if (dx_T) store4(dx_T + (size_t)m * D + 4 * c4, r.x, r.y, r.z, r.w);
+    }
+  }
+  // block partials: [dgain | dbias], warps summed in ascending order
+#pragma unroll
+  for (int i = 0; i < NV; ++i) reinterpret_cast<float4*>(red[warp])[lane + 32 * i] = ag[i];
+  __syncthreads();
+  for (int j = threadIdx.x; j < D; j += blockDim.x) {
     float acc = 0.f;
-    for (int p = 0; p < nparts; ++p) acc += part[(size_t)p * stride + j];
-    out[j] = acc;
+#pragma unroll
+    for (int w = 0; w < kLnBwdWarps; ++w) acc += red[w][j];
+    part[(size_t)blockIdx.x * 2 * D + j] = acc;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NV; ++i) reinterpret_cast<float4*>(red[warp])[lane + 32 * i] = ab[i];
+  __syncthreads();
+  for (int j = threadIdx.x; j < D; j += blockDim.x) {
+    float acc = 0.f;
+#pragma unroll
+    for (int w = 0; w < kLnBwdWarps; ++w) acc += red[w][j];
+    part[(size_t)blockIdx.x * 2 * D + D + j] = acc;
   }
 }
 
@@ -183,17 +358,25 @@ template <typename T>
 void ln_bwd(const float* dy, const float* x, const float* mean, const float* rstd,
             const float* gain, const float* dres, float* dx_out, T* dx_T, float* part,
             float* dgain, float* dbias, int M, int d, cudaStream_t st) {
-  const size_t smem = (size_t)kLnBwdWarps * 2 * d * sizeof(float);
-  if (smem > 48 * 1024)
-    PH_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-  ln_bwd_kernel<T><<<kLnBwdBlocks, kLnBwdWarps * 32, smem, st>>>(dy, x, mean, rstd, gain, dres,
-                                                                 dx_out, dx_T, part, M, d);
+  switch (d) {
+#define PH_LNB(NV)                                                                         \
+  case NV * 128:                                                                           \
+    ln_bwd_vec_kernel<T, NV><<<kLnBwdBlocks, kLnBwdWarps * 32, 0, st>>>(                   \
+        dy, x, mean, rstd, gain, dres, dx_out, dx_T, part, M);                             \
+    break;
+    PH_LNB(1) PH_LNB(2) PH_LNB(3) PH_LNB(4) PH_LNB(5) PH_LNB(6)
+#undef PH_LNB
+    default: {
+      const size_t smem = (size_t)kLnBwdWarps * 2 * d * sizeof(float);
+      if (smem > 48 * 1024)
+        PH_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+      ln_bwd_kernel<T><<<kLnBwdBlocks, kLnBwdWarps * 32, smem, st>>>(dy, x, mean, rstd, gain, dres,
+                                                                     dx_out, dx_T, part, M, d);
+    }
+  }
   PH_LAUNCH_CHECK();
-  colreduce_kernel<<<cdiv(d, 256), 256, 0, st>>>(part, kLnBwdBlocks, d, 2 * d, dgain);
-  PH_LAUNCH_CHECK();
-  colreduce_kernel<<<cdiv(d, 256), 256, 0, st>>>(part + d, kLnBwdBlocks, d, 2 * d, dbias);
-  PH_LAUNCH_CHECK();
+  colreduce(part, kLnBwdBlocks, 2 * d, 2 * d, dgain, d, dbias, st);
 }
 
 // ============================================================================
@@ -203,27 +386,36 @@ void ln_bwd(const float* dy, const float* x, const float* mean, const float* rst
 // lane; warps are reduced in smem in a fixed order.  Pass 2: fixed-order sum
 // over row chunks.  Deterministic; reads the matrix once at HBM speed.
 // ============================================================================
-constexpr int kColRows = 1024;  // rows per chunk
-static int colsum_chunks(int M, int /*N*/) { return (M + kColRows - 1) / kColRows; }
-size_t colsum_part_floats(int M, int N) { return (size_t)colsum_chunks(M, N) * N; }
+// Row chunks are sized so the grid holds about 8 CTAs per SM (at least 64 rows
+// per chunk); the partial count depends only on (M, N, strip width).
+static int colsum_chunks(int M, int N, int strip) {
+  const int strips = (N + strip - 1) / strip;
+  const int want = std::max(1, (kNumSMs * 8 + strips - 1) / strips);
+  return std::max(1, std::min(want, (M + 63) / 64));
+}
+size_t colsum_part_floats(int M, int N) {  // upper bound over element types (bf16 strips are widest)
+  return (size_t)colsum_chunks(M, N, 256) * N;
+}
 
 template <typename T>
 __global__ void __launch_bounds__(256) colsum_part_kernel(const T* __restrict__ x, int M, int N,
+                                                          int rows_per_chunk,
                                                           float* __restrict__ part) {
   constexpr int VEC = 16 / sizeof(T);  // columns per lane
   constexpr int STRIP = 32 * VEC;      // columns per CTA
+  constexpr int U = 8;                 // rows in flight per lane
   __shared__ float red[8][STRIP];
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int c0 = blockIdx.x * STRIP + lane * VEC;
-  const int r0 = blockIdx.y * kColRows, r1 = min(M, r0 + kColRows);
+  const int r0 = blockIdx.y * rows_per_chunk, r1 = min(M, r0 + rows_per_chunk);
   float acc[VEC];
 #pragma unroll
   for (int e = 0; e < VEC; ++e) acc[e] = 0.f;
   const bool full = c0 + VEC <= N && (N % VEC) == 0;
-  for (int r = r0 + warp; r < r1; r += 8 * 4) {
-    T buf[4][VEC];
+  for (int r = r0 + warp; r < r1; r += 8 * U) {
+    T buf[U][VEC];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int rr = r + 8 * u;
       if (rr < r1 && full) {
         *reinterpret_cast<uint4*>(buf[u]) = *reinterpret_cast<const uint4*>(x + (size_t)rr * N + c0);
@@ -234,7 +426,7 @@ __global__ void __launch_bounds__(256) colsum_part_kernel(const T* __restrict__ 
       }
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int e = 0; e < VEC; ++e) acc[e] += to_f<T>(buf[u][e]);
   }
@@ -254,11 +446,12 @@ __global__ void __launch_bounds__(256) colsum_part_kernel(const T* __restrict__ 
 template <typename T>
 void colsum(const T* x, int M, int N, float* part, float* out, cudaStream_t st) {
   constexpr int STRIP = 32 * (16 / sizeof(T));
-  const int chunks = colsum_chunks(M, N);
-  colsum_part_kernel<T><<<dim3(cdiv(N, STRIP), chunks), 256, 0, st>>>(x, M, N, part);
+  const int chunks = colsum_chunks(M, N, STRIP);
+  const int rows = (M + chunks - 1) / chunks;
+  const int used = (M + rows - 1) / rows;
+  colsum_part_kernel<T><<<dim3(cdiv(N, STRIP), used), 256, 0, st>>>(x, M, N, rows, part);
   PH_LAUNCH_CHECK();
-  colreduce_kernel<<<cdiv(N, 256), 256, 0, st>>>(part, chunks, N, N, out);
-  PH_LAUNCH_CHECK();
+  colreduce(part, used, N, N, out, N, nullptr, st);
 }
 
 // ============================================================================
@@ -431,10 +624,184 @@ __global__ void __launch_bounds__(kCeThreads) ce_reg_kernel(bf16* __restrict__ l
   }
 }
 
+// Persistent, smem-pipelined variant (one CTA per SM).  Rows r = blockIdx.x +
+// i*gridDim.x alternate between two shared-memory row buffers.  A producer warp
+// bulk-copies row i+2 into a buffer once the gradient of row i has been
+// bulk-stored out of it, so HBM reads and writes overlap the exp work of the
+// 16 compute warps.  One online (max, sum) pass plus one gradient pass, both
+// over shared memory; every (max, sum) combine runs in a fixed order.
+constexpr int kCePipeWarps = 16, kCePipeThreads = kCePipeWarps * 32;
+constexpr int kCePipeMaxSmem = 232448 - 2048;  // opt-in limit minus the static reduction arrays
+__host__ __device__ inline uint32_t ce_pipe_buf_stride(int V) { return ((uint32_t)V * 2 + 127) & ~127u; }
+static size_t ce_pipe_smem(int V) { return 2 * (size_t)ce_pipe_buf_stride(V) + 64; }
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  const __nv_bfloat162 p = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&p);
+}
+__device__ __forceinline__ void ce_unpack8(const uint4 x, float* v) {
+  const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    v[2 * e] = __uint_as_float(w[e] << 16);
+    v[2 * e + 1] = __uint_as_float(w[e] & 0xffff0000u);
+  }
+}
+__device__ __forceinline__ float ex2_approx(float x) {  // one MUFU.EX2, no range fix-up
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// (m, s) ⊕ (m2, s2) with s measured relative to m
+__device__ __forceinline__ void ce_combine(float& m, float& s, float m2, float s2) {
+  const float mm = fmaxf(m, m2);
+  if (mm == -INFINITY) return;
+  s = s * ex2_approx((m - mm) * 1.4426950408889634f) + s2 * ex2_approx((m2 - mm) * 1.4426950408889634f);
+  m = mm;
+}
+
+__global__ void __launch_bounds__(kCePipeThreads + 32, 1)
+    ce_pipe_kernel(bf16* __restrict__ logits, const int32_t* __restrict__ targets, int M, int V,
+                   float inv_count, double* __restrict__ rowloss, int write_grad) {
+  using namespace sm100;
+  extern __shared__ __align__(128) uint8_t ce_sm[];
+  __shared__ float red_m[kCePipeWarps], red_s[kCePipeWarps];
+  const uint32_t row_bytes = (uint32_t)V * 2, stride = ce_pipe_buf_stride(V);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ce_sm + 2 * stride);
+  uint64_t* done = full + 2;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int G = gridDim.x;
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&done[0], kCePipeWarps);
+    mbar_init(&done[1], kCePipeWarps);
+    mbar_init_fence();
+  }
+  __syncthreads();
+
+  if (warp == kCePipeWarps) {  // ---------------- producer ----------------
+    if (lane == 0) {
+      for (int k = 0; k < 2; ++k) {
+        const int r = blockIdx.x + k * G;
+        if (r < M) {
+          mbar_expect_tx(&full[k], row_bytes);
+          bulk_load(ce_sm + k * stride, logits + (size_t)r * V, row_bytes, &full[k]);
+        }
+      }
+      for (int i = 0;; ++i) {
+        const int r = blockIdx.x + i * G;
+        if (r >= M) break;
+        const int b = i & 1;
+        mbar_wait(&done[b], (i >> 1) & 1);
+        if (write_grad) {
+          bulk_store(logits + (size_t)r * V, ce_sm + b * stride, row_bytes);
+          bulk_commit();
+        }
+        const int r2 = r + 2 * G;
+        if (r2 < M) {
+          if (write_grad) bulk_wait_read<0>();  // buffer read out before it is refilled
+          mbar_expect_tx(&full[b], row_bytes);
+          bulk_load(ce_sm + b * stride, logits + (size_t)r2 * V, row_bytes, &full[b]);
+        }
+      }
+      bulk_wait_all();
+    }
+    return;
+  }
+
+  // ---------------- compute warps ----------------
+  const int nvec = V / 8;
+  constexpr float kL2e = 1.4426950408889634f;
+  for (int i = 0;; ++i) {
+    const int r = blockIdx.x + i * G;
+    if (r >= M) break;
+    const int b = i & 1;
+    uint8_t* buf = ce_sm + b * stride;
+    const uint32_t base = su32(buf);
+    mbar_wait(&full[b], (i >> 1) & 1);
+    // A NaN logit makes s NaN; a +inf logit makes m = +inf and s NaN (inf - inf),
+    // so the reference's NaN loss (tensor.cpp:569-582) is detected from (m, s).
+    float m = -INFINITY, s = 0.f;
+    for (int c = tid; c < nvec; c += kCePipeThreads) {
+      float v[8];
+      ce_unpack8(lds128(base + c * 16), v);
+      const float cm = fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])),
+                             fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7])));
+      if (cm > m) {
+        s *= ex2_approx((m - cm) * kL2e);
+        m = cm;
+      }
+      const float ml2 = m * kL2e;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s += ex2_approx(fmaf(v[e], kL2e, -ml2));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+      ce_combine(m, s, m2, s2);
+    }
+    if (lane == 0) {
+      red_m[warp] = m;
+      red_s[warp] = s;
+    }
+    named_bar_sync(1, kCePipeThreads);
+    m = red_m[0];
+    s = red_s[0];
+#pragma unroll
+    for (int w = 1; w < kCePipeWarps; ++w) ce_combine(m, s, red_m[w], red_s[w]);
+    const bool bad = !(s == s) || m == INFINITY;
+    const int t = targets[r];
+    if (tid == 0) {
+      const float lt = t >= 0 ? __bfloat162float(reinterpret_cast<const bf16*>(buf)[t]) : 0.f;
+      rowloss[r] = t < 0 ? 0.0 : bad ? (double)NAN : (double)logf(s) + (double)m - (double)lt;
+    }
+    named_bar_sync(1, kCePipeThreads);  // l[t] and red_* read before reuse
+    if (write_grad) {
+      const float g = t >= 0 ? inv_count : 0.f;
+      const float gs = g / s, ml2 = m * kL2e;
+      for (int c = tid; c < nvec; c += kCePipeThreads) {
+        float v[8];
+        ce_unpack8(lds128(base + c * 16), v);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = gs * ex2_approx(fmaf(v[e], kL2e, -ml2));
+        const int te = t - c * 8;  // target column within this chunk (if any)
+        if ((unsigned)te < 8u) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (e == te) v[e] -= g;
+        }
+        uint4 o;
+        o.x = pack_bf16x2(v[0], v[1]);
+        o.y = pack_bf16x2(v[2], v[3]);
+        o.z = pack_bf16x2(v[4], v[5]);
+        o.w = pack_bf16x2(v[6], v[7]);
+        sts128(base + c * 16, o);
+      }
+      fence_async_smem();
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&done[b]);
+  }
+}
+
 template <typename T>
 void ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count, double* rowloss,
                 bool write_grad, cudaStream_t st) {
   if constexpr (sizeof(T) == 2) {
+    if (V % 8 == 0 && ce_pipe_smem(V) <= (size_t)kCePipeMaxSmem && M > 0 &&
+        (reinterpret_cast<uintptr_t>(logits) & 15) == 0) {
+      static bool attr = false;
+      if (!attr) {
+        PH_CUDA(cudaFuncSetAttribute(ce_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kCePipeMaxSmem));
+        attr = true;
+      }
+      ce_pipe_kernel<<<std::min(M, kNumSMs), kCePipeThreads + 32, ce_pipe_smem(V), st>>>(
+          logits, targets, M, V, inv_count, rowloss, write_grad ? 1 : 0);
+      PH_LAUNCH_CHECK();
+      return;
+    }
     if (V % 8 == 0 && V <= kCeRegChunks * 8 * kCeThreads &&
         (reinterpret_cast<uintptr_t>(logits) & 15) == 0) {
       ce_reg_kernel<<<M, kCeThreads, 0, st>>>(logits, targets, V, inv_count, rowloss,

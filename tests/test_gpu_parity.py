@@ -18,6 +18,8 @@ TINY = (1, 8, 2, 4, 16, 4)
 HETERO4 = (1, 32, 2, 4, 64, 16)   # configs/hetero4.cfg:15-21 (BASELINE config #1)
 DEFAULT = (2, 64, 2, 4, 64, 32)   # ModelConfig{} model.h:12-18
 DILOCO = (2, 32, 2, 4, 64, 32)    # configs/diloco.cfg, acceptance c7
+WIDE128 = (1, 128, 2, 4, 96, 32)  # d = 128 * NV: register-resident LayerNorm kernels
+WIDE256 = (1, 256, 4, 4, 96, 160)  # dh = 64: tcgen05 attention, ragged S
 
 
 def _mc(F, t):
@@ -36,7 +38,8 @@ def _rel_l2(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
 
-@pytest.mark.parametrize("cfg_t,B", [(TINY, 2), (HETERO4, 4), (DEFAULT, 4)])
+@pytest.mark.parametrize("cfg_t,B", [(TINY, 2), (HETERO4, 4), (DEFAULT, 4), (WIDE128, 2),
+                                     (WIDE256, 2)])
 def test_forward_backward_f32(F, oracle, cfg_t, B):
     mc = ModelCfg(*cfg_t)
     params = oracle.init_params(mc, 3)
@@ -54,7 +57,7 @@ def test_forward_backward_f32(F, oracle, cfg_t, B):
             assert _rel_l2(g[off:off + n], gr) <= 5e-4, name
 
 
-@pytest.mark.parametrize("cfg_t,B", [(HETERO4, 4), (DEFAULT, 4)])
+@pytest.mark.parametrize("cfg_t,B", [(HETERO4, 4), (DEFAULT, 4), (WIDE128, 2), (WIDE256, 2)])
 def test_forward_backward_bf16(F, oracle, cfg_t, B):
     mc = ModelCfg(*cfg_t)
     params = oracle.init_params(mc, 3)
