@@ -8,7 +8,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libphoton.so")
+LIB_PATH = os.environ.get("PHOTON_LIB") or os.path.join(_HERE, "libphoton.so")
 
 u64, i32, dbl, u8 = C.c_uint64, C.c_int32, C.c_double, C.c_uint8
 P = C.POINTER

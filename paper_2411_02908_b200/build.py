@@ -16,8 +16,11 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libphoton.so")
+# PHOTON_BUILD_TRACE=1 builds an instrumented copy (libphoton_trace.so, separate
+# objects) with per-phase clock64 stamps in the attention kernels (tools/attn_trace.py).
+TRACE = os.environ.get("PHOTON_BUILD_TRACE") == "1"
+LIB = os.path.join(PKG, "libphoton_trace.so" if TRACE else "libphoton.so")
+OBJ = os.path.join(PKG, "_build_trace" if TRACE else "_build")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 
@@ -51,7 +54,7 @@ def _compile(src: str, verbose: bool):
     obj = os.path.join(OBJ, name + ".o")
     if not _needs(obj, [src] + _headers()):
         return obj, None
-    cmd = [NVCC] + ARCH + COMMON + EXTRA.get(name, [])
+    cmd = [NVCC] + ARCH + COMMON + EXTRA.get(name, []) + (["-DPHOTON_ATTN_TRACE"] if TRACE else [])
     if src.endswith(".cpp"):
         cmd += ["-x", "cu"]  # host code that includes device headers
     if name.startswith("gemm_tc") or name.startswith("attn_tc"):

@@ -26,6 +26,21 @@ namespace k {
 namespace {
 
 constexpr int TQ = 128, TK = 128, DH = 64;
+
+// Opt-in timeline instrumentation (PHOTON_BUILD_TRACE=1): clock64 stamps of one
+// mid-grid CTA, event e of iteration it at g_attn_trace[e * 64 + it].
+#ifdef PHOTON_ATTN_TRACE
+__device__ unsigned long long g_attn_trace[64 * 64];
+#define ATTN_TRACE(e, it)                                                             \
+  do {                                                                                \
+    if (blockIdx.x == 0 && blockIdx.y == 200 && (it) < 64)                            \
+      g_attn_trace[(e) * 64 + (it)] = clock64();                                      \
+  } while (0)
+#else
+#define ATTN_TRACE(e, it) \
+  do {                    \
+  } while (0)
+#endif
 constexpr int kThreads = 192;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
@@ -108,6 +123,33 @@ __device__ __forceinline__ uint64_t sw128(uint32_t saddr, uint32_t lbo, uint32_t
       "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),      \
       "r"(r[29]), "r"(r[30]), "r"(r[31])                                                        \
       : "memory")
+#define TMEM_LD8(taddr, r)                                                                      \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"          \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),         \
+                 "=r"(r[6]), "=r"(r[7])                                                          \
+               : "r"(taddr))
+#define TMEM_ST8(taddr, r)                                                                      \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(   \
+                   taddr),                                                                       \
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),      \
+               "r"(r[7])                                                                         \
+               : "memory")
+#define TMEM_LD16(taddr, r)                                                                     \
+  asm volatile(                                                                                 \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"  \
+      "%14,%15}, [%16];"                                                                        \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),    \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),             \
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])                                                   \
+      : "r"(taddr))
+#define TMEM_ST16(taddr, r)                                                                     \
+  asm volatile(                                                                                 \
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"   \
+      "%13,%14,%15,%16};" ::"r"(taddr),                                                         \
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),  \
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),        \
+      "r"(r[15])                                                                                \
+      : "memory")
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -119,6 +161,18 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
                "r"(d)
                : "memory");
+}
+__device__ __forceinline__ float ex2(float x) {  // MUFU.EX2 without range fix-up
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float4 lds_f4(const float* p) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(su32(p)));
+  return v;
 }
 __device__ __forceinline__ uint32_t pk(float a, float b) {
   __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
@@ -282,31 +336,31 @@ __global__ void __launch_bounds__(kThreads, 2)
       // P and O are free once PV_{j-1} retired
       if (j >= 1) mbar_wait(o_done, (j - 1) & 1);
       fence_after();
-      if (__any_sync(0xffffffffu, rescale)) {
-#pragma unroll
-        for (int c = 0; c < DH / 32; ++c) {
-          uint32_t u[32];
-          TMEM_LD32(tmem + lane_off + kColO + c * 32, u);
+      if (__any_sync(0xffffffffu, rescale)) {  // 8 columns at a time: s[] stays in registers
+#pragma unroll 1
+        for (int c = 0; c < DH / 8; ++c) {
+          uint32_t u[8];
+          TMEM_LD8(tmem + lane_off + kColO + c * 8, u);
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * scale);
-          TMEM_ST32(tmem + lane_off + kColO + c * 32, u);
+          for (int i = 0; i < 8; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * scale);
+          TMEM_ST8(tmem + lane_off + kColO + c * 8, u);
         }
       }
       l *= scale;
       // P = exp2(s*sl2 - m) -> bf16 pairs into TMEM columns [128, 192)
       float rs = 0.f;
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t pp[32];
+      for (int c = 0; c < 4; ++c) {
+        uint32_t pp[16];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float p0 = exp2f(fmaf(__uint_as_float(s[c * 64 + 2 * i]), sl2, -m));
-          const float p1 = exp2f(fmaf(__uint_as_float(s[c * 64 + 2 * i + 1]), sl2, -m));
+        for (int i = 0; i < 16; ++i) {
+          const float p0 = ex2(fmaf(__uint_as_float(s[c * 32 + 2 * i]), sl2, -m));
+          const float p1 = ex2(fmaf(__uint_as_float(s[c * 32 + 2 * i + 1]), sl2, -m));
           rs += p0 + p1;
           pp[i] = pk(p0, p1);
         }
-        TMEM_ST32(tmem + lane_off + kColP + c * 32, pp);
+        TMEM_ST16(tmem + lane_off + kColP + c * 16, pp);
       }
       l += rs;
       tmem_wait_st();
@@ -472,6 +526,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       for (int it = 0; it < n_it; ++it) {
         const int st = it & 1, qt = kt + it;
         mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);
+        ATTN_TRACE(0, it);
         mbar_expect_tx(&q_full[st], 32768 + 1024);
         tma_load_2d(sQ + st * 16384, &tq, &q_full[st], h * DH, row_base + qt * TQ);
         tma_load_2d(sO + st * 16384, &tdo, &q_full[st], h * DH, row_base + qt * TQ);
@@ -490,6 +545,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       auto issue_grads = [&](int it) {
         const int st = it & 1;
         mbar_wait(p_full, it & 1);
+        ATTN_TRACE(3, it);
         fence_after();
         const uint32_t bo = su32(sO + st * 16384), bq = su32(sQ + st * 16384);
 #pragma unroll
@@ -502,11 +558,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                  (it > 0 || kk > 0) ? 1u : 0u);
         commit(g_done);
         commit(&q_empty[st]);
+        ATTN_TRACE(4, it);
       };
       for (int it = 0; it < n_it; ++it) {
         const int st = it & 1;
         mbar_wait(&q_full[st], (it >> 1) & 1);
+        ATTN_TRACE(1, it);
         mbar_wait(s_empty, (it & 1) ^ 1);
+        ATTN_TRACE(2, it);
         fence_after();
         const uint32_t bq = su32(sQ + st * 16384), bo = su32(sO + st * 16384);
 #pragma unroll
@@ -531,6 +590,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int st = it & 1, q0 = (kt + it) * TQ;
       mbar_wait(&q_full[st], (it >> 1) & 1);  // L, D of this query tile visible
       mbar_wait(s_full, it & 1);
+      if (warp == 2 && lane == 0) ATTN_TRACE(5, it);
       fence_after();
       uint32_t s[64], dp[64];
       TMEM_LD32(tmem + lane_off + hf * 64, s);
@@ -543,21 +603,33 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (lane == 0) mbar_arrive(s_empty);
       const float* L = sL + st * 128 + hf * 64;
       const float* D = sD + st * 128 + hf * 64;
-      const bool diag = kt * TK + TK > q0;  // this key tile meets the diagonal
+      // masking only where this key tile meets the diagonal or the sequence end
+      const bool masked = (kt * TK + TK > q0) || (kt * TK + TK > a.S);
       const bool key_live = key < a.S;
       uint32_t pp[32], dd[32];
+      // dS^T is kept unscaled (the softmax scale is applied to dK at the store)
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        float p0 = exp2f(fmaf(__uint_as_float(s[2 * i]), a.sl2, -L[2 * i]));
-        float p1 = exp2f(fmaf(__uint_as_float(s[2 * i + 1]), a.sl2, -L[2 * i + 1]));
-        const int qc = q0 + hf * 64 + 2 * i;
-        if (!key_live || (diag && key > qc)) p0 = 0.f;
-        if (!key_live || (diag && key > qc + 1)) p1 = 0.f;
-        const float d0 = p0 * (__uint_as_float(dp[2 * i]) - D[2 * i]) * a.scale;
-        const float d1 = p1 * (__uint_as_float(dp[2 * i + 1]) - D[2 * i + 1]) * a.scale;
-        pp[i] = pk(p0, p1);
-        dd[i] = pk(d0, d1);
+      for (int i = 0; i < 16; ++i) {
+        const float4 l4 = lds_f4(L + 4 * i), d4 = lds_f4(D + 4 * i);
+        float p0 = ex2(fmaf(__uint_as_float(s[4 * i]), a.sl2, -l4.x));
+        float p1 = ex2(fmaf(__uint_as_float(s[4 * i + 1]), a.sl2, -l4.y));
+        float p2 = ex2(fmaf(__uint_as_float(s[4 * i + 2]), a.sl2, -l4.z));
+        float p3 = ex2(fmaf(__uint_as_float(s[4 * i + 3]), a.sl2, -l4.w));
+        if (masked) {
+          const int qc = q0 + hf * 64 + 4 * i;
+          p0 = (key_live && key <= qc) ? p0 : 0.f;
+          p1 = (key_live && key <= qc + 1) ? p1 : 0.f;
+          p2 = (key_live && key <= qc + 2) ? p2 : 0.f;
+          p3 = (key_live && key <= qc + 3) ? p3 : 0.f;
+        }
+        pp[2 * i] = pk(p0, p1);
+        pp[2 * i + 1] = pk(p2, p3);
+        dd[2 * i] = pk(p0 * (__uint_as_float(dp[4 * i]) - d4.x),
+                       p1 * (__uint_as_float(dp[4 * i + 1]) - d4.y));
+        dd[2 * i + 1] = pk(p2 * (__uint_as_float(dp[4 * i + 2]) - d4.z),
+                           p3 * (__uint_as_float(dp[4 * i + 3]) - d4.w));
       }
+      if (warp == 2 && lane == 0) ATTN_TRACE(7, it);
       if (it >= 1) mbar_wait(g_done, (it - 1) & 1);  // P^T / dS^T columns free
       fence_after();
       TMEM_ST32(tmem + lane_off + 256 + hf * 32, pp);
@@ -570,7 +642,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_wait(g_done, (n_it - 1) & 1);
     fence_after();
     const int64_t row = (int64_t)(row_base + key) * a.d + h * DH + hf * 32;
-    store_acc_rows(tmem + lane_off + 448 + hf * 32, a.g0 + row, 1.f, key < a.S);  // dK
+    store_acc_rows(tmem + lane_off + 448 + hf * 32, a.g0 + row, a.scale, key < a.S);  // dK
     store_acc_rows(tmem + lane_off + 384 + hf * 32, a.g1 + row, 1.f, key < a.S);  // dV
   }
   fence_before();
@@ -706,16 +778,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(s_empty);
       const int k0 = j * TK + hf * 64;
-      const bool diag = j * TK + TK > q0;
-      uint32_t dd[32];
+      const bool masked = (j * TK + TK > q0) || (j * TK + TK > a.S);
+      uint32_t dd[32];  // dS unscaled (the softmax scale is applied to dQ at the store)
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        float p0 = exp2f(fmaf(__uint_as_float(s[2 * i]), a.sl2, -L));
-        float p1 = exp2f(fmaf(__uint_as_float(s[2 * i + 1]), a.sl2, -L));
-        if (diag && (k0 + 2 * i > qrow || k0 + 2 * i >= a.S)) p0 = 0.f;
-        if (diag && (k0 + 2 * i + 1 > qrow || k0 + 2 * i + 1 >= a.S)) p1 = 0.f;
-        dd[i] = pk(p0 * (__uint_as_float(dp[2 * i]) - D) * a.scale,
-                   p1 * (__uint_as_float(dp[2 * i + 1]) - D) * a.scale);
+        float p0 = ex2(fmaf(__uint_as_float(s[2 * i]), a.sl2, -L));
+        float p1 = ex2(fmaf(__uint_as_float(s[2 * i + 1]), a.sl2, -L));
+        if (masked) {
+          p0 = (k0 + 2 * i <= qrow && k0 + 2 * i < a.S) ? p0 : 0.f;
+          p1 = (k0 + 2 * i + 1 <= qrow && k0 + 2 * i + 1 < a.S) ? p1 : 0.f;
+        }
+        dd[i] = pk(p0 * (__uint_as_float(dp[2 * i]) - D), p1 * (__uint_as_float(dp[2 * i + 1]) - D));
       }
       if (j >= 1) mbar_wait(g_done, (j - 1) & 1);
       fence_after();
@@ -728,7 +801,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_wait(g_done, (n_kt - 1) & 1);
     fence_after();
     store_acc_rows(tmem + lane_off + 320 + hf * 32,
-                   a.g0 + (int64_t)(row_base + qrow) * a.d + h * DH + hf * 32, 1.f, qrow < a.S);
+                   a.g0 + (int64_t)(row_base + qrow) * a.d + h * DH + hf * 32, a.scale, qrow < a.S);
   }
   fence_before();
   __syncthreads();
@@ -753,12 +826,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// [rows][d] bf16, box {64 cols of one head, 128 rows}, 128B swizzle
-CUtensorMap head_map(const void* base, int rows, int d) {
+// [rows][d] bf16, box {64 cols of one head, box_rows rows}, 128B swizzle
+CUtensorMap head_map(const void* base, int rows, int d, int box_rows = 128) {
   CUtensorMap m;
   cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)d * 2};
-  cuuint32_t box[2] = {64, 128};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -786,6 +859,12 @@ float* scratch(size_t n) {
 }
 
 }  // namespace
+
+#ifdef PHOTON_ATTN_TRACE
+extern "C" int photon_debug_attn_trace(unsigned long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, g_attn_trace, sizeof(unsigned long long) * n);
+}
+#endif
 
 bool attn_tc_supported(int dh, int d) { return dh == DH && (d % 8) == 0; }
 

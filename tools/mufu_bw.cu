@@ -1,0 +1,53 @@
+// mufu_bw.cu -- MUFU.EX2 / FFMA issue throughput per SM with independent chains.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/mufu_bw tools/mufu_bw.cu && /tmp/mufu_bw
+#include <cstdio>
+#include <cuda_runtime.h>
+
+template <int OP>
+__global__ void kern(int iters, unsigned long long* cycles, float* sink) {
+  float a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = -1.0f - 1e-3f * (threadIdx.x + i);
+  __syncthreads();
+  const unsigned long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (OP == 0) {
+        asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
+      } else if (OP == 1) {
+        asm volatile("fma.rn.f32 %0, %0, 0f3F7FF000, 0fBC000000;" : "+f"(a[i]));
+      } else {
+        asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(*reinterpret_cast<unsigned*>(&a[i])));
+      }
+    }
+  }
+  __syncthreads();
+  const unsigned long long t1 = clock64();
+  if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  sink[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+int main() {
+  unsigned long long* cyc;
+  float* sink;
+  cudaMalloc(&cyc, 148 * 8);
+  cudaMalloc(&sink, 148 * 1024 * 4);
+  unsigned long long h;
+  const int iters = 2048;
+  const char* names[3] = {"ex2.f32", "ffma", "ex2.bf16x2"};
+  for (int op = 0; op < 3; ++op)
+    for (int warps : {4, 8, 16, 32}) {
+      if (op == 0) kern<0><<<148, warps * 32>>>(iters, cyc, sink);
+      if (op == 1) kern<1><<<148, warps * 32>>>(iters, cyc, sink);
+      if (op == 2) kern<2><<<148, warps * 32>>>(iters, cyc, sink);
+      cudaDeviceSynchronize();
+      cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+      printf("%-11s warps=%2d: %6.1f warp-instr... lane-ops/clk/SM = %.1f\n", names[op], warps,
+             0.0, (double)warps * 32 * 8 * iters / (double)h);
+    }
+  return 0;
+}
