@@ -11,6 +11,11 @@
 //               (residual, GELU pre-activation, accumulate target) arrive by
 //               TMA one chunk ahead.  The second accumulator lets the epilogue
 //               of tile i overlap the main loop of tile i+1.
+// Pair mode (NCTA = 2, cta_group::2): a 2-CTA cluster on one TPC computes a
+// 256 x 256 tile; each CTA stages its own 128 rows of A and half of B, the
+// leader issues M=256 MMAs that write each CTA's 128 accumulator rows into that
+// CTA's TMEM, and completions are multicast to both CTAs.  Per-SM operand
+// traffic through shared memory halves and the ring gets 5 stages.
 // Operands may be K-major or MN-major (the three layouts of tensor.cpp:152-207
 // on canonical [in,out] weights); both are legal UMMA smem layouts, so no
 // transposes are materialised.  Small-tile GEMMs with a long contraction
@@ -162,6 +167,56 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// ---- cluster / CTA-pair wrappers ----
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// shared::cluster address of `local` in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_rank(const void* local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(su32(local)), "r"(rank));
+  return r;
+}
+// Relaxed remote arrive: used only after this CTA's tcgen05.ld of the
+// accumulator completed (wait::ld), so nothing the leader's next MMA
+// overwrites is still being read; a release would cost a GPU-scope fence.
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+// TMA load into this CTA's smem, completing on the pair leader's barrier
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map,
+                                                 uint32_t leader_bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(leader_bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on both CTAs' copy
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(su32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
 // UMMA shared-memory descriptor, SWIZZLE_128B, sm100 version bits.
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
@@ -181,13 +236,14 @@ __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 
 
 // Grouped raster: the tiles in flight share a band of group_m row tiles of A
 // (L2-resident) and sweep N inside it, so A streams from HBM about once.
-__device__ __forceinline__ void tile_coords(const TcParams& p, int tile, int bn, int& m0, int& n0) {
+__device__ __forceinline__ void tile_coords(const TcParams& p, int tile, int bm, int bn, int& m0,
+                                            int& n0) {
   const int per_group = p.group_m * p.num_n;
   const int g = tile / per_group;
   const int first_m = g * p.group_m;
   const int gsz = min(p.group_m, p.num_m - first_m);
   const int r = tile - g * per_group;
-  m0 = (first_m + r % gsz) * BM;
+  m0 = (first_m + r % gsz) * bm;
   n0 = (r / gsz) * bn;
 }
 
@@ -208,19 +264,23 @@ struct EpiMaps {
   CUtensorMap in;   // fp32 residual (ResidBias) or C itself (Accum)
 };
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int NCTA>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ EpiMaps em, const TcParams p) {
+  constexpr int BNL = BN / NCTA;  // B rows (N) staged by this CTA
   constexpr int A_BYTES = BM * BK * 2;
-  constexpr int B_BYTES = BN * BK * 2;
+  constexpr int B_BYTES = BNL * BK * 2;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   constexpr int STAGES = kRingBudget / STAGE_BYTES;
   constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulators
-  // instruction descriptor: D f32, A/B bf16, majors, N, M = 128
+  // instruction descriptor: D f32, A/B bf16, majors, N, M = 128 * NCTA
   constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
                              ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) |
-                             ((uint32_t)(BM >> 4) << 24);
+                             ((uint32_t)((BM * NCTA) >> 4) << 24);
+  const uint32_t rank = NCTA == 2 ? cluster_rank() : 0;
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x / NCTA, ncl = gridDim.x / NCTA;  // cluster id / count
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -237,12 +297,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const Epi epi = static_cast<Epi>(p.epi);
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
+      // pair: only the leader arrives (expecting both CTAs' bytes); the peer's
+      // bytes complete on the leader's copy.  The peer refills a stage only
+      // after the MMA consumed it, so its bytes never leak into an older phase.
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kEpiWarps);
+      mbar_init(&tempty[a], kEpiWarps * NCTA);
     }
     for (int i = 0; i < kEpiWarps; ++i) mbar_init(&inbar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -250,13 +313,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     su32(tmem_slot)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (NCTA == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       su32(tmem_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       su32(tmem_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (NCTA == 2) cluster_sync_all();  // peer barriers initialised before any remote arrive
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -265,32 +336,56 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ================= TMA producer =================
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      // bytes one CTA of the pair lands per k-block (MN-major 64-wide boxes
+      // lying wholly past M / N are skipped: their smem is stale but only feeds
+      // accumulator rows/cols that are never stored)
+      auto stage_tx = [&](int mr, int nr) -> uint32_t {
+        const int ab = A_MN ? max(0, min(BM / 64, (p.M - mr + 63) / 64)) : 1;
+        const int bb = B_MN ? max(0, min(BNL / 64, (p.N - nr + 63) / 64)) : 1;
+        return (A_MN ? ab * 8192 : A_BYTES) + (B_MN ? bb * 8192 : B_BYTES);
+      };
+      const uint32_t leader_full0 = NCTA == 2 ? mapa_rank(&full[0], 0) : 0;
+      for (int u = cid; u < p.units; u += ncl) {
         const int tile = u / p.splits, split = u % p.splits;
         int m0, n0;
-        tile_coords(p, tile, BN, m0, n0);
+        tile_coords(p, tile, BM * NCTA, BN, m0, n0);
+        const int mr = m0 + (int)rank * BM, nr = n0 + (int)rank * BNL;  // this CTA's slices
         const int kb0 = split * p.kb_per_split;
         const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
-        // MN-major 64-wide boxes lying wholly past M / N are skipped: their
-        // smem is stale but only feeds accumulator rows/cols never stored.
-        const int a_boxes = A_MN ? min(BM / 64, (p.M - m0 + 63) / 64) : 1;
-        const int b_boxes = B_MN ? min(BN / 64, (p.N - n0 + 63) / 64) : 1;
-        const uint32_t tx = (A_MN ? a_boxes * 8192 : A_BYTES) + (B_MN ? b_boxes * 8192 : B_BYTES);
+        const int a_boxes = A_MN ? max(0, min(BM / 64, (p.M - mr + 63) / 64)) : 1;
+        const int b_boxes = B_MN ? max(0, min(BNL / 64, (p.N - nr + 63) / 64)) : 1;
+        const uint32_t tx = NCTA == 2 ? stage_tx(m0, n0) + stage_tx(m0 + BM, n0 + BNL)
+                                      : stage_tx(mr, nr);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
-          mbar_expect_tx(&full[stage], tx);
           const int k0 = kb * BK;
-          if (!A_MN) {
-            tma_load_2d(sa, &tmA, &full[stage], k0, m0);
+          if (NCTA == 1) {
+            mbar_expect_tx(&full[stage], tx);
+            if (!A_MN) {
+              tma_load_2d(sa, &tmA, &full[stage], k0, mr);
+            } else {
+              for (int c = 0; c < a_boxes; ++c) tma_load_2d(sa + c * 8192, &tmA, &full[stage], mr + 64 * c, k0);
+            }
+            if (!B_MN) {
+              tma_load_2d(sb, &tmB, &full[stage], k0, nr);
+            } else {
+              for (int c = 0; c < b_boxes; ++c) tma_load_2d(sb + c * 8192, &tmB, &full[stage], nr + 64 * c, k0);
+            }
           } else {
-            for (int c = 0; c < a_boxes; ++c) tma_load_2d(sa + c * 8192, &tmA, &full[stage], m0 + 64 * c, k0);
-          }
-          if (!B_MN) {
-            tma_load_2d(sb, &tmB, &full[stage], k0, n0);
-          } else {
-            for (int c = 0; c < b_boxes; ++c) tma_load_2d(sb + c * 8192, &tmB, &full[stage], n0 + 64 * c, k0);
+            const uint32_t lbar = leader_full0 + stage * 8;  // leader's full[stage]
+            if (leader) mbar_expect_tx(&full[stage], tx);   // its arrive + both CTAs' bytes
+            if (!A_MN) {
+              tma_load_2d_pair(sa, &tmA, lbar, k0, mr);
+            } else {
+              for (int c = 0; c < a_boxes; ++c) tma_load_2d_pair(sa + c * 8192, &tmA, lbar, mr + 64 * c, k0);
+            }
+            if (!B_MN) {
+              tma_load_2d_pair(sb, &tmB, lbar, k0, nr);
+            } else {
+              for (int c = 0; c < b_boxes; ++c) tma_load_2d_pair(sb + c * 8192, &tmB, lbar, nr + 64 * c, k0);
+            }
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -300,13 +395,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ================= MMA issuer =================
+    if (lane == 0 && leader) {
+      // ================= MMA issuer (pair leader) =================
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      for (int u = cid; u < p.units; u += ncl) {
         const int split = u % p.splits;
         const int kb0 = split * p.kb_per_split;
         const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
@@ -324,15 +419,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      : sw128_desc(sa + kk * 32, 16, 1024);
             const uint64_t db = B_MN ? sw128_desc(sb + kk * 2048, 8192, 1024)
                                      : sw128_desc(sb + kk * 32, 16, 1024);
-            tc_mma(d, da, db, IDESC, (kb > kb0 || kk > 0) ? 1u : 0u);
+            if (NCTA == 1) tc_mma(d, da, db, IDESC, (kb > kb0 || kk > 0) ? 1u : 0u);
+            else tc_mma_pair(d, da, db, IDESC, (kb > kb0 || kk > 0) ? 1u : 0u);
           }
-          tc_commit(&empty[stage]);  // smem slot free once these MMAs retire
+          // smem slot free once these MMAs retire
+          if (NCTA == 1) tc_commit(&empty[stage]);
+          else tc_commit_pair(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(&tfull[acc]);  // accumulator ready
+        if (NCTA == 1) tc_commit(&tfull[acc]);  // accumulator ready
+        else tc_commit_pair(&tfull[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -356,11 +455,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool out_bf16 = !splitk && p.c_bf16;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+    const uint32_t leader_tempty0 = NCTA == 2 ? mapa_rank(&tempty[0], 0) : 0;
+    for (int u = cid; u < p.units; u += ncl) {
       const int tile = u / p.splits, split = u % p.splits;
       int m0, n0;
-      tile_coords(p, tile, BN, m0, n0);
-      const int row0 = m0 + q * 32;
+      tile_coords(p, tile, BM * NCTA, BN, m0, n0);
+      const int row0 = m0 + (int)rank * BM + q * 32;
       const bool rows_live = row0 < p.M;
       const int nchunks = min(BN / 32, (p.N - n0 + 31) / 32);
       if (need_in && rows_live && sub < nchunks && lane == 0) {  // overlaps the main loop
@@ -476,7 +576,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {  // this CTA's accumulator rows are drained
+        if (NCTA == 1 || leader) mbar_arrive(&tempty[acc]);
+        else mbar_arrive_remote(leader_tempty0 + acc * 8);
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -485,11 +588,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
-  __syncthreads();
+  if (NCTA == 2) cluster_sync_all();  // no remote arrive / multicast still in flight
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(TMEM_COLS));
+    if (NCTA == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(TMEM_COLS));
   }
 }
 
@@ -579,20 +687,36 @@ CUtensorMap epi_map(const void* base, bool bf, uint64_t N, uint64_t M, int64_t l
                 dims, strides, box, bf ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int NCTA>
 void launch(const CUtensorMap& a, const CUtensorMap& b, const EpiMaps& em, const TcParams& p,
             int grid, cudaStream_t st) {
-  constexpr int STAGE_BYTES = (BM + BN) * BK * 2;
+  constexpr int STAGE_BYTES = (BM + BN / NCTA) * BK * 2;
   constexpr int STAGES = kRingBudget / STAGE_BYTES;
   static_assert(STAGES >= 3, "operand ring too shallow");
   constexpr int SMEM = STAGES * STAGE_BYTES + kEpiWarps * kEpiBytesPerWarp + 1024 + 512;
-  auto kern = gemm_tc_kernel<BN, A_MN, B_MN>;
+  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, NCTA>;
   static bool configured = false;
   if (!configured) {
     PH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
     configured = true;
   }
-  kern<<<grid, kThreads, SMEM, st>>>(a, b, em, p);
+  if (NCTA == 1) {
+    kern<<<grid, kThreads, SMEM, st>>>(a, b, em, p);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    PH_CUDA(cudaLaunchKernelEx(&cfg, kern, a, b, em, p));
+  }
   PH_LAUNCH_CHECK();
 }
 
@@ -637,18 +761,30 @@ bool gemm_tc_supported(const GemmArgs& g) {
 bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
   if (!gemm_tc_supported(g)) return false;
   const int BN = g.N <= 128 ? 128 : 256;
+  static const int pair_env = [] {
+    const char* e = std::getenv("PHOTON_GEMM_PAIR");  // 0 never, 1 by shape, 2 always
+    return e ? std::atoi(e) : 1;
+  }();
+  // CTA pairs (256 x 256 tiles) where they measured faster on the 125M shapes
+  // (tools/gemm_bench.py): wide tiles without split-K, except the GELU'
+  // epilogue (epilogue-bound; the pair couples both CTAs' epilogues).
+  const int kb_all = (g.K + BK - 1) / BK;
+  const bool split_needed = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN) < kNumSMs && kb_all >= 16;
+  const bool pair_ok = BN == 256 && g.M > BM && !split_needed && g.epi != Epi::GeluBwd;
+  const int ncta = (pair_env == 2 || (pair_env == 1 && pair_ok)) && BN == 256 && g.M > BM ? 2 : 1;
+  const int slots = kNumSMs / ncta;  // concurrent tile workers
   TcParams p{};
   p.M = g.M;
   p.N = g.N;
   p.K = g.K;
-  p.num_m = (g.M + BM - 1) / BM;
+  p.num_m = (g.M + BM * ncta - 1) / (BM * ncta);
   p.num_n = (g.N + BN - 1) / BN;
   p.kb_total = (g.K + BK - 1) / BK;
   const int tiles = p.num_m * p.num_n;
   // split-K when the tile grid cannot fill the chip and the contraction is long
   int splits = 1;
-  if (tiles < kNumSMs && p.kb_total >= 16) {
-    splits = std::min(kNumSMs / tiles, p.kb_total / 8);
+  if (tiles < slots && p.kb_total >= 16) {
+    splits = std::min(slots / tiles, p.kb_total / 8);
     splits = std::max(1, std::min(splits, 16));
   }
   p.kb_per_split = (p.kb_total + splits - 1) / splits;
@@ -685,20 +821,25 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
   const CUtensorMap ta = g.a_kmajor ? operand_map(g.A, g.K, g.M, g.lda, BM)
                                     : operand_map(g.A, g.M, g.K, g.lda, 64);
   // B(k,j): K-major -> [N][K] rows; N-major -> [K][N] rows
-  const CUtensorMap tb = g.b_kmajor ? operand_map(g.B, g.K, g.N, g.ldb, BN)
+  const CUtensorMap tb = g.b_kmajor ? operand_map(g.B, g.K, g.N, g.ldb, BN / ncta)
                                     : operand_map(g.B, g.N, g.K, g.ldb, 64);
-  const int grid = std::min(p.units, kNumSMs);
+  const int grid = std::min(p.units, slots) * ncta;
   const bool amn = !g.a_kmajor, bmn = !g.b_kmajor;
   if (BN == 128) {
-    if (!amn && !bmn) launch<128, false, false>(ta, tb, em, p, grid, st);
-    else if (!amn && bmn) launch<128, false, true>(ta, tb, em, p, grid, st);
-    else if (amn && !bmn) launch<128, true, false>(ta, tb, em, p, grid, st);
-    else launch<128, true, true>(ta, tb, em, p, grid, st);
+    if (!amn && !bmn) launch<128, false, false, 1>(ta, tb, em, p, grid, st);
+    else if (!amn && bmn) launch<128, false, true, 1>(ta, tb, em, p, grid, st);
+    else if (amn && !bmn) launch<128, true, false, 1>(ta, tb, em, p, grid, st);
+    else launch<128, true, true, 1>(ta, tb, em, p, grid, st);
+  } else if (ncta == 1) {
+    if (!amn && !bmn) launch<256, false, false, 1>(ta, tb, em, p, grid, st);
+    else if (!amn && bmn) launch<256, false, true, 1>(ta, tb, em, p, grid, st);
+    else if (amn && !bmn) launch<256, true, false, 1>(ta, tb, em, p, grid, st);
+    else launch<256, true, true, 1>(ta, tb, em, p, grid, st);
   } else {
-    if (!amn && !bmn) launch<256, false, false>(ta, tb, em, p, grid, st);
-    else if (!amn && bmn) launch<256, false, true>(ta, tb, em, p, grid, st);
-    else if (amn && !bmn) launch<256, true, false>(ta, tb, em, p, grid, st);
-    else launch<256, true, true>(ta, tb, em, p, grid, st);
+    if (!amn && !bmn) launch<256, false, false, 2>(ta, tb, em, p, grid, st);
+    else if (!amn && bmn) launch<256, false, true, 2>(ta, tb, em, p, grid, st);
+    else if (amn && !bmn) launch<256, true, false, 2>(ta, tb, em, p, grid, st);
+    else launch<256, true, true, 2>(ta, tb, em, p, grid, st);
   }
   if (p.splits > 1) {
     ReduceArgs r{g.M, g.N, p.splits, p.epi, p.c_bf16, g.ldc, ws, g.C, g.bias, g.resid, g.aux};
