@@ -36,6 +36,7 @@ enum {
   PHOTON_ERR_IO = 9,            /* IoError */
   PHOTON_ERR_INTEGRITY = 10,    /* IntegrityError */
   PHOTON_ERR_ROUND_FAILURE = 11,/* RoundFailureError */
+  PHOTON_ERR_PARSE = 12,        /* ParseError */
   PHOTON_ERR_CUDA = 20,         /* device failure (no reference equivalent) */
   PHOTON_ERR_NCCL = 21
 };
@@ -120,11 +121,14 @@ typedef struct {
   double host_ms;             /* host batch staging (BatchStream x tau) + H2D issue */
   uint64_t h2d_bytes;         /* inputs copied host->device this round on this rank */
   uint64_t d2h_bytes;         /* results read back device->host this round */
+  double eval_ppl;            /* RoundRecord::eval_ppl: perplexity of theta_{t+1} on the
+                                 held-out set when the eval cadence fires, else NaN */
 } photon_round_record;
 
 typedef struct photon_ctx photon_ctx;       /* one GPU: device state of one client slot */
 typedef struct photon_plan photon_plan;     /* ShardPlan (data.h:33-62), host */
 typedef struct photon_runner photon_runner; /* FederationRunner (aggregator.h:70-102) */
+typedef struct photon_eval_set photon_eval_set; /* held-out batches (harness.cpp:440-472) */
 
 int photon_abi_version(void);
 const char* photon_status_name(int code);
@@ -268,6 +272,39 @@ uint64_t photon_runner_cursor(const photon_runner* r, uint64_t client);
 int photon_runner_restore(photon_runner* r, const double* theta, const double* velocity,
                           uint64_t next_round, const uint64_t* cursors, uint64_t n_cursors,
                           photon_err* err);
+
+
+/* ---- evaluation and checkpoints -------------------------- */
+/* build_eval_batches (harness.cpp:440-472): per style a held-out corpus from
+ * mix_seed(data_seed, "Eval"), eval_sequences / n_styles sequences each, batches
+ * of eval_batch rows (the last may be short).  Host only. */
+int photon_eval_set_create(const char* const* styles, uint64_t n_styles, uint64_t eval_sequences,
+                           uint64_t data_seed, uint64_t vocab, uint64_t seq_len,
+                           uint64_t eval_batch, photon_eval_set** out, photon_err* err);
+void photon_eval_set_destroy(photon_eval_set* s);
+uint64_t photon_eval_set_batches(const photon_eval_set* s);
+int photon_eval_set_batch(const photon_eval_set* s, uint64_t i, const int32_t** inputs,
+                          const int32_t** targets, uint64_t* batch_size, photon_err* err);
+/* RunnerOptions::eval_every + eval_fn (aggregator.cpp:207-212): theta_{t+1} is
+ * evaluated after round t when t % every == every - 1 or t is the last round;
+ * the eval batches stay resident in HBM (batch i on rank i % world). */
+int photon_runner_set_eval(photon_runner* r, const photon_eval_set* s, uint64_t eval_every,
+                           photon_err* err);
+/* eval_fn(theta) now (e.g. the initial perplexity); collective for world > 1 */
+int photon_runner_eval(photon_runner* r, double* ppl, photon_err* err);
+
+/* PHCK snapshot (checkpoint.h:17-45): byte-identical to the reference writer.
+ * Integrity failures -> PHOTON_ERR_INTEGRITY, layout mismatch -> PHOTON_ERR_SHAPE. */
+uint64_t photon_crc64(const void* data, uint64_t len); /* CRC-64/XZ, checkpoint.h:14-16 */
+int photon_checkpoint_write(const char* path, const photon_model_cfg* m, const double* params,
+                            uint64_t round, photon_err* err);
+int photon_checkpoint_read(const char* path, const photon_model_cfg* m, double* params,
+                           uint64_t* round, photon_err* err);
+/* Resume directory (harness.cpp:802-905): checkpoint.phck (theta, round = next
+ * round), velocity.phck (momentum server), state.json (next_round, cursors,
+ * initial_ppl, sync_events).  Collective for world > 1; rank 0 writes. */
+int photon_runner_save(photon_runner* r, const char* dir, photon_err* err);
+int photon_runner_resume(photon_runner* r, const char* dir, photon_err* err);
 
 #ifdef __cplusplus
 }

@@ -39,6 +39,7 @@ inline void check(int rc, const photon_err& e) {
     case PHOTON_ERR_IO: throw fedsim::IoError(e.msg);
     case PHOTON_ERR_INTEGRITY: throw fedsim::IntegrityError(e.msg);
     case PHOTON_ERR_ROUND_FAILURE: throw fedsim::RoundFailureError(e.msg);
+    case PHOTON_ERR_PARSE: throw fedsim::ParseError(e.msg);
     default: throw std::runtime_error(std::string("photon: ") + e.msg);
   }
 }

@@ -553,6 +553,20 @@ class Reference:
         return float(ppl[0]), float(ppl[1])
 
 
+    def write_checkpoint(self, cfg: ModelCfg, params, round_: int, path: str) -> None:
+        _check(self.lib.ref_write_checkpoint(cfg.as_array(), _p(np.ascontiguousarray(params,
+                                             np.float64), C.c_double), C.c_uint64(round_),
+                                             path.encode()), "ref_write_checkpoint")
+
+    def read_checkpoint(self, cfg: ModelCfg, path: str):
+        out = np.zeros(cfg.param_count())
+        rd = C.c_uint64()
+        _check(self.lib.ref_read_checkpoint(path.encode(), _p(out, C.c_double),
+                                            C.c_uint64(len(out)), C.byref(rd)),
+               "ref_read_checkpoint")
+        return out, int(rd.value)
+
+
 _ORACLE = None
 _REF = None
 

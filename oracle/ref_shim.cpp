@@ -14,6 +14,7 @@
 #include <thread>
 #include <vector>
 
+#include "fedsim/checkpoint.h"
 #include "fedsim/aggregator.h"
 #include "fedsim/baselines.h"
 #include "fedsim/client.h"
@@ -42,6 +43,9 @@ int code_of(const std::exception_ptr& e) {
   catch (const DivergenceError&) { return 8; }
   catch (const NumericError&) { return 7; }
   catch (const RoundFailureError&) { return 11; }
+  catch (const IntegrityError&) { return 10; }
+  catch (const IoError&) { return 9; }
+  catch (const ParseError&) { return 12; }
   catch (...) { return 99; }
 }
 
@@ -326,6 +330,20 @@ int ref_train_sample(const uint64_t* m, const double* t, uint64_t batch, uint64_
         for (auto& e : errs) if (e) std::rethrow_exception(e);
         *seconds_out = std::chrono::duration<double>(t1 - t0).count();
         if (loss_out) *loss_out = losses[0])
+}
+
+// checkpoint.cpp: the reference's PHCK writer / reader on a model-layout ParamVector
+int ref_write_checkpoint(const uint64_t* m, const double* params, uint64_t round,
+                         const char* path) {
+  GUARD(TransformerModel model(mcfg(m)); CheckpointMeta meta; meta.round = round;
+        write_checkpoint(path, to_pv(model, params), meta))
+}
+
+int ref_read_checkpoint(const char* path, double* params, uint64_t n, uint64_t* round) {
+  GUARD(Checkpoint ck = read_checkpoint(path);
+        if (ck.params.total_len() != n) throw ShapeError("size");
+        const std::vector<double> flat = ck.params.flatten();
+        std::copy(flat.begin(), flat.end(), params); *round = ck.meta.round)
 }
 
 }  // extern "C"

@@ -57,7 +57,7 @@ class photon_round_record(C.Structure):
     _fields_ = [("round", u64), ("n_sampled", u64), ("sampled_ids", u64 * 64),
                 ("mean_client_loss", dbl), ("min_client_loss", dbl), ("max_client_loss", dbl),
                 ("local_ms", dbl), ("aggregate_ms", dbl), ("round_ms", dbl), ("tokens", u64),
-                ("host_ms", dbl), ("h2d_bytes", u64), ("d2h_bytes", u64)]
+                ("host_ms", dbl), ("h2d_bytes", u64), ("d2h_bytes", u64), ("eval_ppl", dbl)]
 
 
 _SIGS = {
@@ -127,6 +127,21 @@ _SIGS = {
     "photon_runner_cursor": (u64, [C.c_void_p, u64]),
     "photon_runner_restore": (i32, [C.c_void_p, P(dbl), P(dbl), u64, P(u64), u64,
                                     P(photon_err)]),
+    "photon_eval_set_create": (i32, [P(C.c_char_p), u64, u64, u64, u64, u64, u64,
+                                     P(C.c_void_p), P(photon_err)]),
+    "photon_eval_set_destroy": (None, [C.c_void_p]),
+    "photon_eval_set_batches": (u64, [C.c_void_p]),
+    "photon_eval_set_batch": (i32, [C.c_void_p, u64, P(P(i32)), P(P(i32)), P(u64),
+                                    P(photon_err)]),
+    "photon_runner_set_eval": (i32, [C.c_void_p, C.c_void_p, u64, P(photon_err)]),
+    "photon_runner_eval": (i32, [C.c_void_p, P(dbl), P(photon_err)]),
+    "photon_crc64": (u64, [C.c_void_p, u64]),
+    "photon_checkpoint_write": (i32, [C.c_char_p, P(photon_model_cfg), P(dbl), u64,
+                                      P(photon_err)]),
+    "photon_checkpoint_read": (i32, [C.c_char_p, P(photon_model_cfg), P(dbl), P(u64),
+                                     P(photon_err)]),
+    "photon_runner_save": (i32, [C.c_void_p, C.c_char_p, P(photon_err)]),
+    "photon_runner_resume": (i32, [C.c_void_p, C.c_char_p, P(photon_err)]),
 }
 
 EXPORTED = sorted(_SIGS)

@@ -20,6 +20,9 @@ struct photon_ctx {
 struct photon_runner {
   std::unique_ptr<photon::Runner> r;
 };
+struct photon_eval_set {
+  photon::EvalSet s;
+};
 
 using namespace photon;
 
@@ -101,6 +104,7 @@ const char* photon_status_name(int code) {
     case PHOTON_ERR_IO: return "IoError";
     case PHOTON_ERR_INTEGRITY: return "IntegrityError";
     case PHOTON_ERR_ROUND_FAILURE: return "RoundFailureError";
+    case PHOTON_ERR_PARSE: return "ParseError";
     case PHOTON_ERR_CUDA: return "CudaError";
     case PHOTON_ERR_NCCL: return "NcclError";
   }
@@ -621,6 +625,78 @@ int photon_runner_restore(photon_runner* r, const double* theta, const double* v
                           uint64_t next_round, const uint64_t* cursors, uint64_t n,
                           photon_err* err) {
   return guarded(err, [&] { r->r->restore(theta, velocity, next_round, cursors, n); });
+}
+
+int photon_eval_set_create(const char* const* styles, uint64_t n_styles, uint64_t eval_sequences,
+                           uint64_t data_seed, uint64_t vocab, uint64_t seq_len,
+                           uint64_t eval_batch, photon_eval_set** out, photon_err* err) {
+  return guarded(err, [&] {
+    need(out != nullptr && (styles != nullptr || n_styles == 0), PHOTON_ERR_USAGE,
+         "eval_set_create: null argument");
+    std::vector<std::string> st;
+    for (uint64_t i = 0; i < n_styles; ++i) st.emplace_back(styles[i]);
+    auto es = std::make_unique<photon_eval_set>();
+    es->s = build_eval_set(st, eval_sequences, data_seed, vocab, seq_len, eval_batch);
+    *out = es.release();
+  });
+}
+
+void photon_eval_set_destroy(photon_eval_set* s) { delete s; }
+
+uint64_t photon_eval_set_batches(const photon_eval_set* s) { return s ? s->s.batch_sizes.size() : 0; }
+
+int photon_eval_set_batch(const photon_eval_set* s, uint64_t i, const int32_t** inputs,
+                          const int32_t** targets, uint64_t* batch_size, photon_err* err) {
+  return guarded(err, [&] {
+    need(s != nullptr && i < s->s.batch_sizes.size(), PHOTON_ERR_INDEX, "eval_set_batch: index");
+    uint64_t row = 0;
+    for (uint64_t b = 0; b < i; ++b) row += s->s.batch_sizes[b];
+    *inputs = s->s.inputs.data() + row * s->s.seq_len;
+    *targets = s->s.targets.data() + row * s->s.seq_len;
+    *batch_size = s->s.batch_sizes[i];
+  });
+}
+
+int photon_runner_set_eval(photon_runner* r, const photon_eval_set* s, uint64_t eval_every,
+                           photon_err* err) {
+  return guarded(err, [&] {
+    need(s != nullptr, PHOTON_ERR_USAGE, "runner_set_eval: null eval set");
+    r->r->set_eval(s->s, eval_every);
+  });
+}
+
+int photon_runner_eval(photon_runner* r, double* ppl, photon_err* err) {
+  return guarded(err, [&] {
+    *ppl = r->r->eval_theta();
+    r->r->initial_ppl = r->r->next_round == 0 ? *ppl : r->r->initial_ppl;
+  });
+}
+
+uint64_t photon_crc64(const void* data, uint64_t len) { return crc64(data, len); }
+
+int photon_checkpoint_write(const char* path, const photon_model_cfg* m, const double* params,
+                            uint64_t round, photon_err* err) {
+  return guarded(err, [&] {
+    validate_model(*m);
+    write_phck(path, *m, params, round);
+  });
+}
+
+int photon_checkpoint_read(const char* path, const photon_model_cfg* m, double* params,
+                           uint64_t* round, photon_err* err) {
+  return guarded(err, [&] {
+    validate_model(*m);
+    const uint64_t rd = read_phck(path, *m, params);
+    if (round) *round = rd;
+  });
+}
+
+int photon_runner_save(photon_runner* r, const char* dir, photon_err* err) {
+  return guarded(err, [&] { r->r->save(dir); });
+}
+
+int photon_runner_resume(photon_runner* r, const char* dir, photon_err* err) {
+  return guarded(err, [&] { r->r->resume(dir); });
 }
 
 }  // extern "C"

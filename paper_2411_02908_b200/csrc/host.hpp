@@ -42,6 +42,7 @@ constexpr uint64_t kPurposeShard = 0x53686172ULL;   // "Shar" data.cpp:149
 constexpr uint64_t kPurposeCorpus = 0x436f7270ULL;  // "Corp" data.cpp:59
 constexpr uint64_t kPurposeStream = 0x44617461ULL;  // "Data" data.cpp:202
 constexpr uint64_t kPurposeEpoch = 0x45706f63ULL;   // "Epoc" data.cpp:226
+constexpr uint64_t kPurposeEval = 0x4576616cULL;    // "Eval" harness.cpp:453
 
 // rng.h:37-84 -- mt19937_64 with the reference's pinned draw conversions.
 class Draws {
@@ -110,5 +111,28 @@ struct Plan {
 // client's epoch-shuffled block sequence.  Writes batch*S inputs/targets.
 void stream_rows(const Plan& p, uint64_t client, uint64_t seed, uint64_t cursor,
                  uint64_t batch, int32_t* inputs, int32_t* targets);
+
+// ---- evaluation set / checkpoints (checkpoint.cpp) ---------------------------------
+struct EvalSet {  // build_eval_batches (harness.cpp:440-472)
+  uint64_t seq_len = 0;
+  std::vector<int32_t> inputs, targets;  // concatenated rows
+  std::vector<uint64_t> batch_sizes;
+};
+EvalSet build_eval_set(const std::vector<std::string>& styles, uint64_t eval_sequences,
+                       uint64_t data_seed, uint64_t vocab, uint64_t seq_len, uint64_t eval_batch);
+
+uint64_t crc64(const void* data, size_t len);  // CRC-64/XZ (checkpoint.h:14-16)
+void write_phck(const std::string& path, const photon_model_cfg& m, const double* params,
+                uint64_t round);
+uint64_t read_phck(const std::string& path, const photon_model_cfg& m, double* params);
+
+struct ResumeState {  // PersistedState (harness.cpp:527-535), federated fields
+  uint64_t next_round = 0;
+  double initial_ppl = 0.0;
+  uint64_t sync_events = 0;
+  std::vector<uint64_t> cursors;
+};
+void write_state_json(const std::string& path, const ResumeState& st);
+ResumeState read_state_json(const std::string& path);
 
 }  // namespace photon

@@ -17,6 +17,7 @@
 #include <limits>
 #include <chrono>
 #include <cstring>
+#include <fstream>
 
 #include "kernels.cuh"
 #include "nccl_api.hpp"
@@ -229,7 +230,7 @@ void Runner::run_round(photon_round_record* rec) {
     PH_NCCL(nccl().AllGather(d_theta.ptr + off, d_theta.ptr, shard, ncclFloat, comm, st));
   PH_CUDA(cudaEventRecord(ev_c, st));
   PH_CUDA(cudaEventSynchronize(ev_c));
-  (void)host_ms;
+  if (K >= 2) ++sync_events;
 
   if (rec) {
     std::memset(rec, 0, sizeof(*rec));
@@ -259,8 +260,115 @@ void Runner::run_round(photon_round_record* rec) {
     for (size_t j = 0; j < mine.size(); ++j)
       rec->h2d_bytes += (uint64_t)tau * ((uint64_t)B * S * 3 + V + 1) * 4;
     rec->d2h_bytes = (uint64_t)mine.size() * (tau * sizeof(double) + sizeof(int));
+    rec->eval_ppl = std::numeric_limits<double>::quiet_NaN();
   }
   next_round = round + 1;
+  // aggregator.cpp:207-212: after the boundary, outside the timed round
+  if (eval_every > 0 && (round % eval_every == eval_every - 1 || next_round == fed.rounds)) {
+    const double ppl = eval_theta();
+    if (rec) rec->eval_ppl = ppl;
+  }
+}
+
+void Runner::set_eval(const EvalSet& es, uint64_t every) {
+  PH_CUDA(cudaSetDevice(ctx->device));
+  const int S = (int)es.seq_len, V = (int)train.model.vocab_size;
+  if (es.seq_len != train.model.seq_len)
+    throw Error(PHOTON_ERR_SHAPE, "eval set: seq_len does not match the model");
+  eval_every = every;
+  eval_n = es.batch_sizes.size();
+  eval_dev.clear();
+  eval_ids.clear();
+  eval_valid.assign(eval_n, 0);
+  uint64_t row = 0;
+  for (uint64_t b = 0; b < eval_n; ++b) {
+    const uint64_t B = es.batch_sizes[b];
+    if (B > ctx->max_batch)
+      throw Error(PHOTON_ERR_CONFIG, "eval set: batch exceeds the context's max_batch");
+    const int32_t* in = es.inputs.data() + row * S;
+    const int32_t* tg = es.targets.data() + row * S;
+    for (uint64_t i = 0; i < B * S; ++i) eval_valid[b] += tg[i] >= 0;
+    if ((int)(b % world) == rank) {
+      RoundBatches rb;
+      rb.prepare(1, (int)B, S, V);
+      std::memcpy(rb.tokens.ptr, in, B * S * 4);
+      std::memcpy(rb.targets.ptr, tg, B * S * 4);
+      rb.finalize(V);
+      eval_dev.emplace_back();
+      eval_dev.back().upload(rb, V, ctx->stream);
+      PH_CUDA(cudaStreamSynchronize(ctx->stream));  // rb's pinned buffers die here
+      eval_ids.push_back(b);
+    }
+    row += B;
+  }
+  d_eval.reserve(std::max<uint64_t>(eval_n, 1));
+  h_eval.reserve(std::max<uint64_t>(eval_n, 1));
+}
+
+// model.cpp:176-192: exp(sum_b loss_b * valid_b / sum_b valid_b), batches in order
+double Runner::eval_theta() {
+  if (eval_n == 0) throw Error(PHOTON_ERR_USAGE, "runner: no evaluation set");
+  PH_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  Engine& e = *ctx->eng;
+  PH_CUDA(cudaMemcpyAsync(e.master, d_theta.ptr, P * 4, cudaMemcpyDeviceToDevice, st));
+  e.refresh_shadow();
+  PH_CUDA(cudaMemsetAsync(d_eval.ptr, 0, eval_n * sizeof(double), st));
+  for (size_t j = 0; j < eval_dev.size(); ++j) {
+    const DeviceBatches& db = eval_dev[j];
+    StepBatch sb{db.tokens.ptr, db.targets.ptr, db.csr_off.ptr, db.csr_rows.ptr, db.B, db.S,
+                 db.inv_count[0]};
+    e.forward_backward(sb, d_eval.ptr + eval_ids[j], false);
+  }
+  // every batch loss sits on exactly one rank: the sum reassembles them exactly
+  if (world > 1) PH_NCCL(nccl().AllReduce(d_eval.ptr, d_eval.ptr, eval_n, ncclDouble, ncclSum, comm, st));
+  PH_CUDA(cudaMemcpyAsync(h_eval.ptr, d_eval.ptr, eval_n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  PH_CUDA(cudaStreamSynchronize(st));
+  double nll = 0.0;
+  uint64_t tokens = 0;
+  for (uint64_t b = 0; b < eval_n; ++b) {
+    nll += h_eval.ptr[b] * (double)eval_valid[b];
+    tokens += eval_valid[b];
+  }
+  if (tokens == 0) throw Error(PHOTON_ERR_USAGE, "eval_perplexity: no target tokens");
+  return std::exp(nll / (double)tokens);
+}
+
+// harness.cpp:845-905: checkpoint.phck (theta, meta.round = next round), velocity.phck
+// for a momentum server, state.json
+void Runner::save(const std::string& dir) {
+  std::vector<double> th(P), vel;
+  theta_f64(th.data());
+  if (server.kind == 1) {
+    vel.resize(P);
+    velocity_f64(vel.data());  // collective for world > 1
+  }
+  if (rank != 0) return;
+  write_phck(dir + "/checkpoint.phck", train.model, th.data(), next_round);
+  if (server.kind == 1) write_phck(dir + "/velocity.phck", train.model, vel.data(), next_round);
+  ResumeState s;
+  s.next_round = next_round;
+  s.initial_ppl = initial_ppl;
+  s.sync_events = sync_events;
+  s.cursors = cursors;
+  write_state_json(dir + "/state.json", s);
+}
+
+void Runner::resume(const std::string& dir) {
+  const ResumeState s = read_state_json(dir + "/state.json");
+  if (s.cursors.size() != fed.population) throw Error(PHOTON_ERR_INTEGRITY, "resume: population changed");
+  std::vector<double> th(P), vel(P, 0.0);
+  const uint64_t r = read_phck(dir + "/checkpoint.phck", train.model, th.data());
+  if (r != s.next_round)
+    throw Error(PHOTON_ERR_INTEGRITY, "resume: checkpoint round disagrees with state.json");
+  if (server.kind == 1 && s.next_round > 0) {
+    std::ifstream probe(dir + "/velocity.phck");
+    if (!probe) throw Error(PHOTON_ERR_INTEGRITY, "resume: velocity.phck missing");
+    read_phck(dir + "/velocity.phck", train.model, vel.data());
+  }
+  restore(th.data(), vel.data(), s.next_round, s.cursors.data(), s.cursors.size());
+  initial_ppl = s.initial_ppl;
+  sync_events = s.sync_events;
 }
 
 void Runner::theta_f64(double* out) {

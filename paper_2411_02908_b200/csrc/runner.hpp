@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <set>
+#include <string>
 #include <utility>
 #include <vector>
 
@@ -41,6 +42,17 @@ struct Runner {
   PinnedBuf<int> h_flag;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;
 
+  // per-round evaluation (RunnerOptions::eval_every / eval_fn, aggregator.cpp:207-212):
+  // batch i of the eval set lives on rank i % world, resident in HBM
+  uint64_t eval_every = 0, eval_n = 0;
+  std::vector<DeviceBatches> eval_dev;
+  std::vector<uint64_t> eval_ids, eval_valid;
+  DevBuf<double> d_eval;
+  PinnedBuf<double> h_eval;
+  // harness bookkeeping persisted in state.json (harness.cpp:527-535)
+  double initial_ppl = 0.0;
+  uint64_t sync_events = 0;
+
   Runner(Ctx* c, const photon_fed_cfg& f, const photon_train_cfg& t, const photon_server_cfg& s,
          const Plan* p, const double* theta0, int rank, int world, const uint8_t* nccl_id);
   ~Runner();
@@ -50,6 +62,11 @@ struct Runner {
   void velocity_f64(double* out);
   void restore(const double* theta, const double* velocity, uint64_t next_round,
                const uint64_t* cursors, uint64_t n);
+  void set_eval(const EvalSet& es, uint64_t every);
+  double eval_theta();  // perplexity of the replicated theta (collective for world > 1)
+  // checkpoint.phck + velocity.phck + state.json under dir (collective; rank 0 writes)
+  void save(const std::string& dir);
+  void resume(const std::string& dir);
 };
 
 void validate_server(const photon_server_cfg& s);

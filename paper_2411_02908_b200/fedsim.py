@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import builtins
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -73,13 +74,17 @@ class RoundFailureError(FedsimError):
     pass
 
 
+class ParseError(FedsimError):
+    pass
+
+
 class DeviceError(FedsimError):
     """CUDA / NCCL failure (no reference equivalent)."""
 
 
 _CODE = {1: ConfigError, 2: CapacityError, 3: ShapeError, 4: IndexError, 5: UsageError,
          6: LookupError, 7: NumericError, 9: IoError, 10: IntegrityError, 11: RoundFailureError,
-         20: DeviceError, 21: DeviceError}
+         12: ParseError, 20: DeviceError, 21: DeviceError}
 
 
 def _raise(rc: int, err: A.photon_err):
@@ -274,6 +279,7 @@ class RoundRecord:
     host_ms: float = 0.0
     h2d_bytes: int = 0
     d2h_bytes: int = 0
+    eval_ppl: float = float("nan")  # RoundRecord::eval_ppl (NaN when the cadence skips)
 
 
 # ---------------------------------------------------------------------------
@@ -695,9 +701,12 @@ class FederationRunner:
     def __init__(self, fed: FederationConfig, local: LocalTrainConfig, server: ServerOptConfig,
                  plan: ShardPlan, theta0: np.ndarray, device: int = 0, precision: str = "f32",
                  rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
-                 dropouts: Sequence[Tuple[int, int]] = ()):
+                 dropouts: Sequence[Tuple[int, int]] = (), eval_set: "Optional[EvalSet]" = None,
+                 eval_every: int = 0):
         self.fed, self.local, self.server, self.plan = fed, local, server, plan
-        self.ctx = context(local.model, device, precision, local.batch_size)
+        # the context's activations must also hold the largest eval batch
+        max_batch = max([local.batch_size] + ([eval_set.max_batch()] if eval_set else []))
+        self.ctx = context(local.model, device, precision, max_batch)
         theta0 = _f64(theta0)
         self._P = len(theta0)
         h = C.c_void_p()
@@ -708,6 +717,9 @@ class FederationRunner:
         self._h = h
         for r, c in dropouts:
             A.lib().photon_runner_add_dropout(h, r, c)
+        self._eval_set = eval_set  # keeps the host set alive alongside the runner
+        if eval_set is not None:
+            _call(A.lib().photon_runner_set_eval, h, eval_set._h, eval_every)
 
     def __del__(self):
         if getattr(self, "_h", None) and self._h.value:
@@ -721,7 +733,7 @@ class FederationRunner:
         return RoundRecord(int(rec.round), [int(x) for x in rec.sampled_ids[:min(k, 64)]],
                            rec.mean_client_loss, rec.min_client_loss, rec.max_client_loss,
                            rec.local_ms, rec.aggregate_ms, rec.round_ms, int(rec.tokens),
-                           rec.host_ms, int(rec.h2d_bytes), int(rec.d2h_bytes))
+                           rec.host_ms, int(rec.h2d_bytes), int(rec.d2h_bytes), rec.eval_ppl)
 
     def done(self) -> bool:
         return self.next_round() >= self.fed.rounds
@@ -749,3 +761,71 @@ class FederationRunner:
         cur = np.ascontiguousarray(cursors, np.uint64)
         _call(A.lib().photon_runner_restore, self._h, _dp(_f64(theta)), _dp(_f64(velocity)),
               next_round, cur.ctypes.data_as(C.POINTER(C.c_uint64)), len(cur))
+
+    def evaluate(self) -> float:
+        """eval_fn(theta) (harness.cpp:797-799) on the runner's eval set."""
+        ppl = C.c_double()
+        _call(A.lib().photon_runner_eval, self._h, C.byref(ppl))
+        return ppl.value
+
+    def save(self, directory: str) -> None:
+        """checkpoint.phck + velocity.phck + state.json (harness.cpp:802-905)."""
+        _call(A.lib().photon_runner_save, self._h, os.fsencode(directory))
+
+    def resume(self, directory: str) -> None:
+        _call(A.lib().photon_runner_resume, self._h, os.fsencode(directory))
+
+
+class EvalSet:
+    """build_eval_batches (harness.cpp:440-472): held-out batches from
+    mix_seed(data_seed, "Eval"); host memory, uploaded once by the runner."""
+
+    def __init__(self, styles: Sequence[str], eval_sequences: int, data_seed: int,
+                 model: ModelConfig, eval_batch: int):
+        arr = (C.c_char_p * len(styles))(*[s.encode() for s in styles])
+        h = C.c_void_p()
+        _call(A.lib().photon_eval_set_create, arr, len(styles), eval_sequences, data_seed,
+              model.vocab_size, model.seq_len, eval_batch, C.byref(h))
+        self._h, self.seq_len = h, model.seq_len
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value:
+            A.lib().photon_eval_set_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __len__(self) -> int:
+        return int(A.lib().photon_eval_set_batches(self._h))
+
+    def max_batch(self) -> int:
+        return max((b.batch_size for b in self.batches()), default=0)
+
+    def batches(self) -> List["Batch"]:
+        out = []
+        for i in range(len(self)):
+            pi, pt, b = C.POINTER(C.c_int32)(), C.POINTER(C.c_int32)(), C.c_uint64()
+            _call(A.lib().photon_eval_set_batch, self._h, i, C.byref(pi), C.byref(pt), C.byref(b))
+            n = int(b.value) * self.seq_len
+            out.append(Batch(np.ctypeslib.as_array(pi, (n,)).copy(),
+                             np.ctypeslib.as_array(pt, (n,)).copy(), int(b.value), self.seq_len))
+        return out
+
+
+def crc64(data: bytes) -> int:
+    """CRC-64/XZ (checkpoint.h:14-16)."""
+    buf = C.create_string_buffer(bytes(data), len(data))
+    return int(A.lib().photon_crc64(buf, len(data)))
+
+
+def write_checkpoint(path: str, model: ModelConfig, params: np.ndarray, round: int) -> None:  # noqa: A002
+    """PHCK writer (checkpoint.h:27-41), byte-identical to the reference's."""
+    m = model.c()
+    _call(A.lib().photon_checkpoint_write, os.fsencode(path), C.byref(m), _dp(_f64(params)), round)
+
+
+def read_checkpoint(path: str, model: ModelConfig) -> Tuple[np.ndarray, int]:
+    """PHCK reader (checkpoint.h:42): (params, round); IntegrityError / ShapeError."""
+    m = model.c()
+    out = np.zeros(model.param_count())
+    rd = C.c_uint64()
+    _call(A.lib().photon_checkpoint_read, os.fsencode(path), C.byref(m), _dp(out), C.byref(rd))
+    return out, int(rd.value)

@@ -2,7 +2,8 @@
 count.  Launched by this test as `torchrun --nproc-per-node 2` when >= 2 GPUs
 are visible (gpurun --gpus 2); each rank's theta after R rounds must equal the
 single-GPU runner's theta bit for bit (same kernels, same ascending-order
-aggregation arithmetic, f32 mode)."""
+aggregation arithmetic, f32 mode), and so must the per-round evaluation (eval
+batches sharded over ranks) and the saved resume directory."""
 import os
 import subprocess
 import sys
@@ -33,4 +34,8 @@ def test_world_size_invariance(tmp_path, server):
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     a, b = np.load(out1), np.load(outn)
-    assert a.tobytes() == b.tobytes()
+    assert a.tobytes() == b.tobytes()  # theta, velocity and the per-round eval ppls
+    assert np.all(np.isfinite(a[-3:]))
+    for f in ("checkpoint.phck", "state.json") + (("velocity.phck",) if server == "diloco" else ()):
+        assert open(str(out1) + ".ckpt/" + f, "rb").read() == open(str(outn) + ".ckpt/" + f,
+                                                                     "rb").read()

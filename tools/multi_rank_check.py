@@ -1,4 +1,6 @@
-"""Run 3 rounds of a K=4 federation at world = WORLD_SIZE; rank 0 saves theta."""
+"""Run 3 rounds of a K=4 federation at world = WORLD_SIZE with per-round
+evaluation; rank 0 saves theta | velocity | eval ppls (npy) and the runner's
+resume directory (<out>.ckpt/: checkpoint.phck, velocity.phck, state.json)."""
 import os
 import sys
 
@@ -27,15 +29,21 @@ theta0 = F.TransformerModel(cfg).init_params(1)
 local_cfg = F.LocalTrainConfig(model=cfg, schedule=F.LrSchedule(2e-3, 16, 160, 0.1),
                                local_steps=4, batch_size=4)
 srv = F.ServerOptConfig() if server == "fedavg" else F.diloco_server_opt()
+es = F.EvalSet(["web"], 40, 7, cfg, 8)  # 5 batches: uneven over 2 or 4 ranks
 runner = F.FederationRunner(F.FederationConfig(6, 4, 3, F.Topology.kRingAllReduce, 42), local_cfg,
                             srv, plan, theta0, device=local, precision="f32", rank=rank,
-                            world=world, nccl_id=nccl_id)
-for _ in range(3):
-    runner.run_round()
+                            world=world, nccl_id=nccl_id, eval_set=es, eval_every=1)
+ppls = [runner.run_round().eval_ppl for _ in range(3)]
 theta = runner.theta()
 vel = runner.velocity()
+ckpt = out + ".ckpt"
 if rank == 0:
-    np.save(out, np.concatenate([theta, vel]))
+    os.makedirs(ckpt, exist_ok=True)
+if world > 1:
+    dist.barrier()
+runner.save(ckpt)
+if rank == 0:
+    np.save(out, np.concatenate([theta, vel, np.array(ppls)]))
 if world > 1:
     dist.barrier()
     dist.destroy_process_group()
