@@ -81,6 +81,9 @@ Runner::Runner(Ctx* c, const photon_fed_cfg& f, const photon_train_cfg& t,
   PH_CUDA(cudaEventCreate(&ev_a));
   PH_CUDA(cudaEventCreate(&ev_b));
   PH_CUDA(cudaEventCreate(&ev_c));
+  PH_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+  PH_CUDA(cudaEventCreateWithFlags(&copied[0], cudaEventDisableTiming));
+  PH_CUDA(cudaEventCreateWithFlags(&copied[1], cudaEventDisableTiming));
   if (ws > 1) {
     if (!nccl_id) throw Error(PHOTON_ERR_USAGE, "runner: world > 1 needs an NCCL unique id");
     ncclUniqueId id;
@@ -95,6 +98,43 @@ Runner::~Runner() {
   if (ev_a) cudaEventDestroy(ev_a);
   if (ev_b) cudaEventDestroy(ev_b);
   if (ev_c) cudaEventDestroy(ev_c);
+  if (copy_stream) cudaStreamSynchronize(copy_stream);
+  for (cudaEvent_t e : copied)
+    if (e) cudaEventDestroy(e);
+  if (copy_stream) cudaStreamDestroy(copy_stream);
+}
+
+// Stage round `round`'s batches for this rank's slots into set `set`: host
+// BatchStream port into pinned buffers, then async H2D on copy_stream.  `cur`
+// are the client cursors at the start of that round.  Returns host ms.
+double Runner::stage(uint64_t round, int set, const std::vector<uint64_t>& cur) {
+  const auto t0 = std::chrono::steady_clock::now();
+  // the set's previous H2D (if any) must have read its pinned buffers
+  PH_CUDA(cudaEventSynchronize(copied[set]));
+  const auto sampled = sample_clients(fed.population, fed.clients_per_round, fed.seed, round);
+  const int K = (int)sampled.size();
+  const int tau = (int)train.local_steps, B = (int)train.batch_size, S = (int)plan->seq_len;
+  const int V = (int)train.model.vocab_size;
+  std::vector<int> mine;
+  for (int si = 0; si < K; ++si)
+    if (si % world == rank) mine.push_back(si);
+  if (host_batches[set].size() < mine.size()) {
+    host_batches[set].resize(mine.size());
+    dev_batches[set].resize(mine.size());
+  }
+  for (size_t j = 0; j < mine.size(); ++j) {
+    const uint64_t client = sampled[mine[j]];
+    RoundBatches& hb = host_batches[set][j];
+    hb.prepare(tau, B, S, V);
+    const uint64_t seed = derive(fed.seed, kPurposeStream, client);
+    for (int i = 0; i < tau; ++i)
+      stream_rows(*plan, client, seed, cur[client] + (uint64_t)i * B, B,
+                  hb.tokens.ptr + (size_t)i * B * S, hb.targets.ptr + (size_t)i * B * S);
+    hb.finalize(V);
+    dev_batches[set][j].upload(hb, V, copy_stream);
+  }
+  PH_CUDA(cudaEventRecord(copied[set], copy_stream));
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
 void Runner::run_round(photon_round_record* rec) {
@@ -116,25 +156,11 @@ void Runner::run_round(photon_round_record* rec) {
     PH_CUDA(cudaMemsetAsync(d_models.ptr, 0, d_models.n * 4, st));
   }
 
-  // ---- host: stage every local client's tau batches (BatchStream x tau) and H2D
-  const auto t_host0 = std::chrono::steady_clock::now();
-  if (host_batches.size() < mine.size()) {
-    host_batches.resize(mine.size());
-    dev_batches.resize(mine.size());
-  }
-  for (size_t j = 0; j < mine.size(); ++j) {
-    const uint64_t client = sampled[mine[j]];
-    RoundBatches& hb = host_batches[j];
-    hb.prepare(tau, B, S, V);
-    const uint64_t seed = derive(fed.seed, kPurposeStream, client);
-    for (int i = 0; i < tau; ++i)
-      stream_rows(*plan, client, seed, cursors[client] + (uint64_t)i * B, B,
-                  hb.tokens.ptr + (size_t)i * B * S, hb.targets.ptr + (size_t)i * B * S);
-    hb.finalize(V);
-    dev_batches[j].upload(hb, V, st);
-  }
-  const double host_ms =
-      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
+  // ---- this round's batches: already staged by the previous round, or now
+  double host_ms = 0.0;
+  if (staged_round != round) host_ms = stage(round, buf, cursors);
+  PH_CUDA(cudaStreamWaitEvent(st, copied[buf], 0));
+  std::vector<DeviceBatches>& dev = dev_batches[buf];
 
   // ---- device: the local phase, inputs resident in HBM
   const size_t nm = std::max<size_t>(mine.size(), 1);
@@ -144,9 +170,18 @@ void Runner::run_round(photon_round_record* rec) {
   h_flag.reserve(nm);
   PH_CUDA(cudaEventRecord(ev_a, st));
   for (size_t j = 0; j < mine.size(); ++j)
-    ctx->launch_local_round(train, dev_batches[j], d_theta.ptr, d_models.ptr + j * Ppad, step_base,
+    ctx->launch_local_round(train, dev[j], d_theta.ptr, d_models.ptr + j * Ppad, step_base,
                             d_loss.ptr + j * tau, d_flag.ptr + j);
   PH_CUDA(cudaEventRecord(ev_b, st));
+  // ---- prefetch round t+1 into the other set while the GPU trains round t
+  // (its cursors are known: every sampled client advances, dropped or not)
+  bool prefetched = false;
+  if (round + 1 < fed.rounds) {
+    std::vector<uint64_t> next_cur = cursors;
+    for (int si = 0; si < K; ++si) next_cur[sampled[si]] += (uint64_t)tau * B;
+    stage(round + 1, buf ^ 1, next_cur);
+    prefetched = true;
+  }
   if (!mine.empty()) {
     PH_CUDA(cudaMemcpyAsync(h_loss.ptr, d_loss.ptr, mine.size() * tau * sizeof(double),
                             cudaMemcpyDeviceToHost, st));
@@ -263,6 +298,8 @@ void Runner::run_round(photon_round_record* rec) {
     rec->eval_ppl = std::numeric_limits<double>::quiet_NaN();
   }
   next_round = round + 1;
+  buf ^= 1;  // the prefetched set holds round t+1
+  staged_round = prefetched ? round + 1 : ~0ULL;
   // aggregator.cpp:207-212: after the boundary, outside the timed round
   if (eval_every > 0 && (round % eval_every == eval_every - 1 || next_round == fed.rounds)) {
     const double ppl = eval_theta();
@@ -407,6 +444,7 @@ void Runner::restore(const double* theta, const double* velocity, uint64_t nr,
   PH_CUDA(cudaStreamSynchronize(ctx->stream));
   next_round = nr;
   cursors.assign(cur, cur + n);
+  staged_round = ~0ULL;  // any prefetched batches were for the old cursors
 }
 
 }  // namespace photon

@@ -34,8 +34,16 @@ struct Runner {
   DevBuf<const float*> d_model_ptrs;
   DevBuf<double> d_stats;    // [2K] loss stats / error exchange
   PinnedBuf<double> h_stats;
-  std::vector<RoundBatches> host_batches;   // per local slot (pinned)
-  std::vector<DeviceBatches> dev_batches;   // per local slot
+  // token pipeline: two host/device batch sets alternate by
+  // round; round t+1's tau batches are staged and copied (copy_stream) while the
+  // GPU trains round t
+  std::vector<RoundBatches> host_batches[2];  // per local slot (pinned)
+  std::vector<DeviceBatches> dev_batches[2];  // per local slot
+  int buf = 0;                                // set holding the next round to run
+  uint64_t staged_round = ~0ULL;              // round whose batches sit in set `buf`
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t copied[2] = {nullptr, nullptr};
+  double stage(uint64_t round, int set, const std::vector<uint64_t>& cur);
   DevBuf<double> d_loss;
   DevBuf<int> d_flag;
   PinnedBuf<double> h_loss;

@@ -98,3 +98,18 @@ def test_resume_errors(F, oracle, tmp_path):
     runner.save(str(tmp_path))
     with pytest.raises(F.IntegrityError):  # population changed
         F.FederationRunner(other, local, srv, plan4, theta0).resume(str(tmp_path))
+
+
+def test_token_pipeline_prefetch(F, oracle):
+    """round t+1's batches are staged while round t trains, so
+    only round 0 (and a round after restore) stages on the critical path; the
+    token streams are unchanged (the oracle comparisons of test_gpu_parity.py
+    run multi-round on prefetched batches)."""
+    mc, theta0, plan, local, fed, srv, es = _setup(F, oracle, rounds=4)
+    runner = F.FederationRunner(fed, local, srv, plan, theta0)
+    recs = [runner.run_round() for _ in range(2)]
+    assert recs[0].host_ms > 0 and recs[1].host_ms == 0
+    runner.restore(runner.theta(), runner.velocity(), 2,
+                   [runner.client_cursor(c) for c in range(3)])
+    assert runner.run_round().host_ms > 0  # the restore dropped the prefetch
+    assert runner.run_round().host_ms == 0
