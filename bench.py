@@ -32,6 +32,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 MODEL_125M = (12, 768, 12, 4, 50368, 2048)
+# SURVEY 8(d) configs 2-4 (Photon 125M / 1.3B / 7B, reference architecture)
+MODELS = {"125m": (MODEL_125M, "Photon-125M", "164.04M"),
+          "1.3b": ((24, 2048, 16, 4, 50368, 2048), "Photon-1.3B", "1,419.15M"),
+          "7b": ((32, 4096, 32, 4, 50368, 2048), "Photon-7B", "6,865.22M")}
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 METRIC = "tokens/s/round at 1-8 B200 (125M); FedAvg aggregate GB/s vs roofline"
 
@@ -216,8 +220,9 @@ def run_reference_arm(args):
 
 
 def _config(args):
-    L, d, H, e, V, S = MODEL_125M
-    return {"workload": "Photon-125M federated round (reference architecture, 164.04M params)",
+    shape, name, params = MODELS[args.model]
+    L, d, H, e, V, S = shape
+    return {"workload": f"{name} federated round (reference architecture, {params} params)",
             "model": f"L{L} d{d} H{H} e{e} V{V} S{S}", "clients": args.gpus,
             "clients_per_gpu": 1, "local_steps": args.tau, "batch": args.batch, "seq_len": S,
             "global_batch": args.gpus * args.batch, "server_opt": "nesterov eta=0.1 mu=0.9",
@@ -264,8 +269,8 @@ def run_ours(args):
     from paper_2411_02908_b200 import fedsim as F
 
     hbm, bf16_burst, bf16_sus, peak_src = _peaks()
-    L, d, H, e, V, S = MODEL_125M
-    model = F.ModelConfig(*MODEL_125M)
+    L, d, H, e, V, S = MODELS[args.model][0]
+    model = F.ModelConfig(L, d, H, e, V, S)
     K = world  # weak scaling: one client per GPU
     rounds = args.warmup + args.steps + 1
     tau, B = args.tau, args.batch
@@ -355,7 +360,11 @@ def run_ours(args):
         line["gpu_launches"] = int(prof["launches"]) * args.steps
     if agg:
         line["aggregation"] = agg
-    if world == 1 and not args.no_cpu:
+    if world == 1 and not args.no_cpu and args.model != "125m":
+        # the f64 reference state of 1.3B / 7B exceeds host RAM
+        line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "n/a",
+                                "sample": f"reference CPU path not runnable at {args.model}"}
+    elif world == 1 and not args.no_cpu:
         try:
             v, cores, kind, sample = cpu_sample(args.cpu_seq)
             line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": kind,
@@ -380,6 +389,8 @@ def main(argv=None):
     ap.add_argument("--no-agg", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seq", type=int, default=32)
+    ap.add_argument("--model", default="125m", choices=sorted(MODELS),
+                    help="125m is the contracted workload; 1.3b / 7b are SURVEY 8(d) configs 3-4")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
