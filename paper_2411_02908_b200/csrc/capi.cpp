@@ -72,9 +72,7 @@ void stage_single(Ctx& c, RoundBatches& rb, const int32_t* inputs, const int32_t
 
 void load_params(Ctx& c, const double* params) {
   Engine& e = *c.eng;
-  c.d_f64a.reserve(e.P);
-  PH_CUDA(cudaMemcpyAsync(c.d_f64a.ptr, params, e.P * 8, cudaMemcpyHostToDevice, c.stream));
-  k::f64_to_f32(c.d_f64a.ptr, e.master, e.P, c.stream);
+  c.h2d_f64_to_f32(params, e.master, e.P);
   e.refresh_shadow();
 }
 
@@ -213,11 +211,7 @@ int photon_forward_backward(photon_ctx* ctx, const double* params, const int32_t
     e.forward_backward(sb, c.d_losses.ptr, grads != nullptr);
     c.end_timing();
     PH_CUDA(cudaMemcpy(loss, c.d_losses.ptr, 8, cudaMemcpyDeviceToHost));
-    if (grads) {
-      k::f32_to_f64(e.grads, c.d_f64a.ptr, e.P, c.stream);
-      PH_CUDA(cudaMemcpyAsync(grads, c.d_f64a.ptr, e.P * 8, cudaMemcpyDeviceToHost, c.stream));
-      PH_CUDA(cudaStreamSynchronize(c.stream));
-    }
+    if (grads) c.d2h_f32_to_f64(e.grads, grads, e.P);
   });
 }
 
@@ -277,10 +271,8 @@ int photon_client_round(photon_ctx* ctx, const photon_train_cfg* cfg, const doub
     rb.finalize((int)c.cfg.vocab_size);
     c.begin_timing();
     c.upload(rb);
-    c.d_f64a.reserve(e.P);
     c.d_f32b.reserve(e.P);
-    PH_CUDA(cudaMemcpyAsync(c.d_f64a.ptr, theta_in, e.P * 8, cudaMemcpyHostToDevice, c.stream));
-    k::f64_to_f32(c.d_f64a.ptr, c.d_f32b.ptr, e.P, c.stream);
+    c.h2d_f64_to_f32(theta_in, c.d_f32b.ptr, e.P);
     LocalResult r = c.local_round(*cfg, c.d_f32b.ptr, e.master, step_base);
     if (r.error) {
       Error ex(r.error, r.error == PHOTON_ERR_DIVERGENCE
@@ -292,8 +284,7 @@ int photon_client_round(photon_ctx* ctx, const photon_train_cfg* cfg, const doub
       ex.step = r.error_step;
       throw ex;
     }
-    k::f32_to_f64(e.master, c.d_f64a.ptr, e.P, c.stream);
-    PH_CUDA(cudaMemcpyAsync(theta_out, c.d_f64a.ptr, e.P * 8, cudaMemcpyDeviceToHost, c.stream));
+    c.d2h_f32_to_f64(e.master, theta_out, e.P);
     c.end_timing();
     if (metrics)
       for (uint64_t i = 0; i < tau; ++i)

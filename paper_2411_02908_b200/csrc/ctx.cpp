@@ -1,6 +1,8 @@
 // ctx.cpp -- device context and the device-resident client update.
 #include "ctx.hpp"
 
+#include <algorithm>
+
 #include <cmath>
 
 #include "kernels.cuh"
@@ -142,6 +144,27 @@ void Ctx::launch_local_round(const photon_train_cfg& t, const DeviceBatches& db,
   if (d_theta_out != e.master)
     PH_CUDA(cudaMemcpyAsync(d_theta_out, e.master, P * 4, cudaMemcpyDeviceToDevice, stream));
   PH_CUDA(cudaMemcpyAsync(d_flag, e.bad_step, sizeof(int), cudaMemcpyDeviceToDevice, stream));
+}
+
+constexpr uint64_t kStageChunk = 1ull << 24;  // 16 M values = 128 MB of f64 staging
+
+void Ctx::h2d_f64_to_f32(const double* host, float* dev, uint64_t n) {
+  d_f64a.reserve(std::min(n, kStageChunk));
+  for (uint64_t o = 0; o < n; o += kStageChunk) {
+    const uint64_t c = std::min(kStageChunk, n - o);
+    PH_CUDA(cudaMemcpyAsync(d_f64a.ptr, host + o, c * 8, cudaMemcpyHostToDevice, stream));
+    k::f64_to_f32(d_f64a.ptr, dev + o, c, stream);
+  }
+}
+
+void Ctx::d2h_f32_to_f64(const float* dev, double* host, uint64_t n) {
+  d_f64a.reserve(std::min(n, kStageChunk));
+  for (uint64_t o = 0; o < n; o += kStageChunk) {
+    const uint64_t c = std::min(kStageChunk, n - o);
+    k::f32_to_f64(dev + o, d_f64a.ptr, c, stream);
+    PH_CUDA(cudaMemcpyAsync(host + o, d_f64a.ptr, c * 8, cudaMemcpyDeviceToHost, stream));
+  }
+  PH_CUDA(cudaStreamSynchronize(stream));
 }
 
 LocalResult classify(const double* losses, int tau, int bad) {

@@ -115,6 +115,11 @@ struct Ctx {
   Ctx(int dev, const photon_model_cfg& m, int prec, uint64_t mb);
   ~Ctx();
 
+  // f64 host <-> fp32 device through a bounded staging chunk (d_f64a holds one
+  // chunk, not P doubles: 7B-scale parameter vectors are 55 GB in f64)
+  void h2d_f64_to_f32(const double* host, float* dev, uint64_t n);
+  void d2h_f32_to_f64(const float* dev, double* host, uint64_t n);  // synchronous
+
   void begin_timing();
   double end_timing();  // syncs, returns ms since begin_timing
 

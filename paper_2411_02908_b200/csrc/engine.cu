@@ -117,7 +117,9 @@ class EngineT final : public Engine {
                                                     k::colsum_part_floats((int)M, (int)d)}));
     auto plan = [&](char* p) {
       char* s = p;
-      master = carve<float>(p, P);
+      // + 64: a runner with one local client aggregates straight out of master,
+      // reading whole NCCL shards (up to Ppad = P rounded to 4 * world <= P + 31)
+      master = carve<float>(p, P + 64);
       grads = carve<float>(p, P);
       mom = carve<float>(p, P);
       vel2 = carve<float>(p, P);

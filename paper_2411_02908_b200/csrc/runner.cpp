@@ -70,12 +70,10 @@ Runner::Runner(Ctx* c, const photon_fed_cfg& f, const photon_train_cfg& t,
   cursors.assign(f.population, 0);
   PH_CUDA(cudaSetDevice(c->device));
   d_theta.reserve(Ppad);
-  d_vel.reserve(Ppad);
+  d_vel.reserve(ws > 1 ? shard : Ppad);  // the outer velocity is sharded across ranks
   PH_CUDA(cudaMemsetAsync(d_theta.ptr, 0, Ppad * 4, c->stream));
-  PH_CUDA(cudaMemsetAsync(d_vel.ptr, 0, Ppad * 4, c->stream));
-  c->d_f64a.reserve(P);
-  PH_CUDA(cudaMemcpyAsync(c->d_f64a.ptr, theta0, P * 8, cudaMemcpyHostToDevice, c->stream));
-  k::f64_to_f32(c->d_f64a.ptr, d_theta.ptr, P, c->stream);
+  PH_CUDA(cudaMemsetAsync(d_vel.ptr, 0, d_vel.n * 4, c->stream));
+  c->h2d_f64_to_f32(theta0, d_theta.ptr, P);
   h_stats.reserve(4 * f.clients_per_round + 4);
   d_stats.reserve(4 * f.clients_per_round + 4);
   PH_CUDA(cudaEventCreate(&ev_a));
@@ -151,10 +149,16 @@ void Runner::run_round(photon_round_record* rec) {
   std::vector<int> mine;
   for (int si = 0; si < K; ++si)
     if (si % world == rank) mine.push_back(si);
-  if (d_models.n < mine.size() * Ppad) {
+  // one local client trains in (and is aggregated from) the engine's master;
+  // several keep their results in dedicated slots
+  const bool in_master = mine.size() == 1;
+  if (!in_master && d_models.n < mine.size() * Ppad) {
     d_models.reserve(mine.size() * Ppad);
     PH_CUDA(cudaMemsetAsync(d_models.ptr, 0, d_models.n * 4, st));
   }
+  auto model_ptr = [&](size_t j) -> float* {
+    return in_master ? ctx->eng->master : d_models.ptr + j * Ppad;
+  };
 
   // ---- this round's batches: already staged by the previous round, or now
   double host_ms = 0.0;
@@ -170,7 +174,7 @@ void Runner::run_round(photon_round_record* rec) {
   h_flag.reserve(nm);
   PH_CUDA(cudaEventRecord(ev_a, st));
   for (size_t j = 0; j < mine.size(); ++j)
-    ctx->launch_local_round(train, dev[j], d_theta.ptr, d_models.ptr + j * Ppad, step_base,
+    ctx->launch_local_round(train, dev[j], d_theta.ptr, model_ptr(j), step_base,
                             d_loss.ptr + j * tau, d_flag.ptr + j);
   PH_CUDA(cudaEventRecord(ev_b, st));
   // ---- prefetch round t+1 into the other set while the GPU trains round t
@@ -239,27 +243,35 @@ void Runner::run_round(photon_round_record* rec) {
   const int n = (int)surv.size();
   std::vector<const float*> ptrs(n);
   if (world == 1) {
-    for (int r = 0; r < n; ++r) ptrs[r] = d_models.ptr + (size_t)(surv[r] / world) * Ppad;
+    for (int r = 0; r < n; ++r) ptrs[r] = model_ptr((size_t)(surv[r] / world));
   } else {
-    d_recv.reserve((size_t)n * shard);
+    // received shards land in the AdamW moments when they fit: m and v are dead
+    // between rounds (the next round re-zeroes them) and adjacent in the pool
+    Engine& e = *ctx->eng;
+    const size_t span = (size_t)(e.vel2 - e.mom) + P;
+    float* recv = e.mom;
+    if ((size_t)n * shard > span) {
+      d_recv.reserve((size_t)n * shard);
+      recv = d_recv.ptr;
+    }
     PH_NCCL(nccl().GroupStart());
     for (int r = 0; r < n; ++r) {
       const int si = surv[r], owner = si % world;
       if (owner == rank) {
-        const float* model = d_models.ptr + (size_t)(si / world) * Ppad;
+        const float* model = model_ptr((size_t)(si / world));
         for (int q = 0; q < world; ++q)
           PH_NCCL(nccl().Send(model + (size_t)q * shard, shard, ncclFloat, q, comm, st));
       }
-      PH_NCCL(nccl().Recv(d_recv.ptr + (size_t)r * shard, shard, ncclFloat, owner, comm, st));
+      PH_NCCL(nccl().Recv(recv + (size_t)r * shard, shard, ncclFloat, owner, comm, st));
     }
     PH_NCCL(nccl().GroupEnd());
-    for (int r = 0; r < n; ++r) ptrs[r] = d_recv.ptr + (size_t)r * shard;
+    for (int r = 0; r < n; ++r) ptrs[r] = recv + (size_t)r * shard;
   }
   d_model_ptrs.reserve(n);
   PH_CUDA(cudaMemcpyAsync(d_model_ptrs.ptr, ptrs.data(), n * sizeof(float*), cudaMemcpyHostToDevice, st));
   const uint64_t off = world == 1 ? 0 : (uint64_t)rank * shard;
   const uint64_t len = world == 1 ? P : shard;
-  k::aggregate<float>(d_model_ptrs.ptr, n, len, d_theta.ptr + off, d_vel.ptr + off, server.kind,
+  k::aggregate<float>(d_model_ptrs.ptr, n, len, d_theta.ptr + off, d_vel.ptr, server.kind,
                       server.eta, server.momentum, server.nesterov, st);
   if (world > 1)
     PH_NCCL(nccl().AllGather(d_theta.ptr + off, d_theta.ptr, shard, ncclFloat, comm, st));
@@ -410,25 +422,33 @@ void Runner::resume(const std::string& dir) {
 
 void Runner::theta_f64(double* out) {
   PH_CUDA(cudaSetDevice(ctx->device));
-  ctx->d_f64a.reserve(P);
-  k::f32_to_f64(d_theta.ptr, ctx->d_f64a.ptr, P, ctx->stream);
-  PH_CUDA(cudaMemcpyAsync(out, ctx->d_f64a.ptr, P * 8, cudaMemcpyDeviceToHost, ctx->stream));
-  PH_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->d2h_f32_to_f64(d_theta.ptr, out, P);
 }
 
 void Runner::velocity_f64(double* out) {
   PH_CUDA(cudaSetDevice(ctx->device));
-  const float* src = d_vel.ptr;
-  if (world > 1) {
-    ctx->d_f32a.reserve(Ppad);
-    PH_NCCL(nccl().AllGather(d_vel.ptr + (size_t)rank * shard, ctx->d_f32a.ptr, shard, ncclFloat,
-                          comm, ctx->stream));
-    src = ctx->d_f32a.ptr;
+  if (world == 1) {
+    ctx->d2h_f32_to_f64(d_vel.ptr, out, P);
+    return;
   }
-  ctx->d_f64a.reserve(P);
-  k::f32_to_f64(src, ctx->d_f64a.ptr, P, ctx->stream);
-  PH_CUDA(cudaMemcpyAsync(out, ctx->d_f64a.ptr, P * 8, cudaMemcpyDeviceToHost, ctx->stream));
-  PH_CUDA(cudaStreamSynchronize(ctx->stream));
+  // gather the shards chunk by chunk (bounded scratch): chunk c of every
+  // rank's shard lands at [q][chunk] in d_f32a
+  const uint64_t chunk = std::min<uint64_t>(shard, 1ull << 22);
+  ctx->d_f32a.reserve((size_t)world * chunk);
+  std::vector<double> tmp;
+  for (uint64_t c0 = 0; c0 < shard; c0 += chunk) {
+    const uint64_t len = std::min(chunk, shard - c0);
+    PH_NCCL(nccl().AllGather(d_vel.ptr + c0, ctx->d_f32a.ptr, len, ncclFloat, comm, ctx->stream));
+    tmp.resize((size_t)world * len);
+    // ranks' pieces are len apart in the gather buffer
+    ctx->d2h_f32_to_f64(ctx->d_f32a.ptr, tmp.data(), (uint64_t)world * len);
+    for (int q = 0; q < world; ++q) {
+      const uint64_t dst = (uint64_t)q * shard + c0;
+      if (dst >= P) continue;
+      const uint64_t m = std::min(len, P - dst);
+      std::copy(tmp.begin() + (size_t)q * len, tmp.begin() + (size_t)q * len + m, out + dst);
+    }
+  }
 }
 
 // FederationRunner::restore (aggregator.cpp:78-91)
@@ -436,11 +456,14 @@ void Runner::restore(const double* theta, const double* velocity, uint64_t nr,
                      const uint64_t* cur, uint64_t n) {
   if (n != cursors.size()) throw Error(PHOTON_ERR_USAGE, "restore: cursor vector has wrong length");
   PH_CUDA(cudaSetDevice(ctx->device));
-  ctx->d_f64a.reserve(P);
-  PH_CUDA(cudaMemcpyAsync(ctx->d_f64a.ptr, theta, P * 8, cudaMemcpyHostToDevice, ctx->stream));
-  k::f64_to_f32(ctx->d_f64a.ptr, d_theta.ptr, P, ctx->stream);
-  PH_CUDA(cudaMemcpyAsync(ctx->d_f64a.ptr, velocity, P * 8, cudaMemcpyHostToDevice, ctx->stream));
-  k::f64_to_f32(ctx->d_f64a.ptr, d_vel.ptr, P, ctx->stream);
+  ctx->h2d_f64_to_f32(theta, d_theta.ptr, P);
+  if (world == 1) {
+    ctx->h2d_f64_to_f32(velocity, d_vel.ptr, P);
+  } else {  // this rank's shard only
+    const uint64_t o = (uint64_t)rank * shard;
+    PH_CUDA(cudaMemsetAsync(d_vel.ptr, 0, shard * 4, ctx->stream));
+    if (o < P) ctx->h2d_f64_to_f32(velocity + o, d_vel.ptr, std::min(shard, P - o));
+  }
   PH_CUDA(cudaStreamSynchronize(ctx->stream));
   next_round = nr;
   cursors.assign(cur, cur + n);
