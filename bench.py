@@ -30,6 +30,8 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# stdout carries exactly one JSON line: keep NCCL's version banner off it
+os.environ.setdefault("NCCL_DEBUG", "WARN")
 
 MODEL_125M = (12, 768, 12, 4, 50368, 2048)
 # SURVEY 8(d) configs 2-4 (Photon 125M / 1.3B / 7B, reference architecture)

@@ -194,11 +194,12 @@ ln_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ x,
               const float* __restrict__ gain, const float* dres, float* dx_out,
               T* __restrict__ dx_T, float* __restrict__ part, int M, int d) {
   extern __shared__ float sm[];  // [warps][2][d]
+  const int warps = blockDim.x / 32;  // sized by the launcher to the shared-memory budget
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   float* my = sm + (size_t)warp * 2 * d;
   for (int j = lane; j < 2 * d; j += 32) my[j] = 0.f;
   const float inv_d = 1.0f / (float)d;
-  for (int m = blockIdx.x * kLnBwdWarps + warp; m < M; m += gridDim.x * kLnBwdWarps) {
+  for (int m = blockIdx.x * warps + warp; m < M; m += gridDim.x * warps) {
     const float* dyr = dy + (size_t)m * d;
     const float* xr = x + (size_t)m * d;
     const float mean = mean_in[m], rstd = rstd_in[m];
@@ -229,7 +230,7 @@ ln_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ x,
   // reduce warps -> block partial
   for (int j = threadIdx.x; j < 2 * d; j += blockDim.x) {
     float acc = 0.f;
-    for (int w = 0; w < kLnBwdWarps; ++w) acc += sm[(size_t)w * 2 * d + j];
+    for (int w = 0; w < warps; ++w) acc += sm[(size_t)w * 2 * d + j];
     part[(size_t)blockIdx.x * 2 * d + j] = acc;
   }
 }
@@ -367,12 +368,16 @@ void ln_bwd(const float* dy, const float* x, const float* mean, const float* rst
     PH_LNB(1) PH_LNB(2) PH_LNB(3) PH_LNB(4) PH_LNB(5) PH_LNB(6)
 #undef PH_LNB
     default: {
-      const size_t smem = (size_t)kLnBwdWarps * 2 * d * sizeof(float);
+      // as many warps (<= 8) as [warps][2][d] fp32 partials fit in shared memory
+      const int warps = (int)std::max<size_t>(
+          1, std::min<size_t>(kLnBwdWarps, (size_t)(224 * 1024) / ((size_t)2 * d * sizeof(float))));
+      const size_t smem = (size_t)warps * 2 * d * sizeof(float);
+      if (smem > 224 * 1024) throw Error(PHOTON_ERR_CONFIG, "layer_norm backward: d_model too large");
       if (smem > 48 * 1024)
         PH_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-      ln_bwd_kernel<T><<<kLnBwdBlocks, kLnBwdWarps * 32, smem, st>>>(dy, x, mean, rstd, gain, dres,
-                                                                     dx_out, dx_T, part, M, d);
+      ln_bwd_kernel<T><<<kLnBwdBlocks, warps * 32, smem, st>>>(dy, x, mean, rstd, gain, dres,
+                                                               dx_out, dx_T, part, M, d);
     }
   }
   PH_LAUNCH_CHECK();
