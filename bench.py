@@ -30,8 +30,16 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# stdout carries exactly one JSON line: keep NCCL's version banner off it
-os.environ.setdefault("NCCL_DEBUG", "WARN")
+# stdout carries exactly one JSON line: the line goes to a private copy of the
+# original stdout, and fd 1 is pointed at stderr so that banners printed by
+# native libraries (NCCL's version line, ...) cannot reach the driver's parser
+_JSON_OUT = os.fdopen(os.dup(1), "w")
+os.dup2(2, 1)
+
+
+def _emit(line: dict) -> None:
+    _JSON_OUT.write(json.dumps(line) + "\n")
+    _JSON_OUT.flush()
 
 MODEL_125M = (12, 768, 12, 4, 50368, 2048)
 # SURVEY 8(d) configs 2-4 (Photon 125M / 1.3B / 7B, reference architecture)
@@ -217,7 +225,7 @@ def run_reference_arm(args):
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    _emit(line)
     return 0
 
 
@@ -374,7 +382,7 @@ def run_ours(args):
         except Exception as ex:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "cores": 0,
                                     "kind": "unavailable", "sample": str(ex)[:200]}
-    print(json.dumps(line), flush=True)
+    _emit(line)
     return 0
 
 

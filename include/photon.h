@@ -274,6 +274,15 @@ int photon_runner_restore(photon_runner* r, const double* theta, const double* v
                           photon_err* err);
 
 
+/* Round boundary alone: n_params fp32 parameters, one
+ * synthetic client model per rank, `iters` timed rounds of exchange -> fused
+ * anchored-mean + outer update (server kind/eta/momentum) -> all-gather on
+ * `device`.  *ms_out: mean device ms per boundary on this rank.  Collective
+ * across `world` ranks (nccl_id from rank 0; NULL when world == 1). */
+int photon_debug_boundary(int device, uint64_t n_params, int rank, int world,
+                          const uint8_t* nccl_id, const photon_server_cfg* server, int iters,
+                          double* ms_out, photon_err* err);
+
 /* ---- evaluation and checkpoints -------------------------- */
 /* build_eval_batches (harness.cpp:440-472): per style a held-out corpus from
  * mix_seed(data_seed, "Eval"), eval_sequences / n_styles sequences each, batches

@@ -127,6 +127,8 @@ _SIGS = {
     "photon_runner_cursor": (u64, [C.c_void_p, u64]),
     "photon_runner_restore": (i32, [C.c_void_p, P(dbl), P(dbl), u64, P(u64), u64,
                                     P(photon_err)]),
+    "photon_debug_boundary": (i32, [C.c_int, u64, C.c_int, C.c_int, P(u8), P(photon_server_cfg),
+                                    C.c_int, P(dbl), P(photon_err)]),
     "photon_eval_set_create": (i32, [P(C.c_char_p), u64, u64, u64, u64, u64, u64,
                                      P(C.c_void_p), P(photon_err)]),
     "photon_eval_set_destroy": (None, [C.c_void_p]),

@@ -618,6 +618,68 @@ int photon_runner_restore(photon_runner* r, const double* theta, const double* v
   return guarded(err, [&] { r->r->restore(theta, velocity, next_round, cursors, n); });
 }
 
+int photon_debug_boundary(int device, uint64_t n_params, int rank, int world,
+                          const uint8_t* nccl_id, const photon_server_cfg* server, int iters,
+                          double* ms_out, photon_err* err) {
+  return guarded(err, [&] {
+    need(world >= 1 && rank >= 0 && rank < world && n_params > 0 && iters > 0, PHOTON_ERR_USAGE,
+         "debug_boundary: bad arguments");
+    need(world == 1 || nccl_id != nullptr, PHOTON_ERR_USAGE, "debug_boundary: needs an NCCL id");
+    validate_server(*server);
+    PH_CUDA(cudaSetDevice(device));
+    const uint64_t P = n_params;
+    const uint64_t shard = ((P + world - 1) / world + 3) / 4 * 4, Ppad = shard * world;
+    cudaStream_t st;
+    PH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    DevBuf<float> theta, vel, model, recv;
+    DevBuf<const float*> ptrs;
+    theta.reserve(Ppad);
+    vel.reserve(world > 1 ? shard : Ppad);
+    model.reserve(Ppad);
+    if (world > 1) recv.reserve((size_t)world * shard);
+    PH_CUDA(cudaMemsetAsync(theta.ptr, 0, Ppad * 4, st));
+    PH_CUDA(cudaMemsetAsync(vel.ptr, 0, vel.n * 4, st));
+    PH_CUDA(cudaMemsetAsync(model.ptr, 0, Ppad * 4, st));
+    ncclComm_t comm = nullptr;
+    if (world > 1) {
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof(id));
+      if (nccl().CommInitRank(&comm, world, id, rank) != ncclSuccess)
+        throw Error(PHOTON_ERR_NCCL, "debug_boundary: ncclCommInitRank failed");
+    }
+    std::vector<int> surv(world);
+    for (int s = 0; s < world; ++s) surv[s] = s;  // one client per rank
+    const float* local[1] = {model.ptr};
+    cudaEvent_t e0, e1;
+    PH_CUDA(cudaEventCreate(&e0));
+    PH_CUDA(cudaEventCreate(&e1));
+    try {
+      for (int i = 0; i < 2; ++i)  // warm-up (NCCL connection setup)
+        round_boundary(comm, rank, world, P, shard, surv, local, recv.ptr, ptrs, theta.ptr,
+                       vel.ptr, *server, st);
+      PH_CUDA(cudaEventRecord(e0, st));
+      for (int i = 0; i < iters; ++i)
+        round_boundary(comm, rank, world, P, shard, surv, local, recv.ptr, ptrs, theta.ptr,
+                       vel.ptr, *server, st);
+      PH_CUDA(cudaEventRecord(e1, st));
+      PH_CUDA(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      PH_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      *ms_out = ms / iters;
+    } catch (...) {
+      if (comm) nccl().CommDestroy(comm);
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      cudaStreamDestroy(st);
+      throw;
+    }
+    if (comm) nccl().CommDestroy(comm);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    PH_CUDA(cudaStreamDestroy(st));
+  });
+}
+
 int photon_eval_set_create(const char* const* styles, uint64_t n_styles, uint64_t eval_sequences,
                            uint64_t data_seed, uint64_t vocab, uint64_t seq_len,
                            uint64_t eval_batch, photon_eval_set** out, photon_err* err) {

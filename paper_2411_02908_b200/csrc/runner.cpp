@@ -241,40 +241,22 @@ void Runner::run_round(photon_round_record* rec) {
 
   // ---- round boundary: mean -> pseudo-gradient -> outer step ----
   const int n = (int)surv.size();
-  std::vector<const float*> ptrs(n);
-  if (world == 1) {
-    for (int r = 0; r < n; ++r) ptrs[r] = model_ptr((size_t)(surv[r] / world));
-  } else {
+  std::vector<const float*> local_models(mine.size());
+  for (size_t j = 0; j < mine.size(); ++j) local_models[j] = model_ptr(j);
+  float* recv = nullptr;
+  if (world > 1) {
     // received shards land in the AdamW moments when they fit: m and v are dead
     // between rounds (the next round re-zeroes them) and adjacent in the pool
     Engine& e = *ctx->eng;
     const size_t span = (size_t)(e.vel2 - e.mom) + P;
-    float* recv = e.mom;
+    recv = e.mom;
     if ((size_t)n * shard > span) {
       d_recv.reserve((size_t)n * shard);
       recv = d_recv.ptr;
     }
-    PH_NCCL(nccl().GroupStart());
-    for (int r = 0; r < n; ++r) {
-      const int si = surv[r], owner = si % world;
-      if (owner == rank) {
-        const float* model = model_ptr((size_t)(si / world));
-        for (int q = 0; q < world; ++q)
-          PH_NCCL(nccl().Send(model + (size_t)q * shard, shard, ncclFloat, q, comm, st));
-      }
-      PH_NCCL(nccl().Recv(recv + (size_t)r * shard, shard, ncclFloat, owner, comm, st));
-    }
-    PH_NCCL(nccl().GroupEnd());
-    for (int r = 0; r < n; ++r) ptrs[r] = recv + (size_t)r * shard;
   }
-  d_model_ptrs.reserve(n);
-  PH_CUDA(cudaMemcpyAsync(d_model_ptrs.ptr, ptrs.data(), n * sizeof(float*), cudaMemcpyHostToDevice, st));
-  const uint64_t off = world == 1 ? 0 : (uint64_t)rank * shard;
-  const uint64_t len = world == 1 ? P : shard;
-  k::aggregate<float>(d_model_ptrs.ptr, n, len, d_theta.ptr + off, d_vel.ptr, server.kind,
-                      server.eta, server.momentum, server.nesterov, st);
-  if (world > 1)
-    PH_NCCL(nccl().AllGather(d_theta.ptr + off, d_theta.ptr, shard, ncclFloat, comm, st));
+  round_boundary(comm, rank, world, P, shard, surv, local_models.data(), recv, d_model_ptrs,
+                 d_theta.ptr, d_vel.ptr, server, st);
   PH_CUDA(cudaEventRecord(ev_c, st));
   PH_CUDA(cudaEventSynchronize(ev_c));
   if (K >= 2) ++sync_events;
@@ -317,6 +299,37 @@ void Runner::run_round(photon_round_record* rec) {
     const double ppl = eval_theta();
     if (rec) rec->eval_ppl = ppl;
   }
+}
+
+void round_boundary(ncclComm_t comm, int rank, int world, uint64_t P, uint64_t shard,
+                    const std::vector<int>& surv, const float* const* local_models,
+                    float* recv, DevBuf<const float*>& d_ptrs, float* d_theta, float* d_vel,
+                    const photon_server_cfg& server, cudaStream_t st) {
+  const int n = (int)surv.size();
+  std::vector<const float*> ptrs(n);
+  if (world == 1) {
+    for (int r = 0; r < n; ++r) ptrs[r] = local_models[surv[r]];
+  } else {
+    PH_NCCL(nccl().GroupStart());
+    for (int r = 0; r < n; ++r) {
+      const int si = surv[r], owner = si % world;
+      if (owner == rank) {
+        const float* model = local_models[si / world];
+        for (int q = 0; q < world; ++q)
+          PH_NCCL(nccl().Send(model + (size_t)q * shard, shard, ncclFloat, q, comm, st));
+      }
+      PH_NCCL(nccl().Recv(recv + (size_t)r * shard, shard, ncclFloat, owner, comm, st));
+    }
+    PH_NCCL(nccl().GroupEnd());
+    for (int r = 0; r < n; ++r) ptrs[r] = recv + (size_t)r * shard;
+  }
+  d_ptrs.reserve(n);
+  PH_CUDA(cudaMemcpyAsync(d_ptrs.ptr, ptrs.data(), n * sizeof(float*), cudaMemcpyHostToDevice, st));
+  const uint64_t off = world == 1 ? 0 : (uint64_t)rank * shard;
+  const uint64_t len = world == 1 ? P : shard;
+  k::aggregate<float>(d_ptrs.ptr, n, len, d_theta + off, d_vel, server.kind, server.eta,
+                      server.momentum, server.nesterov, st);
+  if (world > 1) PH_NCCL(nccl().AllGather(d_theta + off, d_theta, shard, ncclFloat, comm, st));
 }
 
 void Runner::set_eval(const EvalSet& es, uint64_t every) {

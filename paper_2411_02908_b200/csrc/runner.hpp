@@ -79,4 +79,16 @@ struct Runner {
 
 void validate_server(const photon_server_cfg& s);
 
+// The round boundary (aggregator.cpp:177-179) over NCCL: every surviving
+// slot's model goes in 1/world shards to the shard owners in ascending slot
+// order (slot si lives on rank si % world), the owner runs the fused
+// anchored-mean -> pseudo-gradient -> outer update on its shard of theta
+// (d_vel holds that shard), and an all-gather rebuilds theta on every rank.
+// world == 1: the fused update over the local models, no communication.
+// Per-GPU wire bytes 2 (world-1)/world * P * 4.
+void round_boundary(ncclComm_t comm, int rank, int world, uint64_t P, uint64_t shard,
+                    const std::vector<int>& surv, const float* const* local_models,
+                    float* recv, DevBuf<const float*>& d_ptrs, float* d_theta, float* d_vel,
+                    const photon_server_cfg& server, cudaStream_t st);
+
 }  // namespace photon
