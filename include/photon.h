@@ -129,6 +129,21 @@ typedef struct photon_ctx photon_ctx;       /* one GPU: device state of one clie
 typedef struct photon_plan photon_plan;     /* ShardPlan (data.h:33-62), host */
 typedef struct photon_runner photon_runner; /* FederationRunner (aggregator.h:70-102) */
 typedef struct photon_eval_set photon_eval_set; /* held-out batches (harness.cpp:440-472) */
+typedef struct photon_central photon_central;   /* run_centralized (baselines.cpp:25-127) */
+
+/* CentralizedConfig, baselines.h:19-35 */
+typedef struct {
+  photon_model_cfg model;
+  photon_adamw_cfg adamw;
+  photon_lr_schedule schedule;
+  int32_t opt;                 /* 0 AdamW, 1 SGD */
+  double sgd_clip_norm;
+  uint64_t n_workers;
+  uint64_t global_batch;       /* divisible by n_workers */
+  uint64_t total_steps;
+  uint64_t opt_reset_interval; /* fresh AdamW state every N steps, 0 = never */
+  double throughput_bps;
+} photon_central_cfg;
 
 int photon_abi_version(void);
 const char* photon_status_name(int code);
@@ -282,6 +297,20 @@ int photon_runner_restore(photon_runner* r, const double* theta, const double* v
 int photon_debug_boundary(int device, uint64_t n_params, int rank, int world,
                           const uint8_t* nccl_id, const photon_server_cfg* server, int iters,
                           double* ms_out, photon_err* err);
+
+/* ---- centralized / DDP baseline (baselines.cpp:25-127) ---------
+ * n_workers data-parallel workers (worker w: shard w, stream_seed(seed, w), on
+ * rank w % world); per step: each worker's gradient, the ascending-worker
+ * anchored mean (NCCL shard exchange + all-gather for world > 1), one shared
+ * AdamW / SGD update.  Non-finite mean loss -> PHOTON_ERR_DIVERGENCE (step). */
+int photon_central_create(photon_ctx* ctx, const photon_central_cfg* cfg, const photon_plan* plan,
+                          uint64_t seed, const double* theta0, int rank, int world,
+                          const uint8_t* nccl_id, photon_central** out, photon_err* err);
+void photon_central_destroy(photon_central* c);
+int photon_central_step(photon_central* c, photon_step_metric* metric, photon_err* err);
+uint64_t photon_central_next_step(const photon_central* c);
+uint64_t photon_central_cursor(const photon_central* c, uint64_t worker);
+int photon_central_theta(photon_central* c, double* out, photon_err* err);
 
 /* ---- evaluation and checkpoints -------------------------- */
 /* build_eval_batches (harness.cpp:440-472): per style a held-out corpus from

@@ -553,6 +553,22 @@ class Reference:
         return float(ppl[0]), float(ppl[1])
 
 
+    def run_centralized(self, cfg: ModelCfg, t: TrainCfg, style, tokens, data_seed, n_workers,
+                        total_steps, reset, seed, theta0):
+        """baselines.cpp:25-127 (t.batch_size is the global batch)."""
+        theta0 = np.ascontiguousarray(theta0, np.float64)
+        out = np.zeros_like(theta0)
+        losses = np.zeros(total_steps)
+        cursors = np.zeros(n_workers, np.uint64)
+        _check(self.lib.ref_run_centralized(cfg.as_array(), t.as_doubles(),
+                                            C.c_int32(STYLES.index(style)), C.c_uint64(tokens),
+                                            C.c_uint64(data_seed), C.c_uint64(n_workers),
+                                            C.c_uint64(total_steps), C.c_uint64(reset),
+                                            C.c_uint64(seed), _p(theta0, C.c_double),
+                                            _p(out, C.c_double), _p(losses, C.c_double),
+                                            _p(cursors, C.c_uint64)), "ref_run_centralized")
+        return out, losses, cursors
+
     def write_checkpoint(self, cfg: ModelCfg, params, round_: int, path: str) -> None:
         _check(self.lib.ref_write_checkpoint(cfg.as_array(), _p(np.ascontiguousarray(params,
                                              np.float64), C.c_double), C.c_uint64(round_),

@@ -332,6 +332,25 @@ int ref_train_sample(const uint64_t* m, const double* t, uint64_t batch, uint64_
         if (loss_out) *loss_out = losses[0])
 }
 
+// baselines.cpp:25-127: the reference's centralized / DDP baseline on an IID
+// plan built like ref_run_rounds'; t[12] is the global batch
+int ref_run_centralized(const uint64_t* m, const double* t, int32_t style, uint64_t tokens,
+                        uint64_t data_seed, uint64_t n_workers, uint64_t total_steps,
+                        uint64_t reset, uint64_t seed, const double* theta0, double* theta_out,
+                        double* step_losses, uint64_t* cursors) {
+  GUARD(LocalTrainConfig lc = tcfg(m, t); TransformerModel model(lc.model);
+        auto plan = make_plan(0, style, tokens, data_seed, (uint32_t)lc.model.vocab_size,
+                              n_workers, lc.model.seq_len);
+        CentralizedConfig cc; cc.model = lc.model; cc.adamw = lc.adamw; cc.schedule = lc.schedule;
+        cc.opt = lc.opt; cc.sgd_clip_norm = lc.sgd_clip_norm; cc.n_workers = n_workers;
+        cc.global_batch = lc.batch_size; cc.total_steps = total_steps;
+        cc.opt_reset_interval = reset;
+        CentralizedResult r = run_centralized(cc, plan, seed, to_pv(model, theta0), 1);
+        copy_out(r.theta, theta_out);
+        for (uint64_t i = 0; i < total_steps; ++i) step_losses[i] = r.steps[i].loss;
+        for (uint64_t w = 0; w < n_workers; ++w) cursors[w] = r.cursors[w])
+}
+
 // checkpoint.cpp: the reference's PHCK writer / reader on a model-layout ParamVector
 int ref_write_checkpoint(const uint64_t* m, const double* params, uint64_t round,
                          const char* path) {

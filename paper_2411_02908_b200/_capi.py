@@ -53,6 +53,13 @@ class photon_step_metric(C.Structure):
     _fields_ = [("loss", dbl), ("tokens", u64), ("sim_seconds", dbl)]
 
 
+class photon_central_cfg(C.Structure):
+    _fields_ = [("model", photon_model_cfg), ("adamw", photon_adamw_cfg),
+                ("schedule", photon_lr_schedule), ("opt", i32), ("sgd_clip_norm", dbl),
+                ("n_workers", u64), ("global_batch", u64), ("total_steps", u64),
+                ("opt_reset_interval", u64), ("throughput_bps", dbl)]
+
+
 class photon_round_record(C.Structure):
     _fields_ = [("round", u64), ("n_sampled", u64), ("sampled_ids", u64 * 64),
                 ("mean_client_loss", dbl), ("min_client_loss", dbl), ("max_client_loss", dbl),
@@ -129,6 +136,13 @@ _SIGS = {
                                     P(photon_err)]),
     "photon_debug_boundary": (i32, [C.c_int, u64, C.c_int, C.c_int, P(u8), P(photon_server_cfg),
                                     C.c_int, P(dbl), P(photon_err)]),
+    "photon_central_create": (i32, [C.c_void_p, P(photon_central_cfg), C.c_void_p, u64, P(dbl),
+                                    C.c_int, C.c_int, P(u8), P(C.c_void_p), P(photon_err)]),
+    "photon_central_destroy": (None, [C.c_void_p]),
+    "photon_central_step": (i32, [C.c_void_p, P(photon_step_metric), P(photon_err)]),
+    "photon_central_next_step": (u64, [C.c_void_p]),
+    "photon_central_cursor": (u64, [C.c_void_p, u64]),
+    "photon_central_theta": (i32, [C.c_void_p, P(dbl), P(photon_err)]),
     "photon_eval_set_create": (i32, [P(C.c_char_p), u64, u64, u64, u64, u64, u64,
                                      P(C.c_void_p), P(photon_err)]),
     "photon_eval_set_destroy": (None, [C.c_void_p]),

@@ -9,6 +9,7 @@
 #include "kernels.cuh"
 #include "nccl_api.hpp"
 #include "runner.hpp"
+#include "central.hpp"
 
 struct photon_plan {
   photon::Plan p;
@@ -22,6 +23,9 @@ struct photon_runner {
 };
 struct photon_eval_set {
   photon::EvalSet s;
+};
+struct photon_central {
+  std::unique_ptr<photon::Central> c;
 };
 
 using namespace photon;
@@ -678,6 +682,35 @@ int photon_debug_boundary(int device, uint64_t n_params, int rank, int world,
     cudaEventDestroy(e1);
     PH_CUDA(cudaStreamDestroy(st));
   });
+}
+
+int photon_central_create(photon_ctx* ctx, const photon_central_cfg* cfg, const photon_plan* plan,
+                          uint64_t seed, const double* theta0, int rank, int world,
+                          const uint8_t* nccl_id, photon_central** out, photon_err* err) {
+  return guarded(err, [&] {
+    need(ctx && cfg && out && theta0, PHOTON_ERR_USAGE, "central_create: null argument");
+    PH_CUDA(cudaSetDevice(ctx->c.device));
+    auto h = std::make_unique<photon_central>();
+    h->c = std::make_unique<Central>(&ctx->c, *cfg, plan ? &plan->p : nullptr, seed, theta0, rank,
+                                     world, nccl_id);
+    *out = h.release();
+  });
+}
+
+void photon_central_destroy(photon_central* c) { delete c; }
+
+int photon_central_step(photon_central* c, photon_step_metric* metric, photon_err* err) {
+  return guarded(err, [&] { c->c->step(metric); });
+}
+
+uint64_t photon_central_next_step(const photon_central* c) { return c->c->t; }
+
+uint64_t photon_central_cursor(const photon_central* c, uint64_t worker) {
+  return worker < c->c->cursors.size() ? c->c->cursors[worker] : 0;
+}
+
+int photon_central_theta(photon_central* c, double* out, photon_err* err) {
+  return guarded(err, [&] { c->c->theta_f64(out); });
 }
 
 int photon_eval_set_create(const char* const* styles, uint64_t n_styles, uint64_t eval_sequences,

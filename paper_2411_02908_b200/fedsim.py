@@ -222,8 +222,29 @@ class ServerOptConfig:
             raise ConfigError("server opt: fedavg is eta=1, momentum=0 by definition")
 
 
-def diloco_server_opt() -> ServerOptConfig:  # baselines.cpp:129-136
-    return ServerOptConfig(ServerOptKind.FedMomentum, 0.1, 0.9, True)
+def diloco_server_opt(momentum: float = 0.9) -> ServerOptConfig:  # baselines.cpp:129-136
+    return ServerOptConfig(ServerOptKind.FedMomentum, 0.1, momentum, True)
+
+
+@dataclass
+class CentralizedConfig:
+    """baselines.h:19-35."""
+    model: ModelConfig = field(default_factory=ModelConfig)
+    adamw: AdamWConfig = field(default_factory=AdamWConfig)
+    schedule: LrSchedule = field(default_factory=LrSchedule)
+    opt: int = ClientOptKind.kAdamW
+    sgd_clip_norm: float = 0.0
+    n_workers: int = 1
+    global_batch: int = 8
+    total_steps: int = 1
+    opt_reset_interval: int = 0
+    throughput_bps: float = 2.0
+
+    def c(self):
+        return A.photon_central_cfg(self.model.c(), self.adamw.c(), self.schedule.c(), self.opt,
+                                    self.sgd_clip_norm, self.n_workers, self.global_batch,
+                                    self.total_steps, self.opt_reset_interval,
+                                    self.throughput_bps)
 
 
 class Topology:
@@ -774,6 +795,70 @@ class FederationRunner:
 
     def resume(self, directory: str) -> None:
         _call(A.lib().photon_runner_resume, self._h, os.fsencode(directory))
+
+
+@dataclass
+class CentralizedResult:
+    """baselines.h:37-42."""
+    theta: np.ndarray
+    steps: List[StepMetric]
+    sync_events: int
+    cursors: List[int]
+
+
+class CentralizedTrainer:
+    """Device-resident run_centralized (baselines.cpp:25-127): worker w on rank
+    w % world, one ascending-order gradient all-reduce and one shared update per
+    step; results do not depend on world."""
+
+    def __init__(self, cfg: CentralizedConfig, plan: ShardPlan, seed: int, theta0: np.ndarray,
+                 device: int = 0, precision: str = "f32", rank: int = 0, world: int = 1,
+                 nccl_id: Optional[bytes] = None):
+        self.cfg, self.plan = cfg, plan
+        per_worker = cfg.global_batch // max(cfg.n_workers, 1)
+        self.ctx = context(cfg.model, device, precision, max(per_worker, 1))
+        theta0 = _f64(theta0)
+        self._P = len(theta0)
+        h = C.c_void_p()
+        c = cfg.c()
+        idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id else None
+        _call(A.lib().photon_central_create, self.ctx.handle, C.byref(c), plan._h, seed,
+              _dp(theta0), rank, world, idbuf, C.byref(h))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value:
+            A.lib().photon_central_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def step(self) -> StepMetric:
+        m = A.photon_step_metric()
+        _call(A.lib().photon_central_step, self._h, C.byref(m))
+        return StepMetric(m.loss, int(m.tokens), m.sim_seconds)
+
+    def next_step(self) -> int:
+        return int(A.lib().photon_central_next_step(self._h))
+
+    def cursor(self, worker: int) -> int:
+        return int(A.lib().photon_central_cursor(self._h, worker))
+
+    def theta(self) -> np.ndarray:
+        out = np.zeros(self._P)
+        _call(A.lib().photon_central_theta, self._h, _dp(out))
+        return out
+
+
+def run_centralized(cfg: CentralizedConfig, plan: ShardPlan, seed: int, theta0: np.ndarray,
+                    n_threads: int = 1, observer=None, **kw) -> CentralizedResult:
+    """baselines.h:47-51 (n_threads is accepted for signature parity)."""
+    tr = CentralizedTrainer(cfg, plan, seed, theta0, **kw)
+    steps = []
+    for t in range(cfg.total_steps):
+        steps.append(tr.step())
+        if observer is not None:
+            observer(t, tr.theta())
+    return CentralizedResult(tr.theta(), steps, cfg.total_steps if cfg.n_workers > 1 else 0,
+                             [tr.cursor(w) for w in range(cfg.n_workers)])
 
 
 class EvalSet:

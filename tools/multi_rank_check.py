@@ -29,6 +29,17 @@ theta0 = F.TransformerModel(cfg).init_params(1)
 local_cfg = F.LocalTrainConfig(model=cfg, schedule=F.LrSchedule(2e-3, 16, 160, 0.1),
                                local_steps=4, batch_size=4)
 srv = F.ServerOptConfig() if server == "fedavg" else F.diloco_server_opt()
+if server == "central":  # DDP baseline: 6 workers, per-step gradient all-reduce
+    ccfg = F.CentralizedConfig(model=cfg, schedule=F.LrSchedule(2e-3, 16, 160, 0.1), n_workers=6,
+                               global_batch=12, total_steps=4, opt_reset_interval=2)
+    res = F.run_centralized(ccfg, plan, 42, theta0, device=local, precision="f32", rank=rank,
+                            world=world, nccl_id=nccl_id)
+    if rank == 0:
+        np.save(out, np.concatenate([res.theta, [s.loss for s in res.steps], res.cursors]))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    sys.exit(0)
 es = F.EvalSet(["web"], 40, 7, cfg, 8)  # 5 batches: uneven over 2 or 4 ranks
 runner = F.FederationRunner(F.FederationConfig(6, 4, 3, F.Topology.kRingAllReduce, 42), local_cfg,
                             srv, plan, theta0, device=local, precision="f32", rank=rank,
