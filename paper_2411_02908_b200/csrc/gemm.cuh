@@ -20,8 +20,8 @@ enum class Epi : int {
   Accum = 1,      // C += acc
   Bias = 2,       // C = acc + bias
   ResidBias = 3,  // C(f32) = resid + (acc + bias)
-  GeluBias = 4,   // aux = acc + bias ; C = gelu(aux)
-  GeluBwd = 5,    // C = acc * gelu'(aux)
+  GeluBias = 4,   // u = acc + bias ; C = gelu(u), aux = gelu'(u)  (the backward's factor)
+  GeluBwd = 5,    // C = acc * aux  (aux = gelu'(u) from the forward)
 };
 
 struct GemmArgs {

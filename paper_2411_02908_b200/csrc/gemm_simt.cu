@@ -78,11 +78,11 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
         case Epi::ResidBias: C[o] = from_f<TC>(g.resid[o] + (v + g.bias[c])); break;
         case Epi::GeluBias: {
           const float pre = v + g.bias[c];
-          aux[o] = from_f<TA>(pre);
+          aux[o] = from_f<TA>(gelu_grad_f(pre));
           C[o] = from_f<TC>(gelu_f(pre));
           break;
         }
-        case Epi::GeluBwd: C[o] = from_f<TC>(v * gelu_grad_f(to_f<TA>(aux[o]))); break;
+        case Epi::GeluBwd: C[o] = from_f<TC>(v * to_f<TA>(aux[o])); break;
       }
     }
   }

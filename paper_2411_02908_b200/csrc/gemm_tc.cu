@@ -260,7 +260,7 @@ __device__ __forceinline__ uint32_t sw128_off(int lane, int j) {
 // Epilogue tensor maps (row-major [M][N] boxes of 32 rows x 32 cols).
 struct EpiMaps {
   CUtensorMap C;    // output (or split-K workspace, 3D [splits][M][N])
-  CUtensorMap aux;  // GELU pre-activation (bf16): stored by GeluBias, loaded by GeluBwd
+  CUtensorMap aux;  // gelu'(u) (bf16): stored by GeluBias, loaded by GeluBwd
   CUtensorMap in;   // fp32 residual (ResidBias) or C itself (Accum)
 };
 
@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(ibar, in_phase);
             in_phase ^= 1;
             const uint32_t ia = su32(ibuf);
-            if (in_bf16) {  // GeluBwd: v *= gelu'(pre)
+            if (in_bf16) {  // GeluBwd: v *= gelu'(u), stored by the forward
               uint32_t w[16];
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
@@ -508,8 +508,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
 #pragma unroll
               for (int e = 0; e < 16; ++e) {
-                v[2 * e] *= gelu_grad_fast(bf_lo(w[e]));
-                v[2 * e + 1] *= gelu_grad_fast(bf_hi(w[e]));
+                v[2 * e] *= bf_lo(w[e]);
+                v[2 * e + 1] *= bf_hi(w[e]);
               }
               // the shared loads are consumed (values used) before the async
               // proxy may overwrite the buffer
@@ -539,14 +539,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           const uint32_t oa = su32(obuf);
           if (epi == Epi::GeluBias && !splitk) {
+            // one Phi / phi evaluation per element: gelu'(u) = Phi + u phi -> aux box
+            // (second 2 KB, the backward's factor), v <- gelu(u) = u Phi
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {  // pre-activation -> aux box (second 2 KB)
-              sts128(oa + 2048 + sw64_off(lane, j), pack2(v[8 * j], v[8 * j + 1]),
-                     pack2(v[8 * j + 2], v[8 * j + 3]), pack2(v[8 * j + 4], v[8 * j + 5]),
-                     pack2(v[8 * j + 6], v[8 * j + 7]));
+            for (int j = 0; j < 4; ++j) {
+              float gp[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                float Phi, phi;
+                phi_Phi(v[8 * j + e], Phi, phi);
+                gp[e] = fmaf(v[8 * j + e], phi, Phi);
+                v[8 * j + e] *= Phi;
+              }
+              sts128(oa + 2048 + sw64_off(lane, j), pack2(gp[0], gp[1]), pack2(gp[2], gp[3]),
+                     pack2(gp[4], gp[5]), pack2(gp[6], gp[7]));
             }
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
           }
           if (out_bf16) {
 #pragma unroll
@@ -627,11 +634,11 @@ __global__ void splitk_reduce_kernel(const ReduceArgs r) {
       case Epi::Bias: out = acc + b; break;
       case Epi::ResidBias: out = r.resid[o] + (acc + b); break;
       case Epi::GeluBias:
-        static_cast<bf16*>(r.aux)[o] = __float2bfloat16_rn(acc + b);
+        static_cast<bf16*>(r.aux)[o] = __float2bfloat16_rn(gelu_grad_f(acc + b));
         out = gelu_f(acc + b);
         break;
       default:
-        out = acc * gelu_grad_f(__bfloat162float(static_cast<const bf16*>(r.aux)[o]));
+        out = acc * __bfloat162float(static_cast<const bf16*>(r.aux)[o]);
         break;
     }
     if (r.c_bf16) static_cast<bf16*>(r.C)[o] = __float2bfloat16_rn(out);
@@ -766,11 +773,10 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
     return e ? std::atoi(e) : 1;
   }();
   // CTA pairs (256 x 256 tiles) where they measured faster on the 125M shapes
-  // (tools/gemm_bench.py): wide tiles without split-K, except the GELU'
-  // epilogue (epilogue-bound; the pair couples both CTAs' epilogues).
+  // (tools/gemm_bench.py): wide tiles without split-K.
   const int kb_all = (g.K + BK - 1) / BK;
   const bool split_needed = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN) < kNumSMs && kb_all >= 16;
-  const bool pair_ok = BN == 256 && g.M > BM && !split_needed && g.epi != Epi::GeluBwd;
+  const bool pair_ok = BN == 256 && g.M > BM && !split_needed;
   const int ncta = (pair_env == 2 || (pair_env == 1 && pair_ok)) && BN == 256 && g.M > BM ? 2 : 1;
   const int slots = kNumSMs / ncta;  // concurrent tile workers
   TcParams p{};
