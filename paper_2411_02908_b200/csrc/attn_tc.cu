@@ -411,28 +411,41 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
+// thread per (row, head): D = dO . O over the head's 64 columns (8 x 16-byte
+// loads of each); consecutive threads take consecutive heads of a row, so a
+// warp streams contiguous rows
 __global__ void attn_bwd_prep_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dO,
                                      const float* __restrict__ lse, float* __restrict__ Lp,
                                      float* __restrict__ Dp, int B, int S, int H, int d, int Spad) {
-  const int lane = threadIdx.x & 31, warps = blockDim.x / 32;
-  const int idx = blockIdx.x * warps + threadIdx.x / 32;  // (bh, i) over Spad
-  if (idx >= B * H * Spad) return;
-  const int i = idx % Spad, bh = idx / Spad, b = bh / H, h = bh % H;
-  if (i >= S) {
-    if (lane == 0) {
-      Lp[idx] = INFINITY;
-      Dp[idx] = 0.f;
+  const int64_t n = (int64_t)B * S * H;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += stride) {
+    const int h = (int)(t % H);
+    const int64_t row = t / H;  // b * S + i
+    const int b = (int)(row / S), i = (int)(row % S);
+    const uint4* po = reinterpret_cast<const uint4*>(o + row * d + h * DH);
+    const uint4* pd = reinterpret_cast<const uint4*>(dO + row * d + h * DH);
+    float acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < DH / 8; ++c) {
+      const uint4 x = po[c], y = pd[c];
+      const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        acc = fmaf(__uint_as_float(xs[e] << 16), __uint_as_float(ys[e] << 16), acc);
+        acc = fmaf(__uint_as_float(xs[e] & 0xffff0000u), __uint_as_float(ys[e] & 0xffff0000u), acc);
+      }
     }
-    return;
+    const int64_t bh = (int64_t)b * H + h;
+    Dp[bh * Spad + i] = acc;
+    Lp[bh * Spad + i] = lse[bh * S + i] * kLog2e;
   }
-  const int64_t off = ((int64_t)(b * S + i)) * d + h * DH + lane * 2;
-  const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(o + off);
-  const __nv_bfloat162 y = *reinterpret_cast<const __nv_bfloat162*>(dO + off);
-  float acc = __bfloat162float(x.x) * __bfloat162float(y.x) + __bfloat162float(x.y) * __bfloat162float(y.y);
-  acc = warp_sum(acc);
-  if (lane == 0) {
-    Dp[idx] = acc;
-    Lp[idx] = lse[(int64_t)bh * S + i] * kLog2e;
+  // padded query slots: P = 0 (lse = +inf) and D = 0
+  const int64_t npad = (int64_t)B * H * (Spad - S);
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < npad; t += stride) {
+    const int64_t bh = t / (Spad - S), i = S + t % (Spad - S);
+    Lp[bh * Spad + i] = INFINITY;
+    Dp[bh * Spad + i] = 0.f;
   }
 }
 
@@ -875,7 +888,8 @@ void attn_bwd_tc(const bf16* q, const bf16* k, const bf16* v, const bf16* o, con
   const int nt = (S + TQ - 1) / TQ, Spad = nt * TQ, rows = B * S;
   float* Lp = scratch((size_t)2 * B * H * Spad);
   float* Dp = Lp + (size_t)B * H * Spad;
-  attn_bwd_prep_kernel<<<(B * H * Spad + 7) / 8, 256, 0, st>>>(o, dO, lse, Lp, Dp, B, S, H, d, Spad);
+  attn_bwd_prep_kernel<<<std::min<int64_t>(((int64_t)B * S * H + 255) / 256, kNumSMs * 16), 256, 0,
+                         st>>>(o, dO, lse, Lp, Dp, B, S, H, d, Spad);
   PH_LAUNCH_CHECK();
   const CUtensorMap mq = head_map(q, rows, d), mk = head_map(k, rows, d), mv = head_map(v, rows, d),
                     mo = head_map(dO, rows, d);
