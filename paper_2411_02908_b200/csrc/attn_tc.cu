@@ -16,7 +16,10 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <atomic>
+#include <cstdlib>
 #include <mutex>
+#include <string>
 
 #include "kernels.cuh"
 
@@ -150,6 +153,19 @@ __device__ __forceinline__ uint64_t sw128(uint32_t saddr, uint32_t lbo, uint32_t
       "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),        \
       "r"(r[15])                                                                                \
       : "memory")
+// CPT consecutive fp32 columns of this thread's lane
+template <int N>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t* r) {
+#pragma unroll
+  for (int c = 0; c < N / 32; ++c) TMEM_LD32(taddr + c * 32, (r + c * 32));
+  if constexpr (N % 32 == 16) TMEM_LD16(taddr + (N / 32) * 32, (r + (N / 32) * 32));
+}
+template <int N>
+__device__ __forceinline__ void tmem_st_cols(uint32_t taddr, const uint32_t* r) {
+#pragma unroll
+  for (int c = 0; c < N / 32; ++c) TMEM_ST32(taddr + c * 32, (r + c * 32));
+  if constexpr (N % 32 == 16) TMEM_ST16(taddr + (N / 32) * 32, (r + (N / 32) * 32));
+}
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -458,17 +474,36 @@ struct BwdArgs {
   bf16* g1;  // dv
 };
 
-constexpr int kBwdThreads = 64 + 8 * 32;  // producer, MMA, 8 softmax warps
+// producer, MMA, SWB softmax warps: SWB/4 warps per TMEM lane quarter, each on
+// CPT = 128 / (SWB/4) columns of the score tile
+#ifndef PHOTON_ATTN_SWB
+#define PHOTON_ATTN_SWB 16
+#endif
+constexpr int SWB = PHOTON_ATTN_SWB;
+constexpr int NCG = SWB / 4;       // column groups
+constexpr int CPT = 128 / NCG;     // score columns per thread
+constexpr int GPT = DH / NCG;      // accumulator columns per thread in the epilogue
+constexpr int kBwdThreads = 64 + SWB * 32;
+// Ring depth of the streamed operand (Q/dO/L/D in dK/dV, K/V in dQ).  A stage is
+// held until the tile's gradient MMAs retire, and a TMA load under the full
+// backward's memory traffic takes ~2.5-3.6k cycles (clock64 traces): two stages
+// left the MMA issuer waiting on loads; four cover the latency.
+#ifndef PHOTON_ATTN_NR
+#define PHOTON_ATTN_NR 4
+#endif
+constexpr int NR = PHOTON_ATTN_NR;
 
-// Store rows of two 64-column fp32 TMEM accumulators (thread = row, column
-// half hf handles 32 columns of each) as bf16 rows of the head slice.
+// Store N columns of a row of a 64-column fp32 TMEM accumulator (thread = row)
+// as bf16 into the head slice.
+template <int N>
 __device__ __forceinline__ void store_acc_rows(uint32_t taddr, bf16* row_ptr, float mul, bool live) {
-  uint32_t u[32];
-  TMEM_LD32(taddr, u);
+  uint32_t u[N];
+  if constexpr (N == 32) TMEM_LD32(taddr, u);
+  else TMEM_LD16(taddr, u);
   tmem_wait_ld();
   if (live) {
 #pragma unroll
-    for (int i = 0; i < 32; i += 8)
+    for (int i = 0; i < N; i += 8)
       *reinterpret_cast<uint4*>(row_ptr + i) =
           make_uint4(pk(__uint_as_float(u[i]) * mul, __uint_as_float(u[i + 1]) * mul),
                      pk(__uint_as_float(u[i + 2]) * mul, __uint_as_float(u[i + 3]) * mul),
@@ -488,19 +523,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                                            ~uintptr_t(1023));
   uint8_t* sK = sm;
   uint8_t* sV = sm + 16384;
-  uint8_t* sQ = sm + 2 * 16384;   // [2]
-  uint8_t* sO = sm + 4 * 16384;   // [2] dO
-  float* sL = reinterpret_cast<float*>(sm + 6 * 16384);  // [2][128]
-  float* sD = sL + 256;                                  // [2][128]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sD + 256);
+  uint8_t* sQ = sm + 2 * 16384;   // [NR]
+  uint8_t* sO = sQ + NR * 16384;  // [NR] dO
+  float* sL = reinterpret_cast<float*>(sO + NR * 16384);  // [NR][128]
+  float* sD = sL + NR * 128;                              // [NR][128]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sD + NR * 128);
   uint64_t* kv_full = bar;
-  uint64_t* q_full = bar + 1;   // [2]
-  uint64_t* q_empty = bar + 3;  // [2]
-  uint64_t* s_full = bar + 5;
-  uint64_t* s_empty = bar + 6;
-  uint64_t* p_full = bar + 7;
-  uint64_t* g_done = bar + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9);
+  uint64_t* q_full = bar + 1;        // [NR]
+  uint64_t* q_empty = bar + 1 + NR;  // [NR]
+  uint64_t* s_full = bar + 1 + 2 * NR;
+  uint64_t* s_empty = s_full + 1;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* g_done = s_full + 3;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 4);
 
   const int nt = (a.S + TQ - 1) / TQ;
   const int kt = blockIdx.x;
@@ -511,13 +546,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   if (warp == 0 && lane == 0) {
     mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NR; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(s_empty, 8);
-    mbar_init(p_full, 8);
+    mbar_init(s_empty, SWB);
+    mbar_init(p_full, SWB);
     mbar_init(g_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -537,8 +572,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tma_load_2d(sK, &tk, kv_full, h * DH, row_base + kt * TK);
       tma_load_2d(sV, &tv, kv_full, h * DH, row_base + kt * TK);
       for (int it = 0; it < n_it; ++it) {
-        const int st = it & 1, qt = kt + it;
-        mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);
+        const int st = it % NR, qt = kt + it;
+        mbar_wait(&q_empty[st], ((it / NR) & 1) ^ 1);
         ATTN_TRACE(0, it);
         mbar_expect_tx(&q_full[st], 32768 + 1024);
         tma_load_2d(sQ + st * 16384, &tq, &q_full[st], h * DH, row_base + qt * TQ);
@@ -556,7 +591,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_wait(kv_full, 0);
       const uint32_t ak = su32(sK), av = su32(sV);
       auto issue_grads = [&](int it) {
-        const int st = it & 1;
+        const int st = it % NR;
         mbar_wait(p_full, it & 1);
         ATTN_TRACE(3, it);
         fence_after();
@@ -574,8 +609,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         ATTN_TRACE(4, it);
       };
       for (int it = 0; it < n_it; ++it) {
-        const int st = it & 1;
-        mbar_wait(&q_full[st], (it >> 1) & 1);
+        const int st = it % NR;
+        mbar_wait(&q_full[st], (it / NR) & 1);
         ATTN_TRACE(1, it);
         mbar_wait(s_empty, (it & 1) ^ 1);
         ATTN_TRACE(2, it);
@@ -595,41 +630,39 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       issue_grads(n_it - 1);
     }
   } else {
-    const int q = warp & 3, hf = (warp - 2) >> 2;  // lane quarter, query-column half
+    const int q = warp & 3, cg = (warp - 2) >> 2;  // lane quarter, query-column group
     const int r = q * 32 + lane;
     const int key = kt * TK + r;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const bool key_live = key < a.S;
     for (int it = 0; it < n_it; ++it) {
-      const int st = it & 1, q0 = (kt + it) * TQ;
-      mbar_wait(&q_full[st], (it >> 1) & 1);  // L, D of this query tile visible
+      const int st = it % NR, q0 = (kt + it) * TQ;
+      mbar_wait(&q_full[st], (it / NR) & 1);  // L, D of this query tile visible
       mbar_wait(s_full, it & 1);
       if (warp == 2 && lane == 0) ATTN_TRACE(5, it);
       fence_after();
-      uint32_t s[64], dp[64];
-      TMEM_LD32(tmem + lane_off + hf * 64, s);
-      TMEM_LD32(tmem + lane_off + hf * 64 + 32, (s + 32));
-      TMEM_LD32(tmem + lane_off + 128 + hf * 64, dp);
-      TMEM_LD32(tmem + lane_off + 128 + hf * 64 + 32, (dp + 32));
+      uint32_t s[CPT], dp[CPT];
+      tmem_ld_cols<CPT>(tmem + lane_off + cg * CPT, s);
+      tmem_ld_cols<CPT>(tmem + lane_off + 128 + cg * CPT, dp);
       tmem_wait_ld();
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(s_empty);
-      const float* L = sL + st * 128 + hf * 64;
-      const float* D = sD + st * 128 + hf * 64;
+      const float* L = sL + st * 128 + cg * CPT;
+      const float* D = sD + st * 128 + cg * CPT;
       // masking only where this key tile meets the diagonal or the sequence end
       const bool masked = (kt * TK + TK > q0) || (kt * TK + TK > a.S);
-      const bool key_live = key < a.S;
-      uint32_t pp[32], dd[32];
+      uint32_t pp[CPT / 2], dd[CPT / 2];
       // dS^T is kept unscaled (the softmax scale is applied to dK at the store)
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
+      for (int i = 0; i < CPT / 4; ++i) {
         const float4 l4 = lds_f4(L + 4 * i), d4 = lds_f4(D + 4 * i);
         float p0 = ex2(fmaf(__uint_as_float(s[4 * i]), a.sl2, -l4.x));
         float p1 = ex2(fmaf(__uint_as_float(s[4 * i + 1]), a.sl2, -l4.y));
         float p2 = ex2(fmaf(__uint_as_float(s[4 * i + 2]), a.sl2, -l4.z));
         float p3 = ex2(fmaf(__uint_as_float(s[4 * i + 3]), a.sl2, -l4.w));
         if (masked) {
-          const int qc = q0 + hf * 64 + 4 * i;
+          const int qc = q0 + cg * CPT + 4 * i;
           p0 = (key_live && key <= qc) ? p0 : 0.f;
           p1 = (key_live && key <= qc + 1) ? p1 : 0.f;
           p2 = (key_live && key <= qc + 2) ? p2 : 0.f;
@@ -645,8 +678,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (warp == 2 && lane == 0) ATTN_TRACE(7, it);
       if (it >= 1) mbar_wait(g_done, (it - 1) & 1);  // P^T / dS^T columns free
       fence_after();
-      TMEM_ST32(tmem + lane_off + 256 + hf * 32, pp);
-      TMEM_ST32(tmem + lane_off + 320 + hf * 32, dd);
+      tmem_st_cols<CPT / 2>(tmem + lane_off + 256 + cg * (CPT / 2), pp);
+      tmem_st_cols<CPT / 2>(tmem + lane_off + 320 + cg * (CPT / 2), dd);
       tmem_wait_st();
       fence_before();
       __syncwarp();
@@ -654,9 +687,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     mbar_wait(g_done, (n_it - 1) & 1);
     fence_after();
-    const int64_t row = (int64_t)(row_base + key) * a.d + h * DH + hf * 32;
-    store_acc_rows(tmem + lane_off + 448 + hf * 32, a.g0 + row, a.scale, key < a.S);  // dK
-    store_acc_rows(tmem + lane_off + 384 + hf * 32, a.g1 + row, 1.f, key < a.S);  // dV
+    const int64_t row = (int64_t)(row_base + key) * a.d + h * DH + cg * GPT;
+    store_acc_rows<GPT>(tmem + lane_off + 448 + cg * GPT, a.g0 + row, a.scale, key_live);  // dK
+    store_acc_rows<GPT>(tmem + lane_off + 384 + cg * GPT, a.g1 + row, 1.f, key_live);      // dV
   }
   fence_before();
   __syncthreads();
@@ -677,17 +710,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                                            ~uintptr_t(1023));
   uint8_t* sQ = sm;
   uint8_t* sO = sm + 16384;
-  uint8_t* sK = sm + 2 * 16384;  // [2]
-  uint8_t* sV = sm + 4 * 16384;  // [2]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 6 * 16384);
+  uint8_t* sK = sm + 2 * 16384;   // [NR]
+  uint8_t* sV = sK + NR * 16384;  // [NR]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + NR * 16384);
   uint64_t* q_full = bar;
-  uint64_t* kv_full = bar + 1;   // [2]
-  uint64_t* kv_empty = bar + 3;  // [2]
-  uint64_t* s_full = bar + 5;
-  uint64_t* s_empty = bar + 6;
-  uint64_t* p_full = bar + 7;
-  uint64_t* g_done = bar + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9);
+  uint64_t* kv_full = bar + 1;        // [NR]
+  uint64_t* kv_empty = bar + 1 + NR;  // [NR]
+  uint64_t* s_full = bar + 1 + 2 * NR;
+  uint64_t* s_empty = s_full + 1;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* g_done = s_full + 3;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 4);
 
   const int nt = (a.S + TQ - 1) / TQ;
   const int qt = nt - 1 - blockIdx.x;
@@ -699,13 +732,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NR; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(s_empty, 8);
-    mbar_init(p_full, 8);
+    mbar_init(s_empty, SWB);
+    mbar_init(p_full, SWB);
     mbar_init(g_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -725,8 +758,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tma_load_2d(sQ, &tq, q_full, h * DH, row_base + q0);
       tma_load_2d(sO, &tdo, q_full, h * DH, row_base + q0);
       for (int j = 0; j < n_kt; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        const int st = j % NR;
+        mbar_wait(&kv_empty[st], ((j / NR) & 1) ^ 1);
         mbar_expect_tx(&kv_full[st], 32768);
         tma_load_2d(sK + st * 16384, &tk, &kv_full[st], h * DH, row_base + j * TK);
         tma_load_2d(sV + st * 16384, &tv, &kv_full[st], h * DH, row_base + j * TK);
@@ -741,7 +774,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_wait(q_full, 0);
       const uint32_t aq = su32(sQ), ao = su32(sO);
       auto issue_dq = [&](int j) {
-        const int st = j & 1;
+        const int st = j % NR;
         mbar_wait(p_full, j & 1);
         fence_after();
         const uint32_t bk = su32(sK + st * 16384);
@@ -753,8 +786,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         commit(&kv_empty[st]);
       };
       for (int j = 0; j < n_kt; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        const int st = j % NR;
+        mbar_wait(&kv_full[st], (j / NR) & 1);
         mbar_wait(s_empty, (j & 1) ^ 1);
         fence_after();
         const uint32_t bk = su32(sK + st * 16384), bv = su32(sV + st * 16384);
@@ -772,7 +805,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       issue_dq(n_kt - 1);
     }
   } else {
-    const int q = warp & 3, hf = (warp - 2) >> 2;  // lane quarter, key-column half
+    const int q = warp & 3, cg = (warp - 2) >> 2;  // lane quarter, key-column group
     const int r = q * 32 + lane;
     const int qrow = q0 + r;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
@@ -781,20 +814,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int j = 0; j < n_kt; ++j) {
       mbar_wait(s_full, j & 1);
       fence_after();
-      uint32_t s[64], dp[64];
-      TMEM_LD32(tmem + lane_off + hf * 64, s);
-      TMEM_LD32(tmem + lane_off + hf * 64 + 32, (s + 32));
-      TMEM_LD32(tmem + lane_off + 128 + hf * 64, dp);
-      TMEM_LD32(tmem + lane_off + 128 + hf * 64 + 32, (dp + 32));
+      uint32_t s[CPT], dp[CPT];
+      tmem_ld_cols<CPT>(tmem + lane_off + cg * CPT, s);
+      tmem_ld_cols<CPT>(tmem + lane_off + 128 + cg * CPT, dp);
       tmem_wait_ld();
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(s_empty);
-      const int k0 = j * TK + hf * 64;
+      const int k0 = j * TK + cg * CPT;
       const bool masked = (j * TK + TK > q0) || (j * TK + TK > a.S);
-      uint32_t dd[32];  // dS unscaled (the softmax scale is applied to dQ at the store)
+      uint32_t dd[CPT / 2];  // dS unscaled (the softmax scale is applied to dQ at the store)
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
+      for (int i = 0; i < CPT / 2; ++i) {
         float p0 = ex2(fmaf(__uint_as_float(s[2 * i]), a.sl2, -L));
         float p1 = ex2(fmaf(__uint_as_float(s[2 * i + 1]), a.sl2, -L));
         if (masked) {
@@ -805,7 +836,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
       if (j >= 1) mbar_wait(g_done, (j - 1) & 1);
       fence_after();
-      TMEM_ST32(tmem + lane_off + 256 + hf * 32, dd);
+      tmem_st_cols<CPT / 2>(tmem + lane_off + 256 + cg * (CPT / 2), dd);
       tmem_wait_st();
       fence_before();
       __syncwarp();
@@ -813,8 +844,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     mbar_wait(g_done, (n_kt - 1) & 1);
     fence_after();
-    store_acc_rows(tmem + lane_off + 320 + hf * 32,
-                   a.g0 + (int64_t)(row_base + qrow) * a.d + h * DH + hf * 32, a.scale, qrow < a.S);
+    store_acc_rows<GPT>(tmem + lane_off + 320 + cg * GPT,
+                        a.g0 + (int64_t)(row_base + qrow) * a.d + h * DH + cg * GPT, a.scale,
+                        qrow < a.S);
   }
   fence_before();
   __syncthreads();
@@ -854,21 +886,32 @@ CUtensorMap head_map(const void* base, int rows, int d, int box_rows = 128) {
   return m;
 }
 
-struct Scratch {
-  float* ptr = nullptr;
-  size_t n = 0;
-  std::mutex mu;
-};
-Scratch g_scratch;
+// per-device scratch for the debug entry point (engines pass their own workspace)
 float* scratch(size_t n) {
-  std::lock_guard<std::mutex> lk(g_scratch.mu);
-  if (n > g_scratch.n) {
-    if (g_scratch.ptr) cudaFree(g_scratch.ptr);
-    g_scratch.ptr = nullptr;
-    PH_CUDA(cudaMalloc(&g_scratch.ptr, n * sizeof(float)));
-    g_scratch.n = n;
+  static std::mutex mu;
+  static float* ptr[64] = {};
+  static size_t cap[64] = {};
+  int dev = 0;
+  PH_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (n > cap[dev]) {
+    if (ptr[dev]) cudaFree(ptr[dev]);
+    ptr[dev] = nullptr;
+    PH_CUDA(cudaMalloc(&ptr[dev], n * sizeof(float)));
+    cap[dev] = n;
   }
-  return g_scratch.ptr;
+  return ptr[dev];
+}
+
+// cudaFuncSetAttribute is per device: set once for each device that launches
+template <typename F>
+void set_smem_once(std::atomic<uint64_t>& done, F kern, int bytes) {
+  int dev = 0;
+  PH_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load() & bit) return;
+  PH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.fetch_or(bit);
 }
 
 }  // namespace
@@ -881,12 +924,18 @@ extern "C" int photon_debug_attn_trace(unsigned long long* out, int n) {
 
 bool attn_tc_supported(int dh, int d) { return dh == DH && (d % 8) == 0; }
 
+size_t attn_bwd_tc_ws_floats(int B, int S, int H) {
+  const size_t Spad = (size_t)(S + TQ - 1) / TQ * TQ;
+  return (size_t)2 * B * H * Spad;
+}
+
 void attn_bwd_tc(const bf16* q, const bf16* k, const bf16* v, const bf16* o, const bf16* dO,
                  const float* lse, bf16* dq, bf16* dk, bf16* dv, int B, int S, int H, int d,
-                 cudaStream_t st) {
+                 float* ws, cudaStream_t st) {
   if (d / H != DH) throw Error(PHOTON_ERR_CONFIG, "attn_bwd_tc: head dim must be 64");
   const int nt = (S + TQ - 1) / TQ, Spad = nt * TQ, rows = B * S;
-  float* Lp = scratch((size_t)2 * B * H * Spad);
+  if (!ws) ws = scratch(attn_bwd_tc_ws_floats(B, S, H));
+  float* Lp = ws;
   float* Dp = Lp + (size_t)B * H * Spad;
   attn_bwd_prep_kernel<<<std::min<int64_t>(((int64_t)B * S * H + 255) / 256, kNumSMs * 16), 256, 0,
                          st>>>(o, dO, lse, Lp, Dp, B, S, H, d, Spad);
@@ -894,16 +943,11 @@ void attn_bwd_tc(const bf16* q, const bf16* k, const bf16* v, const bf16* o, con
   const CUtensorMap mq = head_map(q, rows, d), mk = head_map(k, rows, d), mv = head_map(v, rows, d),
                     mo = head_map(dO, rows, d);
   BwdArgs a{S, H, d, Spad, rsqrtf((float)DH) * kLog2e, rsqrtf((float)DH), Lp, Dp, dk, dv};
-  constexpr int SMEM1 = 1024 + 6 * 16384 + 2048 + 256;
-  constexpr int SMEM2 = 1024 + 6 * 16384 + 256;
-  static bool cfg = false;
-  if (!cfg) {
-    PH_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM1));
-    PH_CUDA(cudaFuncSetAttribute(attn_bwd_dq_tc_kernel,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2));
-    cfg = true;
-  }
+  constexpr int SMEM1 = 1024 + (2 + 2 * NR) * 16384 + NR * 1024 + 256;
+  constexpr int SMEM2 = 1024 + (2 + 2 * NR) * 16384 + 256;
+  static std::atomic<uint64_t> cfg1{0}, cfg2{0};
+  set_smem_once(cfg1, attn_bwd_dkdv_tc_kernel, SMEM1);
+  set_smem_once(cfg2, attn_bwd_dq_tc_kernel, SMEM2);
   dim3 grid(nt, B * H);
   attn_bwd_dkdv_tc_kernel<<<grid, kBwdThreads, SMEM1, st>>>(mq, mk, mv, mo, a);
   PH_LAUNCH_CHECK();
@@ -920,12 +964,8 @@ void attn_fwd_tc(const bf16* q, const bf16* k, const bf16* v, bf16* o, float* ls
   const CUtensorMap mq = head_map(q, rows, d), mk = head_map(k, rows, d), mv = head_map(v, rows, d);
   const FwdArgs a{S, H, d, rsqrtf((float)DH) * kLog2e, o, lse};
   constexpr int SMEM = 1024 + 16384 * 5 + 256;
-  static bool cfg = false;
-  if (!cfg) {
-    PH_CUDA(cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 SMEM));
-    cfg = true;
-  }
+  static std::atomic<uint64_t> cfg{0};
+  set_smem_once(cfg, attn_fwd_tc_kernel, SMEM);
   dim3 grid((S + TQ - 1) / TQ, B * H);
   attn_fwd_tc_kernel<<<grid, kThreads, SMEM, st>>>(mq, mk, mv, a);
   PH_LAUNCH_CHECK();

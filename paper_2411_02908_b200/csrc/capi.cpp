@@ -531,7 +531,7 @@ int photon_debug_attention(int impl, int B, int S, int H, int d, const void* q, 
       auto O = static_cast<const bf16*>(o), DO = static_cast<const bf16*>(dO);
       if (impl == 2)
         k::attn_bwd_tc(Q, K, Vv, O, DO, lse, static_cast<bf16*>(dq), static_cast<bf16*>(dk),
-                       static_cast<bf16*>(dv), B, S, H, d, st);
+                       static_cast<bf16*>(dv), B, S, H, d, nullptr, st);
       else if (impl == 1)
         k::attn_bwd_mma(Q, K, Vv, O, DO, lse, scratch, static_cast<bf16*>(dq),
                         static_cast<bf16*>(dk), static_cast<bf16*>(dv), B, S, H, d, st);

@@ -85,7 +85,7 @@ class EngineT final : public Engine {
   float *x_, *xmid_, *mean1_, *rstd1_, *mean2_, *rstd2_, *meanf_, *rstdf_, *lse_;
   T *h_, *q_, *k_, *v_, *o_, *h2_, *pre_, *u_, *xf_, *logits_;
   // backward scratch
-  float *dx_, *dy_, *Dvec_, *part_;
+  float *dx_, *dy_, *Dvec_, *part_, *attn_ws_;
   T *dxT_, *dpre_, *dq_, *dk_, *dv_, *dO_;
   double* rowloss_;
   // timing
@@ -150,6 +150,9 @@ class EngineT final : public Engine {
       dx_ = carve<float>(p, M * d);
       dy_ = carve<float>(p, M * d);
       Dvec_ = carve<float>(p, rows_bhs);
+      attn_ws_ = sizeof(T) == 2 && k::attn_tc_supported((int)(d_ / H_), (int)d_)
+                     ? carve<float>(p, k::attn_bwd_tc_ws_floats((int)max_batch, (int)Smax_, (int)H_))
+                     : nullptr;
       part_ = carve<float>(p, part_floats);
       dxT_ = carve<T>(p, M * d);
       dpre_ = carve<T>(p, M * hid);
@@ -229,7 +232,7 @@ class EngineT final : public Engine {
                 int B, int S, int H, int d) {
     if constexpr (sizeof(T) == 2) {
       if (attn_mode == 1 && k::attn_tc_supported((int)(d_ / H_), d)) {
-        k::attn_bwd_tc(q, k, v, o, dO, lse, dq_, dk_, dv_, B, S, H, d, stream);
+        k::attn_bwd_tc(q, k, v, o, dO, lse, dq_, dk_, dv_, B, S, H, d, attn_ws_, stream);
         return;
       }
       if (use_mma_attn()) {

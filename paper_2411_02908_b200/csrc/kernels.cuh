@@ -57,13 +57,16 @@ void attn_bwd_mma(const bf16* q, const bf16* k, const bf16* v, const bf16* o, co
                   const float* lse, float* Dvec, bf16* dq, bf16* dk, bf16* dv, int B, int S, int H,
                   int d, cudaStream_t st);
 
-// ---- causal attention forward on tcgen05/TMEM/TMA (dh = 64), attn_tc.cu ----
+// ---- causal attention on tcgen05/TMEM/TMA (dh = 64), attn_tc.cu ----
 bool attn_tc_supported(int dh, int d);
 void attn_fwd_tc(const bf16* q, const bf16* k, const bf16* v, bf16* o, float* lse, int B, int S,
                  int H, int d, cudaStream_t st);
+// Fused deterministic backward; ws = attn_bwd_tc_ws_floats() floats of device
+// workspace owned by the caller (nullptr: a per-device scratch, debug use only).
+size_t attn_bwd_tc_ws_floats(int B, int S, int H);
 void attn_bwd_tc(const bf16* q, const bf16* k, const bf16* v, const bf16* o, const bf16* dO,
                  const float* lse, bf16* dq, bf16* dk, bf16* dv, int B, int S, int H, int d,
-                 cudaStream_t st);
+                 float* ws, cudaStream_t st);
 
 // ---- casts -------------------------------------------------------------------
 void f64_to_f32(const double* in, float* out, uint64_t n, cudaStream_t st);

@@ -74,3 +74,33 @@ def test_attention_photon125m_head_shape():
 @pytest.mark.parametrize("B,S,H", [(2, 128, 2), (1, 256, 3), (2, 200, 2), (1, 64, 1), (3, 384, 2)])
 def test_attention_tcgen05_forward(B, S, H):
     _run(2, B, S, H, 64 * H)
+
+
+def test_attention_tcgen05_backward_deterministic():
+    # the fused backward adds dQ partial sums in a fixed key-tile order: two runs
+    # are bit-identical, and the result does not depend on CTA scheduling
+    from paper_2411_02908_b200 import _capi as A
+
+    B, S, H = 2, 1000, 3
+    d = 64 * H
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q, k, v, dO = (torch.randn(B, S, d, device="cuda", generator=g).bfloat16() for _ in range(4))
+    o = torch.empty_like(q)
+    lse = torch.empty(B * H * S, device="cuda")
+    err = A.photon_err()
+    ms = C.c_double()
+    assert A.lib().photon_debug_attention(2, B, S, H, d, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                          o.data_ptr(), lse.data_ptr(), None, None, None, None,
+                                          None, C.byref(ms), C.byref(err)) == 0, err.msg
+    outs = []
+    for _ in range(3):
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
+        assert A.lib().photon_debug_attention(2, B, S, H, d, q.data_ptr(), k.data_ptr(),
+                                              v.data_ptr(), o.data_ptr(), lse.data_ptr(),
+                                              dO.data_ptr(), None, dq.data_ptr(), dk.data_ptr(),
+                                              dv.data_ptr(), C.byref(ms), C.byref(err)) == 0, err.msg
+        outs.append((dq, dk, dv))
+    for x, y in zip(outs[0], outs[1]):
+        assert torch.equal(x, y)
+    for x, y in zip(outs[0], outs[2]):
+        assert torch.equal(x, y)

@@ -1,4 +1,5 @@
-"""Timeline of one dkdv CTA (key tile 0, head 200) from the instrumented build.
+"""Timeline of one backward CTA (key tile 0, head 200) from the instrumented build.
+  (TRACE_NAMES=fused for the fused kernel's stamp names)
   PHOTON_BUILD_TRACE=1 python -m paper_2411_02908_b200.build
   PHOTON_LIB=paper_2411_02908_b200/libphoton_trace.so python tools/attn_trace.py"""
 import ctypes as C
@@ -31,6 +32,9 @@ rc = A.lib().photon_debug_attn_trace(buf, 64 * 64)
 assert rc == 0, rc
 names = os.environ.get("TRACE_NAMES", "prod_free,mma_qfull,mma_sfree,mma_pready,mma_gissued,"
                        "sm_sready,sm_loaded,sm_computed,sm_gdone,sm_stored").split(",")
+if names == ["fused"]:
+    names = ("prod_free,mma_qfull,mma_sfree,mma_pready,mma_dqfree,sm_sready,sm_computed,sm_gdone,"
+             "sm_pfull,dr_semok,dr_dqfull,dr_release").split(",")
 t0 = min(buf[e * 64] for e in range(len(names)) if buf[e * 64])
 print("cycles relative to the first stamp; one row per iteration")
 print("it " + " ".join(f"{n:>11s}" for n in names))
