@@ -657,20 +657,28 @@ int photon_debug_boundary(int device, uint64_t n_params, int rank, int world,
     cudaEvent_t e0, e1;
     PH_CUDA(cudaEventCreate(&e0));
     PH_CUDA(cudaEventCreate(&e1));
+    std::unique_ptr<PeerBoundary> p2p;
     try {
-      for (int i = 0; i < 2; ++i)  // warm-up (NCCL connection setup)
-        round_boundary(comm, rank, world, P, shard, surv, local, recv.ptr, ptrs, theta.ptr,
-                       vel.ptr, *server, st);
+      if (world > 1 && use_peer_boundary()) {
+        p2p = std::make_unique<PeerBoundary>(comm, rank, world, device);
+        p2p->publish(local, 1, theta.ptr, st);
+      }
+      auto once = [&] {
+        if (p2p) p2p->run(surv, shard, vel.ptr, *server, st);
+        else round_boundary(comm, rank, world, P, shard, surv, local, recv.ptr, ptrs, theta.ptr,
+                            vel.ptr, *server, st);
+      };
+      for (int i = 0; i < 2; ++i) once();  // warm-up (connection setup)
       PH_CUDA(cudaEventRecord(e0, st));
-      for (int i = 0; i < iters; ++i)
-        round_boundary(comm, rank, world, P, shard, surv, local, recv.ptr, ptrs, theta.ptr,
-                       vel.ptr, *server, st);
+      for (int i = 0; i < iters; ++i) once();
       PH_CUDA(cudaEventRecord(e1, st));
       PH_CUDA(cudaEventSynchronize(e1));
       float ms = 0.f;
       PH_CUDA(cudaEventElapsedTime(&ms, e0, e1));
       *ms_out = ms / iters;
+      p2p.reset();
     } catch (...) {
+      p2p.reset();
       if (comm) nccl().CommDestroy(comm);
       cudaEventDestroy(e0);
       cudaEventDestroy(e1);

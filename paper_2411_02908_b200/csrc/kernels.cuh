@@ -96,6 +96,21 @@ void sgd_f64(double* p, const double* g, uint64_t n, const double* norm, double 
 
 // ---- aggregation (param_vector.cpp:120-152, optim.cpp:124-159) -----------------
 // kind: 0 FedAvg, 1 momentum.  models: device array of k device pointers.
+// Round boundary over peer memory (optim.cu): models[c] = surviving client c's
+// full model (ascending slot, IPC-mapped or local), replicas[g] = rank g's
+// theta buffer; this rank updates [off, off+len) of every replica.
+constexpr int kMaxPeerModels = 16;
+constexpr int kMaxPeerWorld = 16;
+struct PeerBoundaryArgs {
+  const float* models[kMaxPeerModels];
+  float* replicas[kMaxPeerWorld];
+  float* vel;  // this rank's velocity shard [len]
+  uint64_t off, len;
+  int n, world, rank, kind, nesterov;
+  float eta, mu;
+};
+void boundary_p2p(const PeerBoundaryArgs& a, cudaStream_t st);
+
 template <typename T>
 void aggregate(const T* const* models, int k, uint64_t n, T* theta, T* velocity, int kind,
                double eta, double mu, int nesterov, cudaStream_t st);

@@ -290,6 +290,64 @@ __global__ void __launch_bounds__(256) aggregate_kernel(const T* const* __restri
   }
 }
 
+// ---- round boundary over peer memory ---------------------------------------------
+// One kernel per rank does the reduce-scatter, the update and the all-gather:
+// for its shard [off, off+len) it loads every surviving client's model straight
+// from the owning GPU's HBM over NVLink (IPC-mapped pointers), forms the
+// anchored mean in ascending client order, applies the outer step with the
+// resident theta_t / velocity shards, and stores theta_{t+1} into EVERY rank's
+// replica.  Same per-element arithmetic as aggregate_kernel (bit-identical for
+// any world size); wire bytes per GPU = 2 (G-1)/G * P * 4 as for ring all-reduce.
+__global__ void __launch_bounds__(256) boundary_p2p_kernel(const __grid_constant__ PeerBoundaryArgs a) {
+  const int k = a.n;
+  const float nk = (float)k;
+  const float* const* models = a.models;
+  const uint64_t nv = a.len / 4, base = a.off / 4;
+  float* mine = a.replicas[a.rank];
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nv;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    // issue every client's load before the first use (NVLink latency ~1-2k cycles)
+    float4 m[kMaxPeerModels];
+#pragma unroll
+    for (int c = 0; c < kMaxPeerModels; ++c)
+      if (c < k) m[c] = reinterpret_cast<const float4*>(models[c])[base + i];
+    float4 th = make_float4(0.f, 0.f, 0.f, 0.f), ve = th;
+    if (a.kind != 0) {
+      th = reinterpret_cast<const float4*>(mine)[base + i];
+      ve = reinterpret_cast<const float4*>(a.vel)[i];
+    }
+    float anchor[4] = {m[0].x, m[0].y, m[0].z, m[0].w};
+    float corr[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int c = 1; c < kMaxPeerModels; ++c) {
+      if (c < k) {
+        corr[0] += m[c].x - anchor[0];
+        corr[1] += m[c].y - anchor[1];
+        corr[2] += m[c].z - anchor[2];
+        corr[3] += m[c].w - anchor[3];
+      }
+    }
+    float t4[4] = {th.x, th.y, th.z, th.w}, v4[4] = {ve.x, ve.y, ve.z, ve.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float mean = corr[e] != 0.f ? anchor[e] + corr[e] / nk : anchor[e];
+      outer_update(t4[e], v4[e], mean, a.kind, a.eta, a.mu, a.nesterov);
+    }
+    const float4 out = make_float4(t4[0], t4[1], t4[2], t4[3]);
+    for (int g = 0; g < a.world; ++g) reinterpret_cast<float4*>(a.replicas[g])[base + i] = out;
+    if (a.kind != 0) reinterpret_cast<float4*>(a.vel)[i] = make_float4(v4[0], v4[1], v4[2], v4[3]);
+  }
+  __threadfence_system();  // the peers' copies are complete before the closing barrier
+}
+
+void boundary_p2p(const PeerBoundaryArgs& a, cudaStream_t st) {
+  if (a.n < 1 || a.n > kMaxPeerModels || a.world < 1 || a.world > kMaxPeerWorld || a.len % 4 ||
+      a.off % 4)
+    throw Error(PHOTON_ERR_USAGE, "boundary_p2p: bad arguments");
+  boundary_p2p_kernel<<<kNumSMs * 8, 256, 0, st>>>(a);
+  PH_LAUNCH_CHECK();
+}
+
 template <typename T>
 void aggregate(const T* const* models, int k, uint64_t n, T* theta, T* velocity, int kind,
                double eta, double mu, int nesterov, cudaStream_t st) {

@@ -16,6 +16,7 @@
 #include <cmath>
 #include <limits>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 
@@ -30,6 +31,11 @@ namespace photon {
     if (r_ != ncclSuccess)                                                               \
       throw Error(PHOTON_ERR_NCCL, std::string(#call) + ": " + nccl().GetErrorString(r_)); \
   } while (0)
+
+bool use_peer_boundary() {
+  const char* e = std::getenv("PHOTON_BOUNDARY");
+  return !(e && std::string(e) == "nccl");
+}
 
 // optim.cpp:105-113
 void validate_server(const photon_server_cfg& s) {
@@ -87,11 +93,13 @@ Runner::Runner(Ctx* c, const photon_fed_cfg& f, const photon_train_cfg& t,
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof(id));
     PH_NCCL(nccl().CommInitRank(&comm, ws, id, rk));
+    if (use_peer_boundary()) p2p = std::make_unique<PeerBoundary>(comm, rk, ws, c->device);
   }
   PH_CUDA(cudaStreamSynchronize(c->stream));
 }
 
 Runner::~Runner() {
+  p2p.reset();
   if (comm) nccl().CommDestroy(comm);
   if (ev_a) cudaEventDestroy(ev_a);
   if (ev_b) cudaEventDestroy(ev_b);
@@ -255,8 +263,13 @@ void Runner::run_round(photon_round_record* rec) {
       recv = d_recv.ptr;
     }
   }
-  round_boundary(comm, rank, world, P, shard, surv, local_models.data(), recv, d_model_ptrs,
-                 d_theta.ptr, d_vel.ptr, server, st);
+  if (p2p && PeerBoundary::supported(n, world)) {
+    p2p->publish(local_models.data(), (int)local_models.size(), d_theta.ptr, st);
+    p2p->run(surv, shard, d_vel.ptr, server, st);
+  } else {
+    round_boundary(comm, rank, world, P, shard, surv, local_models.data(), recv, d_model_ptrs,
+                   d_theta.ptr, d_vel.ptr, server, st);
+  }
   PH_CUDA(cudaEventRecord(ev_c, st));
   PH_CUDA(cudaEventSynchronize(ev_c));
   if (K >= 2) ++sync_events;

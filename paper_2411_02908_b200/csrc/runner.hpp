@@ -4,12 +4,14 @@
 
 #include <nccl.h>
 
+#include <memory>
 #include <set>
 #include <string>
 #include <utility>
 #include <vector>
 
 #include "ctx.hpp"
+#include "p2p.hpp"
 
 namespace photon {
 
@@ -21,6 +23,9 @@ struct Runner {
   const Plan* plan;
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
+  // world > 1: the boundary over NVLink peer memory (PHOTON_BOUNDARY=nccl selects
+  // the NCCL send/recv + all-gather path instead; both are bit-identical)
+  std::unique_ptr<PeerBoundary> p2p;
 
   uint64_t P = 0, shard = 0, Ppad = 0;
   uint64_t next_round = 0;
@@ -78,6 +83,7 @@ struct Runner {
 };
 
 void validate_server(const photon_server_cfg& s);
+bool use_peer_boundary();  // world > 1: NVLink peer memory unless PHOTON_BOUNDARY=nccl
 
 // The round boundary (aggregator.cpp:177-179) over NCCL: every surviving
 // slot's model goes in 1/world shards to the shard owners in ascending slot
