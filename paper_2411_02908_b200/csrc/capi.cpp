@@ -2,6 +2,7 @@
 // (photon::Error, carrying fedsim/errors.h-equivalent codes) are converted to
 // status codes + photon_err here and nowhere else.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -640,7 +641,7 @@ int photon_debug_boundary(int device, uint64_t n_params, int rank, int world,
     theta.reserve(Ppad);
     vel.reserve(world > 1 ? shard : Ppad);
     model.reserve(Ppad);
-    if (world > 1) recv.reserve((size_t)world * shard);
+    if (world > 1 && !use_peer_boundary(Ppad * 4)) recv.reserve((size_t)world * shard);
     PH_CUDA(cudaMemsetAsync(theta.ptr, 0, Ppad * 4, st));
     PH_CUDA(cudaMemsetAsync(vel.ptr, 0, vel.n * 4, st));
     PH_CUDA(cudaMemsetAsync(model.ptr, 0, Ppad * 4, st));
@@ -659,7 +660,7 @@ int photon_debug_boundary(int device, uint64_t n_params, int rank, int world,
     PH_CUDA(cudaEventCreate(&e1));
     std::unique_ptr<PeerBoundary> p2p;
     try {
-      if (world > 1 && use_peer_boundary()) {
+      if (world > 1 && use_peer_boundary(Ppad * 4)) {
         p2p = std::make_unique<PeerBoundary>(comm, rank, world, device);
         p2p->publish(local, 1, theta.ptr, st);
       }

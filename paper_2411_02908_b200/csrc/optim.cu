@@ -5,6 +5,7 @@
 // the reference's FMA-free x86-64 build, so the f64 instantiations reproduce
 // ParamVector::mean / sub / server_step / adamw_step / sgd_step bit for bit.
 // Citations: /root/reference/proj/core/src/{param_vector,optim}.cpp.
+#include <cstdlib>
 #include "kernels.cuh"
 
 namespace photon {
@@ -298,6 +299,7 @@ __global__ void __launch_bounds__(256) aggregate_kernel(const T* const* __restri
 // resident theta_t / velocity shards, and stores theta_{t+1} into EVERY rank's
 // replica.  Same per-element arithmetic as aggregate_kernel (bit-identical for
 // any world size); wire bytes per GPU = 2 (G-1)/G * P * 4 as for ring all-reduce.
+template <int KM>  // KM >= a.n: registers sized to the client count
 __global__ void __launch_bounds__(256) boundary_p2p_kernel(const __grid_constant__ PeerBoundaryArgs a) {
   const int k = a.n;
   const float nk = (float)k;
@@ -307,9 +309,9 @@ __global__ void __launch_bounds__(256) boundary_p2p_kernel(const __grid_constant
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nv;
        i += (uint64_t)gridDim.x * blockDim.x) {
     // issue every client's load before the first use (NVLink latency ~1-2k cycles)
-    float4 m[kMaxPeerModels];
+    float4 m[KM];
 #pragma unroll
-    for (int c = 0; c < kMaxPeerModels; ++c)
+    for (int c = 0; c < KM; ++c)
       if (c < k) m[c] = reinterpret_cast<const float4*>(models[c])[base + i];
     float4 th = make_float4(0.f, 0.f, 0.f, 0.f), ve = th;
     if (a.kind != 0) {
@@ -319,7 +321,7 @@ __global__ void __launch_bounds__(256) boundary_p2p_kernel(const __grid_constant
     float anchor[4] = {m[0].x, m[0].y, m[0].z, m[0].w};
     float corr[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int c = 1; c < kMaxPeerModels; ++c) {
+    for (int c = 1; c < KM; ++c) {
       if (c < k) {
         corr[0] += m[c].x - anchor[0];
         corr[1] += m[c].y - anchor[1];
@@ -344,7 +346,13 @@ void boundary_p2p(const PeerBoundaryArgs& a, cudaStream_t st) {
   if (a.n < 1 || a.n > kMaxPeerModels || a.world < 1 || a.world > kMaxPeerWorld || a.len % 4 ||
       a.off % 4)
     throw Error(PHOTON_ERR_USAGE, "boundary_p2p: bad arguments");
-  boundary_p2p_kernel<<<kNumSMs * 8, 256, 0, st>>>(a);
+  // 8 CTAs per SM: twice the resident count (62-106 registers), more remote
+  // loads in flight than 2 or 4 per SM (measured)
+  const int grid = kNumSMs * 8;
+  if (a.n <= 2) boundary_p2p_kernel<2><<<grid, 256, 0, st>>>(a);
+  else if (a.n <= 4) boundary_p2p_kernel<4><<<grid, 256, 0, st>>>(a);
+  else if (a.n <= 8) boundary_p2p_kernel<8><<<grid, 256, 0, st>>>(a);
+  else boundary_p2p_kernel<kMaxPeerModels><<<grid, 256, 0, st>>>(a);
   PH_LAUNCH_CHECK();
 }
 

@@ -32,9 +32,11 @@ namespace photon {
       throw Error(PHOTON_ERR_NCCL, std::string(#call) + ": " + nccl().GetErrorString(r_)); \
   } while (0)
 
-bool use_peer_boundary() {
+bool use_peer_boundary(uint64_t replica_bytes) {
   const char* e = std::getenv("PHOTON_BOUNDARY");
-  return !(e && std::string(e) == "nccl");
+  if (e && std::string(e) == "nccl") return false;
+  if (e && std::string(e) == "p2p") return true;
+  return PeerBoundary::fits(replica_bytes);
 }
 
 // optim.cpp:105-113
@@ -93,7 +95,7 @@ Runner::Runner(Ctx* c, const photon_fed_cfg& f, const photon_train_cfg& t,
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof(id));
     PH_NCCL(nccl().CommInitRank(&comm, ws, id, rk));
-    if (use_peer_boundary()) p2p = std::make_unique<PeerBoundary>(comm, rk, ws, c->device);
+    if (use_peer_boundary(Ppad * 4)) p2p = std::make_unique<PeerBoundary>(comm, rk, ws, c->device);
   }
   PH_CUDA(cudaStreamSynchronize(c->stream));
 }

@@ -83,7 +83,9 @@ struct Runner {
 };
 
 void validate_server(const photon_server_cfg& s);
-bool use_peer_boundary();  // world > 1: NVLink peer memory unless PHOTON_BOUNDARY=nccl
+// world > 1: NVLink peer memory for replicas up to PeerBoundary::fits, else NCCL;
+// PHOTON_BOUNDARY=nccl|p2p forces either path
+bool use_peer_boundary(uint64_t replica_bytes);
 
 // The round boundary (aggregator.cpp:177-179) over NCCL: every surviving
 // slot's model goes in 1/world shards to the shard owners in ascending slot

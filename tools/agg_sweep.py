@@ -22,7 +22,7 @@ import torch  # noqa: E402
 from paper_2411_02908_b200 import _capi as A  # noqa: E402
 from paper_2411_02908_b200 import fedsim as F  # noqa: E402
 
-NS = [164044480, 1419154624, 6865216704]
+NS = [int(x) for x in os.environ.get("PHOTON_AGG_NS", "164044480,1419154624,6865216704").split(",")]
 world = int(os.environ.get("WORLD_SIZE", "1"))
 rank = int(os.environ.get("RANK", "0"))
 local = int(os.environ.get("LOCAL_RANK", "0"))
