@@ -25,6 +25,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <atomic>
 #include <mutex>
 
 #include "gemm.cuh"
@@ -702,10 +703,12 @@ void launch(const CUtensorMap& a, const CUtensorMap& b, const EpiMaps& em, const
   static_assert(STAGES >= 3, "operand ring too shallow");
   constexpr int SMEM = STAGES * STAGE_BYTES + kEpiWarps * kEpiBytesPerWarp + 1024 + 512;
   auto kern = gemm_tc_kernel<BN, A_MN, B_MN, NCTA>;
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<uint64_t> configured{0};  // per device
+  int dev = 0;
+  PH_CUDA(cudaGetDevice(&dev));
+  if (!(configured.load() & (1ull << (dev & 63)))) {
     PH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-    configured = true;
+    configured.fetch_or(1ull << (dev & 63));
   }
   if (NCTA == 1) {
     kern<<<grid, kThreads, SMEM, st>>>(a, b, em, p);
@@ -727,22 +730,22 @@ void launch(const CUtensorMap& a, const CUtensorMap& b, const EpiMaps& em, const
   PH_LAUNCH_CHECK();
 }
 
-struct Workspace {
-  float* ptr = nullptr;
-  size_t n = 0;
-  std::mutex mu;
-};
-Workspace g_ws;
-
+// split-K partials, per device (launches on one device are stream-ordered by
+// their engine; the buffer only grows)
 float* workspace(size_t n) {
-  std::lock_guard<std::mutex> lk(g_ws.mu);
-  if (n > g_ws.n) {
-    if (g_ws.ptr) cudaFree(g_ws.ptr);
-    g_ws.ptr = nullptr;
-    PH_CUDA(cudaMalloc(&g_ws.ptr, n * sizeof(float)));
-    g_ws.n = n;
+  static std::mutex mu;
+  static float* ptr[64] = {};
+  static size_t cap[64] = {};
+  int dev = 0;
+  PH_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (n > cap[dev]) {
+    if (ptr[dev]) cudaFree(ptr[dev]);
+    ptr[dev] = nullptr;
+    PH_CUDA(cudaMalloc(&ptr[dev], n * sizeof(float)));
+    cap[dev] = n;
   }
-  return g_ws.ptr;
+  return ptr[dev];
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -772,11 +775,11 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
     const char* e = std::getenv("PHOTON_GEMM_PAIR");  // 0 never, 1 by shape, 2 always
     return e ? std::atoi(e) : 1;
   }();
-  // CTA pairs (256 x 256 tiles) where they measured faster on the 125M shapes
-  // (tools/gemm_bench.py): wide tiles without split-K.
-  const int kb_all = (g.K + BK - 1) / BK;
-  const bool split_needed = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN) < kNumSMs && kb_all >= 16;
-  const bool pair_ok = BN == 256 && g.M > BM && !split_needed;
+  // CTA pairs (256 x 256 tiles) wherever N is a 256 multiple-ish and M spans
+  // more than one 128-row tile: wide tiles without split-K, and the split-K
+  // weight gradients (d x d, d x 4d, 4d x d: 25-30% faster than single-CTA
+  // 128 x 256 tiles in tools/gemm_bench.py).
+  const bool pair_ok = BN == 256 && g.M > BM;
   const int ncta = (pair_env == 2 || (pair_env == 1 && pair_ok)) && BN == 256 && g.M > BM ? 2 : 1;
   const int slots = kNumSMs / ncta;  // concurrent tile workers
   TcParams p{};

@@ -1,6 +1,7 @@
 // kernels.cu -- embedding, layer norm, bias-gradient column sums, fused
 // softmax cross-entropy and the SIMT attention path of the client step.
 // Citations: /root/reference/proj/core/src/tensor.cpp.
+#include <atomic>
 #include "kernels.cuh"
 #include "sm100.cuh"
 
@@ -796,11 +797,13 @@ void ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count
   if constexpr (sizeof(T) == 2) {
     if (V % 8 == 0 && ce_pipe_smem(V) <= (size_t)kCePipeMaxSmem && M > 0 &&
         (reinterpret_cast<uintptr_t>(logits) & 15) == 0) {
-      static bool attr = false;
-      if (!attr) {
+      static std::atomic<uint64_t> attr{0};  // per device
+      int dev = 0;
+      PH_CUDA(cudaGetDevice(&dev));
+      if (!(attr.load() & (1ull << (dev & 63)))) {
         PH_CUDA(cudaFuncSetAttribute(ce_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      kCePipeMaxSmem));
-        attr = true;
+        attr.fetch_or(1ull << (dev & 63));
       }
       ce_pipe_kernel<<<std::min(M, kNumSMs), kCePipeThreads + 32, ce_pipe_smem(V), st>>>(
           logits, targets, M, V, inv_count, rowloss, write_grad ? 1 : 0);

@@ -18,7 +18,9 @@ CASES = [
     ("dX  w2   gelu'", M, hid, d, 1, 1, 5, 1),
     ("dX  w1   f32", M, d, hid, 1, 1, 0, 0),
     ("dX  head f32", M, d, V, 1, 1, 0, 0),
+    ("dX  dxd  accum f32", M, d, d, 1, 1, 1, 0),
     ("dW  dxd  (split-K)", d, d, M, 0, 0, 0, 0),
+    ("dW  w2", hid, d, M, 0, 0, 0, 0),
     ("dW  w1", d, hid, M, 0, 0, 0, 0),
     ("dW  head", d, V, M, 0, 0, 0, 0),
 ]

@@ -55,8 +55,8 @@ def main(rep, stem):
         lines.append(f"{d['kernel'][:60]} | {d['grid']} | {us:.1f} | {rd/1e6:.1f} | {wr/1e6:.1f} | "
                      f"{(rd+wr)/us/1e3:.0f} | "
                      f"{d.get('sm__inst_executed_pipe_tmem.avg.pct_of_peak_sustained_active', float('nan')):.1f} | "
-                     f"{d['sm__throughput.avg.pct_of_peak_sustained_elapsed']:.1f} | "
-                     f"{d['launch__registers_per_thread']:.0f}")
+                     f"{d.get('sm__throughput.avg.pct_of_peak_sustained_elapsed', float('nan')):.1f} | "
+                     f"{d.get('launch__registers_per_thread', float('nan')):.0f}")
         per[d["kernel"]].append(d)
     summary = {}
     for k, ds in per.items():
