@@ -50,6 +50,23 @@ MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 METRIC = "tokens/s/round at 1-8 B200 (125M); FedAvg aggregate GB/s vs roofline"
 
 
+NCU_GEMM = os.path.join(ROOT, "profiles", "r01_ncu_gemm_dram.json")
+
+
+def _gemm_traffic():
+    """Mean DRAM bytes (read + write) per gemm_tc launch over the GEMM launches
+    of one 125M client step, from the committed ncu capture
+    (tools/capture_profiles.sh -> profiles/r01_ncu_gemm_dram.json), or None."""
+    try:
+        with open(NCU_GEMM) as f:
+            ks = json.load(f)["kernels"]
+        n = sum(v["launches"] for k, v in ks.items() if "gemm_tc" in k)
+        b = sum(v["launches"] * v["dram_bytes_per_launch"] for k, v in ks.items() if "gemm_tc" in k)
+        return b / n if n else None
+    except Exception:
+        return None
+
+
 def _peaks():
     try:
         with open(MEASURED_PEAKS) as f:
@@ -316,7 +333,8 @@ def run_ours(args):
         torch.cuda.synchronize(local)
         wall = time.perf_counter() - t0
     _barrier(world)
-    dev_ms_max, wall_max = _max_over_ranks([dev_ms, wall], world, local)
+    agg_ms = sum(r.aggregate_ms for r in recs) / max(len(recs), 1)
+    dev_ms_max, wall_max, agg_ms_max = _max_over_ranks([dev_ms, wall, agg_ms], world, local)
     tokens_total = K * tau * B * S * args.steps
     value = tokens_total / (dev_ms_max / 1000.0)
     e2e = tokens_total / wall_max
@@ -364,12 +382,24 @@ def run_ours(args):
         ach = prof["gemm_flops"] / (prof["gemm_ms"] * 1e-3) / 1e12 if prof["gemm_ms"] else 0.0
         line["roofline"] = {"kernel": "gemm_tc (tcgen05, all client-step contractions)",
                             "bound": "tensor", "achieved": ach, "peak": bf16_sus,
-                            "unit": "TFLOP/s", "frac": ach / bf16_sus, "traffic": None,
+                            "unit": "TFLOP/s", "frac": ach / bf16_sus,
+                            "traffic": _gemm_traffic() if args.model == "125m" else None,
+                            "traffic_unit": "DRAM bytes per launch (ncu, mean over one step's GEMMs)",
                             "peak_source": f"{peak_src} bf16 sustained"}
         line["kernel_ms_per_round"] = prof
         line["gpu_launches"] = int(prof["launches"]) * args.steps
     if agg:
         line["aggregation"] = agg
+    if world > 1:
+        # the round boundary as run (NVLink peer-memory kernel, or NCCL above
+        # PeerBoundary::fits): per-GPU wire bytes 2(G-1)/G * P * 4 over the
+        # boundary time (includes the stats all-reduce and the pointer exchange)
+        P = model.param_count()
+        wire = 2 * (world - 1) / world * P * 4
+        line["boundary"] = {"ms_max_over_ranks": agg_ms_max, "wire_bytes_per_gpu": wire,
+                            "busbw_gbs": wire / (agg_ms_max * 1e-3) / 1e9, "nvlink_gbs": 900.0,
+                            "frac": wire / (agg_ms_max * 1e-3) / 1e9 / 900.0,
+                            "path": "p2p" if os.environ.get("PHOTON_BOUNDARY") != "nccl" else "nccl"}
     if world == 1 and not args.no_cpu and args.model != "125m":
         # the f64 reference state of 1.3B / 7B exceeds host RAM
         line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "n/a",
