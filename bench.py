@@ -333,7 +333,7 @@ def run_ours(args):
         torch.cuda.synchronize(local)
         wall = time.perf_counter() - t0
     _barrier(world)
-    agg_ms = sum(r.aggregate_ms for r in recs) / max(len(recs), 1)
+    agg_ms = sum(r.boundary_ms for r in recs) / max(len(recs), 1)
     dev_ms_max, wall_max, agg_ms_max = _max_over_ranks([dev_ms, wall, agg_ms], world, local)
     tokens_total = K * tau * B * S * args.steps
     value = tokens_total / (dev_ms_max / 1000.0)
@@ -393,7 +393,8 @@ def run_ours(args):
     if world > 1:
         # the round boundary as run (NVLink peer-memory kernel, or NCCL above
         # PeerBoundary::fits): per-GPU wire bytes 2(G-1)/G * P * 4 over the
-        # boundary time (includes the stats all-reduce and the pointer exchange)
+        # boundary's device time (RoundRecord.boundary_ms: the fused kernel once
+        # every rank has arrived -- rank skew in the local phase excluded)
         P = model.param_count()
         wire = 2 * (world - 1) / world * P * 4
         line["boundary"] = {"ms_max_over_ranks": agg_ms_max, "wire_bytes_per_gpu": wire,

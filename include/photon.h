@@ -20,7 +20,7 @@
 extern "C" {
 #endif
 
-#define PHOTON_ABI_VERSION 1
+#define PHOTON_ABI_VERSION 2
 
 /* status codes (fedsim/errors.h) */
 enum {
@@ -123,6 +123,9 @@ typedef struct {
   uint64_t d2h_bytes;         /* results read back device->host this round */
   double eval_ppl;            /* RoundRecord::eval_ppl: perplexity of theta_{t+1} on the
                                  held-out set when the eval cadence fires, else NaN */
+  double boundary_ms;         /* device ms of the boundary's data movement + update alone
+                                 (peer-memory path: the fused kernel, after the slowest
+                                 rank arrived; NCCL path / one GPU: the whole boundary) */
 } photon_round_record;
 
 typedef struct photon_ctx photon_ctx;       /* one GPU: device state of one client slot */

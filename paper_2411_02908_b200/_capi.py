@@ -64,7 +64,8 @@ class photon_round_record(C.Structure):
     _fields_ = [("round", u64), ("n_sampled", u64), ("sampled_ids", u64 * 64),
                 ("mean_client_loss", dbl), ("min_client_loss", dbl), ("max_client_loss", dbl),
                 ("local_ms", dbl), ("aggregate_ms", dbl), ("round_ms", dbl), ("tokens", u64),
-                ("host_ms", dbl), ("h2d_bytes", u64), ("d2h_bytes", u64), ("eval_ppl", dbl)]
+                ("host_ms", dbl), ("h2d_bytes", u64), ("d2h_bytes", u64), ("eval_ppl", dbl),
+                ("boundary_ms", dbl)]
 
 
 _SIGS = {
@@ -189,7 +190,7 @@ def lib():
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
-        if L.photon_abi_version() != 1:
+        if L.photon_abi_version() != 2:
             raise ImportError("libphoton.so ABI version mismatch")
         _lib = L
     return _lib

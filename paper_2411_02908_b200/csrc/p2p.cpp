@@ -56,18 +56,40 @@ PeerBoundary::PeerBoundary(ncclComm_t comm, int rank, int world, int device)
   models_.assign(world, {});
   thetas_.assign(world, nullptr);
   peer_flags_.assign(world, nullptr);
+  PH_CUDA(cudaEventCreate(&ev0_));
+  PH_CUDA(cudaEventCreate(&ev1_));
+}
+
+float PeerBoundary::last_kernel_ms() const {
+  float ms = 0.f;
+  PH_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
+  return ms;
 }
 
 PeerBoundary::~PeerBoundary() {
+  if (ev0_) cudaEventDestroy(ev0_);
+  if (ev1_) cudaEventDestroy(ev1_);
   for (auto& kv : opened_) cudaIpcCloseMemHandle(kv.second);
 }
 
 PeerBoundary::Region PeerBoundary::export_ptr(const void* p) const {
   Region r;
   std::memset(&r, 0, sizeof(r));
+  // driver entry point resolved at run time: libphoton.so must load on hosts
+  // without libcuda.so (the CPU test suite)
+  using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static GetRange get_range = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &qr) != cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<GetRange>(f);
+  }();
+  if (!get_range) throw Error(PHOTON_ERR_CUDA, "cuMemGetAddressRange unavailable");
   CUdeviceptr base = 0;
   size_t size = 0;
-  if (cuMemGetAddressRange(&base, &size, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS)
+  if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS)
     throw Error(PHOTON_ERR_CUDA, "peer boundary: pointer is not a device allocation");
   PH_CUDA(cudaIpcGetMemHandle(&r.handle, reinterpret_cast<void*>(base)));
   r.offset = reinterpret_cast<uint64_t>(p) - (uint64_t)base;
@@ -158,7 +180,9 @@ void PeerBoundary::run(const std::vector<int>& surv, uint64_t shard, float* vel,
   a.eta = (float)server.eta;
   a.mu = (float)server.momentum;
   barrier(st);  // every rank's client models are final
+  PH_CUDA(cudaEventRecord(ev0_, st));
   k::boundary_p2p(a, st);
+  PH_CUDA(cudaEventRecord(ev1_, st));
   barrier(st);  // every replica holds theta_{t+1}; nobody reads our models any more
 }
 

@@ -45,6 +45,8 @@ struct PeerBoundary {
   // 520 / 605 GB/s) -- remote address translation over very large mappings.
   // Beyond the bound the NCCL path (staging through small FIFOs) is faster.
   static bool fits(uint64_t bytes) { return bytes <= (uint64_t)24e9; }
+  // device ms of the last run()'s fused kernel (after the opening barrier)
+  float last_kernel_ms() const;
 
  private:
   struct Region {  // one exported pointer
@@ -68,6 +70,7 @@ struct PeerBoundary {
   DevBuf<uint64_t> flags_;  // [world]: flags_[j] = last epoch rank j signalled to us
   DevBuf<uint8_t> tab_dev_;
   uint64_t epoch_ = 0;
+  cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
   std::vector<std::vector<const float*>> models_;  // [rank][local idx] in this address space
   std::vector<float*> thetas_;
   std::vector<uint64_t*> peer_flags_;

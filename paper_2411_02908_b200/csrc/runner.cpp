@@ -87,6 +87,7 @@ Runner::Runner(Ctx* c, const photon_fed_cfg& f, const photon_train_cfg& t,
   PH_CUDA(cudaEventCreate(&ev_a));
   PH_CUDA(cudaEventCreate(&ev_b));
   PH_CUDA(cudaEventCreate(&ev_c));
+  PH_CUDA(cudaEventCreate(&ev_b2));
   PH_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
   PH_CUDA(cudaEventCreateWithFlags(&copied[0], cudaEventDisableTiming));
   PH_CUDA(cudaEventCreateWithFlags(&copied[1], cudaEventDisableTiming));
@@ -106,6 +107,7 @@ Runner::~Runner() {
   if (ev_a) cudaEventDestroy(ev_a);
   if (ev_b) cudaEventDestroy(ev_b);
   if (ev_c) cudaEventDestroy(ev_c);
+  if (ev_b2) cudaEventDestroy(ev_b2);
   if (copy_stream) cudaStreamSynchronize(copy_stream);
   for (cudaEvent_t e : copied)
     if (e) cudaEventDestroy(e);
@@ -265,15 +267,20 @@ void Runner::run_round(photon_round_record* rec) {
       recv = d_recv.ptr;
     }
   }
-  if (p2p && PeerBoundary::supported(n, world)) {
+  const bool peer = p2p && PeerBoundary::supported(n, world);
+  if (peer) {
     p2p->publish(local_models.data(), (int)local_models.size(), d_theta.ptr, st);
     p2p->run(surv, shard, d_vel.ptr, server, st);
   } else {
+    PH_CUDA(cudaEventRecord(ev_b2, st));
     round_boundary(comm, rank, world, P, shard, surv, local_models.data(), recv, d_model_ptrs,
                    d_theta.ptr, d_vel.ptr, server, st);
   }
   PH_CUDA(cudaEventRecord(ev_c, st));
   PH_CUDA(cudaEventSynchronize(ev_c));
+  float bnd_ms = 0.f;
+  if (peer) bnd_ms = p2p->last_kernel_ms();
+  else PH_CUDA(cudaEventElapsedTime(&bnd_ms, ev_b2, ev_c));
   if (K >= 2) ++sync_events;
 
   if (rec) {
@@ -305,6 +312,7 @@ void Runner::run_round(photon_round_record* rec) {
       rec->h2d_bytes += (uint64_t)tau * ((uint64_t)B * S * 3 + V + 1) * 4;
     rec->d2h_bytes = (uint64_t)mine.size() * (tau * sizeof(double) + sizeof(int));
     rec->eval_ppl = std::numeric_limits<double>::quiet_NaN();
+    rec->boundary_ms = bnd_ms;
   }
   next_round = round + 1;
   buf ^= 1;  // the prefetched set holds round t+1

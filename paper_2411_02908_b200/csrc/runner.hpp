@@ -53,7 +53,7 @@ struct Runner {
   DevBuf<int> d_flag;
   PinnedBuf<double> h_loss;
   PinnedBuf<int> h_flag;
-  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr, ev_b2 = nullptr;
 
   // per-round evaluation (RunnerOptions::eval_every / eval_fn, aggregator.cpp:207-212):
   // batch i of the eval set lives on rank i % world, resident in HBM

@@ -301,6 +301,7 @@ class RoundRecord:
     h2d_bytes: int = 0
     d2h_bytes: int = 0
     eval_ppl: float = float("nan")  # RoundRecord::eval_ppl (NaN when the cadence skips)
+    boundary_ms: float = 0.0  # device time of the boundary's exchange + update alone
 
 
 # ---------------------------------------------------------------------------
@@ -754,7 +755,8 @@ class FederationRunner:
         return RoundRecord(int(rec.round), [int(x) for x in rec.sampled_ids[:min(k, 64)]],
                            rec.mean_client_loss, rec.min_client_loss, rec.max_client_loss,
                            rec.local_ms, rec.aggregate_ms, rec.round_ms, int(rec.tokens),
-                           rec.host_ms, int(rec.h2d_bytes), int(rec.d2h_bytes), rec.eval_ppl)
+                           rec.host_ms, int(rec.h2d_bytes), int(rec.d2h_bytes), rec.eval_ppl,
+                           rec.boundary_ms)
 
     def done(self) -> bool:
         return self.next_round() >= self.fed.rounds

@@ -35,7 +35,7 @@ def test_abi_version_and_status_names(F):
     from paper_2411_02908_b200 import _capi
 
     lib = _capi.lib()
-    assert lib.photon_abi_version() == 1
+    assert lib.photon_abi_version() == 2
     for code, name in ((0, b"OK"), (1, b"ConfigError"), (8, b"DivergenceError"),
                        (11, b"RoundFailureError")):
         assert lib.photon_status_name(code) == name
