@@ -111,7 +111,7 @@ class EngineT final : public Engine {
   void allocate() {
     const uint64_t M = Mmax_, d = d_, L = L_, hid = hid_;
     const uint64_t rows_bhs = max_batch * H_ * Smax_;
-    size_t part_floats = std::max<size_t>((size_t)k::ln_bwd_parts() * 2 * d,
+    size_t part_floats = std::max<size_t>((size_t)k::ln_bwd_parts() * 3 * d,
                                           std::max({k::colsum_part_floats((int)M, (int)V_),
                                                     k::colsum_part_floats((int)M, (int)hid),
                                                     k::colsum_part_floats((int)M, (int)d)}));
@@ -334,8 +334,9 @@ void EngineT<T>::forward_backward(const StepBatch& bt, double* loss_dev, bool ba
   mm(d, V, M, xf_, d, false, logits_, V, false, G(off_.head_w), V, DT::F32, Epi::Store);
   {
     Scope sc(this, 2, 0);
+    // the column sums of its output are the last block's b2 gradient
     k::ln_bwd<T>(dy_, xL, meanf_, rstdf_, Pm(off_.lnfg), nullptr, dx_, dxT_, part_, G(off_.lnfg),
-                 G(off_.lnfb), M, d, stream);
+                 G(off_.lnfb), M, d, stream, G(off_.blocks[L - 1].b2));
   }
   for (int l = L - 1; l >= 0; --l) {
     const BlockOffsets& o = off_.blocks[l];
@@ -343,11 +344,7 @@ void EngineT<T>::forward_backward(const StepBatch& bt, double* loss_dev, bool ba
     float* xm = xmid_ + (size_t)l * Md;
     T *h = h_ + l * Md, *q = q_ + l * Md, *kk = k_ + l * Md, *v = v_ + l * Md, *ao = o_ + l * Md;
     T *h2 = h2_ + l * Md, *pre = pre_ + l * Mh, *u = u_ + l * Mh;
-    // x_out = x_mid + (u W2 + b2)
-    {
-      Scope sc(this, 2, 0);
-      k::colsum<float>(dx_, M, d, part_, G(o.b2), stream);
-    }
+    // x_out = x_mid + (u W2 + b2); db2 came with the LayerNorm backward above
     mm(M, hid, d, dxT_, d, true, W(o.w2), d, true, dpre_, hid, TT, Epi::GeluBwd, nullptr, nullptr,
        pre);
     mm(hid, d, M, u, hid, false, dxT_, d, false, G(o.w2), d, DT::F32, Epi::Store);
@@ -360,13 +357,9 @@ void EngineT<T>::forward_backward(const StepBatch& bt, double* loss_dev, bool ba
     mm(d, hid, M, h2, d, false, dpre_, hid, false, G(o.w1), hid, DT::F32, Epi::Store);
     {
       Scope sc(this, 2, 0);
+      // x_mid = x + (o Wo + bo): dbo = column sums of this output
       k::ln_bwd<T>(dy_, xm, mean2_ + (size_t)l * M, rstd2_ + (size_t)l * M, Pm(o.ln2g), dx_, dx_,
-                   dxT_, part_, G(o.ln2g), G(o.ln2b), M, d, stream);
-    }
-    // x_mid = x + (o Wo + bo)
-    {
-      Scope sc(this, 2, 0);
-      k::colsum<float>(dx_, M, d, part_, G(o.bo), stream);
+                   dxT_, part_, G(o.ln2g), G(o.ln2b), M, d, stream, G(o.bo));
     }
     mm(M, d, d, dxT_, d, true, W(o.wo), d, true, dO_, d, TT, Epi::Store);
     mm(d, d, M, ao, d, false, dxT_, d, false, G(o.wo), d, DT::F32, Epi::Store);
@@ -389,8 +382,10 @@ void EngineT<T>::forward_backward(const StepBatch& bt, double* loss_dev, bool ba
     mm(d, d, M, h, d, false, dq_, d, false, G(o.wq), d, DT::F32, Epi::Store);
     {
       Scope sc(this, 2, 0);
+      // the output is block l-1's x_out gradient: its column sums are db2 of l-1
       k::ln_bwd<T>(dy_, x, mean1_ + (size_t)l * M, rstd1_ + (size_t)l * M, Pm(o.ln1g), dx_, dx_,
-                   dxT_, part_, G(o.ln1g), G(o.ln1b), M, d, stream);
+                   dxT_, part_, G(o.ln1g), G(o.ln1b), M, d, stream,
+                   l > 0 ? G(off_.blocks[l - 1].b2) : nullptr);
     }
   }
   {

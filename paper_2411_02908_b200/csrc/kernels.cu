@@ -193,12 +193,12 @@ __global__ void __launch_bounds__(kLnBwdWarps * 32)
 ln_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ x,
               const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
               const float* __restrict__ gain, const float* dres, float* dx_out,
-              T* __restrict__ dx_T, float* __restrict__ part, int M, int d) {
-  extern __shared__ float sm[];  // [warps][2][d]
+              T* __restrict__ dx_T, float* __restrict__ part, int M, int d, int nsum) {
+  extern __shared__ float sm[];  // [warps][nsum][d]: dgain | dbias (| column sums of dx_out)
   const int warps = blockDim.x / 32;  // sized by the launcher to the shared-memory budget
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-  float* my = sm + (size_t)warp * 2 * d;
-  for (int j = lane; j < 2 * d; j += 32) my[j] = 0.f;
+  float* my = sm + (size_t)warp * nsum * d;
+  for (int j = lane; j < nsum * d; j += 32) my[j] = 0.f;
   const float inv_d = 1.0f / (float)d;
   for (int m = blockIdx.x * warps + warp; m < M; m += gridDim.x * warps) {
     const float* dyr = dy + (size_t)m * d;
@@ -225,14 +225,15 @@ ln_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ x,
       if (rr) g += rr[j];
       out[j] = g;
       if (outT) outT[j] = from_f<T>(g);
+      if (nsum == 3) my[2 * d + j] += g;
     }
   }
   __syncthreads();
   // reduce warps -> block partial
-  for (int j = threadIdx.x; j < 2 * d; j += blockDim.x) {
+  for (int j = threadIdx.x; j < nsum * d; j += blockDim.x) {
     float acc = 0.f;
-    for (int w = 0; w < warps; ++w) acc += sm[(size_t)w * 2 * d + j];
-    part[(size_t)blockIdx.x * 2 * d + j] = acc;
+    for (int w = 0; w < warps; ++w) acc += sm[(size_t)w * nsum * d + j];
+    part[(size_t)blockIdx.x * 3 * d + j] = acc;
   }
 }
 
@@ -280,12 +281,15 @@ __global__ void __launch_bounds__(256, 2)
 ln_bwd_vec_kernel(const float* __restrict__ dy, const float* __restrict__ x,
                   const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
                   const float* __restrict__ gain, const float* dres, float* dx_out,
-                  T* __restrict__ dx_T, float* __restrict__ part, int M) {
+                  T* __restrict__ dx_T, float* __restrict__ part, int M, int osum) {
   constexpr int D = NV * 128;
   __shared__ float4 gs[D / 4];
-  __shared__ float red[kLnBwdWarps][D];
+  __shared__ float red[kLnBwdWarps][D];  // per-warp column sums of dx_out, then the reductions
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int j = threadIdx.x; j < D / 4; j += blockDim.x) gs[j] = reinterpret_cast<const float4*>(gain)[j];
+  if (osum)
+    for (int j = lane; j < D / 4; j += 32)
+      reinterpret_cast<float4*>(red[warp])[j] = make_float4(0.f, 0.f, 0.f, 0.f);
   __syncthreads();
   const float inv_d = 1.0f / (float)D;
   float4 ag[NV], ab[NV];
@@ -332,9 +336,27 @@ ln_bwd_vec_kernel(const float* __restrict__ dy, const float* __restrict__ x,
       r.w += rstd * (gv[i].w * gg.w - s1 - ((xv[i].w - mean) * rstd) * s2);
       reinterpret_cast<float4*>(out)[c4] = r;
       if (dx_T) store4(dx_T + (size_t)m * D + 4 * c4, r.x, r.y, r.z, r.w);
+      if (osum) {  // each lane owns these columns of its warp's row: no conflicts
+        float4 a = reinterpret_cast<float4*>(red[warp])[c4];
+        a.x += r.x;
+        a.y += r.y;
+        a.z += r.z;
+        a.w += r.w;
+        reinterpret_cast<float4*>(red[warp])[c4] = a;
+      }
     }
   }
-  // block partials: [dgain | dbias], warps summed in ascending order
+  // block partials: [dgain | dbias | dsum], warps summed in ascending order
+  __syncthreads();
+  if (osum) {
+    for (int j = threadIdx.x; j < D; j += blockDim.x) {
+      float acc = 0.f;
+#pragma unroll
+      for (int w = 0; w < kLnBwdWarps; ++w) acc += red[w][j];
+      part[(size_t)blockIdx.x * 3 * D + 2 * D + j] = acc;
+    }
+    __syncthreads();
+  }
 #pragma unroll
   for (int i = 0; i < NV; ++i) reinterpret_cast<float4*>(red[warp])[lane + 32 * i] = ag[i];
   __syncthreads();
@@ -342,7 +364,7 @@ ln_bwd_vec_kernel(const float* __restrict__ dy, const float* __restrict__ x,
     float acc = 0.f;
 #pragma unroll
     for (int w = 0; w < kLnBwdWarps; ++w) acc += red[w][j];
-    part[(size_t)blockIdx.x * 2 * D + j] = acc;
+    part[(size_t)blockIdx.x * 3 * D + j] = acc;
   }
   __syncthreads();
 #pragma unroll
@@ -352,37 +374,39 @@ ln_bwd_vec_kernel(const float* __restrict__ dy, const float* __restrict__ x,
     float acc = 0.f;
 #pragma unroll
     for (int w = 0; w < kLnBwdWarps; ++w) acc += red[w][j];
-    part[(size_t)blockIdx.x * 2 * D + D + j] = acc;
+    part[(size_t)blockIdx.x * 3 * D + D + j] = acc;
   }
 }
 
 template <typename T>
 void ln_bwd(const float* dy, const float* x, const float* mean, const float* rstd,
             const float* gain, const float* dres, float* dx_out, T* dx_T, float* part,
-            float* dgain, float* dbias, int M, int d, cudaStream_t st) {
+            float* dgain, float* dbias, int M, int d, cudaStream_t st, float* dsum) {
+  const int nsum = dsum ? 3 : 2;
   switch (d) {
 #define PH_LNB(NV)                                                                         \
   case NV * 128:                                                                           \
     ln_bwd_vec_kernel<T, NV><<<kLnBwdBlocks, kLnBwdWarps * 32, 0, st>>>(                   \
-        dy, x, mean, rstd, gain, dres, dx_out, dx_T, part, M);                             \
+        dy, x, mean, rstd, gain, dres, dx_out, dx_T, part, M, dsum ? 1 : 0);               \
     break;
     PH_LNB(1) PH_LNB(2) PH_LNB(3) PH_LNB(4) PH_LNB(5) PH_LNB(6)
 #undef PH_LNB
     default: {
-      // as many warps (<= 8) as [warps][2][d] fp32 partials fit in shared memory
+      // as many warps (<= 8) as [warps][nsum][d] fp32 partials fit in shared memory
       const int warps = (int)std::max<size_t>(
-          1, std::min<size_t>(kLnBwdWarps, (size_t)(224 * 1024) / ((size_t)2 * d * sizeof(float))));
-      const size_t smem = (size_t)warps * 2 * d * sizeof(float);
+          1, std::min<size_t>(kLnBwdWarps, (size_t)(224 * 1024) / ((size_t)nsum * d * sizeof(float))));
+      const size_t smem = (size_t)warps * nsum * d * sizeof(float);
       if (smem > 224 * 1024) throw Error(PHOTON_ERR_CONFIG, "layer_norm backward: d_model too large");
       if (smem > 48 * 1024)
         PH_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
       ln_bwd_kernel<T><<<kLnBwdBlocks, warps * 32, smem, st>>>(dy, x, mean, rstd, gain, dres,
-                                                               dx_out, dx_T, part, M, d);
+                                                               dx_out, dx_T, part, M, d, nsum);
     }
   }
   PH_LAUNCH_CHECK();
-  colreduce(part, kLnBwdBlocks, 2 * d, 2 * d, dgain, d, dbias, st);
+  colreduce(part, kLnBwdBlocks, 2 * d, 3 * d, dgain, d, dbias, st);
+  if (dsum) colreduce(part + 2 * d, kLnBwdBlocks, d, 3 * d, dsum, d, nullptr, st);
 }
 
 // ============================================================================
@@ -1078,7 +1102,7 @@ void f32_to_bf16(const float* in, bf16* out, uint64_t n, cudaStream_t st) {
                           cudaStream_t);                                                        \
   template void ln_bwd<T>(const float*, const float*, const float*, const float*, const float*,   \
                           const float*, float*, T*, float*, float*, float*, int, int,            \
-                          cudaStream_t);                                                        \
+                          cudaStream_t, float*);                                                \
   template void colsum<T>(const T*, int, int, float*, float*, cudaStream_t);                    \
   template void ce_fwd_bwd<T>(T*, const int32_t*, int, int, float, double*, bool, cudaStream_t); \
   template void attn_fwd_simt<T>(const T*, const T*, const T*, T*, float*, int, int, int, int,    \
