@@ -28,7 +28,7 @@ namespace k {
 
 namespace {
 
-constexpr int TQ = 128, TK = 128, DH = 64;
+constexpr int TQ = 128, TK = 128;  // query / key tile (head dims 64 and 128 are templates)
 
 // Opt-in timeline instrumentation (PHOTON_BUILD_TRACE=1): clock64 stamps of one
 // mid-grid CTA, event e of iteration it at g_attn_trace[e * 64 + it].
@@ -164,7 +164,8 @@ template <int N>
 __device__ __forceinline__ void tmem_st_cols(uint32_t taddr, const uint32_t* r) {
 #pragma unroll
   for (int c = 0; c < N / 32; ++c) TMEM_ST32(taddr + c * 32, (r + c * 32));
-  if constexpr (N % 32 == 16) TMEM_ST16(taddr + (N / 32) * 32, (r + (N / 32) * 32));
+  if constexpr (N % 32 >= 16) TMEM_ST16(taddr + (N / 32) * 32, (r + (N / 32) * 32));
+  if constexpr (N % 16 == 8) TMEM_ST8(taddr + (N / 16) * 16, (r + (N / 16) * 16));
 }
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -214,17 +215,21 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, 
 // TMEM columns per CTA: S [0,128) fp32 scores, P [128,192) bf16x2, O [192,256).
 constexpr uint32_t kColS = 0, kColP = 128, kColO = 192;
 
-__global__ void __launch_bounds__(kThreads, 2)
+template <int HD>
+__global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                        const __grid_constant__ CUtensorMap tv, const FwdArgs a) {
-  // smem: Q 16K | K[2] 16K | V[2] 16K | barriers  -> two CTAs per SM
+  // smem: Q | K[2] | V[2] | barriers; 16 KB tiles at HD = 64 (two CTAs per SM),
+  // 32 KB at HD = 128 (one CTA per SM, 512 TMEM columns)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
+  constexpr int NA = HD / 64, TB = 16384 * NA;  // 64-column swizzle atoms per row, tile bytes
+  constexpr uint32_t kColO_ = HD == 64 ? kColO : 256, kCols = HD == 64 ? 256 : 512;
   uint8_t* sQ = sm;
-  uint8_t* sK = sm + 16384;
-  uint8_t* sV = sK + 2 * 16384;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + 2 * 16384);
+  uint8_t* sK = sm + TB;
+  uint8_t* sV = sK + 2 * TB;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + 2 * TB);
   uint64_t* q_full = bar;
   uint64_t* kv_full = bar + 1;   // [2]
   uint64_t* kv_empty = bar + 3;  // [2]
@@ -255,8 +260,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
-        su32(tmem_slot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+        su32(tmem_slot)), "r"(kCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   fence_before();
@@ -266,14 +271,17 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   if (warp == 0) {
     if (lane == 0) {  // ===== producer =====
-      mbar_expect_tx(q_full, 16384);
-      tma_load_2d(sQ, &tq, q_full, h * DH, row_base + q0);
+      mbar_expect_tx(q_full, TB);
+      for (int t = 0; t < NA; ++t)
+        tma_load_2d(sQ + t * 16384, &tq, q_full, h * HD + 64 * t, row_base + q0);
       for (int j = 0; j < n_kt; ++j) {
         const int st = j & 1;
         mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], 32768);
-        tma_load_2d(sK + st * 16384, &tk, &kv_full[st], h * DH, row_base + j * TK);
-        tma_load_2d(sV + st * 16384, &tv, &kv_full[st], h * DH, row_base + j * TK);
+        mbar_expect_tx(&kv_full[st], 2 * TB);
+        for (int t = 0; t < NA; ++t) {
+          tma_load_2d(sK + st * TB + t * 16384, &tk, &kv_full[st], h * HD + 64 * t, row_base + j * TK);
+          tma_load_2d(sV + st * TB + t * 16384, &tv, &kv_full[st], h * HD + 64 * t, row_base + j * TK);
+        }
       }
     }
   } else if (warp == 1) {
@@ -281,17 +289,17 @@ __global__ void __launch_bounds__(kThreads, 2)
       constexpr uint32_t IDS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TK >> 3) << 17) |
                                ((uint32_t)(TQ >> 4) << 24);
       constexpr uint32_t IDO = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
-                               ((uint32_t)(DH >> 3) << 17) | ((uint32_t)(TQ >> 4) << 24);
+                               ((uint32_t)(HD >> 3) << 17) | ((uint32_t)(TQ >> 4) << 24);
       mbar_wait(q_full, 0);
       const uint32_t aq = su32(sQ);
       auto issue_pv = [&](int j) {
         const int st = j & 1;
         mbar_wait(p_full, j & 1);
         fence_after();
-        const uint32_t bv = su32(sV + st * 16384);
+        const uint32_t bv = su32(sV + st * TB);
 #pragma unroll
         for (int kk = 0; kk < TK / 16; ++kk)  // 16 keys = 8 packed bf16x2 TMEM columns
-          mma_ts(tmem + kColO, tmem + kColP + kk * 8, sw128(bv + kk * 2048, 8192, 1024), IDO,
+          mma_ts(tmem + kColO_, tmem + kColP + kk * 8, sw128(bv + kk * 2048, 16384, 1024), IDO,
                  (j > 0 || kk > 0) ? 1u : 0u);
         commit(o_done);
         commit(&kv_empty[st]);
@@ -301,11 +309,13 @@ __global__ void __launch_bounds__(kThreads, 2)
         mbar_wait(&kv_full[st], (j >> 1) & 1);
         mbar_wait(s_empty, (j & 1) ^ 1);  // softmax holds S_{j-1} in registers
         fence_after();
-        const uint32_t bk = su32(sK + st * 16384);
+        const uint32_t bk = su32(sK + st * TB);
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk)
-          mma(tmem + kColS, sw128(aq + kk * 32, 16, 1024), sw128(bk + kk * 32, 16, 1024), IDS,
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          mma(tmem + kColS, sw128(aq + off, 16, 1024), sw128(bk + off, 16, 1024), IDS,
               kk > 0 ? 1u : 0u);
+        }
         commit(s_full);
         if (j > 0) issue_pv(j - 1);
       }
@@ -354,13 +364,13 @@ __global__ void __launch_bounds__(kThreads, 2)
       fence_after();
       if (__any_sync(0xffffffffu, rescale)) {  // 8 columns at a time: s[] stays in registers
 #pragma unroll 1
-        for (int c = 0; c < DH / 8; ++c) {
+        for (int c = 0; c < HD / 8; ++c) {
           uint32_t u[8];
-          TMEM_LD8(tmem + lane_off + kColO + c * 8, u);
+          TMEM_LD8(tmem + lane_off + kColO_ + c * 8, u);
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 8; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * scale);
-          TMEM_ST8(tmem + lane_off + kColO + c * 8, u);
+          TMEM_ST8(tmem + lane_off + kColO_ + c * 8, u);
         }
       }
       l *= scale;
@@ -388,11 +398,11 @@ __global__ void __launch_bounds__(kThreads, 2)
     mbar_wait(o_done, (n_kt - 1) & 1);
     fence_after();
     const float inv = 1.f / l;
-    bf16* orow = a.o + (int64_t)(row_base + qrow) * a.d + h * DH;
+    bf16* orow = a.o + (int64_t)(row_base + qrow) * a.d + h * HD;
 #pragma unroll
-    for (int c = 0; c < DH / 32; ++c) {
+    for (int c = 0; c < HD / 32; ++c) {
       uint32_t u[32];
-      TMEM_LD32(tmem + lane_off + kColO + c * 32, u);
+      TMEM_LD32(tmem + lane_off + kColO_ + c * 32, u);
       tmem_wait_ld();
       if (qrow < a.S) {
 #pragma unroll
@@ -410,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   __syncthreads();
   if (warp == 1) {
     fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
   }
 }
 
@@ -427,9 +437,10 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
-// thread per (row, head): D = dO . O over the head's 64 columns (8 x 16-byte
+// thread per (row, head): D = dO . O over the head's HD columns (16-byte
 // loads of each); consecutive threads take consecutive heads of a row, so a
 // warp streams contiguous rows
+template <int HD>
 __global__ void attn_bwd_prep_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dO,
                                      const float* __restrict__ lse, float* __restrict__ Lp,
                                      float* __restrict__ Dp, int B, int S, int H, int d, int Spad) {
@@ -439,11 +450,11 @@ __global__ void attn_bwd_prep_kernel(const bf16* __restrict__ o, const bf16* __r
     const int h = (int)(t % H);
     const int64_t row = t / H;  // b * S + i
     const int b = (int)(row / S), i = (int)(row % S);
-    const uint4* po = reinterpret_cast<const uint4*>(o + row * d + h * DH);
-    const uint4* pd = reinterpret_cast<const uint4*>(dO + row * d + h * DH);
+    const uint4* po = reinterpret_cast<const uint4*>(o + row * d + h * HD);
+    const uint4* pd = reinterpret_cast<const uint4*>(dO + row * d + h * HD);
     float acc = 0.f;
 #pragma unroll
-    for (int c = 0; c < DH / 8; ++c) {
+    for (int c = 0; c < HD / 8; ++c) {
       const uint4 x = po[c], y = pd[c];
       const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
@@ -482,7 +493,6 @@ struct BwdArgs {
 constexpr int SWB = PHOTON_ATTN_SWB;
 constexpr int NCG = SWB / 4;       // column groups
 constexpr int CPT = 128 / NCG;     // score columns per thread
-constexpr int GPT = DH / NCG;      // accumulator columns per thread in the epilogue
 constexpr int kBwdThreads = 64 + SWB * 32;
 // Ring depth of the streamed operand (Q/dO/L/D in dK/dV, K/V in dQ).  A stage is
 // held until the tile's gradient MMAs retire, and a TMA load under the full
@@ -513,7 +523,11 @@ __device__ __forceinline__ void store_acc_rows(uint32_t taddr, bf16* row_ptr, fl
 }
 
 // ---- dK, dV: CTA per 128-key tile; keys are the TMEM lanes ------------------------
-// TMEM: S^T [0,128)  dP^T [128,256)  P^T [256,320)  dS^T [320,384)  dV [384,448)  dK [448,512)
+// TMEM at HD = 64 (128-query tiles):
+//   S^T [0,128)  dP^T [128,256)  P^T [256,320)  dS^T [320,384)  dV [384,448)  dK [448,512)
+// at HD = 128 (64-query tiles):
+//   S^T [0,64)   dP^T [64,128)   P^T [128,160)  dS^T [160,192)  dV [256,384)  dK [384,512)
+template <int HD>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                             const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
@@ -521,13 +535,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
+  // HD = 128: 64-query tiles so that S^T, dP^T, P^T, dS^T, dV and dK all fit in TMEM
+  constexpr int NA = HD / 64, KB = 16384 * NA;  // swizzle atoms per row, K/V tile bytes
+  constexpr int TQB = HD == 64 ? 128 : 64, QB = TQB * 128 * NA, QA = TQB * 128;  // Q tile, atom
+  constexpr int CPQ = TQB / NCG, GPH = HD / NCG;  // score / accumulator columns per thread
+  constexpr uint32_t colDP = TQB, colP = 2 * TQB, colDS = colP + TQB / 2, colDV = 512 - 2 * HD,
+                     colDK = 512 - HD;
   uint8_t* sK = sm;
-  uint8_t* sV = sm + 16384;
-  uint8_t* sQ = sm + 2 * 16384;   // [NR]
-  uint8_t* sO = sQ + NR * 16384;  // [NR] dO
-  float* sL = reinterpret_cast<float*>(sO + NR * 16384);  // [NR][128]
-  float* sD = sL + NR * 128;                              // [NR][128]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sD + NR * 128);
+  uint8_t* sV = sm + KB;
+  uint8_t* sQ = sm + 2 * KB;   // [NR]
+  uint8_t* sO = sQ + NR * QB;  // [NR] dO
+  float* sL = reinterpret_cast<float*>(sO + NR * QB);  // [NR][TQB]
+  float* sD = sL + NR * TQB;                           // [NR][TQB]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sD + NR * TQB);
   uint64_t* kv_full = bar;
   uint64_t* q_full = bar + 1;        // [NR]
   uint64_t* q_empty = bar + 1 + NR;  // [NR]
@@ -537,11 +557,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* g_done = s_full + 3;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 4);
 
-  const int nt = (a.S + TQ - 1) / TQ;
+  const int ntq = (a.S + TQB - 1) / TQB;
   const int kt = blockIdx.x;
   const int bh = blockIdx.y, b = bh / a.H, h = bh % a.H;
   const int row_base = b * a.S;
-  const int n_it = nt - kt;  // query tiles kt .. nt-1
+  const int qt0 = kt * (TK / TQB);  // first query tile that sees these keys
+  const int n_it = ntq - qt0;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
@@ -568,26 +589,30 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(kv_full, 32768);
-      tma_load_2d(sK, &tk, kv_full, h * DH, row_base + kt * TK);
-      tma_load_2d(sV, &tv, kv_full, h * DH, row_base + kt * TK);
+      mbar_expect_tx(kv_full, 2 * KB);
+      for (int t = 0; t < NA; ++t) {
+        tma_load_2d(sK + t * 16384, &tk, kv_full, h * HD + 64 * t, row_base + kt * TK);
+        tma_load_2d(sV + t * 16384, &tv, kv_full, h * HD + 64 * t, row_base + kt * TK);
+      }
       for (int it = 0; it < n_it; ++it) {
-        const int st = it % NR, qt = kt + it;
+        const int st = it % NR, qt = qt0 + it;
         mbar_wait(&q_empty[st], ((it / NR) & 1) ^ 1);
         ATTN_TRACE(0, it);
-        mbar_expect_tx(&q_full[st], 32768 + 1024);
-        tma_load_2d(sQ + st * 16384, &tq, &q_full[st], h * DH, row_base + qt * TQ);
-        tma_load_2d(sO + st * 16384, &tdo, &q_full[st], h * DH, row_base + qt * TQ);
-        bulk_load(sL + st * 128, a.Lp + (int64_t)bh * a.Spad + qt * TQ, 512, &q_full[st]);
-        bulk_load(sD + st * 128, a.Dp + (int64_t)bh * a.Spad + qt * TQ, 512, &q_full[st]);
+        mbar_expect_tx(&q_full[st], 2 * QB + 8 * TQB);
+        for (int t = 0; t < NA; ++t) {
+          tma_load_2d(sQ + st * QB + t * QA, &tq, &q_full[st], h * HD + 64 * t, row_base + qt * TQB);
+          tma_load_2d(sO + st * QB + t * QA, &tdo, &q_full[st], h * HD + 64 * t, row_base + qt * TQB);
+        }
+        bulk_load(sL + st * TQB, a.Lp + (int64_t)bh * a.Spad + qt * TQB, 4 * TQB, &q_full[st]);
+        bulk_load(sD + st * TQB, a.Dp + (int64_t)bh * a.Spad + qt * TQB, 4 * TQB, &q_full[st]);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t IDS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TQ >> 3) << 17) |
+      constexpr uint32_t IDS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TQB >> 3) << 17) |
                                ((uint32_t)(TK >> 4) << 24);
       constexpr uint32_t IDG = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
-                               ((uint32_t)(DH >> 3) << 17) | ((uint32_t)(TK >> 4) << 24);
+                               ((uint32_t)(HD >> 3) << 17) | ((uint32_t)(TK >> 4) << 24);
       mbar_wait(kv_full, 0);
       const uint32_t ak = su32(sK), av = su32(sV);
       auto issue_grads = [&](int it) {
@@ -595,14 +620,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         mbar_wait(p_full, it & 1);
         ATTN_TRACE(3, it);
         fence_after();
-        const uint32_t bo = su32(sO + st * 16384), bq = su32(sQ + st * 16384);
+        const uint32_t bo = su32(sO + st * QB), bq = su32(sQ + st * QB);
 #pragma unroll
-        for (int kk = 0; kk < TQ / 16; ++kk)  // dV += P^T dO
-          mma_ts(tmem + 384, tmem + 256 + kk * 8, sw128(bo + kk * 2048, 8192, 1024), IDG,
+        for (int kk = 0; kk < TQB / 16; ++kk)  // dV += P^T dO (dO MN-major, QA-byte panels)
+          mma_ts(tmem + colDV, tmem + colP + kk * 8, sw128(bo + kk * 2048, QA, 1024), IDG,
                  (it > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
-        for (int kk = 0; kk < TQ / 16; ++kk)  // dK += dS^T Q
-          mma_ts(tmem + 448, tmem + 320 + kk * 8, sw128(bq + kk * 2048, 8192, 1024), IDG,
+        for (int kk = 0; kk < TQB / 16; ++kk)  // dK += dS^T Q
+          mma_ts(tmem + colDK, tmem + colDS + kk * 8, sw128(bq + kk * 2048, QA, 1024), IDG,
                  (it > 0 || kk > 0) ? 1u : 0u);
         commit(g_done);
         commit(&q_empty[st]);
@@ -615,15 +640,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         mbar_wait(s_empty, (it & 1) ^ 1);
         ATTN_TRACE(2, it);
         fence_after();
-        const uint32_t bq = su32(sQ + st * 16384), bo = su32(sO + st * 16384);
+        const uint32_t bq = su32(sQ + st * QB), bo = su32(sO + st * QB);
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk)  // S^T = K Q^T
-          mma(tmem + 0, sw128(ak + kk * 32, 16, 1024), sw128(bq + kk * 32, 16, 1024), IDS,
-              kk > 0 ? 1u : 0u);
+        for (int kk = 0; kk < HD / 16; ++kk) {  // S^T = K Q^T
+          const uint32_t oa = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * QA + (kk & 3) * 32;
+          mma(tmem + 0, sw128(ak + oa, 16, 1024), sw128(bq + ob, 16, 1024), IDS, kk > 0 ? 1u : 0u);
+        }
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk)  // dP^T = V dO^T
-          mma(tmem + 128, sw128(av + kk * 32, 16, 1024), sw128(bo + kk * 32, 16, 1024), IDS,
+        for (int kk = 0; kk < HD / 16; ++kk) {  // dP^T = V dO^T
+          const uint32_t oa = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * QA + (kk & 3) * 32;
+          mma(tmem + colDP, sw128(av + oa, 16, 1024), sw128(bo + ob, 16, 1024), IDS,
               kk > 0 ? 1u : 0u);
+        }
         commit(s_full);
         if (it > 0) issue_grads(it - 1);
       }
@@ -636,33 +664,33 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const bool key_live = key < a.S;
     for (int it = 0; it < n_it; ++it) {
-      const int st = it % NR, q0 = (kt + it) * TQ;
+      const int st = it % NR, q0 = (qt0 + it) * TQB;
       mbar_wait(&q_full[st], (it / NR) & 1);  // L, D of this query tile visible
       mbar_wait(s_full, it & 1);
       if (warp == 2 && lane == 0) ATTN_TRACE(5, it);
       fence_after();
-      uint32_t s[CPT], dp[CPT];
-      tmem_ld_cols<CPT>(tmem + lane_off + cg * CPT, s);
-      tmem_ld_cols<CPT>(tmem + lane_off + 128 + cg * CPT, dp);
+      uint32_t s[CPQ], dp[CPQ];
+      tmem_ld_cols<CPQ>(tmem + lane_off + cg * CPQ, s);
+      tmem_ld_cols<CPQ>(tmem + lane_off + colDP + cg * CPQ, dp);
       tmem_wait_ld();
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(s_empty);
-      const float* L = sL + st * 128 + cg * CPT;
-      const float* D = sD + st * 128 + cg * CPT;
+      const float* L = sL + st * TQB + cg * CPQ;
+      const float* D = sD + st * TQB + cg * CPQ;
       // masking only where this key tile meets the diagonal or the sequence end
       const bool masked = (kt * TK + TK > q0) || (kt * TK + TK > a.S);
-      uint32_t pp[CPT / 2], dd[CPT / 2];
+      uint32_t pp[CPQ / 2], dd[CPQ / 2];
       // dS^T is kept unscaled (the softmax scale is applied to dK at the store)
 #pragma unroll
-      for (int i = 0; i < CPT / 4; ++i) {
+      for (int i = 0; i < CPQ / 4; ++i) {
         const float4 l4 = lds_f4(L + 4 * i), d4 = lds_f4(D + 4 * i);
         float p0 = ex2(fmaf(__uint_as_float(s[4 * i]), a.sl2, -l4.x));
         float p1 = ex2(fmaf(__uint_as_float(s[4 * i + 1]), a.sl2, -l4.y));
         float p2 = ex2(fmaf(__uint_as_float(s[4 * i + 2]), a.sl2, -l4.z));
         float p3 = ex2(fmaf(__uint_as_float(s[4 * i + 3]), a.sl2, -l4.w));
         if (masked) {
-          const int qc = q0 + cg * CPT + 4 * i;
+          const int qc = q0 + cg * CPQ + 4 * i;
           p0 = (key_live && key <= qc) ? p0 : 0.f;
           p1 = (key_live && key <= qc + 1) ? p1 : 0.f;
           p2 = (key_live && key <= qc + 2) ? p2 : 0.f;
@@ -678,8 +706,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (warp == 2 && lane == 0) ATTN_TRACE(7, it);
       if (it >= 1) mbar_wait(g_done, (it - 1) & 1);  // P^T / dS^T columns free
       fence_after();
-      tmem_st_cols<CPT / 2>(tmem + lane_off + 256 + cg * (CPT / 2), pp);
-      tmem_st_cols<CPT / 2>(tmem + lane_off + 320 + cg * (CPT / 2), dd);
+      tmem_st_cols<CPQ / 2>(tmem + lane_off + colP + cg * (CPQ / 2), pp);
+      tmem_st_cols<CPQ / 2>(tmem + lane_off + colDS + cg * (CPQ / 2), dd);
       tmem_wait_st();
       fence_before();
       __syncwarp();
@@ -687,9 +715,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     mbar_wait(g_done, (n_it - 1) & 1);
     fence_after();
-    const int64_t row = (int64_t)(row_base + key) * a.d + h * DH + cg * GPT;
-    store_acc_rows<GPT>(tmem + lane_off + 448 + cg * GPT, a.g0 + row, a.scale, key_live);  // dK
-    store_acc_rows<GPT>(tmem + lane_off + 384 + cg * GPT, a.g1 + row, 1.f, key_live);      // dV
+    const int64_t row = (int64_t)(row_base + key) * a.d + h * HD + cg * GPH;
+    store_acc_rows<GPH>(tmem + lane_off + colDK + cg * GPH, a.g0 + row, a.scale, key_live);  // dK
+    store_acc_rows<GPH>(tmem + lane_off + colDV + cg * GPH, a.g1 + row, 1.f, key_live);      // dV
   }
   fence_before();
   __syncthreads();
@@ -700,7 +728,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 }
 
 // ---- dQ: CTA per 128-query tile; queries are the TMEM lanes ------------------------
-// TMEM: S [0,128)  dP [128,256)  dS [256,320)  dQ [320,384)
+// TMEM: S [0,128)  dP [128,256)  dS [256,320)  dQ [320,320+HD)
+template <int HD>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                           const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
@@ -708,15 +737,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
+  constexpr int NA = HD / 64, KB = 16384 * NA;  // swizzle atoms per row, tile bytes
+  constexpr int NRQ = HD == 64 ? NR : 2;         // K/V ring depth within 227 KB
+  constexpr int GPH = HD / NCG;
   uint8_t* sQ = sm;
-  uint8_t* sO = sm + 16384;
-  uint8_t* sK = sm + 2 * 16384;   // [NR]
-  uint8_t* sV = sK + NR * 16384;  // [NR]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + NR * 16384);
+  uint8_t* sO = sm + KB;
+  uint8_t* sK = sm + 2 * KB;    // [NRQ]
+  uint8_t* sV = sK + NRQ * KB;  // [NRQ]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + NRQ * KB);
   uint64_t* q_full = bar;
-  uint64_t* kv_full = bar + 1;        // [NR]
-  uint64_t* kv_empty = bar + 1 + NR;  // [NR]
-  uint64_t* s_full = bar + 1 + 2 * NR;
+  uint64_t* kv_full = bar + 1;         // [NRQ]
+  uint64_t* kv_empty = bar + 1 + NRQ;  // [NRQ]
+  uint64_t* s_full = bar + 1 + 2 * NRQ;
   uint64_t* s_empty = s_full + 1;
   uint64_t* p_full = s_full + 2;
   uint64_t* g_done = s_full + 3;
@@ -732,7 +764,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
-    for (int i = 0; i < NR; ++i) {
+    for (int i = 0; i < NRQ; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
@@ -754,15 +786,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(q_full, 32768);
-      tma_load_2d(sQ, &tq, q_full, h * DH, row_base + q0);
-      tma_load_2d(sO, &tdo, q_full, h * DH, row_base + q0);
+      mbar_expect_tx(q_full, 2 * KB);
+      for (int t = 0; t < NA; ++t) {
+        tma_load_2d(sQ + t * 16384, &tq, q_full, h * HD + 64 * t, row_base + q0);
+        tma_load_2d(sO + t * 16384, &tdo, q_full, h * HD + 64 * t, row_base + q0);
+      }
       for (int j = 0; j < n_kt; ++j) {
-        const int st = j % NR;
-        mbar_wait(&kv_empty[st], ((j / NR) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], 32768);
-        tma_load_2d(sK + st * 16384, &tk, &kv_full[st], h * DH, row_base + j * TK);
-        tma_load_2d(sV + st * 16384, &tv, &kv_full[st], h * DH, row_base + j * TK);
+        const int st = j % NRQ;
+        mbar_wait(&kv_empty[st], ((j / NRQ) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[st], 2 * KB);
+        for (int t = 0; t < NA; ++t) {
+          tma_load_2d(sK + st * KB + t * 16384, &tk, &kv_full[st], h * HD + 64 * t, row_base + j * TK);
+          tma_load_2d(sV + st * KB + t * 16384, &tv, &kv_full[st], h * HD + 64 * t, row_base + j * TK);
+        }
       }
     }
   } else if (warp == 1) {
@@ -770,35 +806,38 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       constexpr uint32_t IDS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TK >> 3) << 17) |
                                ((uint32_t)(TQ >> 4) << 24);
       constexpr uint32_t IDG = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
-                               ((uint32_t)(DH >> 3) << 17) | ((uint32_t)(TQ >> 4) << 24);
+                               ((uint32_t)(HD >> 3) << 17) | ((uint32_t)(TQ >> 4) << 24);
       mbar_wait(q_full, 0);
       const uint32_t aq = su32(sQ), ao = su32(sO);
       auto issue_dq = [&](int j) {
-        const int st = j % NR;
+        const int st = j % NRQ;
         mbar_wait(p_full, j & 1);
         fence_after();
-        const uint32_t bk = su32(sK + st * 16384);
+        const uint32_t bk = su32(sK + st * KB);
 #pragma unroll
-        for (int kk = 0; kk < TK / 16; ++kk)  // dQ += dS K
-          mma_ts(tmem + 320, tmem + 256 + kk * 8, sw128(bk + kk * 2048, 8192, 1024), IDG,
+        for (int kk = 0; kk < TK / 16; ++kk)  // dQ += dS K (K MN-major, 16 KB panels)
+          mma_ts(tmem + 320, tmem + 256 + kk * 8, sw128(bk + kk * 2048, 16384, 1024), IDG,
                  (j > 0 || kk > 0) ? 1u : 0u);
         commit(g_done);
         commit(&kv_empty[st]);
       };
       for (int j = 0; j < n_kt; ++j) {
-        const int st = j % NR;
-        mbar_wait(&kv_full[st], (j / NR) & 1);
+        const int st = j % NRQ;
+        mbar_wait(&kv_full[st], (j / NRQ) & 1);
         mbar_wait(s_empty, (j & 1) ^ 1);
         fence_after();
-        const uint32_t bk = su32(sK + st * 16384), bv = su32(sV + st * 16384);
+        const uint32_t bk = su32(sK + st * KB), bv = su32(sV + st * KB);
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk)  // S = Q K^T
-          mma(tmem + 0, sw128(aq + kk * 32, 16, 1024), sw128(bk + kk * 32, 16, 1024), IDS,
-              kk > 0 ? 1u : 0u);
+        for (int kk = 0; kk < HD / 16; ++kk) {  // S = Q K^T
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          mma(tmem + 0, sw128(aq + off, 16, 1024), sw128(bk + off, 16, 1024), IDS, kk > 0 ? 1u : 0u);
+        }
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk)  // dP = dO V^T
-          mma(tmem + 128, sw128(ao + kk * 32, 16, 1024), sw128(bv + kk * 32, 16, 1024), IDS,
+        for (int kk = 0; kk < HD / 16; ++kk) {  // dP = dO V^T
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          mma(tmem + 128, sw128(ao + off, 16, 1024), sw128(bv + off, 16, 1024), IDS,
               kk > 0 ? 1u : 0u);
+        }
         commit(s_full);
         if (j > 0) issue_dq(j - 1);
       }
@@ -844,8 +883,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     mbar_wait(g_done, (n_kt - 1) & 1);
     fence_after();
-    store_acc_rows<GPT>(tmem + lane_off + 320 + cg * GPT,
-                        a.g0 + (int64_t)(row_base + qrow) * a.d + h * DH + cg * GPT, a.scale,
+    store_acc_rows<GPH>(tmem + lane_off + 320 + cg * GPH,
+                        a.g0 + (int64_t)(row_base + qrow) * a.d + h * HD + cg * GPH, a.scale,
                         qrow < a.S);
   }
   fence_before();
@@ -922,53 +961,78 @@ extern "C" int photon_debug_attn_trace(unsigned long long* out, int n) {
 }
 #endif
 
-bool attn_tc_supported(int dh, int d) { return dh == DH && (d % 8) == 0; }
+bool attn_tc_supported(int dh, int d) { return (dh == 64 || dh == 128) && (d % 8) == 0; }
 
 size_t attn_bwd_tc_ws_floats(int B, int S, int H) {
   const size_t Spad = (size_t)(S + TQ - 1) / TQ * TQ;
   return (size_t)2 * B * H * Spad;
 }
 
-void attn_bwd_tc(const bf16* q, const bf16* k, const bf16* v, const bf16* o, const bf16* dO,
+namespace {
+
+template <int HD>
+void attn_bwd_hd(const bf16* q, const bf16* k, const bf16* v, const bf16* o, const bf16* dO,
                  const float* lse, bf16* dq, bf16* dk, bf16* dv, int B, int S, int H, int d,
                  float* ws, cudaStream_t st) {
-  if (d / H != DH) throw Error(PHOTON_ERR_CONFIG, "attn_bwd_tc: head dim must be 64");
   const int nt = (S + TQ - 1) / TQ, Spad = nt * TQ, rows = B * S;
   if (!ws) ws = scratch(attn_bwd_tc_ws_floats(B, S, H));
   float* Lp = ws;
   float* Dp = Lp + (size_t)B * H * Spad;
-  attn_bwd_prep_kernel<<<std::min<int64_t>(((int64_t)B * S * H + 255) / 256, kNumSMs * 16), 256, 0,
-                         st>>>(o, dO, lse, Lp, Dp, B, S, H, d, Spad);
+  attn_bwd_prep_kernel<HD><<<std::min<int64_t>(((int64_t)B * S * H + 255) / 256, kNumSMs * 16), 256,
+                             0, st>>>(o, dO, lse, Lp, Dp, B, S, H, d, Spad);
   PH_LAUNCH_CHECK();
+  constexpr int TQB = HD == 64 ? 128 : 64;  // dK/dV kernel's query tile
   const CUtensorMap mq = head_map(q, rows, d), mk = head_map(k, rows, d), mv = head_map(v, rows, d),
                     mo = head_map(dO, rows, d);
-  BwdArgs a{S, H, d, Spad, rsqrtf((float)DH) * kLog2e, rsqrtf((float)DH), Lp, Dp, dk, dv};
-  constexpr int SMEM1 = 1024 + (2 + 2 * NR) * 16384 + NR * 1024 + 256;
-  constexpr int SMEM2 = 1024 + (2 + 2 * NR) * 16384 + 256;
+  const CUtensorMap mqb = TQB == 128 ? mq : head_map(q, rows, d, TQB),
+                    mob = TQB == 128 ? mo : head_map(dO, rows, d, TQB);
+  BwdArgs a{S, H, d, Spad, rsqrtf((float)HD) * kLog2e, rsqrtf((float)HD), Lp, Dp, dk, dv};
+  constexpr int NA = HD / 64;
+  constexpr int SMEM1 = 1024 + 2 * 16384 * NA + NR * 2 * TQB * 128 * NA + NR * 8 * TQB + 256;
+  constexpr int NRQ = HD == 64 ? NR : 2;
+  constexpr int SMEM2 = 1024 + (2 + 2 * NRQ) * 16384 * NA + 256;
+  static_assert(SMEM1 <= 232448 && SMEM2 <= 232448, "attention backward: shared memory");
   static std::atomic<uint64_t> cfg1{0}, cfg2{0};
-  set_smem_once(cfg1, attn_bwd_dkdv_tc_kernel, SMEM1);
-  set_smem_once(cfg2, attn_bwd_dq_tc_kernel, SMEM2);
+  set_smem_once(cfg1, attn_bwd_dkdv_tc_kernel<HD>, SMEM1);
+  set_smem_once(cfg2, attn_bwd_dq_tc_kernel<HD>, SMEM2);
   dim3 grid(nt, B * H);
-  attn_bwd_dkdv_tc_kernel<<<grid, kBwdThreads, SMEM1, st>>>(mq, mk, mv, mo, a);
+  attn_bwd_dkdv_tc_kernel<HD><<<grid, kBwdThreads, SMEM1, st>>>(mqb, mk, mv, mob, a);
   PH_LAUNCH_CHECK();
   a.g0 = dq;
   a.g1 = nullptr;
-  attn_bwd_dq_tc_kernel<<<grid, kBwdThreads, SMEM2, st>>>(mq, mk, mv, mo, a);
+  attn_bwd_dq_tc_kernel<HD><<<grid, kBwdThreads, SMEM2, st>>>(mq, mk, mv, mo, a);
   PH_LAUNCH_CHECK();
+}
+
+template <int HD>
+void attn_fwd_hd(const bf16* q, const bf16* k, const bf16* v, bf16* o, float* lse, int B, int S,
+                 int H, int d, cudaStream_t st) {
+  const int rows = B * S;
+  const CUtensorMap mq = head_map(q, rows, d), mk = head_map(k, rows, d), mv = head_map(v, rows, d);
+  const FwdArgs a{S, H, d, rsqrtf((float)HD) * kLog2e, o, lse};
+  constexpr int SMEM = 1024 + 16384 * 5 * (HD / 64) + 256;
+  static std::atomic<uint64_t> cfg{0};
+  set_smem_once(cfg, attn_fwd_tc_kernel<HD>, SMEM);
+  dim3 grid((S + TQ - 1) / TQ, B * H);
+  attn_fwd_tc_kernel<HD><<<grid, kThreads, SMEM, st>>>(mq, mk, mv, a);
+  PH_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+void attn_bwd_tc(const bf16* q, const bf16* k, const bf16* v, const bf16* o, const bf16* dO,
+                 const float* lse, bf16* dq, bf16* dk, bf16* dv, int B, int S, int H, int d,
+                 float* ws, cudaStream_t st) {
+  if (d / H == 64) attn_bwd_hd<64>(q, k, v, o, dO, lse, dq, dk, dv, B, S, H, d, ws, st);
+  else if (d / H == 128) attn_bwd_hd<128>(q, k, v, o, dO, lse, dq, dk, dv, B, S, H, d, ws, st);
+  else throw Error(PHOTON_ERR_CONFIG, "attn_bwd_tc: head dim must be 64 or 128");
 }
 
 void attn_fwd_tc(const bf16* q, const bf16* k, const bf16* v, bf16* o, float* lse, int B, int S,
                  int H, int d, cudaStream_t st) {
-  if (d / H != DH) throw Error(PHOTON_ERR_CONFIG, "attn_fwd_tc: head dim must be 64");
-  const int rows = B * S;
-  const CUtensorMap mq = head_map(q, rows, d), mk = head_map(k, rows, d), mv = head_map(v, rows, d);
-  const FwdArgs a{S, H, d, rsqrtf((float)DH) * kLog2e, o, lse};
-  constexpr int SMEM = 1024 + 16384 * 5 + 256;
-  static std::atomic<uint64_t> cfg{0};
-  set_smem_once(cfg, attn_fwd_tc_kernel, SMEM);
-  dim3 grid((S + TQ - 1) / TQ, B * H);
-  attn_fwd_tc_kernel<<<grid, kThreads, SMEM, st>>>(mq, mk, mv, a);
-  PH_LAUNCH_CHECK();
+  if (d / H == 64) attn_fwd_hd<64>(q, k, v, o, lse, B, S, H, d, st);
+  else if (d / H == 128) attn_fwd_hd<128>(q, k, v, o, lse, B, S, H, d, st);
+  else throw Error(PHOTON_ERR_CONFIG, "attn_fwd_tc: head dim must be 64 or 128");
 }
 
 }  // namespace k

@@ -71,9 +71,16 @@ def test_attention_photon125m_head_shape():
     _run(2, 2, 2048, 2, 128)
 
 
-@pytest.mark.parametrize("B,S,H", [(2, 128, 2), (1, 256, 3), (2, 200, 2), (1, 64, 1), (3, 384, 2)])
-def test_attention_tcgen05_forward(B, S, H):
-    _run(2, B, S, H, 64 * H)
+@pytest.mark.parametrize("dh", [64, 128])
+@pytest.mark.parametrize("B,S,H", [(2, 128, 2), (1, 256, 3), (2, 200, 2), (1, 64, 1), (3, 384, 2),
+                                   (1, 320, 1)])
+def test_attention_tcgen05(B, S, H, dh):
+    # forward + backward on tcgen05 (head dims 64 and 128; the 1.3B / 7B heads are 128)
+    _run(2, B, S, H, dh * H)
+
+
+def test_attention_tcgen05_dh128_long():
+    _run(2, 1, 2048, 2, 256)
 
 
 def test_attention_tcgen05_backward_deterministic():
