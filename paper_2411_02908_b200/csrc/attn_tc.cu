@@ -214,6 +214,9 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, 
 
 // TMEM columns per CTA: S [0,128) fp32 scores, P [128,192) bf16x2, O [192,256).
 constexpr uint32_t kColS = 0, kColP = 128, kColO = 192;
+// forward K ring depth: a TMA load under the forward's traffic takes up to ~5k
+// cycles (clock64 trace), more than two tiles of softmax
+constexpr int NKF = 3;
 
 template <int HD>
 __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
@@ -227,17 +230,21 @@ __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
   constexpr int NA = HD / 64, TB = 16384 * NA;  // 64-column swizzle atoms per row, tile bytes
   constexpr uint32_t kColO_ = HD == 64 ? kColO : 256, kCols = HD == 64 ? 256 : 512;
   uint8_t* sQ = sm;
-  uint8_t* sK = sm + TB;
-  uint8_t* sV = sK + 2 * TB;
+  uint8_t* sK = sm + TB;         // [NKF]
+  uint8_t* sV = sK + NKF * TB;   // [2]
   uint64_t* bar = reinterpret_cast<uint64_t*>(sV + 2 * TB);
+  // K and V have separate rings: a K stage is free once S_j retires, a V stage
+  // once PV_j retires, so K_{j+2} streams in while PV_j is still running
   uint64_t* q_full = bar;
-  uint64_t* kv_full = bar + 1;   // [2]
-  uint64_t* kv_empty = bar + 3;  // [2]
-  uint64_t* s_full = bar + 5;
-  uint64_t* s_empty = bar + 6;
-  uint64_t* p_full = bar + 7;
-  uint64_t* o_done = bar + 8;    // one completion per PV_j
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9);
+  uint64_t* s_full = bar + 1;
+  uint64_t* s_empty = bar + 2;
+  uint64_t* p_full = bar + 3;
+  uint64_t* o_done = bar + 4;    // one completion per PV_j
+  uint64_t* v_full = bar + 5;    // [2]
+  uint64_t* v_empty = bar + 7;   // [2]
+  uint64_t* k_full = bar + 9;    // [NKF]
+  uint64_t* k_empty = k_full + NKF;  // [NKF]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(k_empty + NKF);
 
   const int nqt = (a.S + TQ - 1) / TQ;
   const int qt = nqt - 1 - blockIdx.x;  // heavy tiles first
@@ -249,9 +256,13 @@ __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
 
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
+    for (int i = 0; i < NKF; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+    }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
     }
     mbar_init(s_full, 1);
     mbar_init(s_empty, 4);
@@ -270,18 +281,25 @@ __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // ===== producer =====
+    if (lane == 0) {  // ===== producer: Q, then the K ring =====
       mbar_expect_tx(q_full, TB);
       for (int t = 0; t < NA; ++t)
         tma_load_2d(sQ + t * 16384, &tq, q_full, h * HD + 64 * t, row_base + q0);
       for (int j = 0; j < n_kt; ++j) {
+        const int st = j % NKF;
+        mbar_wait(&k_empty[st], ((j / NKF) & 1) ^ 1);
+        ATTN_TRACE(0, j);
+        mbar_expect_tx(&k_full[st], TB);
+        for (int t = 0; t < NA; ++t)
+          tma_load_2d(sK + st * TB + t * 16384, &tk, &k_full[st], h * HD + 64 * t, row_base + j * TK);
+      }
+    } else if (lane == 1) {  // ===== producer: the V ring =====
+      for (int j = 0; j < n_kt; ++j) {
         const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], 2 * TB);
-        for (int t = 0; t < NA; ++t) {
-          tma_load_2d(sK + st * TB + t * 16384, &tk, &kv_full[st], h * HD + 64 * t, row_base + j * TK);
-          tma_load_2d(sV + st * TB + t * 16384, &tv, &kv_full[st], h * HD + 64 * t, row_base + j * TK);
-        }
+        mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&v_full[st], TB);
+        for (int t = 0; t < NA; ++t)
+          tma_load_2d(sV + st * TB + t * 16384, &tv, &v_full[st], h * HD + 64 * t, row_base + j * TK);
       }
     }
   } else if (warp == 1) {
@@ -294,7 +312,9 @@ __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
       const uint32_t aq = su32(sQ);
       auto issue_pv = [&](int j) {
         const int st = j & 1;
+        mbar_wait(&v_full[st], (j >> 1) & 1);
         mbar_wait(p_full, j & 1);
+        ATTN_TRACE(2, j);
         fence_after();
         const uint32_t bv = su32(sV + st * TB);
 #pragma unroll
@@ -302,14 +322,15 @@ __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
           mma_ts(tmem + kColO_, tmem + kColP + kk * 8, sw128(bv + kk * 2048, 16384, 1024), IDO,
                  (j > 0 || kk > 0) ? 1u : 0u);
         commit(o_done);
-        commit(&kv_empty[st]);
+        commit(&v_empty[st]);
       };
       for (int j = 0; j < n_kt; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        const int st = j % NKF;
+        mbar_wait(&k_full[st], (j / NKF) & 1);
         mbar_wait(s_empty, (j & 1) ^ 1);  // softmax holds S_{j-1} in registers
+        ATTN_TRACE(1, j);
         fence_after();
-        const uint32_t bk = su32(sK + st * TB);
+        const uint32_t bk = su32(sK + st * TB);  // st: K stage
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
@@ -317,6 +338,7 @@ __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
               kk > 0 ? 1u : 0u);
         }
         commit(s_full);
+        commit(&k_empty[st]);
         if (j > 0) issue_pv(j - 1);
       }
       issue_pv(n_kt - 1);
@@ -331,6 +353,7 @@ __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
     float m = -INFINITY, l = 0.f;  // m in log2 units
     for (int j = 0; j < n_kt; ++j) {
       mbar_wait(s_full, j & 1);
+      if (warp == 2 && lane == 0) ATTN_TRACE(5, j);
       fence_after();
       uint32_t s[TK];
 #pragma unroll
@@ -359,8 +382,10 @@ __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
         }
         m = mx;
       }
+      if (warp == 2 && lane == 0) ATTN_TRACE(6, j);
       // P and O are free once PV_{j-1} retired
       if (j >= 1) mbar_wait(o_done, (j - 1) & 1);
+      if (warp == 2 && lane == 0) ATTN_TRACE(7, j);
       fence_after();
       if (__any_sync(0xffffffffu, rescale)) {  // 8 columns at a time: s[] stays in registers
 #pragma unroll 1
@@ -393,6 +418,7 @@ __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
+      if (warp == 2 && lane == 0) ATTN_TRACE(8, j);
     }
     // final: O / l, log-sum-exp
     mbar_wait(o_done, (n_kt - 1) & 1);
@@ -1010,7 +1036,7 @@ void attn_fwd_hd(const bf16* q, const bf16* k, const bf16* v, bf16* o, float* ls
   const int rows = B * S;
   const CUtensorMap mq = head_map(q, rows, d), mk = head_map(k, rows, d), mv = head_map(v, rows, d);
   const FwdArgs a{S, H, d, rsqrtf((float)HD) * kLog2e, o, lse};
-  constexpr int SMEM = 1024 + 16384 * 5 * (HD / 64) + 256;
+  constexpr int SMEM = 1024 + 16384 * (3 + NKF) * (HD / 64) + 256;
   static std::atomic<uint64_t> cfg{0};
   set_smem_once(cfg, attn_fwd_tc_kernel<HD>, SMEM);
   dim3 grid((S + TQ - 1) / TQ, B * H);
