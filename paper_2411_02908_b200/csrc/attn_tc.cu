@@ -503,7 +503,7 @@ __global__ void attn_bwd_prep_kernel(const bf16* __restrict__ o, const bf16* __r
 }
 
 struct BwdArgs {
-  int S, H, d, Spad;
+  int S, H, d, Spad, BH;
   float sl2, scale;
   const float* Lp;
   const float* Dp;
@@ -548,7 +548,21 @@ __device__ __forceinline__ void store_acc_rows(uint32_t taddr, bf16* row_ptr, fl
   }
 }
 
-// ---- dK, dV: CTA per 128-key tile; keys are the TMEM lanes ------------------------
+// Both backward kernels are persistent (one CTA per SM): a CTA walks a static
+// list of units, each unit = the tile pair (p, n-1-p) of one head, whose costs
+// (number of 128 x 128 tile pairs) add up to the same n+1 -- so a round-robin
+// over units balances to ~1 %, and the units of a head are adjacent, so the
+// CTAs running concurrently share their heads' Q/dO/K/V in L2.  Tile i+1's K/V
+// (resp. Q/dO) stream in while tile i finishes; the accumulators are drained by
+// the softmax warps while the MMA issuer already computes the next tile's S.
+#define PH_FOR_TILES(ntile)                                                    \
+  for (int u = blockIdx.x; u < a.BH * (((ntile) + 1) / 2); u += gridDim.x)     \
+    for (int hf = 0; hf < 2; ++hf)                                             \
+      if (const int npair_ = ((ntile) + 1) / 2, p_ = u % npair_,               \
+          tile = hf ? (ntile) - 1 - p_ : p_, bh = u / npair_;                  \
+          !(hf && tile == p_))
+
+// ---- dK, dV: 128-key tiles; keys are the TMEM lanes -------------------------------
 // TMEM at HD = 64 (128-query tiles):
 //   S^T [0,128)  dP^T [128,256)  P^T [256,320)  dS^T [320,384)  dV [384,448)  dK [448,512)
 // at HD = 128 (64-query tiles):
@@ -565,34 +579,35 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   constexpr int NA = HD / 64, KB = 16384 * NA;  // swizzle atoms per row, K/V tile bytes
   constexpr int TQB = HD == 64 ? 128 : 64, QB = TQB * 128 * NA, QA = TQB * 128;  // Q tile, atom
   constexpr int CPQ = TQB / NCG, GPH = HD / NCG;  // score / accumulator columns per thread
+  constexpr int NKV = HD == 64 ? 2 : 1;           // K/V buffers (the next tile's prefetch)
   constexpr uint32_t colDP = TQB, colP = 2 * TQB, colDS = colP + TQB / 2, colDV = 512 - 2 * HD,
                      colDK = 512 - HD;
-  uint8_t* sK = sm;
-  uint8_t* sV = sm + KB;
-  uint8_t* sQ = sm + 2 * KB;   // [NR]
-  uint8_t* sO = sQ + NR * QB;  // [NR] dO
+  uint8_t* sK = sm;               // [NKV]
+  uint8_t* sV = sK + NKV * KB;    // [NKV]
+  uint8_t* sQ = sV + NKV * KB;    // [NR]
+  uint8_t* sO = sQ + NR * QB;     // [NR] dO
   float* sL = reinterpret_cast<float*>(sO + NR * QB);  // [NR][TQB]
   float* sD = sL + NR * TQB;                           // [NR][TQB]
   uint64_t* bar = reinterpret_cast<uint64_t*>(sD + NR * TQB);
-  uint64_t* kv_full = bar;
-  uint64_t* q_full = bar + 1;        // [NR]
-  uint64_t* q_empty = bar + 1 + NR;  // [NR]
-  uint64_t* s_full = bar + 1 + 2 * NR;
+  uint64_t* kv_full = bar;                 // [NKV]
+  uint64_t* kv_empty = bar + NKV;          // [NKV]
+  uint64_t* q_full = bar + 2 * NKV;        // [NR]
+  uint64_t* q_empty = q_full + NR;         // [NR]
+  uint64_t* s_full = q_empty + NR;
   uint64_t* s_empty = s_full + 1;
   uint64_t* p_full = s_full + 2;
   uint64_t* g_done = s_full + 3;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 4);
+  uint64_t* acc_empty = s_full + 4;        // dK/dV drained by the softmax warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 5);
 
-  const int ntq = (a.S + TQB - 1) / TQB;
-  const int kt = blockIdx.x;
-  const int bh = blockIdx.y, b = bh / a.H, h = bh % a.H;
-  const int row_base = b * a.S;
-  const int qt0 = kt * (TK / TQB);  // first query tile that sees these keys
-  const int n_it = ntq - qt0;
+  const int nkt = (a.S + TK - 1) / TK, ntq = (a.S + TQB - 1) / TQB;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
-    mbar_init(kv_full, 1);
+    for (int i = 0; i < NKV; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
     for (int i = 0; i < NR; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
@@ -601,6 +616,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(s_empty, SWB);
     mbar_init(p_full, SWB);
     mbar_init(g_done, 1);
+    mbar_init(acc_empty, SWB);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -615,22 +631,29 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(kv_full, 2 * KB);
-      for (int t = 0; t < NA; ++t) {
-        tma_load_2d(sK + t * 16384, &tk, kv_full, h * HD + 64 * t, row_base + kt * TK);
-        tma_load_2d(sV + t * 16384, &tv, kv_full, h * HD + 64 * t, row_base + kt * TK);
-      }
-      for (int it = 0; it < n_it; ++it) {
-        const int st = it % NR, qt = qt0 + it;
-        mbar_wait(&q_empty[st], ((it / NR) & 1) ^ 1);
-        ATTN_TRACE(0, it);
-        mbar_expect_tx(&q_full[st], 2 * QB + 8 * TQB);
+      int ti = 0, gi = 0;
+      PH_FOR_TILES(nkt) {
+        const int kt = tile, b = bh / a.H, h = bh % a.H, row_base = b * a.S;
+        const int qt0 = kt * (TK / TQB), n_it = ntq - qt0;
+        const int kb = ti % NKV;
+        mbar_wait(&kv_empty[kb], ((ti / NKV) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[kb], 2 * KB);
         for (int t = 0; t < NA; ++t) {
-          tma_load_2d(sQ + st * QB + t * QA, &tq, &q_full[st], h * HD + 64 * t, row_base + qt * TQB);
-          tma_load_2d(sO + st * QB + t * QA, &tdo, &q_full[st], h * HD + 64 * t, row_base + qt * TQB);
+          tma_load_2d(sK + kb * KB + t * 16384, &tk, &kv_full[kb], h * HD + 64 * t, row_base + kt * TK);
+          tma_load_2d(sV + kb * KB + t * 16384, &tv, &kv_full[kb], h * HD + 64 * t, row_base + kt * TK);
         }
-        bulk_load(sL + st * TQB, a.Lp + (int64_t)bh * a.Spad + qt * TQB, 4 * TQB, &q_full[st]);
-        bulk_load(sD + st * TQB, a.Dp + (int64_t)bh * a.Spad + qt * TQB, 4 * TQB, &q_full[st]);
+        for (int it = 0; it < n_it; ++it, ++gi) {
+          const int st = gi % NR, qt = qt0 + it;
+          mbar_wait(&q_empty[st], ((gi / NR) & 1) ^ 1);
+          mbar_expect_tx(&q_full[st], 2 * QB + 8 * TQB);
+          for (int t = 0; t < NA; ++t) {
+            tma_load_2d(sQ + st * QB + t * QA, &tq, &q_full[st], h * HD + 64 * t, row_base + qt * TQB);
+            tma_load_2d(sO + st * QB + t * QA, &tdo, &q_full[st], h * HD + 64 * t, row_base + qt * TQB);
+          }
+          bulk_load(sL + st * TQB, a.Lp + (int64_t)bh * a.Spad + qt * TQB, 4 * TQB, &q_full[st]);
+          bulk_load(sD + st * TQB, a.Dp + (int64_t)bh * a.Spad + qt * TQB, 4 * TQB, &q_full[st]);
+        }
+        ++ti;
       }
     }
   } else if (warp == 1) {
@@ -639,111 +662,129 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                                ((uint32_t)(TK >> 4) << 24);
       constexpr uint32_t IDG = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
                                ((uint32_t)(HD >> 3) << 17) | ((uint32_t)(TK >> 4) << 24);
-      mbar_wait(kv_full, 0);
-      const uint32_t ak = su32(sK), av = su32(sV);
-      auto issue_grads = [&](int it) {
-        const int st = it % NR;
-        mbar_wait(p_full, it & 1);
-        ATTN_TRACE(3, it);
+      // gradients of pair g (its ring stage, whether it opens its tile, the tile index)
+      auto issue_grads = [&](int g, int st, bool first, int t) {
+        mbar_wait(p_full, g & 1);
+        if (first && t > 0) mbar_wait(acc_empty, (t - 1) & 1);  // previous dK/dV drained
         fence_after();
         const uint32_t bo = su32(sO + st * QB), bq = su32(sQ + st * QB);
 #pragma unroll
         for (int kk = 0; kk < TQB / 16; ++kk)  // dV += P^T dO (dO MN-major, QA-byte panels)
           mma_ts(tmem + colDV, tmem + colP + kk * 8, sw128(bo + kk * 2048, QA, 1024), IDG,
-                 (it > 0 || kk > 0) ? 1u : 0u);
+                 (!first || kk > 0) ? 1u : 0u);
 #pragma unroll
         for (int kk = 0; kk < TQB / 16; ++kk)  // dK += dS^T Q
           mma_ts(tmem + colDK, tmem + colDS + kk * 8, sw128(bq + kk * 2048, QA, 1024), IDG,
-                 (it > 0 || kk > 0) ? 1u : 0u);
+                 (!first || kk > 0) ? 1u : 0u);
         commit(g_done);
         commit(&q_empty[st]);
-        ATTN_TRACE(4, it);
       };
-      for (int it = 0; it < n_it; ++it) {
-        const int st = it % NR;
-        mbar_wait(&q_full[st], (it / NR) & 1);
-        ATTN_TRACE(1, it);
-        mbar_wait(s_empty, (it & 1) ^ 1);
-        ATTN_TRACE(2, it);
-        fence_after();
-        const uint32_t bq = su32(sQ + st * QB), bo = su32(sO + st * QB);
+      int ti = 0, gi = 0;
+      int pend = -1, pend_st = 0, pend_t = 0;
+      bool pend_first = false;
+      PH_FOR_TILES(nkt) {
+        (void)bh;
+        const int kt = tile, qt0 = kt * (TK / TQB), n_it = ntq - qt0;
+        const int kb = ti % NKV;
+        mbar_wait(&kv_full[kb], (ti / NKV) & 1);
+        const uint32_t ak = su32(sK + kb * KB), av = su32(sV + kb * KB);
+        for (int it = 0; it < n_it; ++it, ++gi) {
+          const int st = gi % NR;
+          mbar_wait(&q_full[st], (gi / NR) & 1);
+          mbar_wait(s_empty, (gi & 1) ^ 1);
+          fence_after();
+          const uint32_t bq = su32(sQ + st * QB), bo = su32(sO + st * QB);
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {  // S^T = K Q^T
-          const uint32_t oa = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * QA + (kk & 3) * 32;
-          mma(tmem + 0, sw128(ak + oa, 16, 1024), sw128(bq + ob, 16, 1024), IDS, kk > 0 ? 1u : 0u);
-        }
+          for (int kk = 0; kk < HD / 16; ++kk) {  // S^T = K Q^T
+            const uint32_t oa = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * QA + (kk & 3) * 32;
+            mma(tmem + 0, sw128(ak + oa, 16, 1024), sw128(bq + ob, 16, 1024), IDS, kk > 0 ? 1u : 0u);
+          }
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {  // dP^T = V dO^T
-          const uint32_t oa = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * QA + (kk & 3) * 32;
-          mma(tmem + colDP, sw128(av + oa, 16, 1024), sw128(bo + ob, 16, 1024), IDS,
-              kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < HD / 16; ++kk) {  // dP^T = V dO^T
+            const uint32_t oa = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * QA + (kk & 3) * 32;
+            mma(tmem + colDP, sw128(av + oa, 16, 1024), sw128(bo + ob, 16, 1024), IDS,
+                kk > 0 ? 1u : 0u);
+          }
+          commit(s_full);
+          if (it == n_it - 1) commit(&kv_empty[kb]);  // this tile's K/V no longer read
+          if (pend >= 0) issue_grads(pend, pend_st, pend_first, pend_t);
+          pend = gi;
+          pend_st = st;
+          pend_first = it == 0;
+          pend_t = ti;
         }
-        commit(s_full);
-        if (it > 0) issue_grads(it - 1);
+        ++ti;
       }
-      issue_grads(n_it - 1);
+      if (pend >= 0) issue_grads(pend, pend_st, pend_first, pend_t);
     }
   } else {
     const int q = warp & 3, cg = (warp - 2) >> 2;  // lane quarter, query-column group
     const int r = q * 32 + lane;
-    const int key = kt * TK + r;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const bool key_live = key < a.S;
-    for (int it = 0; it < n_it; ++it) {
-      const int st = it % NR, q0 = (qt0 + it) * TQB;
-      mbar_wait(&q_full[st], (it / NR) & 1);  // L, D of this query tile visible
-      mbar_wait(s_full, it & 1);
-      if (warp == 2 && lane == 0) ATTN_TRACE(5, it);
-      fence_after();
-      uint32_t s[CPQ], dp[CPQ];
-      tmem_ld_cols<CPQ>(tmem + lane_off + cg * CPQ, s);
-      tmem_ld_cols<CPQ>(tmem + lane_off + colDP + cg * CPQ, dp);
-      tmem_wait_ld();
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(s_empty);
-      const float* L = sL + st * TQB + cg * CPQ;
-      const float* D = sD + st * TQB + cg * CPQ;
-      // masking only where this key tile meets the diagonal or the sequence end
-      const bool masked = (kt * TK + TK > q0) || (kt * TK + TK > a.S);
-      uint32_t pp[CPQ / 2], dd[CPQ / 2];
-      // dS^T is kept unscaled (the softmax scale is applied to dK at the store)
+    int gi = 0;
+    PH_FOR_TILES(nkt) {
+      const int kt = tile, b = bh / a.H, h = bh % a.H, row_base = b * a.S;
+      const int qt0 = kt * (TK / TQB), n_it = ntq - qt0;
+      const int key = kt * TK + r;
+      const bool key_live = key < a.S;
+      for (int it = 0; it < n_it; ++it, ++gi) {
+        const int st = gi % NR, q0 = (qt0 + it) * TQB;
+        mbar_wait(&q_full[st], (gi / NR) & 1);  // L, D of this query tile visible
+        mbar_wait(s_full, gi & 1);
+        fence_after();
+        uint32_t s[CPQ], dp[CPQ];
+        tmem_ld_cols<CPQ>(tmem + lane_off + cg * CPQ, s);
+        tmem_ld_cols<CPQ>(tmem + lane_off + colDP + cg * CPQ, dp);
+        tmem_wait_ld();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_empty);
+        const float* L = sL + st * TQB + cg * CPQ;
+        const float* D = sD + st * TQB + cg * CPQ;
+        // masking only where this key tile meets the diagonal or the sequence end
+        const bool masked = (kt * TK + TK > q0) || (kt * TK + TK > a.S);
+        uint32_t pp[CPQ / 2], dd[CPQ / 2];
+        // dS^T is kept unscaled (the softmax scale is applied to dK at the store)
 #pragma unroll
-      for (int i = 0; i < CPQ / 4; ++i) {
-        const float4 l4 = lds_f4(L + 4 * i), d4 = lds_f4(D + 4 * i);
-        float p0 = ex2(fmaf(__uint_as_float(s[4 * i]), a.sl2, -l4.x));
-        float p1 = ex2(fmaf(__uint_as_float(s[4 * i + 1]), a.sl2, -l4.y));
-        float p2 = ex2(fmaf(__uint_as_float(s[4 * i + 2]), a.sl2, -l4.z));
-        float p3 = ex2(fmaf(__uint_as_float(s[4 * i + 3]), a.sl2, -l4.w));
-        if (masked) {
-          const int qc = q0 + cg * CPQ + 4 * i;
-          p0 = (key_live && key <= qc) ? p0 : 0.f;
-          p1 = (key_live && key <= qc + 1) ? p1 : 0.f;
-          p2 = (key_live && key <= qc + 2) ? p2 : 0.f;
-          p3 = (key_live && key <= qc + 3) ? p3 : 0.f;
+        for (int i = 0; i < CPQ / 4; ++i) {
+          const float4 l4 = lds_f4(L + 4 * i), d4 = lds_f4(D + 4 * i);
+          float p0 = ex2(fmaf(__uint_as_float(s[4 * i]), a.sl2, -l4.x));
+          float p1 = ex2(fmaf(__uint_as_float(s[4 * i + 1]), a.sl2, -l4.y));
+          float p2 = ex2(fmaf(__uint_as_float(s[4 * i + 2]), a.sl2, -l4.z));
+          float p3 = ex2(fmaf(__uint_as_float(s[4 * i + 3]), a.sl2, -l4.w));
+          if (masked) {
+            const int qc = q0 + cg * CPQ + 4 * i;
+            p0 = (key_live && key <= qc) ? p0 : 0.f;
+            p1 = (key_live && key <= qc + 1) ? p1 : 0.f;
+            p2 = (key_live && key <= qc + 2) ? p2 : 0.f;
+            p3 = (key_live && key <= qc + 3) ? p3 : 0.f;
+          }
+          pp[2 * i] = pk(p0, p1);
+          pp[2 * i + 1] = pk(p2, p3);
+          dd[2 * i] = pk(p0 * (__uint_as_float(dp[4 * i]) - d4.x),
+                         p1 * (__uint_as_float(dp[4 * i + 1]) - d4.y));
+          dd[2 * i + 1] = pk(p2 * (__uint_as_float(dp[4 * i + 2]) - d4.z),
+                             p3 * (__uint_as_float(dp[4 * i + 3]) - d4.w));
         }
-        pp[2 * i] = pk(p0, p1);
-        pp[2 * i + 1] = pk(p2, p3);
-        dd[2 * i] = pk(p0 * (__uint_as_float(dp[4 * i]) - d4.x),
-                       p1 * (__uint_as_float(dp[4 * i + 1]) - d4.y));
-        dd[2 * i + 1] = pk(p2 * (__uint_as_float(dp[4 * i + 2]) - d4.z),
-                           p3 * (__uint_as_float(dp[4 * i + 3]) - d4.w));
+        if (gi >= 1) mbar_wait(g_done, (gi - 1) & 1);  // P^T / dS^T columns free
+        fence_after();
+        tmem_st_cols<CPQ / 2>(tmem + lane_off + colP + cg * (CPQ / 2), pp);
+        tmem_st_cols<CPQ / 2>(tmem + lane_off + colDS + cg * (CPQ / 2), dd);
+        tmem_wait_st();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full);
       }
-      if (warp == 2 && lane == 0) ATTN_TRACE(7, it);
-      if (it >= 1) mbar_wait(g_done, (it - 1) & 1);  // P^T / dS^T columns free
+      // the tile's dK / dV are complete once its last gradient MMAs retire
+      mbar_wait(g_done, (gi - 1) & 1);
       fence_after();
-      tmem_st_cols<CPQ / 2>(tmem + lane_off + colP + cg * (CPQ / 2), pp);
-      tmem_st_cols<CPQ / 2>(tmem + lane_off + colDS + cg * (CPQ / 2), dd);
-      tmem_wait_st();
+      const int64_t row = (int64_t)(row_base + key) * a.d + h * HD + cg * GPH;
+      store_acc_rows<GPH>(tmem + lane_off + colDK + cg * GPH, a.g0 + row, a.scale, key_live);  // dK
+      store_acc_rows<GPH>(tmem + lane_off + colDV + cg * GPH, a.g1 + row, 1.f, key_live);      // dV
       fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(acc_empty);
     }
-    mbar_wait(g_done, (n_it - 1) & 1);
-    fence_after();
-    const int64_t row = (int64_t)(row_base + key) * a.d + h * HD + cg * GPH;
-    store_acc_rows<GPH>(tmem + lane_off + colDK + cg * GPH, a.g0 + row, a.scale, key_live);  // dK
-    store_acc_rows<GPH>(tmem + lane_off + colDV + cg * GPH, a.g1 + row, 1.f, key_live);      // dV
   }
   fence_before();
   __syncthreads();
@@ -753,7 +794,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   }
 }
 
-// ---- dQ: CTA per 128-query tile; queries are the TMEM lanes ------------------------
+// ---- dQ: 128-query tiles; queries are the TMEM lanes --------------------------------
 // TMEM: S [0,128)  dP [128,256)  dS [256,320)  dQ [320,320+HD)
 template <int HD>
 __global__ void __launch_bounds__(kBwdThreads, 1)
@@ -765,31 +806,32 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                                            ~uintptr_t(1023));
   constexpr int NA = HD / 64, KB = 16384 * NA;  // swizzle atoms per row, tile bytes
   constexpr int NRQ = HD == 64 ? NR : 2;         // K/V ring depth within 227 KB
+  constexpr int NQO = HD == 64 ? 2 : 1;          // Q/dO buffers (the next tile's prefetch)
   constexpr int GPH = HD / NCG;
-  uint8_t* sQ = sm;
-  uint8_t* sO = sm + KB;
-  uint8_t* sK = sm + 2 * KB;    // [NRQ]
-  uint8_t* sV = sK + NRQ * KB;  // [NRQ]
+  uint8_t* sQ = sm;                // [NQO]
+  uint8_t* sO = sQ + NQO * KB;     // [NQO]
+  uint8_t* sK = sO + NQO * KB;     // [NRQ]
+  uint8_t* sV = sK + NRQ * KB;     // [NRQ]
   uint64_t* bar = reinterpret_cast<uint64_t*>(sV + NRQ * KB);
-  uint64_t* q_full = bar;
-  uint64_t* kv_full = bar + 1;         // [NRQ]
-  uint64_t* kv_empty = bar + 1 + NRQ;  // [NRQ]
-  uint64_t* s_full = bar + 1 + 2 * NRQ;
+  uint64_t* qo_full = bar;                 // [NQO]
+  uint64_t* qo_empty = bar + NQO;          // [NQO]
+  uint64_t* kv_full = bar + 2 * NQO;       // [NRQ]
+  uint64_t* kv_empty = kv_full + NRQ;      // [NRQ]
+  uint64_t* s_full = kv_empty + NRQ;
   uint64_t* s_empty = s_full + 1;
   uint64_t* p_full = s_full + 2;
   uint64_t* g_done = s_full + 3;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 4);
+  uint64_t* acc_empty = s_full + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 5);
 
-  const int nt = (a.S + TQ - 1) / TQ;
-  const int qt = nt - 1 - blockIdx.x;
-  const int bh = blockIdx.y, b = bh / a.H, h = bh % a.H;
-  const int row_base = b * a.S;
-  const int q0 = qt * TQ;
-  const int n_kt = qt + 1;
+  const int nqt = (a.S + TQ - 1) / TQ;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
-    mbar_init(q_full, 1);
+    for (int i = 0; i < NQO; ++i) {
+      mbar_init(&qo_full[i], 1);
+      mbar_init(&qo_empty[i], 1);
+    }
     for (int i = 0; i < NRQ; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
@@ -798,6 +840,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(s_empty, SWB);
     mbar_init(p_full, SWB);
     mbar_init(g_done, 1);
+    mbar_init(acc_empty, SWB);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -812,19 +855,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(q_full, 2 * KB);
-      for (int t = 0; t < NA; ++t) {
-        tma_load_2d(sQ + t * 16384, &tq, q_full, h * HD + 64 * t, row_base + q0);
-        tma_load_2d(sO + t * 16384, &tdo, q_full, h * HD + 64 * t, row_base + q0);
-      }
-      for (int j = 0; j < n_kt; ++j) {
-        const int st = j % NRQ;
-        mbar_wait(&kv_empty[st], ((j / NRQ) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], 2 * KB);
+      int ti = 0, gj = 0;
+      PH_FOR_TILES(nqt) {
+        const int qt = tile, b = bh / a.H, h = bh % a.H, row_base = b * a.S;
+        const int qb = ti % NQO;
+        mbar_wait(&qo_empty[qb], ((ti / NQO) & 1) ^ 1);
+        mbar_expect_tx(&qo_full[qb], 2 * KB);
         for (int t = 0; t < NA; ++t) {
-          tma_load_2d(sK + st * KB + t * 16384, &tk, &kv_full[st], h * HD + 64 * t, row_base + j * TK);
-          tma_load_2d(sV + st * KB + t * 16384, &tv, &kv_full[st], h * HD + 64 * t, row_base + j * TK);
+          tma_load_2d(sQ + qb * KB + t * 16384, &tq, &qo_full[qb], h * HD + 64 * t, row_base + qt * TQ);
+          tma_load_2d(sO + qb * KB + t * 16384, &tdo, &qo_full[qb], h * HD + 64 * t, row_base + qt * TQ);
         }
+        for (int j = 0; j <= qt; ++j, ++gj) {
+          const int st = gj % NRQ;
+          mbar_wait(&kv_empty[st], ((gj / NRQ) & 1) ^ 1);
+          mbar_expect_tx(&kv_full[st], 2 * KB);
+          for (int t = 0; t < NA; ++t) {
+            tma_load_2d(sK + st * KB + t * 16384, &tk, &kv_full[st], h * HD + 64 * t, row_base + j * TK);
+            tma_load_2d(sV + st * KB + t * 16384, &tv, &kv_full[st], h * HD + 64 * t, row_base + j * TK);
+          }
+        }
+        ++ti;
       }
     }
   } else if (warp == 1) {
@@ -833,85 +883,105 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                                ((uint32_t)(TQ >> 4) << 24);
       constexpr uint32_t IDG = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
                                ((uint32_t)(HD >> 3) << 17) | ((uint32_t)(TQ >> 4) << 24);
-      mbar_wait(q_full, 0);
-      const uint32_t aq = su32(sQ), ao = su32(sO);
-      auto issue_dq = [&](int j) {
-        const int st = j % NRQ;
-        mbar_wait(p_full, j & 1);
+      auto issue_dq = [&](int g, int st, bool first, int t) {
+        mbar_wait(p_full, g & 1);
+        if (first && t > 0) mbar_wait(acc_empty, (t - 1) & 1);  // previous dQ drained
         fence_after();
         const uint32_t bk = su32(sK + st * KB);
 #pragma unroll
         for (int kk = 0; kk < TK / 16; ++kk)  // dQ += dS K (K MN-major, 16 KB panels)
           mma_ts(tmem + 320, tmem + 256 + kk * 8, sw128(bk + kk * 2048, 16384, 1024), IDG,
-                 (j > 0 || kk > 0) ? 1u : 0u);
+                 (!first || kk > 0) ? 1u : 0u);
         commit(g_done);
         commit(&kv_empty[st]);
       };
-      for (int j = 0; j < n_kt; ++j) {
-        const int st = j % NRQ;
-        mbar_wait(&kv_full[st], (j / NRQ) & 1);
-        mbar_wait(s_empty, (j & 1) ^ 1);
-        fence_after();
-        const uint32_t bk = su32(sK + st * KB), bv = su32(sV + st * KB);
+      int ti = 0, gj = 0;
+      int pend = -1, pend_st = 0, pend_t = 0;
+      bool pend_first = false;
+      PH_FOR_TILES(nqt) {
+        (void)bh;
+        const int qt = tile, qb = ti % NQO;
+        mbar_wait(&qo_full[qb], (ti / NQO) & 1);
+        const uint32_t aq = su32(sQ + qb * KB), ao = su32(sO + qb * KB);
+        for (int j = 0; j <= qt; ++j, ++gj) {
+          const int st = gj % NRQ;
+          mbar_wait(&kv_full[st], (gj / NRQ) & 1);
+          mbar_wait(s_empty, (gj & 1) ^ 1);
+          fence_after();
+          const uint32_t bk = su32(sK + st * KB), bv = su32(sV + st * KB);
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {  // S = Q K^T
-          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          mma(tmem + 0, sw128(aq + off, 16, 1024), sw128(bk + off, 16, 1024), IDS, kk > 0 ? 1u : 0u);
-        }
+          for (int kk = 0; kk < HD / 16; ++kk) {  // S = Q K^T
+            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+            mma(tmem + 0, sw128(aq + off, 16, 1024), sw128(bk + off, 16, 1024), IDS, kk > 0 ? 1u : 0u);
+          }
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {  // dP = dO V^T
-          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          mma(tmem + 128, sw128(ao + off, 16, 1024), sw128(bv + off, 16, 1024), IDS,
-              kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < HD / 16; ++kk) {  // dP = dO V^T
+            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+            mma(tmem + 128, sw128(ao + off, 16, 1024), sw128(bv + off, 16, 1024), IDS,
+                kk > 0 ? 1u : 0u);
+          }
+          commit(s_full);
+          if (j == qt) commit(&qo_empty[qb]);  // this tile's Q/dO no longer read
+          if (pend >= 0) issue_dq(pend, pend_st, pend_first, pend_t);
+          pend = gj;
+          pend_st = st;
+          pend_first = j == 0;
+          pend_t = ti;
         }
-        commit(s_full);
-        if (j > 0) issue_dq(j - 1);
+        ++ti;
       }
-      issue_dq(n_kt - 1);
+      if (pend >= 0) issue_dq(pend, pend_st, pend_first, pend_t);
     }
   } else {
     const int q = warp & 3, cg = (warp - 2) >> 2;  // lane quarter, key-column group
     const int r = q * 32 + lane;
-    const int qrow = q0 + r;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const float L = a.Lp[(int64_t)bh * a.Spad + qrow];
-    const float D = a.Dp[(int64_t)bh * a.Spad + qrow];
-    for (int j = 0; j < n_kt; ++j) {
-      mbar_wait(s_full, j & 1);
-      fence_after();
-      uint32_t s[CPT], dp[CPT];
-      tmem_ld_cols<CPT>(tmem + lane_off + cg * CPT, s);
-      tmem_ld_cols<CPT>(tmem + lane_off + 128 + cg * CPT, dp);
-      tmem_wait_ld();
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(s_empty);
-      const int k0 = j * TK + cg * CPT;
-      const bool masked = (j * TK + TK > q0) || (j * TK + TK > a.S);
-      uint32_t dd[CPT / 2];  // dS unscaled (the softmax scale is applied to dQ at the store)
+    int gj = 0;
+    PH_FOR_TILES(nqt) {
+      const int qt = tile, b = bh / a.H, h = bh % a.H, row_base = b * a.S;
+      const int q0 = qt * TQ, qrow = q0 + r;
+      const float L = a.Lp[(int64_t)bh * a.Spad + qrow];
+      const float D = a.Dp[(int64_t)bh * a.Spad + qrow];
+      for (int j = 0; j <= qt; ++j, ++gj) {
+        mbar_wait(s_full, gj & 1);
+        fence_after();
+        uint32_t s[CPT], dp[CPT];
+        tmem_ld_cols<CPT>(tmem + lane_off + cg * CPT, s);
+        tmem_ld_cols<CPT>(tmem + lane_off + 128 + cg * CPT, dp);
+        tmem_wait_ld();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_empty);
+        const int k0 = j * TK + cg * CPT;
+        const bool masked = (j * TK + TK > q0) || (j * TK + TK > a.S);
+        uint32_t dd[CPT / 2];  // dS unscaled (the softmax scale is applied to dQ at the store)
 #pragma unroll
-      for (int i = 0; i < CPT / 2; ++i) {
-        float p0 = ex2(fmaf(__uint_as_float(s[2 * i]), a.sl2, -L));
-        float p1 = ex2(fmaf(__uint_as_float(s[2 * i + 1]), a.sl2, -L));
-        if (masked) {
-          p0 = (k0 + 2 * i <= qrow && k0 + 2 * i < a.S) ? p0 : 0.f;
-          p1 = (k0 + 2 * i + 1 <= qrow && k0 + 2 * i + 1 < a.S) ? p1 : 0.f;
+        for (int i = 0; i < CPT / 2; ++i) {
+          float p0 = ex2(fmaf(__uint_as_float(s[2 * i]), a.sl2, -L));
+          float p1 = ex2(fmaf(__uint_as_float(s[2 * i + 1]), a.sl2, -L));
+          if (masked) {
+            p0 = (k0 + 2 * i <= qrow && k0 + 2 * i < a.S) ? p0 : 0.f;
+            p1 = (k0 + 2 * i + 1 <= qrow && k0 + 2 * i + 1 < a.S) ? p1 : 0.f;
+          }
+          dd[i] = pk(p0 * (__uint_as_float(dp[2 * i]) - D), p1 * (__uint_as_float(dp[2 * i + 1]) - D));
         }
-        dd[i] = pk(p0 * (__uint_as_float(dp[2 * i]) - D), p1 * (__uint_as_float(dp[2 * i + 1]) - D));
+        if (gj >= 1) mbar_wait(g_done, (gj - 1) & 1);
+        fence_after();
+        tmem_st_cols<CPT / 2>(tmem + lane_off + 256 + cg * (CPT / 2), dd);
+        tmem_wait_st();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full);
       }
-      if (j >= 1) mbar_wait(g_done, (j - 1) & 1);
+      mbar_wait(g_done, (gj - 1) & 1);
       fence_after();
-      tmem_st_cols<CPT / 2>(tmem + lane_off + 256 + cg * (CPT / 2), dd);
-      tmem_wait_st();
+      store_acc_rows<GPH>(tmem + lane_off + 320 + cg * GPH,
+                          a.g0 + (int64_t)(row_base + qrow) * a.d + h * HD + cg * GPH, a.scale,
+                          qrow < a.S);
       fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(acc_empty);
     }
-    mbar_wait(g_done, (n_kt - 1) & 1);
-    fence_after();
-    store_acc_rows<GPH>(tmem + lane_off + 320 + cg * GPH,
-                        a.g0 + (int64_t)(row_base + qrow) * a.d + h * HD + cg * GPH, a.scale,
-                        qrow < a.S);
   }
   fence_before();
   __syncthreads();
@@ -920,6 +990,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
+#undef PH_FOR_TILES
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1012,16 +1083,17 @@ void attn_bwd_hd(const bf16* q, const bf16* k, const bf16* v, const bf16* o, con
                     mo = head_map(dO, rows, d);
   const CUtensorMap mqb = TQB == 128 ? mq : head_map(q, rows, d, TQB),
                     mob = TQB == 128 ? mo : head_map(dO, rows, d, TQB);
-  BwdArgs a{S, H, d, Spad, rsqrtf((float)HD) * kLog2e, rsqrtf((float)HD), Lp, Dp, dk, dv};
+  BwdArgs a{S, H, d, Spad, B * H, rsqrtf((float)HD) * kLog2e, rsqrtf((float)HD), Lp, Dp, dk, dv};
   constexpr int NA = HD / 64;
-  constexpr int SMEM1 = 1024 + 2 * 16384 * NA + NR * 2 * TQB * 128 * NA + NR * 8 * TQB + 256;
-  constexpr int NRQ = HD == 64 ? NR : 2;
-  constexpr int SMEM2 = 1024 + (2 + 2 * NRQ) * 16384 * NA + 256;
+  constexpr int NKV = HD == 64 ? 2 : 1, NRQ = HD == 64 ? NR : 2, NQO = HD == 64 ? 2 : 1;
+  constexpr int SMEM1 = 1024 + 2 * NKV * 16384 * NA + NR * 2 * TQB * 128 * NA + NR * 8 * TQB + 512;
+  constexpr int SMEM2 = 1024 + (2 * NQO + 2 * NRQ) * 16384 * NA + 512;
   static_assert(SMEM1 <= 232448 && SMEM2 <= 232448, "attention backward: shared memory");
   static std::atomic<uint64_t> cfg1{0}, cfg2{0};
   set_smem_once(cfg1, attn_bwd_dkdv_tc_kernel<HD>, SMEM1);
   set_smem_once(cfg2, attn_bwd_dq_tc_kernel<HD>, SMEM2);
-  dim3 grid(nt, B * H);
+  // persistent: one CTA per SM over the units (tile pairs) of both kernels
+  const int grid = std::min(kNumSMs, B * H * ((nt + 1) / 2));
   attn_bwd_dkdv_tc_kernel<HD><<<grid, kBwdThreads, SMEM1, st>>>(mqb, mk, mv, mob, a);
   PH_LAUNCH_CHECK();
   a.g0 = dq;
