@@ -84,6 +84,24 @@ __device__ __forceinline__ void phi_Phi(float x, float& Phi, float& phi) {
   Phi = 0.5f * (1.0f + erf_x);
   phi = 0.39894228040143267794f * e;
 }
+// GELU(x) = x Phi(x) and GELU'(x) = Phi(x) + x phi(x) together, for the GEMM
+// epilogue: the same A&S 7.1.26 erf, with the 1/2 of Phi folded into the
+// coefficients so that w = Phi(-|x|) = t (b1 + t (b2 + ...)) exp(-x^2/2) and
+// Phi = x >= 0 ? 1 - w : w -- 16 FP ops + 2 MUFU per element.
+__device__ __forceinline__ void gelu_pair(float x, float& g, float& gp) {
+  const float z = fabsf(x) * 0.70710678118654752440f;
+  float t, e;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f, z, 1.0f)));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x * (x * -0.72134752044448170f)));  // exp(-x^2/2)
+  float p = fmaf(0.5307027145f, t, -0.7265760135f);
+  p = fmaf(p, t, 0.7107068705f);
+  p = fmaf(p, t, -0.142248368f);
+  p = fmaf(p, t, 0.127414796f);
+  const float w = p * t * e;
+  const float Phi = x >= 0.f ? 1.0f - w : w;
+  g = x * Phi;
+  gp = fmaf(x * 0.39894228040143267794f, e, Phi);
+}
 __device__ __forceinline__ float gelu_fast(float x) {
   float Phi, phi;
   phi_Phi(x, Phi, phi);

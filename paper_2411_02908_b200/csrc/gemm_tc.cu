@@ -471,27 +471,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
+      // bias of a chunk, loaded one chunk ahead: its global-load latency overlaps
+      // the previous chunk instead of following the TMEM load
+      const bool has_bias =
+          !splitk && (epi == Epi::Bias || epi == Epi::ResidBias || epi == Epi::GeluBias);
+      float4 bb[8];
+      auto load_bias = [&](int col0) {
+        if (col0 + 32 <= p.N) {
+          const float4* b4 = reinterpret_cast<const float4*>(p.bias + col0);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) bb[j] = b4[j];
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            bb[j] = make_float4(col0 + 4 * j < p.N ? p.bias[col0 + 4 * j] : 0.f,
+                                col0 + 4 * j + 1 < p.N ? p.bias[col0 + 4 * j + 1] : 0.f,
+                                col0 + 4 * j + 2 < p.N ? p.bias[col0 + 4 * j + 2] : 0.f,
+                                col0 + 4 * j + 3 < p.N ? p.bias[col0 + 4 * j + 3] : 0.f);
+        }
+      };
+      if (has_bias && rows_live && sub < nchunks) load_bias(n0 + sub * 32);
       if (rows_live) {
 #pragma unroll 1
         for (int c = sub; c < nchunks; c += 2) {
           const int col0 = n0 + c * 32;
           float v[32];
           tmem_ld32(taddr + c * 32, v);  // v[j] = acc[row0 + lane][col0 + j]
-          if (!splitk && (epi == Epi::Bias || epi == Epi::ResidBias || epi == Epi::GeluBias)) {
-            if (col0 + 32 <= p.N) {
-              const float4* b4 = reinterpret_cast<const float4*>(p.bias + col0);
+          if (has_bias) {
 #pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const float4 b = b4[j];
-                v[4 * j] += b.x;
-                v[4 * j + 1] += b.y;
-                v[4 * j + 2] += b.z;
-                v[4 * j + 3] += b.w;
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] += col0 + j < p.N ? p.bias[col0 + j] : 0.f;
+            for (int j = 0; j < 8; ++j) {
+              v[4 * j] += bb[j].x;
+              v[4 * j + 1] += bb[j].y;
+              v[4 * j + 2] += bb[j].z;
+              v[4 * j + 3] += bb[j].w;
             }
+            if (c + 2 < nchunks) load_bias(col0 + 64);
           }
           if (need_in) {
             mbar_wait(ibar, in_phase);
@@ -546,12 +560,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 4; ++j) {
               float gp[8];
 #pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                float Phi, phi;
-                phi_Phi(v[8 * j + e], Phi, phi);
-                gp[e] = fmaf(v[8 * j + e], phi, Phi);
-                v[8 * j + e] *= Phi;
-              }
+              for (int e = 0; e < 8; ++e) gelu_pair(v[8 * j + e], v[8 * j + e], gp[e]);
               sts128(oa + 2048 + sw64_off(lane, j), pack2(gp[0], gp[1]), pack2(gp[2], gp[3]),
                      pack2(gp[4], gp[5]), pack2(gp[6], gp[7]));
             }

@@ -13,6 +13,8 @@ CASES = [
     ("fwd qkv  [M,d]x[d,d] +b", M, d, d, 1, 0, 2, 1),
     ("fwd o    +b +resid f32", M, d, d, 1, 0, 3, 0),
     ("fwd w1   +b gelu", M, hid, d, 1, 0, 4, 1),
+    ("fwd w1   +b (no gelu)", M, hid, d, 1, 0, 2, 1),
+    ("fwd w1   store", M, hid, d, 1, 0, 0, 1),
     ("fwd w2   +b +resid", M, d, hid, 1, 0, 3, 0),
     ("fwd head +b", M, V, d, 1, 0, 2, 1),
     ("dX  w2   gelu'", M, hid, d, 1, 1, 5, 1),
