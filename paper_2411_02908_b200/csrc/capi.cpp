@@ -487,6 +487,13 @@ int photon_debug_gemm(int impl, int M, int N, int K, const void* A, int64_t lda,
     g.C = C; g.ldc = ldc; g.c = c_dtype ? DT::BF16 : DT::F32;
     g.epi = static_cast<Epi>(epi);
     g.bias = bias; g.resid = resid; g.aux = aux;
+    if (const char* ns = std::getenv("PHOTON_DEBUG_NSEG")) {  // timing experiments: A/B repeated
+      g.nseg = std::atoi(ns);
+      for (int i = 1; i < g.nseg && i < 3; ++i) {
+        g.A_seg[i] = A;
+        g.B_seg[i] = B;
+      }
+    }
     cudaStream_t st;
     cudaEvent_t e0, e1;
     PH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));

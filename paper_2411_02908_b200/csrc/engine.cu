@@ -374,9 +374,26 @@ void EngineT<T>::forward_backward(const StepBatch& bt, double* loss_dev, bool ba
       k::colsum<T>(dk_, M, d, part_, G(o.bk), stream);
       k::colsum<T>(dq_, M, d, part_, G(o.bq), stream);
     }
-    mm(M, d, d, dv_, d, true, W(o.wv), d, true, dy_, d, DT::F32, Epi::Store);
-    mm(M, d, d, dk_, d, true, W(o.wk), d, true, dy_, d, DT::F32, Epi::Accum);
-    mm(M, d, d, dq_, d, true, W(o.wq), d, true, dy_, d, DT::F32, Epi::Accum);
+    // dy = dv Wv^T + dk Wk^T + dq Wq^T: one K-concatenated contraction on the
+    // tensor-core path (one fp32 pass over dy instead of a store + two RMWs)
+    if (sizeof(T) == 2 && gemm_mode == 1 && d % 64 == 0) {
+      GemmArgs g;
+      g.M = M; g.N = d; g.K = d;
+      g.A = dv_; g.lda = d; g.a_kmajor = true;
+      g.B = W(o.wv); g.ldb = d; g.b_kmajor = true;
+      g.ab = dt_of<T>();
+      g.C = dy_; g.ldc = d; g.c = DT::F32;
+      g.epi = Epi::Store;
+      g.nseg = 3;
+      g.A_seg[1] = dk_; g.B_seg[1] = W(o.wk);
+      g.A_seg[2] = dq_; g.B_seg[2] = W(o.wq);
+      Scope sc(this, 0, 2.0 * M * d * 3.0 * d);
+      if (!gemm_tc(g, stream)) throw Error(PHOTON_ERR_CONFIG, "tcgen05 GEMM: K-concatenated dX");
+    } else {
+      mm(M, d, d, dv_, d, true, W(o.wv), d, true, dy_, d, DT::F32, Epi::Store);
+      mm(M, d, d, dk_, d, true, W(o.wk), d, true, dy_, d, DT::F32, Epi::Accum);
+      mm(M, d, d, dq_, d, true, W(o.wq), d, true, dy_, d, DT::F32, Epi::Accum);
+    }
     mm(d, d, M, h, d, false, dv_, d, false, G(o.wv), d, DT::F32, Epi::Store);
     mm(d, d, M, h, d, false, dk_, d, false, G(o.wk), d, DT::F32, Epi::Store);
     mm(d, d, M, h, d, false, dq_, d, false, G(o.wq), d, DT::F32, Epi::Store);

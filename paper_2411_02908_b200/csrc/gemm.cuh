@@ -40,6 +40,12 @@ struct GemmArgs {
   const float* bias = nullptr;   // [N]
   const float* resid = nullptr;  // fp32, leading dim ldc
   void* aux = nullptr;           // operand type, leading dim ldc
+  // K concatenation: C = epi(sum_s A_s B_s) over nseg operand pairs of the same
+  // shape / layout (segment 0 is A, B); one accumulator, one output pass --
+  // e.g. dX of LayerNorm-1 = dv Wv^T + dk Wk^T + dq Wq^T (tcgen05 path only)
+  int nseg = 1;
+  const void* A_seg[3] = {nullptr, nullptr, nullptr};
+  const void* B_seg[3] = {nullptr, nullptr, nullptr};
 };
 
 void gemm_simt(const GemmArgs& g, cudaStream_t st);

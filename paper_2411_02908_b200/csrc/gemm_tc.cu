@@ -40,9 +40,15 @@ constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kEpiBytesPerWarp = 8192;  // out 4 KB + in 4 KB
 constexpr int kRingBudget = 232448 - kEpiWarps * kEpiBytesPerWarp - 2048;
 
+struct OperandMaps {  // per K segment: A and B tensor maps
+  CUtensorMap a[3];
+  CUtensorMap b[3];
+};
+
 struct TcParams {
   int M, N, K;
   int num_m, num_n, splits, kb_total, kb_per_split, units;
+  int kb_seg;  // k-blocks per operand segment (kb_total = nseg * kb_seg)
   int group_m;  // raster: bands of group_m M-tiles, N-tiles swept inside a band
   int epi;     // Epi
   int c_bf16;  // output dtype
@@ -267,7 +273,7 @@ struct EpiMaps {
 
 template <int BN, bool A_MN, bool B_MN, int NCTA>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+    gemm_tc_kernel(const __grid_constant__ OperandMaps om,
                    const __grid_constant__ EpiMaps em, const TcParams p) {
   constexpr int BNL = BN / NCTA;  // B rows (N) staged by this CTA
   constexpr int A_BYTES = BM * BK * 2;
@@ -310,8 +316,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < kEpiWarps; ++i) mbar_init(&inbar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&om.a[0])) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&om.b[0])) : "memory");
   }
   if (warp == 1) {
     if (NCTA == 1) {
@@ -361,31 +367,34 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
-          const int k0 = kb * BK;
+          const int seg = kb / p.kb_seg;  // K-concatenated operand pair
+          const int k0 = (kb - seg * p.kb_seg) * BK;
+          const CUtensorMap* tmA = &om.a[seg];
+          const CUtensorMap* tmB = &om.b[seg];
           if (NCTA == 1) {
             mbar_expect_tx(&full[stage], tx);
             if (!A_MN) {
-              tma_load_2d(sa, &tmA, &full[stage], k0, mr);
+              tma_load_2d(sa, tmA, &full[stage], k0, mr);
             } else {
-              for (int c = 0; c < a_boxes; ++c) tma_load_2d(sa + c * 8192, &tmA, &full[stage], mr + 64 * c, k0);
+              for (int c = 0; c < a_boxes; ++c) tma_load_2d(sa + c * 8192, tmA, &full[stage], mr + 64 * c, k0);
             }
             if (!B_MN) {
-              tma_load_2d(sb, &tmB, &full[stage], k0, nr);
+              tma_load_2d(sb, tmB, &full[stage], k0, nr);
             } else {
-              for (int c = 0; c < b_boxes; ++c) tma_load_2d(sb + c * 8192, &tmB, &full[stage], nr + 64 * c, k0);
+              for (int c = 0; c < b_boxes; ++c) tma_load_2d(sb + c * 8192, tmB, &full[stage], nr + 64 * c, k0);
             }
           } else {
             const uint32_t lbar = leader_full0 + stage * 8;  // leader's full[stage]
             if (leader) mbar_expect_tx(&full[stage], tx);   // its arrive + both CTAs' bytes
             if (!A_MN) {
-              tma_load_2d_pair(sa, &tmA, lbar, k0, mr);
+              tma_load_2d_pair(sa, tmA, lbar, k0, mr);
             } else {
-              for (int c = 0; c < a_boxes; ++c) tma_load_2d_pair(sa + c * 8192, &tmA, lbar, mr + 64 * c, k0);
+              for (int c = 0; c < a_boxes; ++c) tma_load_2d_pair(sa + c * 8192, tmA, lbar, mr + 64 * c, k0);
             }
             if (!B_MN) {
-              tma_load_2d_pair(sb, &tmB, lbar, k0, nr);
+              tma_load_2d_pair(sb, tmB, lbar, k0, nr);
             } else {
-              for (int c = 0; c < b_boxes; ++c) tma_load_2d_pair(sb + c * 8192, &tmB, lbar, nr + 64 * c, k0);
+              for (int c = 0; c < b_boxes; ++c) tma_load_2d_pair(sb + c * 8192, tmB, lbar, nr + 64 * c, k0);
             }
           }
           if (++stage == STAGES) {
@@ -705,8 +714,7 @@ CUtensorMap epi_map(const void* base, bool bf, uint64_t N, uint64_t M, int64_t l
 }
 
 template <int BN, bool A_MN, bool B_MN, int NCTA>
-void launch(const CUtensorMap& a, const CUtensorMap& b, const EpiMaps& em, const TcParams& p,
-            int grid, cudaStream_t st) {
+void launch(const OperandMaps& om, const EpiMaps& em, const TcParams& p, int grid, cudaStream_t st) {
   constexpr int STAGE_BYTES = (BM + BN / NCTA) * BK * 2;
   constexpr int STAGES = kRingBudget / STAGE_BYTES;
   static_assert(STAGES >= 3, "operand ring too shallow");
@@ -720,7 +728,7 @@ void launch(const CUtensorMap& a, const CUtensorMap& b, const EpiMaps& em, const
     configured.fetch_or(1ull << (dev & 63));
   }
   if (NCTA == 1) {
-    kern<<<grid, kThreads, SMEM, st>>>(a, b, em, p);
+    kern<<<grid, kThreads, SMEM, st>>>(om, em, p);
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -734,7 +742,7 @@ void launch(const CUtensorMap& a, const CUtensorMap& b, const EpiMaps& em, const
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    PH_CUDA(cudaLaunchKernelEx(&cfg, kern, a, b, em, p));
+    PH_CUDA(cudaLaunchKernelEx(&cfg, kern, om, em, p));
   }
   PH_LAUNCH_CHECK();
 }
@@ -766,6 +774,8 @@ bool gemm_tc_supported(const GemmArgs& g) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return false;
   if ((g.lda & 7) || (g.ldb & 7)) return false;  // TMA: 16-byte row strides
   if (!aligned16(g.A) || !aligned16(g.B) || !aligned16(g.C)) return false;
+  for (int s = 1; s < g.nseg; ++s)
+    if (!aligned16(g.A_seg[s]) || !aligned16(g.B_seg[s])) return false;
   if ((g.ldc * (g.c == DT::BF16 ? 2 : 4)) & 15) return false;
   if ((g.epi == Epi::GeluBias || g.epi == Epi::GeluBwd) && (g.c != DT::BF16 || !aligned16(g.aux)))
     return false;
@@ -797,7 +807,10 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
   p.K = g.K;
   p.num_m = (g.M + BM * ncta - 1) / (BM * ncta);
   p.num_n = (g.N + BN - 1) / BN;
-  p.kb_total = (g.K + BK - 1) / BK;
+  if (g.nseg < 1 || g.nseg > 3 || (g.nseg > 1 && g.K % BK))
+    throw Error(PHOTON_ERR_USAGE, "gemm_tc: K segments need 1..3 segments of whole k-blocks");
+  p.kb_seg = (g.K + BK - 1) / BK;
+  p.kb_total = p.kb_seg * g.nseg;
   const int tiles = p.num_m * p.num_n;
   // split-K when the tile grid cannot fill the chip and the contraction is long
   int splits = 1;
@@ -835,29 +848,33 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
     if (g.epi == Epi::Accum) em.in = epi_map(g.C, false, g.N, g.M, g.ldc);
   }
 
-  // A(i,k): K-major -> [M][K] rows; MN-major -> [K][M] rows
-  const CUtensorMap ta = g.a_kmajor ? operand_map(g.A, g.K, g.M, g.lda, BM)
-                                    : operand_map(g.A, g.M, g.K, g.lda, 64);
-  // B(k,j): K-major -> [N][K] rows; N-major -> [K][N] rows
-  const CUtensorMap tb = g.b_kmajor ? operand_map(g.B, g.K, g.N, g.ldb, BN / ncta)
-                                    : operand_map(g.B, g.N, g.K, g.ldb, 64);
+  OperandMaps om;
+  for (int sgi = 0; sgi < g.nseg; ++sgi) {
+    const void* A = sgi == 0 ? g.A : g.A_seg[sgi];
+    const void* B = sgi == 0 ? g.B : g.B_seg[sgi];
+    // A(i,k): K-major -> [M][K] rows; MN-major -> [K][M] rows
+    om.a[sgi] = g.a_kmajor ? operand_map(A, g.K, g.M, g.lda, BM) : operand_map(A, g.M, g.K, g.lda, 64);
+    // B(k,j): K-major -> [N][K] rows; N-major -> [K][N] rows
+    om.b[sgi] = g.b_kmajor ? operand_map(B, g.K, g.N, g.ldb, BN / ncta)
+                           : operand_map(B, g.N, g.K, g.ldb, 64);
+  }
   const int grid = std::min(p.units, slots) * ncta;
   const bool amn = !g.a_kmajor, bmn = !g.b_kmajor;
   if (BN == 128) {
-    if (!amn && !bmn) launch<128, false, false, 1>(ta, tb, em, p, grid, st);
-    else if (!amn && bmn) launch<128, false, true, 1>(ta, tb, em, p, grid, st);
-    else if (amn && !bmn) launch<128, true, false, 1>(ta, tb, em, p, grid, st);
-    else launch<128, true, true, 1>(ta, tb, em, p, grid, st);
+    if (!amn && !bmn) launch<128, false, false, 1>(om, em, p, grid, st);
+    else if (!amn && bmn) launch<128, false, true, 1>(om, em, p, grid, st);
+    else if (amn && !bmn) launch<128, true, false, 1>(om, em, p, grid, st);
+    else launch<128, true, true, 1>(om, em, p, grid, st);
   } else if (ncta == 1) {
-    if (!amn && !bmn) launch<256, false, false, 1>(ta, tb, em, p, grid, st);
-    else if (!amn && bmn) launch<256, false, true, 1>(ta, tb, em, p, grid, st);
-    else if (amn && !bmn) launch<256, true, false, 1>(ta, tb, em, p, grid, st);
-    else launch<256, true, true, 1>(ta, tb, em, p, grid, st);
+    if (!amn && !bmn) launch<256, false, false, 1>(om, em, p, grid, st);
+    else if (!amn && bmn) launch<256, false, true, 1>(om, em, p, grid, st);
+    else if (amn && !bmn) launch<256, true, false, 1>(om, em, p, grid, st);
+    else launch<256, true, true, 1>(om, em, p, grid, st);
   } else {
-    if (!amn && !bmn) launch<256, false, false, 2>(ta, tb, em, p, grid, st);
-    else if (!amn && bmn) launch<256, false, true, 2>(ta, tb, em, p, grid, st);
-    else if (amn && !bmn) launch<256, true, false, 2>(ta, tb, em, p, grid, st);
-    else launch<256, true, true, 2>(ta, tb, em, p, grid, st);
+    if (!amn && !bmn) launch<256, false, false, 2>(om, em, p, grid, st);
+    else if (!amn && bmn) launch<256, false, true, 2>(om, em, p, grid, st);
+    else if (amn && !bmn) launch<256, true, false, 2>(om, em, p, grid, st);
+    else launch<256, true, true, 2>(om, em, p, grid, st);
   }
   if (p.splits > 1) {
     ReduceArgs r{g.M, g.N, p.splits, p.epi, p.c_bf16, g.ldc, ws, g.C, g.bias, g.resid, g.aux};
