@@ -252,9 +252,15 @@ int photon_debug_gemm(int impl, int M, int N, int K, const void* A, int64_t lda,
                       int64_t ldc, int c_dtype, int epi, const float* bias, const float* resid,
                       void* aux, int iters, double* ms, photon_err* err);
 
+/* Bias-gradient column sums out[N] = sum_i x[i][:] of a device matrix x [M, N]
+ * (bf16 when x_bf16, else fp32), as the engine computes them (add_bias
+ * backward, tensor.cpp:279-285).  *ms = device time of the call. */
+int photon_debug_colsum(const void* x, int x_bf16, int M, int N, float* out, double* ms,
+                        photon_err* err);
+
 /* Causal attention on device pointers (bf16 q,k,v,o,dO,dq,dk,dv as [B*S, d]
  * with head h in columns [h*dh,(h+1)*dh); lse, scratch fp32 [B*H*S]):
- * impl 0 = SIMT, 1 = mma.sync tensor core, 2 = tcgen05 forward (dh = 64).
+ * impl 0 = SIMT, 1 = mma.sync tensor core, 2 = tcgen05 (dh = 64 or 128).
  * dO == NULL: forward only.  *ms = device
  * time of the call. */
 int photon_debug_attention(int impl, int B, int S, int H, int d, const void* q, const void* k,

@@ -519,6 +519,31 @@ int photon_debug_gemm(int impl, int M, int N, int K, const void* A, int64_t lda,
   });
 }
 
+int photon_debug_colsum(const void* x, int x_bf16, int M, int N, float* out, double* ms,
+                        photon_err* err) {
+  return guarded(err, [&] {
+    need(x && out && M > 0 && N > 0, PHOTON_ERR_USAGE, "debug_colsum: bad arguments");
+    DevBuf<float> part;
+    part.reserve(std::max<size_t>(k::colsum_part_floats(M, N), 1));
+    cudaStream_t st;
+    cudaEvent_t e0, e1;
+    PH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    PH_CUDA(cudaEventCreate(&e0));
+    PH_CUDA(cudaEventCreate(&e1));
+    PH_CUDA(cudaEventRecord(e0, st));
+    if (x_bf16) k::colsum<bf16>(static_cast<const bf16*>(x), M, N, part.ptr, out, st);
+    else k::colsum<float>(static_cast<const float*>(x), M, N, part.ptr, out, st);
+    PH_CUDA(cudaEventRecord(e1, st));
+    PH_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    PH_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    if (ms) *ms = t;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(st);
+  });
+}
+
 int photon_debug_attention(int impl, int B, int S, int H, int d, const void* q, const void* k,
                            const void* v, void* o, float* lse, const void* dO, float* scratch,
                            void* dq, void* dk, void* dv, double* ms, photon_err* err) {

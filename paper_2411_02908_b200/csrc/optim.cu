@@ -73,26 +73,27 @@ void clip_finalize(const double* part, double clip, double* norm_out, float* cf_
   PH_LAUNCH_CHECK();
 }
 
-// ---- AdamW (optim.cpp:61-90): f64 arithmetic over fp32 storage ------------------
-__device__ __forceinline__ void adamw_elem(float& p, float g, float& m, float& v, double cf,
-                                           double lr, double b1, double b2, double bc1,
-                                           double bc2, double eps, double wd) {
-  const double gj = (double)g * cf;
-  const double mm = b1 * (double)m + (1.0 - b1) * gj;
-  const double vv = b2 * (double)v + (1.0 - b2) * gj * gj;
-  const double pp = (double)p;
-  const double np = pp - lr * ((mm / bc1) / (sqrt(vv / bc2) + eps) + wd * pp);
-  m = (float)mm;
-  v = (float)vv;
-  p = (float)np;
+// ---- AdamW (optim.cpp:61-90) over fp32 storage -------------------------------------
+// The device engine's optimizer: fp32 arithmetic with the step constants folded
+// on the host (1/bc1, 1/bc2), two MUFU-free IEEE operations per element (sqrt,
+// division) -- HBM-bound at 30 B/param.  The exact f64 form of the reference
+// (bit-exact for the f64 C ABI) is adamw_f64_kernel below.
+__device__ __forceinline__ void adamw_elem(float& p, float g, float& m, float& v, float cf,
+                                           float lr, float b1, float b2, float ib1, float ib2,
+                                           float eps, float wd) {
+  const float gj = g * cf;
+  const float mm = b1 * m + (1.0f - b1) * gj;
+  const float vv = b2 * v + ((1.0f - b2) * gj) * gj;
+  p = p - lr * ((mm * ib1) / (sqrtf(vv * ib2) + eps) + wd * p);
+  m = mm;
+  v = vv;
 }
 
-__global__ void adamw_f32_kernel(float* __restrict__ p, const float* __restrict__ g,
-                                 float* __restrict__ m, float* __restrict__ v,
-                                 bf16* __restrict__ shadow, uint64_t n, const float* cfp,
-                                 double lr, double b1, double b2, double bc1, double bc2,
-                                 double eps, double wd) {
-  const double cf = (double)*cfp;
+__global__ void __launch_bounds__(256) adamw_f32_kernel(
+    float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v,
+    bf16* __restrict__ shadow, uint64_t n, const float* cfp, float lr, float b1, float b2, float ib1,
+    float ib2, float eps, float wd) {
+  const float cf = *cfp;
   const uint64_t n4 = n / 4;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4;
        i += (uint64_t)gridDim.x * blockDim.x) {
@@ -100,10 +101,10 @@ __global__ void adamw_f32_kernel(float* __restrict__ p, const float* __restrict_
     const float4 G = reinterpret_cast<const float4*>(g)[i];
     float4 Mm = reinterpret_cast<float4*>(m)[i];
     float4 Vv = reinterpret_cast<float4*>(v)[i];
-    adamw_elem(P.x, G.x, Mm.x, Vv.x, cf, lr, b1, b2, bc1, bc2, eps, wd);
-    adamw_elem(P.y, G.y, Mm.y, Vv.y, cf, lr, b1, b2, bc1, bc2, eps, wd);
-    adamw_elem(P.z, G.z, Mm.z, Vv.z, cf, lr, b1, b2, bc1, bc2, eps, wd);
-    adamw_elem(P.w, G.w, Mm.w, Vv.w, cf, lr, b1, b2, bc1, bc2, eps, wd);
+    adamw_elem(P.x, G.x, Mm.x, Vv.x, cf, lr, b1, b2, ib1, ib2, eps, wd);
+    adamw_elem(P.y, G.y, Mm.y, Vv.y, cf, lr, b1, b2, ib1, ib2, eps, wd);
+    adamw_elem(P.z, G.z, Mm.z, Vv.z, cf, lr, b1, b2, ib1, ib2, eps, wd);
+    adamw_elem(P.w, G.w, Mm.w, Vv.w, cf, lr, b1, b2, ib1, ib2, eps, wd);
     reinterpret_cast<float4*>(p)[i] = P;
     reinterpret_cast<float4*>(m)[i] = Mm;
     reinterpret_cast<float4*>(v)[i] = Vv;
@@ -117,7 +118,7 @@ __global__ void adamw_f32_kernel(float* __restrict__ p, const float* __restrict_
   }
   for (uint64_t i = n4 * 4 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    adamw_elem(p[i], g[i], m[i], v[i], cf, lr, b1, b2, bc1, bc2, eps, wd);
+    adamw_elem(p[i], g[i], m[i], v[i], cf, lr, b1, b2, ib1, ib2, eps, wd);
     if (shadow) shadow[i] = __float2bfloat16_rn(p[i]);
   }
 }
@@ -125,8 +126,9 @@ __global__ void adamw_f32_kernel(float* __restrict__ p, const float* __restrict_
 void adamw_f32(float* p, const float* g, float* m, float* v, bf16* shadow, uint64_t n,
                const float* cf, double lr, double b1, double b2, double bc1, double bc2,
                double eps, double wd, cudaStream_t st) {
-  adamw_f32_kernel<<<kNumSMs * 8, 256, 0, st>>>(p, g, m, v, shadow, n, cf, lr, b1, b2, bc1, bc2,
-                                                eps, wd);
+  adamw_f32_kernel<<<kNumSMs * 8, 256, 0, st>>>(p, g, m, v, shadow, n, cf, (float)lr, (float)b1,
+                                                (float)b2, (float)(1.0 / bc1), (float)(1.0 / bc2),
+                                                (float)eps, (float)wd);
   PH_LAUNCH_CHECK();
 }
 

@@ -85,3 +85,25 @@ def test_gemm_epilogues(epi, c_bf16, shape):
     M, N, K = shape
     _run(1, M, N, K, True, False, epi, c_bf16)
     _run(0, M, N, K, True, False, epi, c_bf16)
+
+
+@pytest.mark.parametrize("M,N,bf", [(4096, 50368, 1), (1000, 8192, 1), (300, 768, 1), (257, 3072, 0),
+                                    (2048, 16384, 1)])
+def test_bias_grad_colsum(M, N, bf):
+    # the head bias (N = V) takes the whole-row shared-memory kernel, the others
+    # the strip kernel; both against a float64 torch column sum
+    import ctypes as C
+
+    from paper_2411_02908_b200 import _capi as A
+
+    g = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.randn(M, N, device="cuda", generator=g)
+    x = x.bfloat16() if bf else x
+    out = torch.empty(N, device="cuda")
+    ms = C.c_double()
+    err = A.photon_err()
+    assert A.lib().photon_debug_colsum(x.data_ptr(), bf, M, N, out.data_ptr(), C.byref(ms),
+                                       C.byref(err)) == 0, err.msg
+    torch.cuda.synchronize()
+    ref = x.double().sum(0)
+    assert (out.double() - ref).abs().max().item() <= 1e-3 * (1 + ref.abs().max().item())
