@@ -436,6 +436,7 @@ static bool colsum_wide_ok(int N, size_t elem) {
 size_t colsum_part_floats(int M, int N) {  // upper bound over element types (bf16 strips are widest)
   size_t n = (size_t)colsum_chunks(M, N, 256) * N;
   if (colsum_wide_ok(N, 2)) n = std::max(n, (size_t)kNumSMs * N);
+  if (N % 8 == 0 && N / 8 <= 1024) n = std::max(n, (size_t)kNumSMs * 2 * N);  // colsum_rows
   return n;
 }
 
@@ -519,6 +520,55 @@ __global__ void __launch_bounds__(256) colsum_part_kernel(const T* __restrict__ 
   }
 }
 
+// Moderate rows (N / 8 <= 1024 bf16 columns-of-8: the b1 / q / k / v biases):
+// thread = (row slot, 8-column chunk); a CTA reads `slots` whole rows per step
+// (contiguous), four steps in flight, sums in registers; slots reduced in a
+// fixed order through shared memory at the end.  Row ranges are contiguous per
+// CTA, partials reduced in CTA order.
+constexpr int kColsumRowsCtas = kNumSMs * 2;
+static int colsum_rows_slots(int N) { return std::max(1, 1024 / (N / 8)); }
+static bool colsum_rows_ok(int N, size_t elem) {
+  return elem == 2 && (N % 8) == 0 && N / 8 <= 1024 && N >= 256;
+}
+
+__global__ void __launch_bounds__(1024, 2)
+    colsum_rows_kernel(const bf16* __restrict__ x, int M, int N, int slots, float* __restrict__ part) {
+  extern __shared__ float red[];  // [slots][N]
+  const int nch = N / 8;
+  const int slot = threadIdx.x / nch, ch = threadIdx.x % nch;
+  const int per = (M + gridDim.x - 1) / gridDim.x;
+  const int r0 = blockIdx.x * per, r1 = min(M, r0 + per);
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (slot < slots) {
+    constexpr int U = 4;
+    for (int r = r0 + slot; r < r1; r += U * slots) {
+      uint4 u[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int rr = r + k * slots;
+        u[k] = rr < r1 ? reinterpret_cast<const uint4*>(x + (size_t)rr * N)[ch] : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const uint32_t w[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          acc[2 * e] += __uint_as_float(w[e] << 16);
+          acc[2 * e + 1] += __uint_as_float(w[e] & 0xffff0000u);
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) red[(size_t)slot * N + ch * 8 + e] = acc[e];
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    float t = 0.f;
+    for (int s2 = 0; s2 < slots; ++s2) t += red[(size_t)s2 * N + j];
+    part[(size_t)blockIdx.x * N + j] = t;
+  }
+}
+
 template <typename T>
 void colsum(const T* x, int M, int N, float* part, float* out, cudaStream_t st) {
   if constexpr (sizeof(T) == 2) {
@@ -537,6 +587,26 @@ void colsum(const T* x, int M, int N, float* part, float* out, cudaStream_t st) 
           reinterpret_cast<const bf16*>(x), M, N, part);
       PH_LAUNCH_CHECK();
       colreduce(part, kNumSMs, N, N, out, N, nullptr, st);
+      return;
+    }
+    if (colsum_rows_ok(N, sizeof(T)) && M >= 4 * kColsumRowsCtas &&
+        (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+      const int slots = colsum_rows_slots(N);
+      const int smem = slots * N * 4;
+      if (smem > 48 * 1024) {
+        static std::atomic<uint64_t> attr{0};
+        int dev = 0;
+        PH_CUDA(cudaGetDevice(&dev));
+        if (!(attr.load() & (1ull << (dev & 63)))) {
+          PH_CUDA(cudaFuncSetAttribute(colsum_rows_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+          attr.fetch_or(1ull << (dev & 63));
+        }
+      }
+      colsum_rows_kernel<<<kColsumRowsCtas, 1024, smem, st>>>(reinterpret_cast<const bf16*>(x), M, N,
+                                                              slots, part);
+      PH_LAUNCH_CHECK();
+      colreduce(part, kColsumRowsCtas, N, N, out, N, nullptr, st);
       return;
     }
   }

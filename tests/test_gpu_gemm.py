@@ -88,10 +88,12 @@ def test_gemm_epilogues(epi, c_bf16, shape):
 
 
 @pytest.mark.parametrize("M,N,bf", [(4096, 50368, 1), (1000, 8192, 1), (300, 768, 1), (257, 3072, 0),
-                                    (2048, 16384, 1)])
+                                    (2048, 16384, 1), (65536, 768, 1), (8192, 3072, 1),
+                                    (5000, 256, 1), (3001, 1032, 1)])
 def test_bias_grad_colsum(M, N, bf):
-    # the head bias (N = V) takes the whole-row shared-memory kernel, the others
-    # the strip kernel; both against a float64 torch column sum
+    # the head bias (N = V) takes the whole-row shared-memory kernel, moderate
+    # widths the row-slot kernel, small inputs the strip kernel; all against a
+    # float64 torch column sum
     import ctypes as C
 
     from paper_2411_02908_b200 import _capi as A
