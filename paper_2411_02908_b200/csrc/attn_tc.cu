@@ -39,7 +39,15 @@ __device__ unsigned long long g_attn_trace[64 * 64];
     if (blockIdx.x == 0 && blockIdx.y == 200 && (it) < 64)                            \
       g_attn_trace[(e) * 64 + (it)] = clock64();                                      \
   } while (0)
+// persistent kernels: CTA 0, global pair index g
+#define ATTN_TRACE_P(e, g)                                                            \
+  do {                                                                                \
+    if (blockIdx.x == 0 && (g) < 64) g_attn_trace[(e) * 64 + (g)] = clock64();        \
+  } while (0)
 #else
+#define ATTN_TRACE_P(e, g) \
+  do {                     \
+  } while (0)
 #define ATTN_TRACE(e, it) \
   do {                    \
   } while (0)
@@ -645,6 +653,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int it = 0; it < n_it; ++it, ++gi) {
           const int st = gi % NR, qt = qt0 + it;
           mbar_wait(&q_empty[st], ((gi / NR) & 1) ^ 1);
+          ATTN_TRACE_P(0, gi);
           mbar_expect_tx(&q_full[st], 2 * QB + 8 * TQB);
           for (int t = 0; t < NA; ++t) {
             tma_load_2d(sQ + st * QB + t * QA, &tq, &q_full[st], h * HD + 64 * t, row_base + qt * TQB);
@@ -665,6 +674,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       // gradients of pair g (its ring stage, whether it opens its tile, the tile index)
       auto issue_grads = [&](int g, int st, bool first, int t) {
         mbar_wait(p_full, g & 1);
+        ATTN_TRACE_P(3, g);
         if (first && t > 0) mbar_wait(acc_empty, (t - 1) & 1);  // previous dK/dV drained
         fence_after();
         const uint32_t bo = su32(sO + st * QB), bq = su32(sQ + st * QB);
@@ -691,7 +701,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int it = 0; it < n_it; ++it, ++gi) {
           const int st = gi % NR;
           mbar_wait(&q_full[st], (gi / NR) & 1);
+          ATTN_TRACE_P(1, gi);
           mbar_wait(s_empty, (gi & 1) ^ 1);
+          ATTN_TRACE_P(2, gi);
           fence_after();
           const uint32_t bq = su32(sQ + st * QB), bo = su32(sO + st * QB);
 #pragma unroll
@@ -731,6 +743,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int st = gi % NR, q0 = (qt0 + it) * TQB;
         mbar_wait(&q_full[st], (gi / NR) & 1);  // L, D of this query tile visible
         mbar_wait(s_full, gi & 1);
+        if (warp == 2 && lane == 0) ATTN_TRACE_P(5, gi);
         fence_after();
         uint32_t s[CPQ], dp[CPQ];
         tmem_ld_cols<CPQ>(tmem + lane_off + cg * CPQ, s);
@@ -739,6 +752,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(s_empty);
+        if (warp == 2 && lane == 0) ATTN_TRACE_P(6, gi);
         const float* L = sL + st * TQB + cg * CPQ;
         const float* D = sD + st * TQB + cg * CPQ;
         // masking only where this key tile meets the diagonal or the sequence end
@@ -766,7 +780,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           dd[2 * i + 1] = pk(p2 * (__uint_as_float(dp[4 * i + 2]) - d4.z),
                              p3 * (__uint_as_float(dp[4 * i + 3]) - d4.w));
         }
+        if (warp == 2 && lane == 0) ATTN_TRACE_P(7, gi);
         if (gi >= 1) mbar_wait(g_done, (gi - 1) & 1);  // P^T / dS^T columns free
+        if (warp == 2 && lane == 0) ATTN_TRACE_P(8, gi);
         fence_after();
         tmem_st_cols<CPQ / 2>(tmem + lane_off + colP + cg * (CPQ / 2), pp);
         tmem_st_cols<CPQ / 2>(tmem + lane_off + colDS + cg * (CPQ / 2), dd);
@@ -774,6 +790,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full);
+        if (warp == 2 && lane == 0) ATTN_TRACE_P(9, gi);
       }
       // the tile's dK / dV are complete once its last gradient MMAs retire
       mbar_wait(g_done, (gi - 1) & 1);
