@@ -272,10 +272,16 @@ static void colreduce(const float* part, int nparts, int n, int stride, float* o
   PH_LAUNCH_CHECK();
 }
 
-// Register-resident variant for d = 128 * NV: one warp per row, x and dy read
-// once as float4, dgain/dbias accumulated per lane (each lane owns fixed
-// columns) and reduced over the block's warps in a fixed order at the end.
-// dres may alias dx_out (in-place residual accumulation), so neither is restrict.
+// Register-resident variant for d = 128 * NV: one warp per row, x, dy and the
+// residual gradient of a row all requested before any arithmetic (one DRAM
+// latency per row instead of two), each read once as float4.  The column
+// accumulators -- dgain, dbias and the column sums of the output -- live in
+// shared memory per warp (each lane owns fixed columns: no conflicts), which
+// keeps the registers for the loads in flight; warps are reduced in a fixed
+// order at the end.  dres may alias dx_out (in-place residual accumulation),
+// so neither is restrict.
+constexpr int kLnBwdVecSmem(int D) { return (D / 4) * 16 + 3 * kLnBwdWarps * D * 4; }
+
 template <typename T, int NV>
 __global__ void __launch_bounds__(256, 2)
 ln_bwd_vec_kernel(const float* __restrict__ dy, const float* __restrict__ x,
@@ -283,98 +289,88 @@ ln_bwd_vec_kernel(const float* __restrict__ dy, const float* __restrict__ x,
                   const float* __restrict__ gain, const float* dres, float* dx_out,
                   T* __restrict__ dx_T, float* __restrict__ part, int M, int osum) {
   constexpr int D = NV * 128;
-  __shared__ float4 gs[D / 4];
-  __shared__ float red[kLnBwdWarps][D];  // per-warp column sums of dx_out, then the reductions
+  extern __shared__ float4 lnb_sm[];
+  float4* gs = lnb_sm;                                      // [D/4] gain
+  float* red = reinterpret_cast<float*>(lnb_sm + D / 4);    // [3][warps][D]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float4* ag = reinterpret_cast<float4*>(red + (size_t)(0 * kLnBwdWarps + warp) * D);
+  float4* ab = reinterpret_cast<float4*>(red + (size_t)(1 * kLnBwdWarps + warp) * D);
+  float4* ao = reinterpret_cast<float4*>(red + (size_t)(2 * kLnBwdWarps + warp) * D);
   for (int j = threadIdx.x; j < D / 4; j += blockDim.x) gs[j] = reinterpret_cast<const float4*>(gain)[j];
-  if (osum)
-    for (int j = lane; j < D / 4; j += 32)
-      reinterpret_cast<float4*>(red[warp])[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    ag[lane + 32 * i] = z;
+    ab[lane + 32 * i] = z;
+    ao[lane + 32 * i] = z;
+  }
   __syncthreads();
   const float inv_d = 1.0f / (float)D;
-  float4 ag[NV], ab[NV];
-#pragma unroll
-  for (int i = 0; i < NV; ++i) ag[i] = ab[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int m = blockIdx.x * kLnBwdWarps + warp; m < M; m += gridDim.x * kLnBwdWarps) {
     const float4* xr = reinterpret_cast<const float4*>(x + (size_t)m * D);
     const float4* gr = reinterpret_cast<const float4*>(dy + (size_t)m * D);
-    float4 xv[NV], gv[NV];
+    const float4* rr = dres ? reinterpret_cast<const float4*>(dres + (size_t)m * D) : nullptr;
+    float4 xv[NV], gv[NV], rv[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       xv[i] = xr[lane + 32 * i];
       gv[i] = gr[lane + 32 * i];
+      rv[i] = rr ? rr[lane + 32 * i] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     const float mean = mean_in[m], rstd = rstd_in[m];
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
-      const float4 gg = gs[lane + 32 * i];
+      const int c4 = lane + 32 * i;
+      const float4 gg = gs[c4];
+      float4 a = ag[c4], b = ab[c4];
 #define PH_LNB_ACC(c)                                 \
   {                                                   \
     const float xh = (xv[i].c - mean) * rstd;         \
     const float dxh = gv[i].c * gg.c;                 \
     s1 += dxh;                                        \
     s2 += dxh * xh;                                   \
-    ag[i].c += gv[i].c * xh;                          \
-    ab[i].c += gv[i].c;                               \
+    a.c += gv[i].c * xh;                              \
+    b.c += gv[i].c;                                   \
   }
       PH_LNB_ACC(x) PH_LNB_ACC(y) PH_LNB_ACC(z) PH_LNB_ACC(w)
 #undef PH_LNB_ACC
+      ag[c4] = a;
+      ab[c4] = b;
     }
     s1 = warp_sum(s1) * inv_d;
     s2 = warp_sum(s2) * inv_d;
     float* out = dx_out + (size_t)m * D;
-    const float* rr = dres ? dres + (size_t)m * D : nullptr;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const int c4 = lane + 32 * i;
       const float4 gg = gs[c4];
-      float4 r = rr ? reinterpret_cast<const float4*>(rr)[c4] : make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 r = rv[i];
       r.x += rstd * (gv[i].x * gg.x - s1 - ((xv[i].x - mean) * rstd) * s2);
       r.y += rstd * (gv[i].y * gg.y - s1 - ((xv[i].y - mean) * rstd) * s2);
       r.z += rstd * (gv[i].z * gg.z - s1 - ((xv[i].z - mean) * rstd) * s2);
       r.w += rstd * (gv[i].w * gg.w - s1 - ((xv[i].w - mean) * rstd) * s2);
       reinterpret_cast<float4*>(out)[c4] = r;
       if (dx_T) store4(dx_T + (size_t)m * D + 4 * c4, r.x, r.y, r.z, r.w);
-      if (osum) {  // each lane owns these columns of its warp's row: no conflicts
-        float4 a = reinterpret_cast<float4*>(red[warp])[c4];
-        a.x += r.x;
-        a.y += r.y;
-        a.z += r.z;
-        a.w += r.w;
-        reinterpret_cast<float4*>(red[warp])[c4] = a;
+      if (osum) {
+        float4 o = ao[c4];
+        o.x += r.x;
+        o.y += r.y;
+        o.z += r.z;
+        o.w += r.w;
+        ao[c4] = o;
       }
     }
   }
   // block partials: [dgain | dbias | dsum], warps summed in ascending order
   __syncthreads();
-  if (osum) {
-    for (int j = threadIdx.x; j < D; j += blockDim.x) {
-      float acc = 0.f;
-#pragma unroll
-      for (int w = 0; w < kLnBwdWarps; ++w) acc += red[w][j];
-      part[(size_t)blockIdx.x * 3 * D + 2 * D + j] = acc;
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < NV; ++i) reinterpret_cast<float4*>(red[warp])[lane + 32 * i] = ag[i];
-  __syncthreads();
-  for (int j = threadIdx.x; j < D; j += blockDim.x) {
+  const int nsum = osum ? 3 : 2;
+  for (int j = threadIdx.x; j < nsum * D; j += blockDim.x) {
+    const int a = j / D, c = j % D;
     float acc = 0.f;
 #pragma unroll
-    for (int w = 0; w < kLnBwdWarps; ++w) acc += red[w][j];
+    for (int w = 0; w < kLnBwdWarps; ++w) acc += red[(size_t)(a * kLnBwdWarps + w) * D + c];
     part[(size_t)blockIdx.x * 3 * D + j] = acc;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < NV; ++i) reinterpret_cast<float4*>(red[warp])[lane + 32 * i] = ab[i];
-  __syncthreads();
-  for (int j = threadIdx.x; j < D; j += blockDim.x) {
-    float acc = 0.f;
-#pragma unroll
-    for (int w = 0; w < kLnBwdWarps; ++w) acc += red[w][j];
-    part[(size_t)blockIdx.x * 3 * D + D + j] = acc;
   }
 }
 
@@ -385,10 +381,20 @@ void ln_bwd(const float* dy, const float* x, const float* mean, const float* rst
   const int nsum = dsum ? 3 : 2;
   switch (d) {
 #define PH_LNB(NV)                                                                         \
-  case NV * 128:                                                                           \
-    ln_bwd_vec_kernel<T, NV><<<kLnBwdBlocks, kLnBwdWarps * 32, 0, st>>>(                   \
+  case NV * 128: {                                                                         \
+    static std::atomic<uint64_t> attr{0};                                                  \
+    int dev = 0;                                                                           \
+    PH_CUDA(cudaGetDevice(&dev));                                                          \
+    if (!(attr.load() & (1ull << (dev & 63)))) {                                           \
+      PH_CUDA(cudaFuncSetAttribute(ln_bwd_vec_kernel<T, NV>,                               \
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,            \
+                                   kLnBwdVecSmem(NV * 128)));                              \
+      attr.fetch_or(1ull << (dev & 63));                                                   \
+    }                                                                                      \
+    ln_bwd_vec_kernel<T, NV><<<kLnBwdBlocks, kLnBwdWarps * 32, kLnBwdVecSmem(NV * 128), st>>>( \
         dy, x, mean, rstd, gain, dres, dx_out, dx_T, part, M, dsum ? 1 : 0);               \
-    break;
+    break;                                                                                 \
+  }
     PH_LNB(1) PH_LNB(2) PH_LNB(3) PH_LNB(4) PH_LNB(5) PH_LNB(6)
 #undef PH_LNB
     default: {
