@@ -67,6 +67,15 @@ def _gemm_traffic():
         return None
 
 
+def _boundary_path(n_params: int) -> str:
+    """Which boundary the runner takes (runner.cpp use_peer_boundary): NVLink peer
+    memory up to 24 GB per fp32 replica, NCCL beyond or when forced."""
+    forced = os.environ.get("PHOTON_BOUNDARY")
+    if forced in ("nccl", "p2p"):
+        return forced
+    return "p2p" if n_params * 4 <= 24e9 else "nccl"
+
+
 def _peaks():
     try:
         with open(MEASURED_PEAKS) as f:
@@ -400,7 +409,7 @@ def run_ours(args):
         line["boundary"] = {"ms_max_over_ranks": agg_ms_max, "wire_bytes_per_gpu": wire,
                             "busbw_gbs": wire / (agg_ms_max * 1e-3) / 1e9, "nvlink_gbs": 900.0,
                             "frac": wire / (agg_ms_max * 1e-3) / 1e9 / 900.0,
-                            "path": "p2p" if os.environ.get("PHOTON_BOUNDARY") != "nccl" else "nccl"}
+                            "path": _boundary_path(P)}
     if world == 1 and not args.no_cpu and args.model != "125m":
         # the f64 reference state of 1.3B / 7B exceeds host RAM
         line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "n/a",
