@@ -109,3 +109,28 @@ def test_bias_grad_colsum(M, N, bf):
     torch.cuda.synchronize()
     ref = x.double().sum(0)
     assert (out.double() - ref).abs().max().item() <= 1e-3 * (1 + ref.abs().max().item())
+
+
+def test_k_concatenated_gemm(monkeypatch):
+    # photon_debug_gemm with PHOTON_DEBUG_NSEG=3 repeats (A, B) as three K
+    # segments into one accumulator: C = 3 A B (the LayerNorm-1 dX contraction
+    # dv Wv^T + dk Wk^T + dq Wq^T uses the same kernel path with distinct pairs)
+    import ctypes as C
+
+    from paper_2411_02908_b200 import _capi as A
+
+    M, N, K = 512, 768, 256
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    b = torch.randn(N, K, device="cuda", generator=g).bfloat16()  # K-major B (dX layout)
+    c = torch.zeros(M, N, device="cuda")
+    ms = C.c_double()
+    err = A.photon_err()
+    monkeypatch.setenv("PHOTON_DEBUG_NSEG", "3")
+    rc = A.lib().photon_debug_gemm(1, M, N, K, a.data_ptr(), K, 1, b.data_ptr(), K, 1, 1,
+                                   c.data_ptr(), N, 0, 0, None, None, None, 1, C.byref(ms),
+                                   C.byref(err))
+    assert rc == 0, err.msg
+    torch.cuda.synchronize()
+    ref = 3.0 * (a.float() @ b.float().t())
+    assert (c - ref).abs().max().item() <= 1e-3 * ref.abs().max().item()

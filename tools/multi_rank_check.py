@@ -29,6 +29,7 @@ theta0 = F.TransformerModel(cfg).init_params(1)
 local_cfg = F.LocalTrainConfig(model=cfg, schedule=F.LrSchedule(2e-3, 16, 160, 0.1),
                                local_steps=4, batch_size=4)
 srv = F.ServerOptConfig() if server == "fedavg" else F.diloco_server_opt()
+drop = server.endswith("_drop")  # parameter server with a simulated dropout in round 1
 if server == "central":  # DDP baseline: 6 workers, per-step gradient all-reduce
     ccfg = F.CentralizedConfig(model=cfg, schedule=F.LrSchedule(2e-3, 16, 160, 0.1), n_workers=6,
                                global_batch=12, total_steps=4, opt_reset_interval=2)
@@ -41,9 +42,13 @@ if server == "central":  # DDP baseline: 6 workers, per-step gradient all-reduce
         dist.destroy_process_group()
     sys.exit(0)
 es = F.EvalSet(["web"], 40, 7, cfg, 8)  # 5 batches: uneven over 2 or 4 ranks
-runner = F.FederationRunner(F.FederationConfig(6, 4, 3, F.Topology.kRingAllReduce, 42), local_cfg,
+topo = F.Topology.kParameterServer if drop else F.Topology.kRingAllReduce
+# with a dropout: the second sampled client of round 1 never reports (3 survivors)
+dropouts = [(1, F.sample_clients(6, 4, 42, 1)[1])] if drop else []
+runner = F.FederationRunner(F.FederationConfig(6, 4, 3, topo, 42), local_cfg,
                             srv, plan, theta0, device=local, precision="f32", rank=rank,
-                            world=world, nccl_id=nccl_id, eval_set=es, eval_every=1)
+                            world=world, nccl_id=nccl_id, eval_set=es, eval_every=1,
+                            dropouts=dropouts)
 ppls = [runner.run_round().eval_ppl for _ in range(3)]
 theta = runner.theta()
 vel = runner.velocity()
