@@ -163,6 +163,70 @@ __global__ void __launch_bounds__(256) ln_fwd_vec_kernel(const float* __restrict
   }
 }
 
+// Wide rows (d = 512 * WPR: 1,024 .. 4,096, the 1.3B / 7B widths): WPR warps of
+// a CTA share a row, each holding its 512-column slice in registers (4 float4
+// per lane); the two row sums cross warps through shared memory (double-
+// buffered by row parity, partials added in warp order), one named barrier per
+// sum.  8 / WPR rows in flight per CTA.
+template <typename T, int WPR>
+__global__ void __launch_bounds__(256) ln_fwd_split_kernel(const float* __restrict__ x,
+                                                           const float* __restrict__ gain,
+                                                           const float* __restrict__ bias,
+                                                           T* __restrict__ y,
+                                                           float* __restrict__ mean_out,
+                                                           float* __restrict__ rstd_out, int M) {
+  constexpr int NV = 4, D = NV * 128 * WPR, G = 8 / WPR;
+  __shared__ float red[2][2][8];  // [row parity][sum][warp]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, grp = warp / WPR, wi = warp % WPR;
+  const int c4base = wi * NV * 32;  // float4 index of this warp's slice
+  const float inv_d = 1.0f / (float)D;
+  int it = 0;
+  for (int m = blockIdx.x * G + grp; m < M; m += gridDim.x * G, ++it) {
+    const float4* xr = reinterpret_cast<const float4*>(x + (size_t)m * D) + c4base;
+    float4 v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = xr[lane + 32 * i];
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) s += ((v[i].x + v[i].y) + v[i].z) + v[i].w;
+    s = warp_sum(s);
+    float* rs = red[it & 1][0];
+    if (lane == 0) rs[warp] = s;
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(WPR * 32) : "memory");
+    float tot = 0.f;
+#pragma unroll
+    for (int w = 0; w < WPR; ++w) tot += rs[grp * WPR + w];
+    const float mean = tot * inv_d;
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const float a = v[i].x - mean, b = v[i].y - mean, cc = v[i].z - mean, e = v[i].w - mean;
+      q += ((a * a + b * b) + cc * cc) + e * e;
+    }
+    q = warp_sum(q);
+    float* rq = red[it & 1][1];
+    if (lane == 0) rq[warp] = q;
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(WPR * 32) : "memory");
+    float qt = 0.f;
+#pragma unroll
+    for (int w = 0; w < WPR; ++w) qt += rq[grp * WPR + w];
+    const float rstd = rsqrtf(qt * inv_d + 1e-5f);
+    T* yr = y + (size_t)m * D;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c4 = c4base + lane + 32 * i;
+      const float4 g = reinterpret_cast<const float4*>(gain)[c4];
+      const float4 b = reinterpret_cast<const float4*>(bias)[c4];
+      store4(yr + 4 * c4, g.x * ((v[i].x - mean) * rstd) + b.x, g.y * ((v[i].y - mean) * rstd) + b.y,
+             g.z * ((v[i].z - mean) * rstd) + b.z, g.w * ((v[i].w - mean) * rstd) + b.w);
+    }
+    if (wi == 0 && lane == 0) {
+      mean_out[m] = mean;
+      rstd_out[m] = rstd;
+    }
+  }
+}
+
 template <typename T>
 void ln_fwd(const float* x, const float* gain, const float* bias, T* y, float* mean, float* rstd,
             int M, int d, cudaStream_t st) {
@@ -172,8 +236,15 @@ void ln_fwd(const float* x, const float* gain, const float* bias, T* y, float* m
   case NV * 128:                                                                         \
     ln_fwd_vec_kernel<T, NV><<<grid, 256, 0, st>>>(x, gain, bias, y, mean, rstd, M);      \
     break;
-    PH_LNF(1) PH_LNF(2) PH_LNF(3) PH_LNF(4) PH_LNF(5) PH_LNF(6) PH_LNF(8)
+    PH_LNF(1) PH_LNF(2) PH_LNF(3) PH_LNF(4) PH_LNF(5) PH_LNF(6)
 #undef PH_LNF
+#define PH_LNFS(WPR)                                                                      \
+  case 512 * WPR:                                                                          \
+    ln_fwd_split_kernel<T, WPR><<<std::min<int>(cdiv(M, 8 / WPR), kNumSMs * 8), 256, 0, st>>>( \
+        x, gain, bias, y, mean, rstd, M);                                                  \
+    break;
+    PH_LNFS(2) PH_LNFS(4) PH_LNFS(8)
+#undef PH_LNFS
     default:
       ln_fwd_kernel<T><<<std::min<int>(cdiv(M, 8), kNumSMs * 16), 256, 0, st>>>(x, gain, bias, y,
                                                                                 mean, rstd, M, d);
@@ -374,6 +445,108 @@ ln_bwd_vec_kernel(const float* __restrict__ dy, const float* __restrict__ x,
   }
 }
 
+// Wide rows (d = 512 * WPR): WPR warps share a row as in ln_fwd_split_kernel;
+// x, dy and the residual gradient of the row slice are requested up front,
+// the two row sums cross warps through shared memory, and each lane keeps the
+// dgain / dbias / output-column-sum accumulators of its fixed 16 columns in
+// registers; row groups are reduced through shared memory in a fixed order.
+template <typename T, int WPR>
+__global__ void __launch_bounds__(256, 1)
+ln_bwd_split_kernel(const float* __restrict__ dy, const float* __restrict__ x,
+                    const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
+                    const float* __restrict__ gain, const float* dres, float* dx_out,
+                    T* __restrict__ dx_T, float* __restrict__ part, int M, int osum) {
+  constexpr int NV = 4, D = NV * 128 * WPR, G = 8 / WPR;
+  extern __shared__ float lnbs_sm[];          // [G][D] final reduction
+  __shared__ float red[2][2][8];              // [row parity][sum][warp]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, grp = warp / WPR, wi = warp % WPR;
+  const int c4base = wi * NV * 32;
+  const float inv_d = 1.0f / (float)D;
+  float4 ag[NV], ab[NV], ao[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) ag[i] = ab[i] = ao[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  int it = 0;
+  for (int m = blockIdx.x * G + grp; m < M; m += gridDim.x * G, ++it) {
+    const float4* xr = reinterpret_cast<const float4*>(x + (size_t)m * D) + c4base;
+    const float4* gr = reinterpret_cast<const float4*>(dy + (size_t)m * D) + c4base;
+    const float4* rr = dres ? reinterpret_cast<const float4*>(dres + (size_t)m * D) + c4base : nullptr;
+    float4 xv[NV], gv[NV], rv[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      xv[i] = xr[lane + 32 * i];
+      gv[i] = gr[lane + 32 * i];
+      rv[i] = rr ? rr[lane + 32 * i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const float mean = mean_in[m], rstd = rstd_in[m];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const float4 gg = reinterpret_cast<const float4*>(gain)[c4base + lane + 32 * i];
+#define PH_LNB_ACC(c)                                 \
+  {                                                   \
+    const float xh = (xv[i].c - mean) * rstd;         \
+    const float dxh = gv[i].c * gg.c;                 \
+    s1 += dxh;                                        \
+    s2 += dxh * xh;                                   \
+    ag[i].c += gv[i].c * xh;                          \
+    ab[i].c += gv[i].c;                               \
+  }
+      PH_LNB_ACC(x) PH_LNB_ACC(y) PH_LNB_ACC(z) PH_LNB_ACC(w)
+#undef PH_LNB_ACC
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    float* r1 = red[it & 1][0];
+    float* r2 = red[it & 1][1];
+    if (lane == 0) {
+      r1[warp] = s1;
+      r2[warp] = s2;
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(WPR * 32) : "memory");
+    float t1 = 0.f, t2 = 0.f;
+#pragma unroll
+    for (int w = 0; w < WPR; ++w) {
+      t1 += r1[grp * WPR + w];
+      t2 += r2[grp * WPR + w];
+    }
+    t1 *= inv_d;
+    t2 *= inv_d;
+    float* out = dx_out + (size_t)m * D;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c4 = c4base + lane + 32 * i;
+      const float4 gg = reinterpret_cast<const float4*>(gain)[c4];
+      float4 r = rv[i];
+      r.x += rstd * (gv[i].x * gg.x - t1 - ((xv[i].x - mean) * rstd) * t2);
+      r.y += rstd * (gv[i].y * gg.y - t1 - ((xv[i].y - mean) * rstd) * t2);
+      r.z += rstd * (gv[i].z * gg.z - t1 - ((xv[i].z - mean) * rstd) * t2);
+      r.w += rstd * (gv[i].w * gg.w - t1 - ((xv[i].w - mean) * rstd) * t2);
+      reinterpret_cast<float4*>(out)[c4] = r;
+      if (dx_T) store4(dx_T + (size_t)m * D + 4 * c4, r.x, r.y, r.z, r.w);
+      ao[i].x += r.x;
+      ao[i].y += r.y;
+      ao[i].z += r.z;
+      ao[i].w += r.w;
+    }
+  }
+  // block partials [dgain | dbias | dsum]: the G row groups summed in order
+  const int nsum = osum ? 3 : 2;
+  for (int a = 0; a < nsum; ++a) {
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      reinterpret_cast<float4*>(lnbs_sm + (size_t)grp * D)[c4base + lane + 32 * i] =
+          a == 0 ? ag[i] : a == 1 ? ab[i] : ao[i];
+    __syncthreads();
+    for (int j = threadIdx.x; j < D; j += blockDim.x) {
+      float acc = 0.f;
+#pragma unroll
+      for (int g = 0; g < G; ++g) acc += lnbs_sm[(size_t)g * D + j];
+      part[(size_t)blockIdx.x * 3 * D + a * D + j] = acc;
+    }
+  }
+}
+
 template <typename T>
 void ln_bwd(const float* dy, const float* x, const float* mean, const float* rstd,
             const float* gain, const float* dres, float* dx_out, T* dx_T, float* part,
@@ -397,6 +570,15 @@ void ln_bwd(const float* dy, const float* x, const float* mean, const float* rst
   }
     PH_LNB(1) PH_LNB(2) PH_LNB(3) PH_LNB(4) PH_LNB(5) PH_LNB(6)
 #undef PH_LNB
+#define PH_LNBS(WPR)                                                                       \
+  case 512 * WPR: {                                                                        \
+    constexpr int smem = (8 / WPR) * 512 * WPR * 4;                                        \
+    ln_bwd_split_kernel<T, WPR><<<kLnBwdBlocks, 256, smem, st>>>(                          \
+        dy, x, mean, rstd, gain, dres, dx_out, dx_T, part, M, dsum ? 1 : 0);               \
+    break;                                                                                 \
+  }
+    PH_LNBS(2) PH_LNBS(4) PH_LNBS(8)
+#undef PH_LNBS
     default: {
       // as many warps (<= 8) as [warps][nsum][d] fp32 partials fit in shared memory
       const int warps = (int)std::max<size_t>(

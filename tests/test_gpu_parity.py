@@ -20,6 +20,8 @@ DEFAULT = (2, 64, 2, 4, 64, 32)   # ModelConfig{} model.h:12-18
 DILOCO = (2, 32, 2, 4, 64, 32)    # configs/diloco.cfg, acceptance c7
 WIDE128 = (1, 128, 2, 4, 96, 32)  # d = 128 * NV: register-resident LayerNorm kernels
 WIDE256 = (1, 256, 4, 4, 96, 160)  # dh = 64: tcgen05 attention, ragged S
+WIDE1024 = (1, 1024, 16, 4, 96, 32)  # d = 512 * 2: row-split LayerNorm kernels
+WIDE2048 = (1, 2048, 16, 4, 96, 16)  # d = 512 * 4, dh = 128 (the 1.3B widths)
 
 
 def _mc(F, t):
@@ -39,7 +41,7 @@ def _rel_l2(a, b):
 
 
 @pytest.mark.parametrize("cfg_t,B", [(TINY, 2), (HETERO4, 4), (DEFAULT, 4), (WIDE128, 2),
-                                     (WIDE256, 2)])
+                                     (WIDE256, 2), (WIDE1024, 2), (WIDE2048, 2)])
 def test_forward_backward_f32(F, oracle, cfg_t, B):
     mc = ModelCfg(*cfg_t)
     params = oracle.init_params(mc, 3)
@@ -57,7 +59,8 @@ def test_forward_backward_f32(F, oracle, cfg_t, B):
             assert _rel_l2(g[off:off + n], gr) <= 5e-4, name
 
 
-@pytest.mark.parametrize("cfg_t,B", [(HETERO4, 4), (DEFAULT, 4), (WIDE128, 2), (WIDE256, 2)])
+@pytest.mark.parametrize("cfg_t,B", [(HETERO4, 4), (DEFAULT, 4), (WIDE128, 2), (WIDE256, 2),
+                                     (WIDE1024, 2), (WIDE2048, 2)])
 def test_forward_backward_bf16(F, oracle, cfg_t, B):
     mc = ModelCfg(*cfg_t)
     params = oracle.init_params(mc, 3)
