@@ -505,12 +505,8 @@ template <int DH>
 void launch_fwd(const bf16* q, const bf16* k, const bf16* v, bf16* o, float* lse, int B, int S,
                 int H, int d, cudaStream_t st) {
   const size_t smem = fwd_smem<DH>();
-  static bool cfg = false;
-  if (!cfg) {
-    PH_CUDA(cudaFuncSetAttribute(attn_fwd_mma_kernel<DH>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    cfg = true;
-  }
+  static std::atomic<uint64_t> cfg{0};
+  set_max_smem_once(cfg, attn_fwd_mma_kernel<DH>, (int)smem);
   dim3 grid((S + BT - 1) / BT, B * H);
   attn_fwd_mma_kernel<DH><<<grid, kWarps * 32, smem, st>>>(q, k, v, o, lse, S, H, d,
                                                            rsqrtf((float)DH));
@@ -524,16 +520,9 @@ void launch_bwd(const bf16* q, const bf16* k, const bf16* v, const bf16* o, cons
   const int rows = B * H * S;
   attn_dot_kernel<<<(rows + 7) / 8, 256, 0, st>>>(o, dO, Dv, B, S, H, d);
   PH_LAUNCH_CHECK();
-  static bool cfg = false;
-  if (!cfg) {
-    PH_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv_mma_kernel<DH>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)bwd_smem_dkdv<DH>()));
-    PH_CUDA(cudaFuncSetAttribute(attn_bwd_dq_mma_kernel<DH>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)bwd_smem_dq<DH>()));
-    cfg = true;
-  }
+  static std::atomic<uint64_t> cfg1{0}, cfg2{0};
+  set_max_smem_once(cfg1, attn_bwd_dkdv_mma_kernel<DH>, (int)bwd_smem_dkdv<DH>());
+  set_max_smem_once(cfg2, attn_bwd_dq_mma_kernel<DH>, (int)bwd_smem_dq<DH>());
   dim3 grid((S + BT - 1) / BT, B * H);
   const float scale = rsqrtf((float)DH);
   attn_bwd_dkdv_mma_kernel<DH><<<grid, kWarps * 32, bwd_smem_dkdv<DH>(), st>>>(

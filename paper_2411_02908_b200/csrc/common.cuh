@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 
 #include "host.hpp"
@@ -23,6 +24,18 @@ namespace photon {
 #define PH_LAUNCH_CHECK() PH_CUDA(cudaGetLastError())
 
 using bf16 = __nv_bfloat16;
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) applies per device: set it
+// once for every device that launches the kernel (bit per device in `done`).
+template <typename K>
+inline void set_max_smem_once(std::atomic<uint64_t>& done, K kern, int bytes) {
+  int dev = 0;
+  PH_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load() & bit) return;
+  PH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.fetch_or(bit);
+}
 
 constexpr int kNumSMs = 148;
 
