@@ -1073,56 +1073,71 @@ __global__ void __launch_bounds__(kCePipeThreads + 32, 1)
     uint8_t* buf = ce_sm + b * stride;
     const uint32_t base = su32(buf);
     mbar_wait(&full[b], (i >> 1) & 1);
-    // A NaN logit makes s NaN; a +inf logit makes m = +inf and s NaN (inf - inf),
-    // so the reference's NaN loss (tensor.cpp:569-582) is detected from (m, s).
-    float m = -INFINITY, s = 0.f;
+    // Three passes over the row in shared memory with ONE exponential per logit
+    // (MUFU was the limit with two): (1) row max; (2) e = exp(l - m), row sum,
+    // e written back in place as bf16 when the gradient is wanted (l[t] is read
+    // first); (3) dl = e * g / s - g * onehot(t), the target column recomputed
+    // from l[t] in fp32 (p - 1 cancels; the bf16 copy of e would not do).  A NaN
+    // logit makes s NaN and a +inf logit m = +inf and s NaN, so the reference's
+    // NaN loss (tensor.cpp:569-582) is detected from (m, s).
+    float m = -INFINITY;
     for (int c = tid; c < nvec; c += kCePipeThreads) {
       float v[8];
       ce_unpack8(lds128(base + c * 16), v);
-      const float cm = fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])),
-                             fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7])));
-      if (cm > m) {
-        s *= ex2_approx((m - cm) * kL2e);
-        m = cm;
-      }
-      const float ml2 = m * kL2e;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) s += ex2_approx(fmaf(v[e], kL2e, -ml2));
+      m = fmaxf(m, fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])),
+                         fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7]))));
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
-      ce_combine(m, s, m2, s2);
-    }
-    if (lane == 0) {
-      red_m[warp] = m;
-      red_s[warp] = s;
-    }
+    m = warp_max(m);
+    if (lane == 0) red_m[warp] = m;
     named_bar_sync(1, kCePipeThreads);
     m = red_m[0];
+#pragma unroll
+    for (int w = 1; w < kCePipeWarps; ++w) m = fmaxf(m, red_m[w]);
+    const int t = targets[r];
+    const float lt = t >= 0 ? __bfloat162float(reinterpret_cast<const bf16*>(buf)[t]) : 0.f;
+    named_bar_sync(1, kCePipeThreads);  // red_* and l[t] read before reuse / overwrite
+    const float ml2 = m * kL2e;
+    float s = 0.f;
+    for (int c = tid; c < nvec; c += kCePipeThreads) {
+      float v[8];
+      ce_unpack8(lds128(base + c * 16), v);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        v[e] = ex2_approx(fmaf(v[e], kL2e, -ml2));
+        s += v[e];
+      }
+      if (write_grad) {
+        uint4 o;
+        o.x = pack_bf16x2(v[0], v[1]);
+        o.y = pack_bf16x2(v[2], v[3]);
+        o.z = pack_bf16x2(v[4], v[5]);
+        o.w = pack_bf16x2(v[6], v[7]);
+        sts128(base + c * 16, o);
+      }
+    }
+    s = warp_sum(s);
+    if (lane == 0) red_s[warp] = s;
+    named_bar_sync(1, kCePipeThreads);
     s = red_s[0];
 #pragma unroll
-    for (int w = 1; w < kCePipeWarps; ++w) ce_combine(m, s, red_m[w], red_s[w]);
+    for (int w = 1; w < kCePipeWarps; ++w) s += red_s[w];
     const bool bad = !(s == s) || m == INFINITY;
-    const int t = targets[r];
-    if (tid == 0) {
-      const float lt = t >= 0 ? __bfloat162float(reinterpret_cast<const bf16*>(buf)[t]) : 0.f;
+    if (tid == 0)
       rowloss[r] = t < 0 ? 0.0 : bad ? (double)NAN : (double)logf(s) + (double)m - (double)lt;
-    }
-    named_bar_sync(1, kCePipeThreads);  // l[t] and red_* read before reuse
     if (write_grad) {
       const float g = t >= 0 ? inv_count : 0.f;
-      const float gs = g / s, ml2 = m * kL2e;
+      const float gs = g / s;
       for (int c = tid; c < nvec; c += kCePipeThreads) {
         float v[8];
         ce_unpack8(lds128(base + c * 16), v);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) v[e] = gs * ex2_approx(fmaf(v[e], kL2e, -ml2));
+        for (int e = 0; e < 8; ++e) v[e] *= gs;
         const int te = t - c * 8;  // target column within this chunk (if any)
         if ((unsigned)te < 8u) {
+          const float pt = gs * ex2_approx(fmaf(lt, kL2e, -ml2)) - g;
 #pragma unroll
           for (int e = 0; e < 8; ++e)
-            if (e == te) v[e] -= g;
+            if (e == te) v[e] = pt;
         }
         uint4 o;
         o.x = pack_bf16x2(v[0], v[1]);
@@ -1133,6 +1148,7 @@ __global__ void __launch_bounds__(kCePipeThreads + 32, 1)
       }
       fence_async_smem();
     }
+    named_bar_sync(1, kCePipeThreads);  // red_s read by every thread before the next row
     __syncwarp();
     if (lane == 0) mbar_arrive(&done[b]);
   }
