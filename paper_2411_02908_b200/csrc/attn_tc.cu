@@ -471,38 +471,47 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
-// thread per (row, head): D = dO . O over the head's HD columns (16-byte
-// loads of each); consecutive threads take consecutive heads of a row, so a
-// warp streams contiguous rows
+// D = dO . O per (row, head), warp per row: lane l streams the 16-byte vectors
+// l, l + 32, ... of the row (contiguous 512 B per instruction), the HD / 8
+// lanes of a head sum their partial dot products with butterfly shuffles, and
+// the head's first lane writes D and lse (log2 units) into the padded arrays.
 template <int HD>
 __global__ void attn_bwd_prep_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dO,
                                      const float* __restrict__ lse, float* __restrict__ Lp,
                                      float* __restrict__ Dp, int B, int S, int H, int d, int Spad) {
-  const int64_t n = (int64_t)B * S * H;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += stride) {
-    const int h = (int)(t % H);
-    const int64_t row = t / H;  // b * S + i
+  constexpr int VPH = HD / 8;  // 16-byte vectors per head
+  const int nvec = d / 8, lane = threadIdx.x & 31;
+  const int warps = blockDim.x / 32;
+  const int64_t rows = (int64_t)B * S;
+  for (int64_t row = (int64_t)blockIdx.x * warps + threadIdx.x / 32; row < rows;
+       row += (int64_t)gridDim.x * warps) {
+    const uint4* po = reinterpret_cast<const uint4*>(o + row * d);
+    const uint4* pd = reinterpret_cast<const uint4*>(dO + row * d);
     const int b = (int)(row / S), i = (int)(row % S);
-    const uint4* po = reinterpret_cast<const uint4*>(o + row * d + h * HD);
-    const uint4* pd = reinterpret_cast<const uint4*>(dO + row * d + h * HD);
-    float acc = 0.f;
+    for (int v0 = 0; v0 < nvec; v0 += 32) {
+      const int v = v0 + lane;
+      float acc = 0.f;
+      if (v < nvec) {
+        const uint4 x = po[v], y = pd[v];
+        const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
-    for (int c = 0; c < HD / 8; ++c) {
-      const uint4 x = po[c], y = pd[c];
-      const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+        for (int e = 0; e < 4; ++e) {
+          acc = fmaf(__uint_as_float(xs[e] << 16), __uint_as_float(ys[e] << 16), acc);
+          acc = fmaf(__uint_as_float(xs[e] & 0xffff0000u), __uint_as_float(ys[e] & 0xffff0000u), acc);
+        }
+      }
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        acc = fmaf(__uint_as_float(xs[e] << 16), __uint_as_float(ys[e] << 16), acc);
-        acc = fmaf(__uint_as_float(xs[e] & 0xffff0000u), __uint_as_float(ys[e] & 0xffff0000u), acc);
+      for (int off = 1; off < VPH; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if (v < nvec && v % VPH == 0) {
+        const int64_t bh = (int64_t)b * H + v / VPH;
+        Dp[bh * Spad + i] = acc;
+        Lp[bh * Spad + i] = lse[bh * S + i] * kLog2e;
       }
     }
-    const int64_t bh = (int64_t)b * H + h;
-    Dp[bh * Spad + i] = acc;
-    Lp[bh * Spad + i] = lse[bh * S + i] * kLog2e;
   }
   // padded query slots: P = 0 (lse = +inf) and D = 0
   const int64_t npad = (int64_t)B * H * (Spad - S);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < npad; t += stride) {
     const int64_t bh = t / (Spad - S), i = S + t % (Spad - S);
     Lp[bh * Spad + i] = INFINITY;
@@ -1092,8 +1101,8 @@ void attn_bwd_hd(const bf16* q, const bf16* k, const bf16* v, const bf16* o, con
   if (!ws) ws = scratch(attn_bwd_tc_ws_floats(B, S, H));
   float* Lp = ws;
   float* Dp = Lp + (size_t)B * H * Spad;
-  attn_bwd_prep_kernel<HD><<<std::min<int64_t>(((int64_t)B * S * H + 255) / 256, kNumSMs * 16), 256,
-                             0, st>>>(o, dO, lse, Lp, Dp, B, S, H, d, Spad);
+  attn_bwd_prep_kernel<HD><<<std::min<int64_t>(((int64_t)B * S + 7) / 8, kNumSMs * 16), 256, 0,
+                             st>>>(o, dO, lse, Lp, Dp, B, S, H, d, Spad);
   PH_LAUNCH_CHECK();
   constexpr int TQB = HD == 64 ? 128 : 64;  // dK/dV kernel's query tile
   const CUtensorMap mq = head_map(q, rows, d), mk = head_map(k, rows, d), mv = head_map(v, rows, d),

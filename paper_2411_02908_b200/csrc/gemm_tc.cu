@@ -665,6 +665,41 @@ __global__ void splitk_reduce_kernel(const ReduceArgs r) {
   }
 }
 
+// The weight-gradient case (Store into fp32, N % 4 == 0): 16-byte accesses, the
+// split partials of a float4 loaded together and added in split order (the
+// same order as splitk_reduce_kernel, so the result is unchanged).
+__global__ void splitk_reduce_store4_kernel(const float* __restrict__ ws, int M, int N, int splits,
+                                            float* __restrict__ C, int64_t ldc) {
+  const int n4 = N / 4;
+  const int64_t total4 = (int64_t)M * n4, total = (int64_t)M * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 acc = reinterpret_cast<const float4*>(ws)[i];
+    int s = 1;
+    for (; s + 3 < splits; s += 4) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = reinterpret_cast<const float4*>(ws + (s + u) * total)[i];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc.x += v[u].x;
+        acc.y += v[u].y;
+        acc.z += v[u].z;
+        acc.w += v[u].w;
+      }
+    }
+    for (; s < splits; ++s) {
+      const float4 v = reinterpret_cast<const float4*>(ws + s * total)[i];
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    const int64_t row = i / n4, c4 = i - row * n4;
+    *reinterpret_cast<float4*>(C + row * ldc + 4 * c4) = acc;
+  }
+}
+
 // ---- host side ----------------------------------------------------------------------
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -877,8 +912,13 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
     else launch<256, true, true, 2>(om, em, p, grid, st);
   }
   if (p.splits > 1) {
-    ReduceArgs r{g.M, g.N, p.splits, p.epi, p.c_bf16, g.ldc, ws, g.C, g.bias, g.resid, g.aux};
-    splitk_reduce_kernel<<<kNumSMs * 4, 256, 0, st>>>(r);
+    if (g.epi == Epi::Store && !p.c_bf16 && g.N % 4 == 0 && g.ldc % 4 == 0 && aligned16(g.C)) {
+      splitk_reduce_store4_kernel<<<kNumSMs * 4, 256, 0, st>>>(ws, g.M, g.N, p.splits,
+                                                               static_cast<float*>(g.C), g.ldc);
+    } else {
+      ReduceArgs r{g.M, g.N, p.splits, p.epi, p.c_bf16, g.ldc, ws, g.C, g.bias, g.resid, g.aux};
+      splitk_reduce_kernel<<<kNumSMs * 4, 256, 0, st>>>(r);
+    }
     PH_LAUNCH_CHECK();
   }
   return true;
