@@ -95,7 +95,7 @@ void run(const char* name) {
 }
 
 // 2-CTA pair: leader issues M=256 x N MMAs (cta_group::2), both CTAs hold operands.
-template <int N>
+template <int N, int TS = 0>  // TS: A from TMEM (the attention backward's dV / dK form)
 __global__ void __cluster_dims__(2, 1, 1) mma_pair_kernel(int n_mma, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -126,10 +126,17 @@ __global__ void __cluster_dims__(2, 1, 1) mma_pair_kernel(int n_mma, unsigned lo
     for (int i = 0; i < n_mma; ++i) {
       const int kk = i & 3;
       const uint64_t ad = sw128(a + kk * 32, 16, 1024), bd = sw128(b + kk * 32, 16, 1024);
-      asm volatile(
-          "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-          "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-          "l"(ad), "l"(bd), "r"(idesc), "r"(1));
+      if (TS) {
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + 256),
+            "r"(tmem + 384 + kk * 8), "l"(bd), "r"(idesc), "r"(1));
+      } else {
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+            "l"(ad), "l"(bd), "r"(idesc), "r"(1));
+      }
     }
     const unsigned long long t1 = clock64();
     asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
@@ -148,20 +155,20 @@ __global__ void __cluster_dims__(2, 1, 1) mma_pair_kernel(int n_mma, unsigned lo
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-template <int N>
+template <int N, int TS = 0>
 void run_pair() {
   unsigned long long* d;
   unsigned long long h[2];
   cudaMalloc(&d, 16);
   const int smem = 65536 + 1024;
-  cudaFuncSetAttribute(mma_pair_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(mma_pair_kernel<N, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   for (int n : {8, 64, 512}) {
-    mma_pair_kernel<N><<<148, 128, smem>>>(n, d);
+    mma_pair_kernel<N, TS><<<148, 128, smem>>>(n, d);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("pair: %s\n", cudaGetErrorString(e)); return; }
     cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
-    printf("PAIR M=256       N=%3d  %4d MMAs: issue %7llu cyc, done %7llu cyc -> %6.1f cyc/MMA (1-CTA M128 equiv %d)\n",
-           N, n, h[0], h[1], (double)h[1] / n, 128 * N / 256);
+    printf("PAIR M=256 %s   N=%3d  %4d MMAs: issue %7llu cyc, done %7llu cyc -> %6.1f cyc/MMA (1-CTA M128 equiv %d)\n",
+           TS ? "TS" : "SS", N, n, h[0], h[1], (double)h[1] / n, 128 * N / 256);
   }
   cudaFree(d);
 }
@@ -169,6 +176,9 @@ void run_pair() {
 int main() {
   run_pair<256>();
   run_pair<128>();
+  run_pair<64>();
+  run_pair<128, 1>();
+  run_pair<64, 1>();
   run<64, 0>("SS Kmaj");
   run<64, 1>("SS MNmaj");
   run<64, 2>("TS MNmaj");
