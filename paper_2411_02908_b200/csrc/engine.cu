@@ -324,7 +324,12 @@ void EngineT<T>::forward_backward(const StepBatch& bt, double* loss_dev, bool ba
   }
 
   // ---------------- backward (reverse topological order) ----------------
-  PH_CUDA(cudaMemsetAsync(grads, 0, P * sizeof(float), stream));
+  // every gradient entry is written (stored, never accumulated) by exactly one
+  // kernel below -- except the position embeddings of positions this batch
+  // does not reach (S < seq_len), which are zero
+  if ((uint64_t)S < Smax_)
+    PH_CUDA(cudaMemsetAsync(G(off_.pos) + (size_t)S * d, 0, (Smax_ - S) * d * sizeof(float),
+                            stream));
   // logits = add_bias(xf W_head, b_head)
   {
     Scope sc(this, 2, 0);
