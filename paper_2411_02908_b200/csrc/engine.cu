@@ -85,7 +85,7 @@ class EngineT final : public Engine {
   float *x_, *xmid_, *mean1_, *rstd1_, *mean2_, *rstd2_, *meanf_, *rstdf_, *lse_;
   T *h_, *q_, *k_, *v_, *o_, *h2_, *pre_, *u_, *xf_, *logits_;
   // backward scratch
-  float *dx_, *dy_, *Dvec_, *part_, *attn_ws_;
+  float *dx_, *dy_, *Dvec_, *part_, *attn_ws_, *gemm_ws_;
   T *dxT_, *dpre_, *dq_, *dk_, *dv_, *dO_;
   double* rowloss_;
   // timing
@@ -150,6 +150,7 @@ class EngineT final : public Engine {
       dx_ = carve<float>(p, M * d);
       dy_ = carve<float>(p, M * d);
       Dvec_ = carve<float>(p, rows_bhs);
+      gemm_ws_ = sizeof(T) == 2 ? carve<float>(p, kGemmWsFloats) : nullptr;
       attn_ws_ = sizeof(T) == 2 && k::attn_tc_supported((int)(d_ / H_), (int)d_)
                      ? carve<float>(p, k::attn_bwd_tc_ws_floats((int)max_batch, (int)Smax_, (int)H_))
                      : nullptr;
@@ -253,6 +254,7 @@ class EngineT final : public Engine {
     g.ab = dt_of<T>();
     g.C = C; g.ldc = ldc; g.c = cdt;
     g.epi = epi; g.bias = bias; g.resid = resid; g.aux = aux;
+    g.ws = gemm_ws_; g.ws_floats = gemm_ws_ ? kGemmWsFloats : 0;
     Scope sc(this, 0, 2.0 * M * N * (double)K);
     if (sizeof(T) == 2 && gemm_mode == 1) {
       if (!gemm_tc(g, stream))
@@ -392,6 +394,7 @@ void EngineT<T>::forward_backward(const StepBatch& bt, double* loss_dev, bool ba
       g.nseg = 3;
       g.A_seg[1] = dk_; g.B_seg[1] = W(o.wk);
       g.A_seg[2] = dq_; g.B_seg[2] = W(o.wq);
+      g.ws = gemm_ws_; g.ws_floats = kGemmWsFloats;
       Scope sc(this, 0, 2.0 * M * d * 3.0 * d);
       if (!gemm_tc(g, stream)) throw Error(PHOTON_ERR_CONFIG, "tcgen05 GEMM: K-concatenated dX");
     } else {

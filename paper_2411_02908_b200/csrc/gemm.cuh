@@ -46,7 +46,14 @@ struct GemmArgs {
   int nseg = 1;
   const void* A_seg[3] = {nullptr, nullptr, nullptr};
   const void* B_seg[3] = {nullptr, nullptr, nullptr};
+  // split-K partials: caller-owned (engines pass their own, so engines sharing a
+  // device never share partials); nullptr = a per-device scratch (debug / tests)
+  float* ws = nullptr;
+  size_t ws_floats = 0;
 };
+// split-K partial floats any tcgen05 GEMM can need: splits * M * N <= the
+// concurrent tile slots times one (pair) tile
+constexpr size_t kGemmWsFloats = (size_t)148 * 128 * 256;
 
 void gemm_simt(const GemmArgs& g, cudaStream_t st);
 // tcgen05 + TMA path (bf16 operands); returns false when the shape/layout is

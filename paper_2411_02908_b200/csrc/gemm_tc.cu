@@ -870,7 +870,8 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
   EpiMaps em{};
   float* ws = nullptr;
   if (p.splits > 1) {
-    ws = workspace((size_t)p.splits * g.M * g.N);
+    const size_t need = (size_t)p.splits * g.M * g.N;
+    ws = g.ws && g.ws_floats >= need ? g.ws : workspace(need);
     cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.M, (cuuint64_t)p.splits};
     cuuint64_t strides[2] = {(cuuint64_t)g.N * 4, (cuuint64_t)g.N * g.M * 4};
     cuuint32_t box[3] = {32, 32, 1};
