@@ -68,6 +68,7 @@ class EngineT final : public Engine {
   }
   ~EngineT() override {
     if (pool_) cudaFree(pool_);
+    if (master_alloc_) cudaFree(master_alloc_);
     for (auto& e : ev_pool_) cudaEventDestroy(e);
   }
 
@@ -81,6 +82,9 @@ class EngineT final : public Engine {
   ModelOffsets off_;
   uint64_t d_, H_, hid_, V_, L_, Smax_, Mmax_;
   char* pool_ = nullptr;
+  // master is its own allocation: the multi-GPU boundary exports it through
+  // CUDA IPC, and peers then map P * 4 bytes rather than the whole pool
+  float* master_alloc_ = nullptr;
   // activations
   float *x_, *xmid_, *mean1_, *rstd1_, *mean2_, *rstd2_, *meanf_, *rstdf_, *lse_;
   T *h_, *q_, *k_, *v_, *o_, *h2_, *pre_, *u_, *xf_, *logits_;
@@ -117,9 +121,7 @@ class EngineT final : public Engine {
                                                     k::colsum_part_floats((int)M, (int)d)}));
     auto plan = [&](char* p) {
       char* s = p;
-      // + 64: a runner with one local client aggregates straight out of master,
-      // reading whole NCCL shards (up to Ppad = P rounded to 4 * world <= P + 31)
-      master = carve<float>(p, P + 64);
+      // master: separate allocation (see master_alloc_)
       grads = carve<float>(p, P);
       mom = carve<float>(p, P);
       vel2 = carve<float>(p, P);
@@ -165,6 +167,11 @@ class EngineT final : public Engine {
       return (size_t)(p - s);
     };
     const size_t bytes = plan(reinterpret_cast<char*>(256));  // dry run for the size
+    // + 64: a runner with one local client aggregates straight out of master,
+    // reading whole boundary shards (up to Ppad = P rounded to 4 * world <= P + 31)
+    PH_CUDA(cudaMalloc(&master_alloc_, (P + 64) * sizeof(float)));
+    master = master_alloc_;
+    PH_CUDA(cudaMemsetAsync(master, 0, (P + 64) * sizeof(float), stream));
     PH_CUDA(cudaMalloc(&pool_, bytes + 256));
     plan(pool_);
     PH_CUDA(cudaMemsetAsync(pool_, 0, bytes, stream));
