@@ -396,6 +396,10 @@ def run_ours(args):
                             "traffic_unit": "DRAM bytes per launch (ncu, mean over one step's GEMMs)",
                             "peak_source": f"{peak_src} bf16 sustained"}
         line["kernel_ms_per_round"] = prof
+        if prof["attn_ms"]:
+            att = prof["attn_flops"] / (prof["attn_ms"] * 1e-3) / 1e12
+            line["attention"] = {"kernel": "attn_*_tc (tcgen05; backward counted as 2.5x forward FLOPs)",
+                                 "achieved_tflops": att, "frac_of_bf16_sustained": att / bf16_sus}
         line["gpu_launches"] = int(prof["launches"]) * args.steps
     if agg:
         line["aggregation"] = agg
