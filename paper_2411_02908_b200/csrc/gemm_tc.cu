@@ -465,6 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool out_bf16 = !splitk && p.c_bf16;
     int acc = 0;
     uint32_t acc_phase = 0;
+    int stage_i = 0;  // epilogues without an input alternate two staging buffers (across tiles)
     const uint32_t leader_tempty0 = NCTA == 2 ? mapa_rank(&tempty[0], 0) : 0;
     for (int u = cid; u < p.units; u += ncl) {
       const int tile = u / p.splits, split = u % p.splits;
@@ -502,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (has_bias && rows_live && sub < nchunks) load_bias(n0 + sub * 32);
       if (rows_live) {
 #pragma unroll 1
-        for (int c = sub; c < nchunks; c += 2) {
+        for (int c = sub; c < nchunks; c += 2, ++stage_i) {
           const int col0 = n0 + c * 32;
           float v[32];
           tmem_ld32(taddr + c * 32, v);  // v[j] = acc[row0 + lane][col0 + j]
@@ -559,9 +560,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           // stage the chunk once the previous store from this buffer has read it
-          if (lane == 0) bulk_wait_read<0>();
+          // (with two buffers the store of the previous chunk may still be reading)
+          uint8_t* sbuf = (!need_in && (stage_i & 1)) ? ibuf : obuf;
+          if (lane == 0) {
+            if (need_in) bulk_wait_read<0>();
+            else bulk_wait_read<1>();
+          }
           __syncwarp();
-          const uint32_t oa = su32(obuf);
+          const uint32_t oa = su32(sbuf);
           if (epi == Epi::GeluBias && !splitk) {
             // one Phi / phi evaluation per element: gelu'(u) = Phi + u phi -> aux box
             // (second 2 KB, the backward's factor), v <- gelu(u) = u Phi
@@ -591,10 +597,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) {
             if (splitk) {
-              tma_store_3d(&em.C, obuf, col0, row0, split);
+              tma_store_3d(&em.C, sbuf, col0, row0, split);
             } else {
-              tma_store_2d(&em.C, obuf, col0, row0);
-              if (epi == Epi::GeluBias) tma_store_2d(&em.aux, obuf + 2048, col0, row0);
+              tma_store_2d(&em.C, sbuf, col0, row0);
+              if (epi == Epi::GeluBias) tma_store_2d(&em.aux, sbuf + 2048, col0, row0);
             }
             bulk_commit();
           }
