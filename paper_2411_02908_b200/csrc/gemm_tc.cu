@@ -561,10 +561,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           // stage the chunk once the previous store from this buffer has read it
           // (with two buffers the store of the previous chunk may still be reading)
-          uint8_t* sbuf = (!need_in && (stage_i & 1)) ? ibuf : obuf;
+          // GeluBwd (bf16 in, bf16 out: 2 KB chunks) alternates the two halves of obuf
+          const bool two_bufs = !need_in || (in_bf16 && out_bf16);
+          uint8_t* sbuf = (two_bufs && (stage_i & 1)) ? (need_in ? obuf + 2048 : ibuf) : obuf;
           if (lane == 0) {
-            if (need_in) bulk_wait_read<0>();
-            else bulk_wait_read<1>();
+            if (two_bufs) bulk_wait_read<1>();
+            else bulk_wait_read<0>();
           }
           __syncwarp();
           const uint32_t oa = su32(sbuf);
