@@ -115,6 +115,32 @@ __device__ __forceinline__ void gelu_pair(float x, float& g, float& gp) {
   g = x * Phi;
   gp = fmaf(x * 0.39894228040143267794f, e, Phi);
 }
+// gelu_pair on two elements with sm_100's packed fp32 FMA / MUL / ADD (one
+// issue slot per pair): the GeluBias epilogue is issue-bound, not MUFU-bound.
+// Same A&S 7.1.26 evaluation; Phi = 1/2 + sign(x) (1/2 - w) and the 1/sqrt(2)
+// folded into the first coefficient (ulp-level differences from gelu_pair).
+__device__ __forceinline__ void gelu_pair2(float2 x, float2& g, float2& gp) {
+  constexpr float c0 = 0.3275911f * 0.70710678118654752440f;
+  float2 t, e;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.x) : "f"(fmaf(c0, fabsf(x.x), 1.0f)));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.y) : "f"(fmaf(c0, fabsf(x.y), 1.0f)));
+  const float2 q = __fmul2_rn(x, __fmul2_rn(x, make_float2(-0.72134752044448170f, -0.72134752044448170f)));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(q.x));  // exp(-x^2/2)
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(q.y));
+  float2 p = __ffma2_rn(make_float2(0.5307027145f, 0.5307027145f), t,
+                        make_float2(-0.7265760135f, -0.7265760135f));
+  p = __ffma2_rn(p, t, make_float2(0.7107068705f, 0.7107068705f));
+  p = __ffma2_rn(p, t, make_float2(-0.142248368f, -0.142248368f));
+  p = __ffma2_rn(p, t, make_float2(0.127414796f, 0.127414796f));
+  const float2 w = __fmul2_rn(__fmul2_rn(p, t), e);  // Phi(-|x|), in (0, 1/2]
+  float2 h = __ffma2_rn(w, make_float2(-1.0f, -1.0f), make_float2(0.5f, 0.5f));
+  h.x = copysignf(h.x, x.x);
+  h.y = copysignf(h.y, x.y);
+  const float2 Phi = __fadd2_rn(h, make_float2(0.5f, 0.5f));
+  g = __fmul2_rn(x, Phi);
+  gp = __ffma2_rn(__fmul2_rn(x, make_float2(0.39894228040143267794f, 0.39894228040143267794f)), e,
+                  Phi);
+}
 __device__ __forceinline__ float gelu_fast(float x) {
   float Phi, phi;
   phi_Phi(x, Phi, phi);

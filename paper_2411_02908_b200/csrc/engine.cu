@@ -118,7 +118,10 @@ class EngineT final : public Engine {
     size_t part_floats = std::max<size_t>((size_t)k::ln_bwd_parts() * 3 * d,
                                           std::max({k::colsum_part_floats((int)M, (int)V_),
                                                     k::colsum_part_floats((int)M, (int)hid),
-                                                    k::colsum_part_floats((int)M, (int)d)}));
+                                                    k::colsum_part_floats((int)M, (int)d),
+                                                    // b1 partials of the GeluBwd epilogue
+                                                    (size_t)(M / 32) * hid +
+                                                        k::colsum_parts_scratch_floats((int)hid)}));
     auto plan = [&](char* p) {
       char* s = p;
       // master: separate allocation (see master_alloc_)
@@ -253,7 +256,7 @@ class EngineT final : public Engine {
 
   void mm(int M, int N, int K, const void* A, int64_t lda, bool ak, const void* B, int64_t ldb,
           bool bk, void* C, int64_t ldc, DT cdt, Epi epi, const float* bias = nullptr,
-          const float* resid = nullptr, void* aux = nullptr) {
+          const float* resid = nullptr, void* aux = nullptr, float* colsum_part = nullptr) {
     GemmArgs g;
     g.M = M; g.N = N; g.K = K;
     g.A = A; g.lda = lda; g.a_kmajor = ak;
@@ -262,6 +265,7 @@ class EngineT final : public Engine {
     g.C = C; g.ldc = ldc; g.c = cdt;
     g.epi = epi; g.bias = bias; g.resid = resid; g.aux = aux;
     g.ws = gemm_ws_; g.ws_floats = gemm_ws_ ? kGemmWsFloats : 0;
+    g.colsum_part = colsum_part;
     Scope sc(this, 0, 2.0 * M * N * (double)K);
     if (sizeof(T) == 2 && gemm_mode == 1) {
       if (!gemm_tc(g, stream))
@@ -359,13 +363,27 @@ void EngineT<T>::forward_backward(const StepBatch& bt, double* loss_dev, bool ba
     T *h = h_ + l * Md, *q = q_ + l * Md, *kk = k_ + l * Md, *v = v_ + l * Md, *ao = o_ + l * Md;
     T *h2 = h2_ + l * Md, *pre = pre_ + l * Mh, *u = u_ + l * Mh;
     // x_out = x_mid + (u W2 + b2); db2 came with the LayerNorm backward above
+    // pre = h2 W1 + b1: on the tensor-core path the GeluBwd epilogue also emits
+    // the column sums of every 32-row block of dpre (fp32, before rounding)
+    bool fuse_b1 = false;
+    if (sizeof(T) == 2 && gemm_mode == 1 && M % 32 == 0) {
+      GemmArgs ga;
+      ga.M = M; ga.N = hid; ga.K = d;
+      ga.A = dxT_; ga.lda = d; ga.a_kmajor = true;
+      ga.B = W(o.w2); ga.ldb = d; ga.b_kmajor = true;
+      ga.ab = TT; ga.C = dpre_; ga.ldc = hid; ga.c = TT;
+      ga.epi = Epi::GeluBwd; ga.aux = pre;
+      fuse_b1 = gemm_tc_single_pass(ga);
+    }
     mm(M, hid, d, dxT_, d, true, W(o.w2), d, true, dpre_, hid, TT, Epi::GeluBwd, nullptr, nullptr,
-       pre);
+       pre, fuse_b1 ? part_ : nullptr);
     mm(hid, d, M, u, hid, false, dxT_, d, false, G(o.w2), d, DT::F32, Epi::Store);
-    // pre = h2 W1 + b1
     {
       Scope sc(this, 2, 0);
-      k::colsum<T>(dpre_, M, hid, part_, G(o.b1), stream);
+      if (fuse_b1)
+        k::colsum_parts(part_, M / 32, hid, part_ + (size_t)(M / 32) * hid, G(o.b1), stream);
+      else
+        k::colsum<T>(dpre_, M, hid, part_, G(o.b1), stream);
     }
     mm(M, d, hid, dpre_, hid, true, W(o.w1), hid, true, dy_, d, DT::F32, Epi::Store);
     mm(d, hid, M, h2, d, false, dpre_, hid, false, G(o.w1), hid, DT::F32, Epi::Store);

@@ -50,12 +50,18 @@ struct GemmArgs {
   // device never share partials); nullptr = a per-device scratch (debug / tests)
   float* ws = nullptr;
   size_t ws_floats = 0;
+  // GeluBwd without split-K, M % 32 == 0: the epilogue also writes the column
+  // sums of each 32-row block of the fp32 result (before the bf16 rounding) to
+  // colsum_part[M / 32][N] -- the bias gradient's partials, read by colsum_parts
+  float* colsum_part = nullptr;
 };
 // split-K partial floats any tcgen05 GEMM can need: splits * M * N <= the
 // concurrent tile slots times one (pair) tile
 constexpr size_t kGemmWsFloats = (size_t)148 * 128 * 256;
 
 void gemm_simt(const GemmArgs& g, cudaStream_t st);
+// true when gemm_tc runs g in one pass (no split-K), e.g. for colsum_part
+bool gemm_tc_single_pass(const GemmArgs& g);
 // tcgen05 + TMA path (bf16 operands); returns false when the shape/layout is
 // outside what the kernel supports (caller falls back to gemm_simt only in
 // tests -- the engine treats that as a configuration error).

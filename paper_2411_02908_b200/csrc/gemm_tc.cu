@@ -53,6 +53,7 @@ struct TcParams {
   int epi;     // Epi
   int c_bf16;  // output dtype
   const float* bias;
+  float* colsum_part;  // GeluBwd: per-32-row column sums [M / 32][N] (or nullptr)
 };
 
 // ---- PTX wrappers -------------------------------------------------------------
@@ -509,11 +510,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld32(taddr + c * 32, v);  // v[j] = acc[row0 + lane][col0 + j]
           if (has_bias) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              v[4 * j] += bb[j].x;
-              v[4 * j + 1] += bb[j].y;
-              v[4 * j + 2] += bb[j].z;
-              v[4 * j + 3] += bb[j].w;
+            for (int j = 0; j < 8; ++j) {  // packed adds (FADD2), same rounding
+              const float2 lo = __fadd2_rn(make_float2(v[4 * j], v[4 * j + 1]), make_float2(bb[j].x, bb[j].y));
+              const float2 hi =
+                  __fadd2_rn(make_float2(v[4 * j + 2], v[4 * j + 3]), make_float2(bb[j].z, bb[j].w));
+              v[4 * j] = lo.x;
+              v[4 * j + 1] = lo.y;
+              v[4 * j + 2] = hi.x;
+              v[4 * j + 3] = hi.y;
             }
             if (c + 2 < nchunks) load_bias(col0 + 64);
           }
@@ -577,7 +581,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 4; ++j) {
               float gp[8];
 #pragma unroll
-              for (int e = 0; e < 8; ++e) gelu_pair(v[8 * j + e], v[8 * j + e], gp[e]);
+              for (int e = 0; e < 8; e += 2) {
+                float2 g2, gp2;
+                gelu_pair2(make_float2(v[8 * j + e], v[8 * j + e + 1]), g2, gp2);
+                v[8 * j + e] = g2.x;
+                v[8 * j + e + 1] = g2.y;
+                gp[e] = gp2.x;
+                gp[e + 1] = gp2.y;
+              }
               sts128(oa + 2048 + sw64_off(lane, j), pack2(gp[0], gp[1]), pack2(gp[2], gp[3]),
                      pack2(gp[4], gp[5]), pack2(gp[6], gp[7]));
             }
@@ -605,6 +616,21 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (epi == Epi::GeluBias) tma_store_2d(&em.aux, sbuf + 2048, col0, row0);
             }
             bulk_commit();
+          }
+          if (epi == Epi::GeluBwd && p.colsum_part) {
+            // column sums of this warp's 32 rows: a butterfly reduce-scatter
+            // leaves column (col0 + lane) in v[0] of lane `lane`
+#pragma unroll
+            for (int w = 16; w >= 1; w >>= 1) {
+              const bool up = lane & w;
+#pragma unroll
+              for (int i = 0; i < w; ++i) {
+                const float send = up ? v[i] : v[i + w];
+                const float keep = up ? v[i + w] : v[i];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+              }
+            }
+            if (col0 + lane < p.N) p.colsum_part[(size_t)(row0 >> 5) * p.N + col0 + lane] = v[0];
           }
         }
       }
@@ -830,19 +856,47 @@ bool gemm_tc_supported(const GemmArgs& g) {
   return true;
 }
 
-bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
-  if (!gemm_tc_supported(g)) return false;
-  const int BN = g.N <= 128 ? 128 : 256;
-  static const int pair_env = [] {
+namespace {
+int pair_env() {
+  static const int v = [] {
     const char* e = std::getenv("PHOTON_GEMM_PAIR");  // 0 never, 1 by shape, 2 always
     return e ? std::atoi(e) : 1;
   }();
+  return v;
+}
+// split-K factor of a shape (1 = single pass): the tile grid cannot fill the
+// chip and the contraction is long
+int split_count(int M, int N, int K, int nseg, int ncta, int BN) {
+  const int slots = kNumSMs / ncta;
+  const int tiles = ((M + BM * ncta - 1) / (BM * ncta)) * ((N + BN - 1) / BN);
+  const int kb_total = ((K + BK - 1) / BK) * nseg;
+  int splits = 1;
+  if (tiles < slots && kb_total >= 16) {
+    splits = std::min(slots / tiles, kb_total / 8);
+    splits = std::max(1, std::min(splits, 16));
+  }
+  const int per = (kb_total + splits - 1) / splits;
+  return (kb_total + per - 1) / per;
+}
+int cta_count(const GemmArgs& g, int BN) {
+  const bool pair_ok = BN == 256 && g.M > BM;
+  return (pair_env() == 2 || (pair_env() == 1 && pair_ok)) && BN == 256 && g.M > BM ? 2 : 1;
+}
+}  // namespace
+
+bool gemm_tc_single_pass(const GemmArgs& g) {
+  const int BN = g.N <= 128 ? 128 : 256;
+  return gemm_tc_supported(g) && split_count(g.M, g.N, g.K, g.nseg, cta_count(g, BN), BN) == 1;
+}
+
+bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
+  if (!gemm_tc_supported(g)) return false;
+  const int BN = g.N <= 128 ? 128 : 256;
   // CTA pairs (256 x 256 tiles) wherever N is a 256 multiple-ish and M spans
   // more than one 128-row tile: wide tiles without split-K, and the split-K
   // weight gradients (d x d, d x 4d, 4d x d: 25-30% faster than single-CTA
   // 128 x 256 tiles in tools/gemm_bench.py).
-  const bool pair_ok = BN == 256 && g.M > BM;
-  const int ncta = (pair_env == 2 || (pair_env == 1 && pair_ok)) && BN == 256 && g.M > BM ? 2 : 1;
+  const int ncta = cta_count(g, BN);
   const int slots = kNumSMs / ncta;  // concurrent tile workers
   TcParams p{};
   p.M = g.M;
@@ -855,12 +909,7 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
   p.kb_seg = (g.K + BK - 1) / BK;
   p.kb_total = p.kb_seg * g.nseg;
   const int tiles = p.num_m * p.num_n;
-  // split-K when the tile grid cannot fill the chip and the contraction is long
-  int splits = 1;
-  if (tiles < slots && p.kb_total >= 16) {
-    splits = std::min(slots / tiles, p.kb_total / 8);
-    splits = std::max(1, std::min(splits, 16));
-  }
+  const int splits = split_count(g.M, g.N, g.K, g.nseg, ncta, BN);
   p.kb_per_split = (p.kb_total + splits - 1) / splits;
   p.splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
   p.units = tiles * p.splits;
@@ -874,6 +923,9 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
   p.epi = static_cast<int>(g.epi);
   p.c_bf16 = g.c == DT::BF16;
   p.bias = g.bias;
+  p.colsum_part = g.colsum_part;
+  if (g.colsum_part && (g.epi != Epi::GeluBwd || p.splits > 1 || g.M % 32))
+    throw Error(PHOTON_ERR_USAGE, "gemm_tc: fused column sums need GeluBwd, no split-K, M % 32 == 0");
 
   EpiMaps em{};
   float* ws = nullptr;

@@ -343,6 +343,45 @@ static void colreduce(const float* part, int nparts, int n, int stride, float* o
   PH_LAUNCH_CHECK();
 }
 
+// First level of a many-part column reduction: CTA (x, y) sums parts
+// [y * per, (y + 1) * per) of 32 columns in the colreduce order and writes
+// row y of `out` ([gridDim.y][n]).
+__global__ void __launch_bounds__(256) colreduce_rows_kernel(const float* __restrict__ part, int nparts,
+                                                             int per, int n, float* __restrict__ out) {
+  __shared__ float red[8][33];
+  const int cl = threadIdx.x & 31, s = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + cl;
+  const int p0 = blockIdx.y * per, p1 = min(nparts, p0 + per);
+  float acc = 0.f;
+  if (j < n) {
+    int p = p0 + s;
+    for (; p + 8 < p1; p += 16) {
+      const float a = part[(size_t)p * n + j], b = part[(size_t)(p + 8) * n + j];
+      acc = (acc + a) + b;
+    }
+    for (; p < p1; p += 8) acc += part[(size_t)p * n + j];
+  }
+  red[s][cl] = acc;
+  __syncthreads();
+  if (s == 0 && j < n) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w][cl];
+    out[(size_t)blockIdx.y * n + j] = t;
+  }
+}
+
+size_t colsum_parts_scratch_floats(int N) { return (size_t)kColsumPartGroups * N; }
+
+void colsum_parts(const float* part, int nparts, int N, float* scratch, float* out, cudaStream_t st) {
+  const int groups = std::min(kColsumPartGroups, nparts);
+  const int per = cdiv(nparts, groups);
+  const int used = cdiv(nparts, per);
+  colreduce_rows_kernel<<<dim3(cdiv(N, 32), used), 256, 0, st>>>(part, nparts, per, N, scratch);
+  PH_LAUNCH_CHECK();
+  colreduce(scratch, used, N, N, out, N, nullptr, st);
+}
+
 // Register-resident variant for d = 128 * NV: one warp per row, x, dy and the
 // residual gradient of a row all requested before any arithmetic (one DRAM
 // latency per row instead of two), each read once as float4.  The column

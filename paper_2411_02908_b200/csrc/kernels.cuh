@@ -34,6 +34,12 @@ int ln_bwd_parts();
 template <typename T>
 void colsum(const T* x, int M, int N, float* part, float* out, cudaStream_t st);
 size_t colsum_part_floats(int M, int N);
+// Column sums from caller-written partials part[nparts][N] (e.g. the per-32-row
+// sums a GEMM epilogue emits): fixed-order two-level reduction through
+// `scratch` (colsum_parts_scratch_floats(N) floats) into out[N].
+constexpr int kColsumPartGroups = 64;
+size_t colsum_parts_scratch_floats(int N);
+void colsum_parts(const float* part, int nparts, int N, float* scratch, float* out, cudaStream_t st);
 
 // ---- softmax cross-entropy fwd+bwd (tensor.cpp:544-603) --------------------
 // logits [M,V] overwritten with dlogits = (softmax - onehot) * inv_count;

@@ -25,6 +25,10 @@ CASES = [
     ("dW  w2", hid, d, M, 0, 0, 0, 0),
     ("dW  w1", d, hid, M, 0, 0, 0, 0),
     ("dW  head", d, V, M, 0, 0, 0, 0),
+    # layout / fusion probes: the dW shapes with K-major operands, one N = 3d qkv
+    ("probe dW dxd K-major", d, d, M, 1, 1, 0, 0),
+    ("probe dW w1 K-major", d, hid, M, 1, 1, 0, 0),
+    ("probe fwd qkv N=3d +b", M, 3 * d, d, 1, 0, 2, 1),
 ]
 impl = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 tot_f, tot_t = 0.0, 0.0
