@@ -526,6 +526,11 @@ struct BwdArgs {
   const float* Dp;
   bf16* g0;  // dk (dkdv kernel) or dq (dq kernel)
   bf16* g1;  // dv
+  // optional column sums (the q / k / v bias gradients' partials): per
+  // 32-row block of a sequence, [B * nblk][d] for g0 and g1 (nullptr = none)
+  float* s0;
+  float* s1;
+  int nblk;
 };
 
 // producer, MMA, SWB softmax warps: SWB/4 warps per TMEM lane quarter, each on
@@ -548,8 +553,12 @@ constexpr int NR = PHOTON_ATTN_NR;
 
 // Store N columns of a row of a 64-column fp32 TMEM accumulator (thread = row)
 // as bf16 into the head slice.
+// With `part`, also the column sums of the warp's 32 rows (fp32, before the
+// rounding; dead rows count 0): a butterfly reduce-scatter leaves column
+// `lane` in f[0] of lanes < N, which write part[lane].
 template <int N>
-__device__ __forceinline__ void store_acc_rows(uint32_t taddr, bf16* row_ptr, float mul, bool live) {
+__device__ __forceinline__ void store_acc_rows(uint32_t taddr, bf16* row_ptr, float mul, bool live,
+                                               float* part = nullptr) {
   uint32_t u[N];
   if constexpr (N == 32) TMEM_LD32(taddr, u);
   else TMEM_LD16(taddr, u);
@@ -562,6 +571,25 @@ __device__ __forceinline__ void store_acc_rows(uint32_t taddr, bf16* row_ptr, fl
                      pk(__uint_as_float(u[i + 2]) * mul, __uint_as_float(u[i + 3]) * mul),
                      pk(__uint_as_float(u[i + 4]) * mul, __uint_as_float(u[i + 5]) * mul),
                      pk(__uint_as_float(u[i + 6]) * mul, __uint_as_float(u[i + 7]) * mul));
+  }
+  if (part) {  // warp-uniform
+    const int lane = threadIdx.x & 31;
+    float f[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) f[i] = live ? __uint_as_float(u[i]) * mul : 0.f;
+#pragma unroll
+    for (int w = N / 2; w >= 1; w >>= 1) {
+      const bool up = lane & w;
+#pragma unroll
+      for (int i = 0; i < w; ++i) {
+        const float send = up ? f[i] : f[i + w];
+        const float keep = up ? f[i + w] : f[i];
+        f[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+      }
+    }
+#pragma unroll
+    for (int w = N; w < 32; w <<= 1) f[0] += __shfl_xor_sync(0xffffffffu, f[0], w);
+    if (lane < N) part[lane] = f[0];
   }
 }
 
@@ -805,8 +833,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_wait(g_done, (gi - 1) & 1);
       fence_after();
       const int64_t row = (int64_t)(row_base + key) * a.d + h * HD + cg * GPH;
-      store_acc_rows<GPH>(tmem + lane_off + colDK + cg * GPH, a.g0 + row, a.scale, key_live);  // dK
-      store_acc_rows<GPH>(tmem + lane_off + colDV + cg * GPH, a.g1 + row, 1.f, key_live);      // dV
+      // the warp's 32 keys are one column-sum block (if any of them is live)
+      const bool sums = a.s0 && kt * TK + q * 32 < a.S;
+      const int64_t prow = ((int64_t)b * a.nblk + kt * (TK / 32) + q) * a.d + h * HD + cg * GPH;
+      store_acc_rows<GPH>(tmem + lane_off + colDK + cg * GPH, a.g0 + row, a.scale, key_live,
+                          sums ? a.s0 + prow : nullptr);  // dK
+      store_acc_rows<GPH>(tmem + lane_off + colDV + cg * GPH, a.g1 + row, 1.f, key_live,
+                          sums ? a.s1 + prow : nullptr);  // dV
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty);
@@ -1001,9 +1034,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
       mbar_wait(g_done, (gj - 1) & 1);
       fence_after();
+      const bool sums = a.s0 && q0 + q * 32 < a.S;
       store_acc_rows<GPH>(tmem + lane_off + 320 + cg * GPH,
                           a.g0 + (int64_t)(row_base + qrow) * a.d + h * HD + cg * GPH, a.scale,
-                          qrow < a.S);
+                          qrow < a.S,
+                          sums ? a.s0 + ((int64_t)b * a.nblk + qt * (TQ / 32) + q) * a.d + h * HD +
+                                     cg * GPH
+                               : nullptr);
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty);
@@ -1096,7 +1133,7 @@ namespace {
 template <int HD>
 void attn_bwd_hd(const bf16* q, const bf16* k, const bf16* v, const bf16* o, const bf16* dO,
                  const float* lse, bf16* dq, bf16* dk, bf16* dv, int B, int S, int H, int d,
-                 float* ws, cudaStream_t st) {
+                 float* ws, float* sums, cudaStream_t st) {
   const int nt = (S + TQ - 1) / TQ, Spad = nt * TQ, rows = B * S;
   if (!ws) ws = scratch(attn_bwd_tc_ws_floats(B, S, H));
   float* Lp = ws;
@@ -1109,7 +1146,10 @@ void attn_bwd_hd(const bf16* q, const bf16* k, const bf16* v, const bf16* o, con
                     mo = head_map(dO, rows, d);
   const CUtensorMap mqb = TQB == 128 ? mq : head_map(q, rows, d, TQB),
                     mob = TQB == 128 ? mo : head_map(dO, rows, d, TQB);
-  BwdArgs a{S, H, d, Spad, B * H, rsqrtf((float)HD) * kLog2e, rsqrtf((float)HD), Lp, Dp, dk, dv};
+  const int nblk = (S + 31) / 32;
+  const size_t P = (size_t)B * nblk * d;  // sums: dq, dk, dv partials
+  BwdArgs a{S,  H,  d,  Spad, B * H, rsqrtf((float)HD) * kLog2e, rsqrtf((float)HD), Lp, Dp, dk, dv,
+            sums ? sums + P : nullptr, sums ? sums + 2 * P : nullptr, nblk};
   constexpr int NA = HD / 64;
   constexpr int NKV = HD == 64 ? 2 : 1, NRQ = HD == 64 ? NR : 2, NQO = HD == 64 ? 2 : 1;
   constexpr int SMEM1 = 1024 + 2 * NKV * 16384 * NA + NR * 2 * TQB * 128 * NA + NR * 8 * TQB + 512;
@@ -1124,6 +1164,8 @@ void attn_bwd_hd(const bf16* q, const bf16* k, const bf16* v, const bf16* o, con
   PH_LAUNCH_CHECK();
   a.g0 = dq;
   a.g1 = nullptr;
+  a.s0 = sums;
+  a.s1 = nullptr;
   attn_bwd_dq_tc_kernel<HD><<<grid, kBwdThreads, SMEM2, st>>>(mq, mk, mv, mo, a);
   PH_LAUNCH_CHECK();
 }
@@ -1146,9 +1188,9 @@ void attn_fwd_hd(const bf16* q, const bf16* k, const bf16* v, bf16* o, float* ls
 
 void attn_bwd_tc(const bf16* q, const bf16* k, const bf16* v, const bf16* o, const bf16* dO,
                  const float* lse, bf16* dq, bf16* dk, bf16* dv, int B, int S, int H, int d,
-                 float* ws, cudaStream_t st) {
-  if (d / H == 64) attn_bwd_hd<64>(q, k, v, o, dO, lse, dq, dk, dv, B, S, H, d, ws, st);
-  else if (d / H == 128) attn_bwd_hd<128>(q, k, v, o, dO, lse, dq, dk, dv, B, S, H, d, ws, st);
+                 float* ws, cudaStream_t st, float* sums) {
+  if (d / H == 64) attn_bwd_hd<64>(q, k, v, o, dO, lse, dq, dk, dv, B, S, H, d, ws, sums, st);
+  else if (d / H == 128) attn_bwd_hd<128>(q, k, v, o, dO, lse, dq, dk, dv, B, S, H, d, ws, sums, st);
   else throw Error(PHOTON_ERR_CONFIG, "attn_bwd_tc: head dim must be 64 or 128");
 }
 

@@ -121,7 +121,11 @@ class EngineT final : public Engine {
                                                     k::colsum_part_floats((int)M, (int)d),
                                                     // b1 partials of the GeluBwd epilogue
                                                     (size_t)(M / 32) * hid +
-                                                        k::colsum_parts_scratch_floats((int)hid)}));
+                                                        k::colsum_parts_scratch_floats((int)hid),
+                                                    // q / k / v partials of the attention backward
+                                                    k::attn_bwd_sums_floats((int)max_batch,
+                                                                            (int)Smax_, (int)d) +
+                                                        k::colsum_parts_scratch_floats((int)d)}));
     auto plan = [&](char* p) {
       char* s = p;
       // master: separate allocation (see master_alloc_)
@@ -239,19 +243,21 @@ class EngineT final : public Engine {
     }
     k::attn_fwd_simt<T>(q, k, v, o, lse, B, S, H, d, stream);
   }
-  void attn_bwd(const T* q, const T* k, const T* v, const T* o, const T* dO, const float* lse,
+  // true when the q / k / v column sums came with it (attn_bwd_sums_floats in part_)
+  bool attn_bwd(const T* q, const T* k, const T* v, const T* o, const T* dO, const float* lse,
                 int B, int S, int H, int d) {
     if constexpr (sizeof(T) == 2) {
       if (attn_mode == 1 && k::attn_tc_supported((int)(d_ / H_), d)) {
-        k::attn_bwd_tc(q, k, v, o, dO, lse, dq_, dk_, dv_, B, S, H, d, attn_ws_, stream);
-        return;
+        k::attn_bwd_tc(q, k, v, o, dO, lse, dq_, dk_, dv_, B, S, H, d, attn_ws_, stream, part_);
+        return true;
       }
       if (use_mma_attn()) {
         k::attn_bwd_mma(q, k, v, o, dO, lse, Dvec_, dq_, dk_, dv_, B, S, H, d, stream);
-        return;
+        return false;
       }
     }
     k::attn_bwd_simt<T>(q, k, v, o, dO, lse, Dvec_, dq_, dk_, dv_, B, S, H, d, stream);
+    return false;
   }
 
   void mm(int M, int N, int K, const void* A, int64_t lda, bool ak, const void* B, int64_t ldb,
@@ -395,16 +401,26 @@ void EngineT<T>::forward_backward(const StepBatch& bt, double* loss_dev, bool ba
     }
     mm(M, d, d, dxT_, d, true, W(o.wo), d, true, dO_, d, TT, Epi::Store);
     mm(d, d, M, ao, d, false, dxT_, d, false, G(o.wo), d, DT::F32, Epi::Store);
+    bool qkv_sums;
     {
       Scope sc(this, 1, 2.5 * attn_fwd_flops);
-      attn_bwd(q, kk, v, ao, dO_, lse_ + (size_t)l * B * H * S, B, S, H, d);
+      qkv_sums = attn_bwd(q, kk, v, ao, dO_, lse_ + (size_t)l * B * H * S, B, S, H, d);
     }
     // q,k,v = h W{q,k,v} + b{q,k,v}; LN1's output grad sums v, k, q in that order
     {
       Scope sc(this, 2, 0);
-      k::colsum<T>(dv_, M, d, part_, G(o.bv), stream);
-      k::colsum<T>(dk_, M, d, part_, G(o.bk), stream);
-      k::colsum<T>(dq_, M, d, part_, G(o.bq), stream);
+      if (qkv_sums) {  // partials from the attention backward's stores
+        const int np = B * ((S + 31) / 32);
+        const size_t P = (size_t)np * d;
+        float* scr = part_ + 3 * P;
+        k::colsum_parts(part_ + 2 * P, np, d, scr, G(o.bv), stream);
+        k::colsum_parts(part_ + P, np, d, scr, G(o.bk), stream);
+        k::colsum_parts(part_, np, d, scr, G(o.bq), stream);
+      } else {
+        k::colsum<T>(dv_, M, d, part_, G(o.bv), stream);
+        k::colsum<T>(dk_, M, d, part_, G(o.bk), stream);
+        k::colsum<T>(dq_, M, d, part_, G(o.bq), stream);
+      }
     }
     // dy = dv Wv^T + dk Wk^T + dq Wq^T: one K-concatenated contraction on the
     // tensor-core path (one fp32 pass over dy instead of a store + two RMWs)

@@ -75,7 +75,11 @@ void attn_fwd_tc(const bf16* q, const bf16* k, const bf16* v, bf16* o, float* ls
 size_t attn_bwd_tc_ws_floats(int B, int S, int H);
 void attn_bwd_tc(const bf16* q, const bf16* k, const bf16* v, const bf16* o, const bf16* dO,
                  const float* lse, bf16* dq, bf16* dk, bf16* dv, int B, int S, int H, int d,
-                 float* ws, cudaStream_t st);
+                 float* ws, cudaStream_t st, float* sums = nullptr);
+// sums (optional): the kernels also write per-32-row column sums of dq, dk, dv
+// (the q / k / v bias gradients' partials) as three consecutive
+// [B * ceil(S / 32)][d] blocks, for colsum_parts
+inline size_t attn_bwd_sums_floats(int B, int S, int d) { return (size_t)3 * B * ((S + 31) / 32) * d; }
 
 // ---- casts -------------------------------------------------------------------
 void f64_to_f32(const double* in, float* out, uint64_t n, cudaStream_t st);
