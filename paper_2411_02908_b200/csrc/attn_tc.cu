@@ -563,20 +563,17 @@ __device__ __forceinline__ void store_acc_rows(uint32_t taddr, bf16* row_ptr, fl
   if constexpr (N == 32) TMEM_LD32(taddr, u);
   else TMEM_LD16(taddr, u);
   tmem_wait_ld();
+  float f[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) f[i] = live ? __uint_as_float(u[i]) * mul : 0.f;
   if (live) {
 #pragma unroll
     for (int i = 0; i < N; i += 8)
-      *reinterpret_cast<uint4*>(row_ptr + i) =
-          make_uint4(pk(__uint_as_float(u[i]) * mul, __uint_as_float(u[i + 1]) * mul),
-                     pk(__uint_as_float(u[i + 2]) * mul, __uint_as_float(u[i + 3]) * mul),
-                     pk(__uint_as_float(u[i + 4]) * mul, __uint_as_float(u[i + 5]) * mul),
-                     pk(__uint_as_float(u[i + 6]) * mul, __uint_as_float(u[i + 7]) * mul));
+      *reinterpret_cast<uint4*>(row_ptr + i) = make_uint4(pk(f[i], f[i + 1]), pk(f[i + 2], f[i + 3]),
+                                                          pk(f[i + 4], f[i + 5]), pk(f[i + 6], f[i + 7]));
   }
   if (part) {  // warp-uniform
     const int lane = threadIdx.x & 31;
-    float f[N];
-#pragma unroll
-    for (int i = 0; i < N; ++i) f[i] = live ? __uint_as_float(u[i]) * mul : 0.f;
 #pragma unroll
     for (int w = N / 2; w >= 1; w >>= 1) {
       const bool up = lane & w;
