@@ -553,17 +553,16 @@ constexpr int NR = PHOTON_ATTN_NR;
 
 // Store N columns of a row of a 64-column fp32 TMEM accumulator (thread = row)
 // as bf16 into the head slice.
-// With `part`, also the column sums of the warp's 32 rows (fp32, before the
-// rounding; dead rows count 0): a butterfly reduce-scatter leaves column
-// `lane` in f[0] of lanes < N, which write part[lane].
+// Store N columns of a row of an fp32 TMEM accumulator (thread = row), scaled
+// by `mul`, as bf16 into the head slice; f keeps the scaled fp32 values (0 for
+// a dead row) for warp_colsum.
 template <int N>
 __device__ __forceinline__ void store_acc_rows(uint32_t taddr, bf16* row_ptr, float mul, bool live,
-                                               float* part = nullptr) {
+                                               float (&f)[N]) {
   uint32_t u[N];
   if constexpr (N == 32) TMEM_LD32(taddr, u);
   else TMEM_LD16(taddr, u);
   tmem_wait_ld();
-  float f[N];
 #pragma unroll
   for (int i = 0; i < N; ++i) f[i] = live ? __uint_as_float(u[i]) * mul : 0.f;
   if (live) {
@@ -572,22 +571,26 @@ __device__ __forceinline__ void store_acc_rows(uint32_t taddr, bf16* row_ptr, fl
       *reinterpret_cast<uint4*>(row_ptr + i) = make_uint4(pk(f[i], f[i + 1]), pk(f[i + 2], f[i + 3]),
                                                           pk(f[i + 4], f[i + 5]), pk(f[i + 6], f[i + 7]));
   }
-  if (part) {  // warp-uniform
-    const int lane = threadIdx.x & 31;
+}
+// Column sums of the warp's 32 rows of f (the bias gradients' partials): a
+// butterfly reduce-scatter leaves column `lane` in f[0] of lanes < N, which
+// write part[lane].  Runs after the accumulator is released to the MMA warp.
+template <int N>
+__device__ __forceinline__ void warp_colsum(float (&f)[N], float* part) {
+  const int lane = threadIdx.x & 31;
 #pragma unroll
-    for (int w = N / 2; w >= 1; w >>= 1) {
-      const bool up = lane & w;
+  for (int w = N / 2; w >= 1; w >>= 1) {
+    const bool up = lane & w;
 #pragma unroll
-      for (int i = 0; i < w; ++i) {
-        const float send = up ? f[i] : f[i + w];
-        const float keep = up ? f[i + w] : f[i];
-        f[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
-      }
+    for (int i = 0; i < w; ++i) {
+      const float send = up ? f[i] : f[i + w];
+      const float keep = up ? f[i + w] : f[i];
+      f[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
     }
-#pragma unroll
-    for (int w = N; w < 32; w <<= 1) f[0] += __shfl_xor_sync(0xffffffffu, f[0], w);
-    if (lane < N) part[lane] = f[0];
   }
+#pragma unroll
+  for (int w = N; w < 32; w <<= 1) f[0] += __shfl_xor_sync(0xffffffffu, f[0], w);
+  if (lane < N) part[lane] = f[0];
 }
 
 // Both backward kernels are persistent (one CTA per SM): a CTA walks a static
@@ -833,13 +836,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       // the warp's 32 keys are one column-sum block (if any of them is live)
       const bool sums = a.s0 && kt * TK + q * 32 < a.S;
       const int64_t prow = ((int64_t)b * a.nblk + kt * (TK / 32) + q) * a.d + h * HD + cg * GPH;
-      store_acc_rows<GPH>(tmem + lane_off + colDK + cg * GPH, a.g0 + row, a.scale, key_live,
-                          sums ? a.s0 + prow : nullptr);  // dK
-      store_acc_rows<GPH>(tmem + lane_off + colDV + cg * GPH, a.g1 + row, 1.f, key_live,
-                          sums ? a.s1 + prow : nullptr);  // dV
+      float fk[GPH], fv[GPH];
+      store_acc_rows<GPH>(tmem + lane_off + colDK + cg * GPH, a.g0 + row, a.scale, key_live, fk);  // dK
+      store_acc_rows<GPH>(tmem + lane_off + colDV + cg * GPH, a.g1 + row, 1.f, key_live, fv);      // dV
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty);
+      if (sums) {
+        warp_colsum<GPH>(fk, a.s0 + prow);
+        warp_colsum<GPH>(fv, a.s1 + prow);
+      }
     }
   }
   fence_before();
@@ -1032,15 +1038,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_wait(g_done, (gj - 1) & 1);
       fence_after();
       const bool sums = a.s0 && q0 + q * 32 < a.S;
+      float fq[GPH];
       store_acc_rows<GPH>(tmem + lane_off + 320 + cg * GPH,
                           a.g0 + (int64_t)(row_base + qrow) * a.d + h * HD + cg * GPH, a.scale,
-                          qrow < a.S,
-                          sums ? a.s0 + ((int64_t)b * a.nblk + qt * (TQ / 32) + q) * a.d + h * HD +
-                                     cg * GPH
-                               : nullptr);
+                          qrow < a.S, fq);
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty);
+      if (sums) warp_colsum<GPH>(fq, a.s0 + ((int64_t)b * a.nblk + qt * (TQ / 32) + q) * a.d + h * HD + cg * GPH);
     }
   }
   fence_before();
