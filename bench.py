@@ -363,11 +363,19 @@ def run_ours(args):
 
     agg = None
     if rank == 0 and not args.no_agg:
+        import torch
+
         P = model.param_count()
-        gbs, ms, nbytes = aggregation_sweep(runner.ctx, P, args.agg_k)
-        agg = {"n_params": P, "clients": args.agg_k, "kernel": "fused anchored-mean+nesterov f32",
-               "ms": ms, "algorithmic_bytes": nbytes, "achieved_gbs": gbs, "peak_gbs": hbm,
-               "frac": gbs / hbm}
+        # the side measurement needs (k + 2) * P fp32 beside the resident engine;
+        # at 7B that leaves room for few (or no) client models -- shrink k, never OOM
+        free, _ = torch.cuda.mem_get_info(runner.ctx.device)
+        k_fit = min(args.agg_k, int((free - (2 << 30)) // (4 * P)) - 2)
+        if k_fit >= 2:
+            gbs, ms, nbytes = aggregation_sweep(runner.ctx, P, k_fit)
+            agg = {"n_params": P, "clients": k_fit,
+                   "kernel": "fused anchored-mean+nesterov f32", "ms": ms,
+                   "algorithmic_bytes": nbytes, "achieved_gbs": gbs, "peak_gbs": hbm,
+                   "frac": gbs / hbm}
 
     if rank != 0:
         return 0
