@@ -256,6 +256,8 @@ def test_golden_local_round_and_rounds(oracle):
     # SURVEY 8c recorded values (same runs)
     assert float.fromhex(GOLD["rounds_hetero4_P2K2_tau16_4rounds"]["fedavg"]["round_losses"][-1]) \
         == 1.6591960376792079
+    assert float.fromhex(GOLD["rounds_hetero4_P2K2_tau16_4rounds"]["diloco"]["round_losses"][-1]) \
+        == 2.8408618129986269
 
 
 # ---- 3. live reference (when built here) -------------------------------------------------
