@@ -675,23 +675,33 @@ __global__ void __launch_bounds__(kColsumWideThreads, 1)
   __syncthreads();
   const int per = (M + gridDim.x - 1) / gridDim.x;
   const int r0 = blockIdx.x * per, r1 = min(M, r0 + per);
-  for (int r = r0; r < r1; r += 2) {
-    const bool two = r + 1 < r1;
+  // four rows per pass (four 16-byte loads in flight per thread before the
+  // first add): acc += (r0 + r1) + (r2 + r3), rows in a fixed order
+  for (int r = r0; r < r1; r += 4) {
     const uint4* a = reinterpret_cast<const uint4*>(x + (size_t)r * N);
-    const uint4* b = reinterpret_cast<const uint4*>(x + (size_t)(r + 1) * N);
     for (int c = threadIdx.x; c < nvec; c += blockDim.x) {
-      const uint4 u = a[c];
-      const uint4 w = two ? b[c] : make_uint4(0u, 0u, 0u, 0u);
-      const uint32_t us[4] = {u.x, u.y, u.z, u.w}, ws[4] = {w.x, w.y, w.z, w.w};
+      uint4 u[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        u[k] = r + k < r1 ? a[(size_t)k * nvec + c] : make_uint4(0u, 0u, 0u, 0u);
+      float f[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t w0 = (&u[0].x)[j], w1 = (&u[1].x)[j], w2 = (&u[2].x)[j], w3 = (&u[3].x)[j];
+        f[2 * j] = (__uint_as_float(w0 << 16) + __uint_as_float(w1 << 16)) +
+                   (__uint_as_float(w2 << 16) + __uint_as_float(w3 << 16));
+        f[2 * j + 1] = (__uint_as_float(w0 & 0xffff0000u) + __uint_as_float(w1 & 0xffff0000u)) +
+                       (__uint_as_float(w2 & 0xffff0000u) + __uint_as_float(w3 & 0xffff0000u));
+      }
       float4 lo = acc4[2 * c], hi = acc4[2 * c + 1];
-      lo.x += __uint_as_float(us[0] << 16) + __uint_as_float(ws[0] << 16);
-      lo.y += __uint_as_float(us[0] & 0xffff0000u) + __uint_as_float(ws[0] & 0xffff0000u);
-      lo.z += __uint_as_float(us[1] << 16) + __uint_as_float(ws[1] << 16);
-      lo.w += __uint_as_float(us[1] & 0xffff0000u) + __uint_as_float(ws[1] & 0xffff0000u);
-      hi.x += __uint_as_float(us[2] << 16) + __uint_as_float(ws[2] << 16);
-      hi.y += __uint_as_float(us[2] & 0xffff0000u) + __uint_as_float(ws[2] & 0xffff0000u);
-      hi.z += __uint_as_float(us[3] << 16) + __uint_as_float(ws[3] << 16);
-      hi.w += __uint_as_float(us[3] & 0xffff0000u) + __uint_as_float(ws[3] & 0xffff0000u);
+      lo.x += f[0];
+      lo.y += f[1];
+      lo.z += f[2];
+      lo.w += f[3];
+      hi.x += f[4];
+      hi.y += f[5];
+      hi.z += f[6];
+      hi.w += f[7];
       acc4[2 * c] = lo;
       acc4[2 * c + 1] = hi;
     }
