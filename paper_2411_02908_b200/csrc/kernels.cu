@@ -675,23 +675,28 @@ __global__ void __launch_bounds__(kColsumWideThreads, 1)
   __syncthreads();
   const int per = (M + gridDim.x - 1) / gridDim.x;
   const int r0 = blockIdx.x * per, r1 = min(M, r0 + per);
-  // four rows per pass (four 16-byte loads in flight per thread before the
-  // first add): acc += (r0 + r1) + (r2 + r3), rows in a fixed order
-  for (int r = r0; r < r1; r += 4) {
+  // eight rows per pass (eight 16-byte loads in flight per thread before the
+  // first add): acc += ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7)), fixed order
+  for (int r = r0; r < r1; r += 8) {
     const uint4* a = reinterpret_cast<const uint4*>(x + (size_t)r * N);
     for (int c = threadIdx.x; c < nvec; c += blockDim.x) {
-      uint4 u[4];
+      uint4 u[8];
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < 8; ++k)
         u[k] = r + k < r1 ? a[(size_t)k * nvec + c] : make_uint4(0u, 0u, 0u, 0u);
       float f[8];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const uint32_t w0 = (&u[0].x)[j], w1 = (&u[1].x)[j], w2 = (&u[2].x)[j], w3 = (&u[3].x)[j];
-        f[2 * j] = (__uint_as_float(w0 << 16) + __uint_as_float(w1 << 16)) +
-                   (__uint_as_float(w2 << 16) + __uint_as_float(w3 << 16));
-        f[2 * j + 1] = (__uint_as_float(w0 & 0xffff0000u) + __uint_as_float(w1 & 0xffff0000u)) +
-                       (__uint_as_float(w2 & 0xffff0000u) + __uint_as_float(w3 & 0xffff0000u));
+        float lo8[8], hi8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t w = (&u[k].x)[j];
+          lo8[k] = __uint_as_float(w << 16);
+          hi8[k] = __uint_as_float(w & 0xffff0000u);
+        }
+        f[2 * j] = ((lo8[0] + lo8[1]) + (lo8[2] + lo8[3])) + ((lo8[4] + lo8[5]) + (lo8[6] + lo8[7]));
+        f[2 * j + 1] =
+            ((hi8[0] + hi8[1]) + (hi8[2] + hi8[3])) + ((hi8[4] + hi8[5]) + (hi8[6] + hi8[7]));
       }
       float4 lo = acc4[2 * c], hi = acc4[2 * c + 1];
       lo.x += f[0];
