@@ -14,7 +14,11 @@ tokens/round = K * tau * B * S.
          host BatchStream staging, pinned H2D of the round's tokens, the round,
          D2H of the step losses -- wall clock, max over ranks.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--tau T] [--impl reference]
+  --impl reference  the reference's own FederationRunner (oracle/_ref, built from
+         /root/reference sources) on the host cores: at --model small the
+         identical round (same_config), at 125m a stated reduced-context sample.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--model M] [--impl reference]
 """
 from __future__ import annotations
 
@@ -42,10 +46,21 @@ def _emit(line: dict) -> None:
     _JSON_OUT.flush()
 
 MODEL_125M = (12, 768, 12, 4, 50368, 2048)
-# SURVEY 8(d) configs 2-4 (Photon 125M / 1.3B / 7B, reference architecture)
-MODELS = {"125m": (MODEL_125M, "Photon-125M", "164.04M"),
+# the hetero4 decoder (configs/hetero4.cfg:15-21, the one
+# config the reference CPU path runs in full), Photon 125M / 1.3B / 7B
+MODELS = {"small": ((1, 32, 2, 4, 64, 16), "hetero4 decoder (config 1)", "17,440"),
+          "125m": (MODEL_125M, "Photon-125M", "164.04M"),
           "1.3b": ((24, 2048, 16, 4, 50368, 2048), "Photon-1.3B", "1,419.15M"),
           "7b": ((32, 4096, 32, 4, 50368, 2048), "Photon-7B", "6,865.22M")}
+# per model: (tau, B, clients per GPU, LrSchedule(eta_max, warmup, decay, alpha))
+RUN = {"small": (16, 4, 2, (2e-3, 16, 160, 0.1)),   # hetero4.cfg:37-42, 2 clients
+       "125m": (64, 32, 1, (6e-4, 64, 1024, 0.1)),
+       "1.3b": (64, 32, 1, (6e-4, 64, 1024, 0.1)),
+       "7b": (64, 32, 1, (6e-4, 64, 1024, 0.1))}
+# the reference CPU arm at 125M: the full S = 2048 step costs ~15 min of f64 per
+# client, so each client of its FederationRunner round runs the same
+# architecture at a reduced sequence length (stated in its config)
+REF_SEQ_125M = 32
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 METRIC = "tokens/s/round at 1-8 B200 (125M); FedAvg aggregate GB/s vs roofline"
 
@@ -182,74 +197,105 @@ def _bcast_bytes(b: bytes, world, local):
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the reference's own client step (oracle/_ref) on host cores
+# CPU baseline: the reference's own FederationRunner (oracle/_ref) on host cores
 # ---------------------------------------------------------------------------
-def _cpu_threads():
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            return next(l.split(":", 1)[1].strip() for l in f if l.startswith("model name"))
+    except Exception:
+        return "unknown"
+
+
+def _cpu_threads(per_client_gb: float = 9.0):
     n = os.cpu_count() or 1
     try:
         with open("/proc/meminfo") as f:
             avail_kb = next(int(l.split()[1]) for l in f if l.startswith("MemAvailable"))
-        by_mem = max(1, int(avail_kb / 1024 / 1024 / 9))  # ~7-8 GB per 125M f64 client
+        by_mem = max(1, int(avail_kb / 1024 / 1024 / per_client_gb))
     except Exception:
         by_mem = 4
     return max(1, min(n, by_mem, 64))
 
 
-def cpu_sample(seq: int = 32, threads: int | None = None):
-    """(tokens/s, cores, kind, sample description) of the reference CPU path."""
-    from oracle import ModelCfg, TrainCfg, load_reference
+def ref_rounds(model: str, gpus: int, rounds: int, warmup: int = 1):
+    """The reference's FederationRunner::run_round (aggregator.cpp:93-220) on the
+    host: n_threads = min(K, nproc), eval_every = 0, no checkpoints; corpus,
+    partition, streams and init exactly as our arm builds them.  Returns
+    (tokens/s from the median round, per-round seconds, description dict).
 
-    threads = threads or _cpu_threads()
+    small: the identical workload our arm runs (K = 2 per GPU, tau 16, B 4).
+    125m:  K = host threads clients, tau = 1, B = 1 at S = REF_SEQ_125M --
+           the same architecture with a shorter context (labelled as such)."""
+    from oracle import ModelCfg, ServerCfg, TrainCfg, load_oracle, load_reference
+
+    shape = list(MODELS[model][0])
+    tau, B, per_gpu, sched = RUN[model]
+    if model == "small":
+        K = per_gpu * gpus
+        threads = min(K, os.cpu_count() or 1)
+    else:
+        shape[5] = REF_SEQ_125M
+        tau, B = 1, 1
+        K = threads = _cpu_threads()
+    mc = ModelCfg(*shape)
+    S, V = shape[5], shape[4]
+    t = TrainCfg(eta_max=sched[0], warmup_steps=sched[1], decay_steps=sched[2], alpha=sched[3],
+                 local_steps=tau, batch_size=B)
+    n_tok = K * tau * B * (S + 1) * (rounds + warmup) + S + 1
     ref = load_reference()
-    mc = ModelCfg(*MODEL_125M)
-    t = TrainCfg(eta_max=6e-4, warmup_steps=64, decay_steps=1024, alpha=0.1, batch_size=1)
-    if ref is not None:
-        secs, _ = ref.train_sample(mc, t, 1, seq, 1, threads)
-        kind = "reference"
-    else:  # the C restatement, single thread per client (oracle port)
-        import numpy as np
-
-        from oracle import load_oracle
-
-        o = load_oracle()
-        p = o.init_params(mc, 1)
-        corpus = o.generate_corpus("web", 4 * (seq + 1), 7, mc.vocab_size)
-        t0 = time.perf_counter()
-        o.forward_backward(mc, p, corpus[:seq].astype(np.int32), corpus[1:seq + 1].astype(np.int32),
-                           1, seq)
-        secs = time.perf_counter() - t0
-        threads = 1
-        kind = "port"
-    tokens = threads * seq
-    sample = (f"{threads} reference clients x 1 local AdamW step, B=1 x S={seq} tokens each, "
-              f"125M reference architecture (f64, {threads} host threads)")
-    return tokens / secs, threads, kind, sample
+    kind = "reference"
+    if ref is None:
+        raise RuntimeError("oracle/_ref (the reference built from its own sources) is missing")
+    theta0 = load_oracle().init_params(mc, 1)
+    _, _, _, secs = ref.run_rounds(mc, t, ServerCfg(1, 0.1, 0.9, 1), 0, "web", n_tok, 7, K, K,
+                                   rounds + warmup, 42, 2, threads, theta0)
+    timed = list(secs[warmup:])
+    tokens = K * tau * B * S
+    L, d, H, e = shape[:4]
+    desc = {"model": f"L{L} d{d} H{H} e{e} V{V} S{S}", "clients": K, "local_steps": tau,
+            "batch": B, "seq_len": S, "tokens_per_round": tokens, "threads": threads,
+            "nproc": os.cpu_count(), "cpu_model": _cpu_model(), "kind": kind,
+            "round_seconds": timed, "warmup_rounds": warmup,
+            "how": "FederationRunner::run_round, eval_every=0, n_threads=min(K, nproc); "
+                   "median of the timed rounds"}
+    return tokens / statistics.median(timed), timed, desc
 
 
 def run_reference_arm(args):
     rank, world, local = _dist_setup(args.gpus)
     if rank != 0:
         return 0
-    # bounded samples of the reference's own CPU client step; one per "step"
-    for _ in range(args.warmup):
-        cpu_sample(args.cpu_seq)
-    vals = []
+    # one FederationRunner session: W warm-up rounds, then K timed rounds
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        v, cores, kind, sample = cpu_sample(args.cpu_seq)
-        vals.append(v)
+    # at 125m every round is ~10-30 s of f64 work per host thread: one warm-up
+    # round (SURVEY 8(d)), so the arm ends within minutes
+    warm = args.warmup if args.model == "small" else 1
+    value, secs, desc = ref_rounds(args.model, args.gpus, args.steps, warmup=warm)
     wall = time.perf_counter() - t0
-    value = statistics.median(vals)
+    same = args.model == "small"
+    cfg = dict(_config(args), precision="f64 (the reference's own arithmetic)",
+               clients=desc["clients"], local_steps=desc["local_steps"], batch=desc["batch"],
+               seq_len=desc["seq_len"], model=desc["model"],
+               global_batch=desc["clients"] * desc["batch"], threads=desc["threads"],
+               nproc=desc["nproc"], cpu_model=desc["cpu_model"], same_config=same)
+    if not same:
+        cfg["sample_of"] = _config(args)["model"]
+    sample = (f"{desc['clients']} reference clients x tau={desc['local_steps']} x "
+              f"B={desc['batch']} x S={desc['seq_len']} per round, {desc['model']}, "
+              f"{desc['threads']} host threads ({desc['cpu_model']}, nproc {desc['nproc']}); "
+              f"median of {len(secs)} FederationRunner rounds after {warm} warm-up")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 * wall / max(args.steps, 1), "higher_is_better": True,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": warm,
+        "ms_per_step": 1000.0 * statistics.median(secs), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(_config(args), precision="f64 (the reference's own arithmetic)"),
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": kind,
-                         "sample": sample},
+        "config": cfg,
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": desc["threads"],
+                         "kind": desc["kind"], "sample": sample},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "round_seconds": secs, "wall_s": wall,
     }
     _emit(line)
     return 0
@@ -258,12 +304,15 @@ def run_reference_arm(args):
 def _config(args):
     shape, name, params = MODELS[args.model]
     L, d, H, e, V, S = shape
+    per_gpu = RUN[args.model][2]
+    server = "nesterov eta=0.1 mu=0.9"
     return {"workload": f"{name} federated round (reference architecture, {params} params)",
-            "model": f"L{L} d{d} H{H} e{e} V{V} S{S}", "clients": args.gpus,
-            "clients_per_gpu": 1, "local_steps": args.tau, "batch": args.batch, "seq_len": S,
-            "global_batch": args.gpus * args.batch, "server_opt": "nesterov eta=0.1 mu=0.9",
-            "parallelism": f"fed{args.gpus}", "precision": args.precision,
-            "l2": "inputs larger than L2 (weights+activations >> 126 MB)"}
+            "model": f"L{L} d{d} H{H} e{e} V{V} S{S}", "clients": args.gpus * per_gpu,
+            "clients_per_gpu": per_gpu, "local_steps": args.tau, "batch": args.batch,
+            "seq_len": S, "global_batch": args.gpus * per_gpu * args.batch,
+            "server_opt": server, "parallelism": f"fed{args.gpus}", "precision": args.precision,
+            "l2": "inputs larger than L2 (weights+activations >> 126 MB)"
+            if args.model != "small" else "model and batch fit in L2 (config 1 is tiny)"}
 
 
 # ---------------------------------------------------------------------------
@@ -307,15 +356,17 @@ def run_ours(args):
     hbm, bf16_burst, bf16_sus, peak_src = _peaks()
     L, d, H, e, V, S = MODELS[args.model][0]
     model = F.ModelConfig(L, d, H, e, V, S)
-    K = world  # weak scaling: one client per GPU
+    per_gpu = RUN[args.model][2]
+    K = world * per_gpu  # weak scaling: clients per GPU fixed
     rounds = args.warmup + args.steps + 1
     tau, B = args.tau, args.batch
+    sched = RUN[args.model][3]
     # corpus: one epoch per client per round of tau*B blocks of S+1 tokens
     n_tok = K * tau * B * (S + 1) + S + 1
     corpus = F.generate_corpus("web", n_tok, 7, V)
     plan = F.partition_iid(corpus, K, S, 7)
     theta0 = F.TransformerModel(model).init_params(1)
-    local_cfg = F.LocalTrainConfig(model=model, schedule=F.LrSchedule(6e-4, 64, 1024, 0.1),
+    local_cfg = F.LocalTrainConfig(model=model, schedule=F.LrSchedule(*sched),
                                    local_steps=tau, batch_size=B)
     server = F.ServerOptConfig(1, 0.1, 0.9, True)
     nccl_id = _bcast_bytes(F.nccl_unique_id() if rank == 0 else b"", world, local) \
@@ -362,7 +413,7 @@ def run_ours(args):
                 "attn_launches": times[6], "launches": times[7]}
 
     agg = None
-    if rank == 0 and not args.no_agg:
+    if rank == 0 and not args.no_agg and args.model != "small":
         import torch
 
         P = model.param_count()
@@ -422,15 +473,23 @@ def run_ours(args):
                             "busbw_gbs": wire / (agg_ms_max * 1e-3) / 1e9, "nvlink_gbs": 900.0,
                             "frac": wire / (agg_ms_max * 1e-3) / 1e9 / 900.0,
                             "path": _boundary_path(P)}
-    if world == 1 and not args.no_cpu and args.model != "125m":
+    if world == 1 and not args.no_cpu and args.model not in ("125m", "small"):
         # the f64 reference state of 1.3B / 7B exceeds host RAM
         line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "n/a",
                                 "sample": f"reference CPU path not runnable at {args.model}"}
     elif world == 1 and not args.no_cpu:
         try:
-            v, cores, kind, sample = cpu_sample(args.cpu_seq)
-            line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": kind,
-                                    "sample": sample}
+            # one bounded FederationRunner round of the reference (no warm-up:
+            # keeps the default bench within minutes; --impl reference is the
+            # warmed, median-of-rounds measurement)
+            v, secs, desc = ref_rounds(args.model, 1, 1, warmup=0)
+            line["cpu_baseline"] = {
+                "value": v, "unit": "tokens/s", "cores": desc["threads"], "kind": desc["kind"],
+                "sample": f"{desc['clients']} reference clients x tau={desc['local_steps']} x "
+                          f"B={desc['batch']} x S={desc['seq_len']}, {desc['model']}, one "
+                          f"FederationRunner round on {desc['threads']} host threads "
+                          f"({desc['cpu_model']}, nproc {desc['nproc']})",
+                "same_config": args.model == "small"}
         except Exception as ex:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "cores": 0,
                                     "kind": "unavailable", "sample": str(ex)[:200]}
@@ -444,16 +503,20 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--tau", type=int, default=int(os.environ.get("PHOTON_BENCH_TAU", "64")))
-    ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--tau", type=int, default=None, help="local steps (default per model)")
+    ap.add_argument("--batch", type=int, default=None, help="local batch (default per model)")
     ap.add_argument("--precision", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--agg-k", type=int, default=8)
     ap.add_argument("--no-agg", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seq", type=int, default=32)
     ap.add_argument("--model", default="125m", choices=sorted(MODELS),
-                    help="125m is the contracted workload; 1.3b / 7b are SURVEY 8(d) configs 3-4")
+                    help="125m is the contracted workload; small / 1.3b / 7b are SURVEY "
+                         "8(d) configs 1, 3, 4 (small: both arms run the identical round)")
     args = ap.parse_args(argv)
+    if args.tau is None:
+        args.tau = int(os.environ.get("PHOTON_BENCH_TAU", RUN[args.model][0]))
+    if args.batch is None:
+        args.batch = RUN[args.model][1]
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

@@ -258,6 +258,25 @@ int photon_debug_gemm(int impl, int M, int N, int K, const void* A, int64_t lda,
 int photon_debug_colsum(const void* x, int x_bf16, int M, int N, float* out, double* ms,
                         photon_err* err);
 
+/* Softmax cross-entropy forward + backward on a device logits matrix [M, V]
+ * (bf16 when logits_bf16, else fp32), as the engine runs it
+ * (tensor.cpp:544-603): rowloss[M] (f64) = logsumexp - logit[target]; with
+ * write_grad the logits are overwritten by (softmax - onehot) * inv_count and,
+ * when dbias != NULL, dbias[V] receives their column sums (the head-bias
+ * gradient, tensor.cpp:279-285).  *ms = device time of the call. */
+int photon_debug_ce(void* logits, int logits_bf16, const int32_t* targets, int M, int V,
+                    float inv_count, double* rowloss, int write_grad, float* dbias, double* ms,
+                    photon_err* err);
+
+/* LayerNorm forward (+ backward when dy != NULL) on device pointers, as the
+ * engine runs them (tensor.cpp:322-394): x, gain, bias, dy, dres fp32; y and
+ * dxT bf16 when y_bf16 else fp32; mean / rstd fp32 [M]; dx = dres + LN'(dy);
+ * dgain / dbias [d]; dsum (optional) = column sums of dx. */
+int photon_debug_layernorm(int y_bf16, int M, int d, const float* x, const float* gain,
+                           const float* bias, void* y, float* mean, float* rstd, const float* dy,
+                           const float* dres, float* dx, void* dxT, float* dgain, float* dbias,
+                           float* dsum, double* ms, photon_err* err);
+
 /* Causal attention on device pointers (bf16 q,k,v,o,dO,dq,dk,dv as [B*S, d]
  * with head h in columns [h*dh,(h+1)*dh); lse, scratch fp32 [B*H*S]):
  * impl 0 = SIMT, 1 = mma.sync tensor core, 2 = tcgen05 (dh = 64 or 128).

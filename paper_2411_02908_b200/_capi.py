@@ -118,6 +118,10 @@ _SIGS = {
                                 C.c_int, P(dbl), P(photon_err)]),
     "photon_debug_colsum": (i32, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, P(dbl),
                                   P(photon_err)]),
+    "photon_debug_ce": (i32, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_float,
+                              C.c_void_p, C.c_int, C.c_void_p, P(dbl), P(photon_err)]),
+    "photon_debug_layernorm": (i32, [C.c_int, C.c_int, C.c_int] + [C.c_void_p] * 14 +
+                               [P(dbl), P(photon_err)]),
     "photon_debug_attention": (i32, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

@@ -544,6 +544,88 @@ int photon_debug_colsum(const void* x, int x_bf16, int M, int N, float* out, dou
   });
 }
 
+// Cross-entropy forward+backward exactly as the engine runs it (tensor.cpp:544-603)
+// plus the head-bias gradient (the column sums of dlogits, tensor.cpp:279-285)
+// when dbias != NULL: fused into the CE pass where the kernel supports the shape,
+// else the engine's separate column-sum pass.
+int photon_debug_ce(void* logits, int logits_bf16, const int32_t* targets, int M, int V,
+                    float inv_count, double* rowloss, int write_grad, float* dbias, double* ms,
+                    photon_err* err) {
+  return guarded(err, [&] {
+    need(logits && targets && rowloss && M > 0 && V > 1, PHOTON_ERR_USAGE,
+         "debug_ce: bad arguments");
+    DevBuf<float> part;
+    part.reserve(std::max(k::colsum_part_floats(M, V), k::ce_bias_part_floats(V)));
+    cudaStream_t st;
+    cudaEvent_t e0, e1;
+    PH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    PH_CUDA(cudaEventCreate(&e0));
+    PH_CUDA(cudaEventCreate(&e1));
+    PH_CUDA(cudaEventRecord(e0, st));
+    if (logits_bf16) {
+      auto* l = static_cast<bf16*>(logits);
+      const bool fused = k::ce_fwd_bwd<bf16>(l, targets, M, V, inv_count, rowloss, write_grad != 0,
+                                             st, write_grad ? dbias : nullptr, part.ptr);
+      if (dbias && write_grad && !fused) k::colsum<bf16>(l, M, V, part.ptr, dbias, st);
+    } else {
+      auto* l = static_cast<float*>(logits);
+      k::ce_fwd_bwd<float>(l, targets, M, V, inv_count, rowloss, write_grad != 0, st);
+      if (dbias && write_grad) k::colsum<float>(l, M, V, part.ptr, dbias, st);
+    }
+    PH_CUDA(cudaEventRecord(e1, st));
+    PH_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    PH_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    if (ms) *ms = t;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(st);
+  });
+}
+
+// LayerNorm forward (and, with dy != NULL, backward) exactly as the engine runs
+// them (tensor.cpp:322-394): y in bf16 when y_bf16 else fp32; the backward
+// writes dx = dres + LN'(dy) (dres may be NULL), its bf16/fp32 copy dxT, the
+// gain / bias gradients and (dsum != NULL) the column sums of dx.
+int photon_debug_layernorm(int y_bf16, int M, int d, const float* x, const float* gain,
+                           const float* bias, void* y, float* mean, float* rstd, const float* dy,
+                           const float* dres, float* dx, void* dxT, float* dgain, float* dbias,
+                           float* dsum, double* ms, photon_err* err) {
+  return guarded(err, [&] {
+    need(x && gain && bias && y && mean && rstd && M > 0 && d > 0, PHOTON_ERR_USAGE,
+         "debug_layernorm: bad arguments");
+    need(!dy || (dx && dxT && dgain && dbias), PHOTON_ERR_USAGE,
+         "debug_layernorm: backward needs dx, dxT, dgain, dbias");
+    DevBuf<float> part;
+    part.reserve((size_t)k::ln_bwd_parts() * 3 * d);
+    cudaStream_t st;
+    cudaEvent_t e0, e1;
+    PH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    PH_CUDA(cudaEventCreate(&e0));
+    PH_CUDA(cudaEventCreate(&e1));
+    PH_CUDA(cudaEventRecord(e0, st));
+    if (y_bf16) {
+      k::ln_fwd<bf16>(x, gain, bias, static_cast<bf16*>(y), mean, rstd, M, d, st);
+      if (dy)
+        k::ln_bwd<bf16>(dy, x, mean, rstd, gain, dres, dx, static_cast<bf16*>(dxT), part.ptr,
+                        dgain, dbias, M, d, st, dsum);
+    } else {
+      k::ln_fwd<float>(x, gain, bias, static_cast<float*>(y), mean, rstd, M, d, st);
+      if (dy)
+        k::ln_bwd<float>(dy, x, mean, rstd, gain, dres, dx, static_cast<float*>(dxT), part.ptr,
+                         dgain, dbias, M, d, st, dsum);
+    }
+    PH_CUDA(cudaEventRecord(e1, st));
+    PH_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    PH_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    if (ms) *ms = t;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(st);
+  });
+}
+
 int photon_debug_attention(int impl, int B, int S, int H, int d, const void* q, const void* k,
                            const void* v, void* o, float* lse, const void* dO, float* scratch,
                            void* dq, void* dk, void* dv, double* ms, photon_err* err) {

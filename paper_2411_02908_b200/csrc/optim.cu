@@ -62,7 +62,10 @@ __global__ void clip_finalize_kernel(const double* __restrict__ part, int nparts
     if (norm_out) *norm_out = norm;
     const bool finite = isfinite(norm);
     if (!finite && bad_step && *bad_step == 0) *bad_step = step + 1;
-    *cf_out = (finite && clip > 0.0 && norm > clip) ? (float)(clip / norm) : 1.0f;
+    // a non-finite norm poisons cf with NaN: the optimizer kernels then leave
+    // params and moments untouched, as optim.cpp:52-54 throws before mutating
+    *cf_out = !finite ? __int_as_float(0x7fffffff)
+                      : (clip > 0.0 && norm > clip) ? (float)(clip / norm) : 1.0f;
   }
 }
 
@@ -94,6 +97,7 @@ __global__ void __launch_bounds__(256) adamw_f32_kernel(
     bf16* __restrict__ shadow, uint64_t n, const float* cfp, float lr, float b1, float b2, float ib1,
     float ib2, float eps, float wd) {
   const float cf = *cfp;
+  if (cf != cf) return;  // NumericError step: no update (clip_finalize_kernel)
   const uint64_t n4 = n / 4;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4;
        i += (uint64_t)gridDim.x * blockDim.x) {
@@ -137,6 +141,7 @@ __global__ void sgd_f32_kernel(float* __restrict__ p, const float* __restrict__ 
                                bf16* __restrict__ shadow, uint64_t n, const float* cfp,
                                double lr) {
   const double cf = (double)*cfp;
+  if (cf != cf) return;  // NumericError step: no update (clip_finalize_kernel)
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const float np = (float)((double)p[i] - lr * ((double)g[i] * cf));
@@ -242,9 +247,14 @@ __global__ void __launch_bounds__(256) aggregate_kernel(const T* const* __restri
                                                         int k, uint64_t n, T* __restrict__ theta,
                                                         T* __restrict__ vel, int kind, T eta,
                                                         T mu, int nesterov) {
-  __shared__ const T* models[kMaxModelsSmem];
-  for (int i = threadIdx.x; i < k; i += blockDim.x) models[i] = models_g[i];
+  // the pointer table is staged in shared memory when it fits; more models
+  // (ParamVector::mean has no limit) are read straight from the global table
+  __shared__ const T* models_s[kMaxModelsSmem];
+  const bool in_smem = k <= kMaxModelsSmem;
+  if (in_smem)
+    for (int i = threadIdx.x; i < k; i += blockDim.x) models_s[i] = models_g[i];
   __syncthreads();
+  const T* const* models = in_smem ? models_s : models_g;
   const T nk = (T)k;
   constexpr int V = 16 / sizeof(T);  // elements per 128-bit access
   using Vec = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
@@ -303,6 +313,7 @@ __global__ void __launch_bounds__(256) aggregate_kernel(const T* const* __restri
 // any world size); wire bytes per GPU = 2 (G-1)/G * P * 4 as for ring all-reduce.
 template <int KM>  // KM >= a.n: registers sized to the client count
 __global__ void __launch_bounds__(256) boundary_p2p_kernel(const __grid_constant__ PeerBoundaryArgs a) {
+  if (a.abort && *a.abort) return;  // a peer never arrived: PeerBoundary::check() reports it
   const int k = a.n;
   const float nk = (float)k;
   const float* const* models = a.models;
@@ -361,7 +372,7 @@ void boundary_p2p(const PeerBoundaryArgs& a, cudaStream_t st) {
 template <typename T>
 void aggregate(const T* const* models, int k, uint64_t n, T* theta, T* velocity, int kind,
                double eta, double mu, int nesterov, cudaStream_t st) {
-  if (k < 1 || k > kMaxModelsSmem) throw Error(PHOTON_ERR_USAGE, "aggregate: bad model count");
+  if (k < 1) throw Error(PHOTON_ERR_USAGE, "aggregate: bad model count");
   aggregate_kernel<T><<<kNumSMs * 4, 256, 0, st>>>(models, k, n, theta, velocity, kind, (T)eta,
                                                    (T)mu, nesterov);
   PH_LAUNCH_CHECK();
@@ -370,9 +381,12 @@ void aggregate(const T* const* models, int k, uint64_t n, T* theta, T* velocity,
 template <typename T>
 __global__ void mean_kernel(const T* const* __restrict__ models_g, int k, uint64_t n,
                             T* __restrict__ out) {
-  __shared__ const T* models[kMaxModelsSmem];
-  for (int i = threadIdx.x; i < k; i += blockDim.x) models[i] = models_g[i];
+  __shared__ const T* models_s[kMaxModelsSmem];
+  const bool in_smem = k <= kMaxModelsSmem;
+  if (in_smem)
+    for (int i = threadIdx.x; i < k; i += blockDim.x) models_s[i] = models_g[i];
   __syncthreads();
+  const T* const* models = in_smem ? models_s : models_g;
   const T nk = (T)k;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
        j += (uint64_t)gridDim.x * blockDim.x)
@@ -380,7 +394,7 @@ __global__ void mean_kernel(const T* const* __restrict__ models_g, int k, uint64
 }
 template <typename T>
 void mean_only(const T* const* models, int k, uint64_t n, T* out, cudaStream_t st) {
-  if (k < 1 || k > kMaxModelsSmem) throw Error(PHOTON_ERR_USAGE, "mean: bad model count");
+  if (k < 1) throw Error(PHOTON_ERR_USAGE, "mean: bad model count");
   mean_kernel<T><<<kNumSMs * 4, 256, 0, st>>>(models, k, n, out);
   PH_LAUNCH_CHECK();
 }

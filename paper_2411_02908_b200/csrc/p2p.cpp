@@ -22,13 +22,16 @@ namespace {
 struct FlagArgs {
   uint64_t* peer[k::kMaxPeerWorld];  // rank j's flag array, mapped here
   uint64_t* mine;
+  int* abort;  // this rank's abort word (device), checked by the host after the boundary
   uint64_t epoch;
   int rank, world;
 };
 
 // Thread j signals rank j (writes epoch into rank j's flags[rank]) and waits
 // for rank j's signal in our flags[j].  A peer that never arrives (dead rank)
-// traps after ~20 s instead of hanging the GPU.
+// sets the abort word after ~20 s and the wait ends: the boundary kernel then
+// does nothing and PeerBoundary::check() raises a host error -- no sticky
+// device fault, no hang.
 __global__ void peer_barrier_kernel(const __grid_constant__ FlagArgs a) {
   const int j = threadIdx.x;
   if (j >= a.world) return;
@@ -40,7 +43,11 @@ __global__ void peer_barrier_kernel(const __grid_constant__ FlagArgs a) {
     uint64_t v;
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a.mine + j) : "memory");
     if (v >= a.epoch) break;
-    if (clock64() - t0 > (1ll << 35)) __trap();
+    if (*(volatile int*)a.abort) break;  // another lane already gave up
+    if (clock64() - t0 > (1ll << 35)) {
+      atomicMax(a.abort, j + 1);  // 1 + the rank that did not arrive
+      break;
+    }
     __nanosleep(64);
   }
 }
@@ -52,6 +59,8 @@ PeerBoundary::PeerBoundary(ncclComm_t comm, int rank, int world, int device)
   if (world > k::kMaxPeerWorld) throw Error(PHOTON_ERR_CONFIG, "peer boundary: world too large");
   flags_.reserve(world);
   PH_CUDA(cudaMemset(flags_.ptr, 0, world * sizeof(uint64_t)));
+  abort_.reserve(1);
+  PH_CUDA(cudaMemset(abort_.ptr, 0, sizeof(int)));
   tab_dev_.reserve((size_t)world * sizeof(Table));
   models_.assign(world, {});
   thetas_.assign(world, nullptr);
@@ -149,6 +158,7 @@ void PeerBoundary::barrier(cudaStream_t st) {
   std::memset(&a, 0, sizeof(a));
   for (int q = 0; q < world_; ++q) a.peer[q] = peer_flags_[q];
   a.mine = flags_.ptr;
+  a.abort = abort_.ptr;
   a.epoch = ++epoch_;
   a.rank = rank_;
   a.world = world_;
@@ -179,11 +189,20 @@ void PeerBoundary::run(const std::vector<int>& surv, uint64_t shard, float* vel,
   a.nesterov = server.nesterov;
   a.eta = (float)server.eta;
   a.mu = (float)server.momentum;
+  a.abort = abort_.ptr;
   barrier(st);  // every rank's client models are final
   PH_CUDA(cudaEventRecord(ev0_, st));
   k::boundary_p2p(a, st);
   PH_CUDA(cudaEventRecord(ev1_, st));
   barrier(st);  // every replica holds theta_{t+1}; nobody reads our models any more
+}
+
+void PeerBoundary::check() {
+  int h = 0;
+  PH_CUDA(cudaMemcpy(&h, abort_.ptr, sizeof(int), cudaMemcpyDeviceToHost));
+  if (h)
+    throw Error(PHOTON_ERR_NCCL, "peer boundary: rank " + std::to_string(h - 1) +
+                                     " did not reach the round boundary within ~20 s");
 }
 
 }  // namespace photon

@@ -47,6 +47,9 @@ struct PeerBoundary {
   static bool fits(uint64_t bytes) { return bytes <= (uint64_t)24e9; }
   // device ms of the last run()'s fused kernel (after the opening barrier)
   float last_kernel_ms() const;
+  // after run() has completed on the stream: throws if a peer never arrived
+  // (the barrier timed out; the boundary kernel was skipped)
+  void check();
 
  private:
   struct Region {  // one exported pointer
@@ -68,6 +71,7 @@ struct PeerBoundary {
   ncclComm_t comm_;
   int rank_, world_, device_;
   DevBuf<uint64_t> flags_;  // [world]: flags_[j] = last epoch rank j signalled to us
+  DevBuf<int> abort_;       // 0, or 1 + the rank a barrier gave up on
   DevBuf<uint8_t> tab_dev_;
   uint64_t epoch_ = 0;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;

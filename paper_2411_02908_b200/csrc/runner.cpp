@@ -245,6 +245,9 @@ void Runner::run_round(photon_round_record* rec) {
     cursors[sampled[si]] += (uint64_t)tau * B;
     if (!dropouts.count({round, sampled[si]})) surv.push_back(si);
   }
+  // from here a failed round leaves the cursors advanced (aggregator.cpp:146-151):
+  // a retry must stream from them, not reuse this round's staged batches
+  if (surv.empty() || ((int)surv.size() < K && fed.topology == 2)) staged_round = ~0ULL;
   if (surv.empty())
     throw Error(PHOTON_ERR_ROUND_FAILURE, "round " + std::to_string(round) + ": no surviving clients");
   if ((int)surv.size() < K && fed.topology == 2)
@@ -267,7 +270,10 @@ void Runner::run_round(photon_round_record* rec) {
       recv = d_recv.ptr;
     }
   }
-  const bool peer = p2p && PeerBoundary::supported(n, world);
+  // every rank must take the same path: the local model count of the busiest
+  // rank (slot si lives on rank si % world) is known to all ranks from K
+  const int max_local = (K + world - 1) / world;
+  const bool peer = p2p && PeerBoundary::supported(n, world) && max_local <= k::kMaxPeerModels;
   if (peer) {
     p2p->publish(local_models.data(), (int)local_models.size(), d_theta.ptr, st);
     p2p->run(surv, shard, d_vel.ptr, server, st);
@@ -278,6 +284,7 @@ void Runner::run_round(photon_round_record* rec) {
   }
   PH_CUDA(cudaEventRecord(ev_c, st));
   PH_CUDA(cudaEventSynchronize(ev_c));
+  if (peer) p2p->check();  // a peer that never arrived: a host-side error, not a trap
   float bnd_ms = 0.f;
   if (peer) bnd_ms = p2p->last_kernel_ms();
   else PH_CUDA(cudaEventElapsedTime(&bnd_ms, ev_b2, ev_c));

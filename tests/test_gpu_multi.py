@@ -18,13 +18,22 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SCRIPT = os.path.join(ROOT, "tools", "multi_rank_check.py")
 
 
+CASES = [(s, "auto") for s in ("fedavg", "diloco", "diloco_drop", "central", "diloco_many")] + \
+        [(s, b) for s in ("fedavg", "diloco", "diloco_k8") for b in ("p2p", "nccl")]
+
+
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("server", ["fedavg", "diloco", "diloco_drop", "central"])
-def test_world_size_invariance(tmp_path, server):
+@pytest.mark.parametrize("server,boundary", CASES)
+def test_world_size_invariance(tmp_path, server, boundary):
+    """Both boundary paths (NVLink peer-memory kernel, NCCL send/recv + fused
+    update + all-gather; PHOTON_BOUNDARY forces one) and 1 / 2 local clients
+    per rank give theta bit-identical to one GPU."""
     n = min(torch.cuda.device_count(), 4)
     out1 = tmp_path / "w1.npy"
     outn = tmp_path / "wn.npy"
     env = dict(os.environ, PYTHONPATH=ROOT)
+    if boundary != "auto":
+        env["PHOTON_BOUNDARY"] = boundary
     r = subprocess.run([sys.executable, SCRIPT, str(out1), server], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr

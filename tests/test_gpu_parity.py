@@ -334,3 +334,82 @@ def test_runner_guards(F, oracle):
         F.FederationRunner(F.FederationConfig(4, 2, 1), local, F.ServerOptConfig(), plan, theta0)
     with pytest.raises(F.ConfigError):
         F.FederationRunner(F.FederationConfig(2, 3, 1), local, F.ServerOptConfig(), plan, theta0)
+
+
+@pytest.mark.parametrize("opt", [0, 1])
+def test_local_round_post_process_clip(F, oracle, opt):
+    """post_process clip-update-norm (client.cpp:96-110): the round update
+    theta_k - theta_t is rescaled to the threshold when its norm exceeds it.
+    Tolerances as test_local_round_f32 (AdamW 2e-4, SGD 1e-6 max-abs)."""
+    mc = ModelCfg(*HETERO4)
+    theta0 = oracle.init_params(mc, 1)
+    corpus = oracle.generate_corpus("web", 50000, 7, 64)
+    oplan = oracle.plan_iid(corpus, 2, 16, 7)
+    plan = F.partition_iid(corpus, 2, 16, 7)
+    tol = 2e-4 if opt == 0 else 1e-6
+    # the unclipped update norm decides which thresholds clip
+    t = TrainCfg(eta_max=2e-3, warmup_steps=16, decay_steps=160, alpha=0.1, local_steps=16,
+                 batch_size=4, opt=opt)
+    th_free, _, _ = oracle.local_round(mc, t, theta0, oplan, 1, 42, 0, 1, 16)
+    norm = float(np.linalg.norm(th_free - theta0))
+    assert norm > 0
+    for thr in (0.25 * norm, 0.9 * norm, 4.0 * norm):
+        t.post_kind, t.post_threshold = 1, thr
+        th_ref, loss_ref, _ = oracle.local_round(mc, t, theta0, oplan, 1, 42, 0, 1, 16)
+        local = _hetero4_train(F, opt=opt)
+        local.post = F.PostProcessPolicy(1, thr)
+        stream = F.BatchStream(plan, 1, 4, 16, F.stream_seed(42, 1))
+        res = F.run_local_round(theta0, stream, local, 1, 1, 16)
+        assert np.max(np.abs(res.theta - th_ref)) <= tol, thr
+        got = float(np.linalg.norm(res.theta - theta0))
+        if thr < norm:  # clipped: the update norm is the threshold
+            assert abs(got - thr) / thr <= 1e-3
+        else:           # identity branch
+            assert abs(got - norm) / norm <= 1e-3
+    local = _hetero4_train(F, opt=opt)
+    local.post = F.PostProcessPolicy(1, 0.0)
+    with pytest.raises(F.ConfigError):
+        F.run_local_round(theta0, F.BatchStream(plan, 1, 4, 16, F.stream_seed(42, 1)), local,
+                          1, 1, 16)
+
+
+def test_runner_post_process_clip(F, oracle):
+    """The clip post-process inside FederationRunner rounds (aggregator.cpp:114 ->
+    client.cpp:156): 3 rounds of DiLoCo, theta and velocity vs the oracle."""
+    mc = ModelCfg(*HETERO4)
+    theta0 = oracle.init_params(mc, 1)
+    corpus = oracle.generate_corpus("web", 200000, 7, 64)
+    oplan = oracle.plan_iid(corpus, 2, 16, 7)
+    t = TrainCfg(eta_max=2e-3, warmup_steps=16, decay_steps=160, alpha=0.1, local_steps=16,
+                 batch_size=4, post_kind=1, post_threshold=0.05)
+    server = ServerCfg(1, 0.1, 0.9, 1)
+    th_ref, vel_ref = theta0.copy(), np.zeros_like(theta0)
+    cursors = np.zeros(2, np.uint64)
+    for r in range(3):
+        oracle.run_round(mc, t, server, oplan, 2, 2, 42, r, th_ref, vel_ref, cursors)
+    local = _hetero4_train(F)
+    local.post = F.PostProcessPolicy(1, 0.05)
+    runner = F.FederationRunner(F.FederationConfig(2, 2, 3, F.Topology.kRingAllReduce, 42),
+                                local, F.ServerOptConfig(1, 0.1, 0.9, True),
+                                F.partition_iid(corpus, 2, 16, 7), theta0)
+    for _ in range(3):
+        runner.run_round()
+    assert np.max(np.abs(runner.theta() - th_ref)) <= 5e-4
+    assert np.max(np.abs(runner.velocity() - vel_ref)) <= 5e-4
+
+
+def test_f64_mean_more_models_than_smem_table(F, oracle):
+    # ParamVector::mean has no model-count limit (param_vector.cpp:127-152): past
+    # the 256-entry shared-memory pointer table the kernel reads the global table
+    rng = np.random.default_rng(7)
+    n = 1001
+    models = [rng.normal(size=n) * 0.02 for _ in range(300)]
+    assert np.array_equal(F.ParamVector.mean(models), oracle.mean(models))
+    theta = rng.normal(size=n) * 0.02
+    mean = oracle.mean(models)
+    v_ref = np.zeros(n)
+    out_ref = oracle.server_step(ServerCfg(1, 0.1, 0.9, 1), theta, oracle.sub(theta, mean), mean,
+                                 v_ref)
+    st = F.ServerOptState(F.ServerOptConfig(1, 0.1, 0.9, True), np.zeros(n))
+    assert np.array_equal(F.aggregate(models, theta, st), out_ref)
+    assert np.array_equal(st.velocity, v_ref)
