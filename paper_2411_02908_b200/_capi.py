@@ -120,7 +120,7 @@ _SIGS = {
                                   P(photon_err)]),
     "photon_debug_ce": (i32, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_float,
                               C.c_void_p, C.c_int, C.c_void_p, P(dbl), P(photon_err)]),
-    "photon_debug_layernorm": (i32, [C.c_int, C.c_int, C.c_int] + [C.c_void_p] * 14 +
+    "photon_debug_layernorm": (i32, [C.c_int, C.c_int, C.c_int] + [C.c_void_p] * 13 +
                                [P(dbl), P(photon_err)]),
     "photon_debug_attention": (i32, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

@@ -497,6 +497,8 @@ int photon_debug_gemm(int impl, int M, int N, int K, const void* A, int64_t lda,
     cudaStream_t st;
     cudaEvent_t e0, e1;
     PH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    // the inputs come from other streams (torch's): complete them first
+    PH_CUDA(cudaDeviceSynchronize());
     PH_CUDA(cudaEventCreate(&e0));
     PH_CUDA(cudaEventCreate(&e1));
     const int n = std::max(iters, 1);
@@ -528,6 +530,8 @@ int photon_debug_colsum(const void* x, int x_bf16, int M, int N, float* out, dou
     cudaStream_t st;
     cudaEvent_t e0, e1;
     PH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    // the inputs come from other streams (torch's): complete them first
+    PH_CUDA(cudaDeviceSynchronize());
     PH_CUDA(cudaEventCreate(&e0));
     PH_CUDA(cudaEventCreate(&e1));
     PH_CUDA(cudaEventRecord(e0, st));
@@ -546,8 +550,7 @@ int photon_debug_colsum(const void* x, int x_bf16, int M, int N, float* out, dou
 
 // Cross-entropy forward+backward exactly as the engine runs it (tensor.cpp:544-603)
 // plus the head-bias gradient (the column sums of dlogits, tensor.cpp:279-285)
-// when dbias != NULL: fused into the CE pass where the kernel supports the shape,
-// else the engine's separate column-sum pass.
+// when dbias != NULL: the engine's column-sum pass over the written dlogits.
 int photon_debug_ce(void* logits, int logits_bf16, const int32_t* targets, int M, int V,
                     float inv_count, double* rowloss, int write_grad, float* dbias, double* ms,
                     photon_err* err) {
@@ -555,18 +558,19 @@ int photon_debug_ce(void* logits, int logits_bf16, const int32_t* targets, int M
     need(logits && targets && rowloss && M > 0 && V > 1, PHOTON_ERR_USAGE,
          "debug_ce: bad arguments");
     DevBuf<float> part;
-    part.reserve(std::max(k::colsum_part_floats(M, V), k::ce_bias_part_floats(V)));
+    part.reserve(k::colsum_part_floats(M, V));
     cudaStream_t st;
     cudaEvent_t e0, e1;
     PH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    // the inputs come from other streams (torch's): complete them first
+    PH_CUDA(cudaDeviceSynchronize());
     PH_CUDA(cudaEventCreate(&e0));
     PH_CUDA(cudaEventCreate(&e1));
     PH_CUDA(cudaEventRecord(e0, st));
     if (logits_bf16) {
       auto* l = static_cast<bf16*>(logits);
-      const bool fused = k::ce_fwd_bwd<bf16>(l, targets, M, V, inv_count, rowloss, write_grad != 0,
-                                             st, write_grad ? dbias : nullptr, part.ptr);
-      if (dbias && write_grad && !fused) k::colsum<bf16>(l, M, V, part.ptr, dbias, st);
+      k::ce_fwd_bwd<bf16>(l, targets, M, V, inv_count, rowloss, write_grad != 0, st);
+      if (dbias && write_grad) k::colsum<bf16>(l, M, V, part.ptr, dbias, st);
     } else {
       auto* l = static_cast<float*>(logits);
       k::ce_fwd_bwd<float>(l, targets, M, V, inv_count, rowloss, write_grad != 0, st);
@@ -601,6 +605,8 @@ int photon_debug_layernorm(int y_bf16, int M, int d, const float* x, const float
     cudaStream_t st;
     cudaEvent_t e0, e1;
     PH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    // the inputs come from other streams (torch's): complete them first
+    PH_CUDA(cudaDeviceSynchronize());
     PH_CUDA(cudaEventCreate(&e0));
     PH_CUDA(cudaEventCreate(&e1));
     PH_CUDA(cudaEventRecord(e0, st));
@@ -633,6 +639,8 @@ int photon_debug_attention(int impl, int B, int S, int H, int d, const void* q, 
     cudaStream_t st;
     cudaEvent_t e0, e1;
     PH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    // the inputs come from other streams (torch's): complete them first
+    PH_CUDA(cudaDeviceSynchronize());
     PH_CUDA(cudaEventCreate(&e0));
     PH_CUDA(cudaEventCreate(&e1));
     auto Q = static_cast<const bf16*>(q), K = static_cast<const bf16*>(k),

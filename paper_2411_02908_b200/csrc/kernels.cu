@@ -1208,235 +1208,11 @@ __global__ void __launch_bounds__(kCePipeThreads + 32, 1)
   }
 }
 
-// ---- cross-entropy with the head-bias gradient fused (CTA pairs) ------------
-// The head bias gradient is the column sum of dlogits (add_bias backward,
-// tensor.cpp:279-285): a second pass over the 6.6 GB bf16 dlogits at the 125M
-// shape.  Here a 2-CTA cluster splits every row by columns: each CTA streams
-// only its half of the row (two 50 KB buffers at V = 50,368), which leaves room
-// for an fp32 column accumulator of its half (100 KB) in shared memory.  The
-// row max and the row sum are exchanged between the pair through distributed
-// shared memory (a remote store + a remote mbarrier arrive, release / acquire at
-// cluster scope), so both halves see the same (m, s) bit for bit.  Thread t owns
-// the 8-column chunks t, t + 512, ... of its half in every row, so the
-// accumulator needs no atomics; rows are visited in a fixed order per cluster
-// and the per-cluster partials are reduced in cluster order (deterministic).
-// The sums are taken over the fp32 gradient values before their bf16 rounding.
-constexpr int kCePairClusters = kNumSMs / 2;
-__host__ __device__ inline int ce_pair_half0(int V) { return (V / 8 + 1) / 2; }  // chunks of rank 0
-static size_t ce_pair_smem(int V) {
-  const size_t h = (size_t)ce_pair_half0(V);
-  return 2 * ((h * 16 + 127) & ~(size_t)127) + h * 32 + 128;
-}
-size_t ce_bias_part_floats(int V) { return (size_t)kCePairClusters * V; }
-
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "LAB_WAITC:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra LAB_WAITC;\n"
-      "}\n" ::"r"(sm100::su32(b)),
-      "r"(parity)
-      : "memory");
-}
-// value -> the peer CTA's `slot`, then one arrive on the peer's `bar`
-__device__ __forceinline__ void ce_pair_send(float* slot, uint64_t* bar, uint32_t peer, float v) {
-  uint32_t rs, rb;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rs) : "r"(sm100::su32(slot)), "r"(peer));
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(sm100::su32(bar)), "r"(peer));
-  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(rs), "f"(v) : "memory");
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
-}
-__device__ __forceinline__ void ce_cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
-                   : "memory");
-}
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCePipeThreads + 32, 1)
-    ce_pair_kernel(bf16* __restrict__ logits, const int32_t* __restrict__ targets, int M, int V,
-                   float inv_count, double* __restrict__ rowloss, float* __restrict__ part) {
-  using namespace sm100;
-  extern __shared__ __align__(128) uint8_t ce_sm[];
-  __shared__ float red_m[kCePipeWarps], red_s[kCePipeWarps];
-  __shared__ float peer_m[2], peer_s[2];  // written by the other CTA of the pair
-  uint32_t rank;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-  const uint32_t peer = rank ^ 1u;
-  const int half0 = ce_pair_half0(V), nvec = V / 8;
-  const int c0 = rank ? half0 : 0;                 // first 8-column chunk of this half
-  const int nv = rank ? nvec - half0 : half0;      // chunks in this half
-  const uint32_t bytes = (uint32_t)nv * 16;
-  const uint32_t stride = ((uint32_t)half0 * 16 + 127) & ~127u;
-  float* acc = reinterpret_cast<float*>(ce_sm + 2 * stride);  // [half0 * 8]
-  uint64_t* full = reinterpret_cast<uint64_t*>(ce_sm + 2 * stride + (size_t)half0 * 32);
-  uint64_t* done = full + 2;
-  uint64_t* xm = full + 4;  // peer's row max arrived
-  uint64_t* xs = full + 5;  // peer's row sum arrived
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int cid = blockIdx.x >> 1, G = gridDim.x >> 1;
-  if (tid == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
-    mbar_init(&done[0], kCePipeWarps);
-    mbar_init(&done[1], kCePipeWarps);
-    mbar_init(xm, 1);
-    mbar_init(xs, 1);
-    mbar_init_fence();
-  }
-  for (int i = tid; i < nv * 2; i += blockDim.x)
-    reinterpret_cast<float4*>(acc)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  __syncthreads();
-  ce_cluster_sync();  // the peer's barriers are initialised before any remote arrive
-
-  if (warp == kCePipeWarps) {  // ---------------- producer ----------------
-    if (lane == 0) {
-      for (int k = 0; k < 2; ++k) {
-        const int r = cid + k * G;
-        if (r < M) {
-          mbar_expect_tx(&full[k], bytes);
-          bulk_load(ce_sm + k * stride, logits + (size_t)r * V + (size_t)c0 * 8, bytes, &full[k]);
-        }
-      }
-      for (int i = 0;; ++i) {
-        const int r = cid + i * G;
-        if (r >= M) break;
-        const int b = i & 1;
-        mbar_wait(&done[b], (i >> 1) & 1);
-        bulk_store(logits + (size_t)r * V + (size_t)c0 * 8, ce_sm + b * stride, bytes);
-        bulk_commit();
-        const int r2 = r + 2 * G;
-        if (r2 < M) {
-          bulk_wait_read<0>();  // buffer read out before it is refilled
-          mbar_expect_tx(&full[b], bytes);
-          bulk_load(ce_sm + b * stride, logits + (size_t)r2 * V + (size_t)c0 * 8, bytes, &full[b]);
-        }
-      }
-      bulk_wait_all();
-    }
-  } else {  // ---------------- compute warps ----------------
-    constexpr float kL2e = 1.4426950408889634f;
-    for (int i = 0;; ++i) {
-      const int r = cid + i * G;
-      if (r >= M) break;
-      const int b = i & 1, par = i & 1;
-      uint8_t* buf = ce_sm + b * stride;
-      const uint32_t base = su32(buf);
-      mbar_wait(&full[b], (i >> 1) & 1);
-      // (1) max of this half, combined with the peer's
-      float m = -INFINITY;
-      for (int c = tid; c < nv; c += kCePipeThreads) {
-        float v[8];
-        ce_unpack8(lds128(base + c * 16), v);
-        m = fmaxf(m, fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])),
-                           fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7]))));
-      }
-      m = warp_max(m);
-      if (lane == 0) red_m[warp] = m;
-      named_bar_sync(1, kCePipeThreads);
-      m = red_m[0];
-#pragma unroll
-      for (int w = 1; w < kCePipeWarps; ++w) m = fmaxf(m, red_m[w]);
-      if (tid == 0) ce_pair_send(&peer_m[par], xm, peer, m);
-      const int t = targets[r];
-      const int tc = t >= 0 ? t / 8 - c0 : -1;                // target chunk within this half
-      const bool own_t = t >= 0 && tc >= 0 && tc < nv;
-      const float lt = own_t ? __bfloat162float(reinterpret_cast<const bf16*>(buf)[t - c0 * 8]) : 0.f;
-      mbar_wait_cluster(xm, par);
-      m = fmaxf(m, peer_m[par]);
-      named_bar_sync(1, kCePipeThreads);  // red_m read before reuse
-      // (2) e = exp(l - m) written back in place, sum of this half, pair sum
-      const float ml2 = m * kL2e;
-      float s = 0.f;
-      for (int c = tid; c < nv; c += kCePipeThreads) {
-        float v[8];
-        ce_unpack8(lds128(base + c * 16), v);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          v[e] = ex2_approx(fmaf(v[e], kL2e, -ml2));
-          s += v[e];
-        }
-        uint4 o;
-        o.x = pack_bf16x2(v[0], v[1]);
-        o.y = pack_bf16x2(v[2], v[3]);
-        o.z = pack_bf16x2(v[4], v[5]);
-        o.w = pack_bf16x2(v[6], v[7]);
-        sts128(base + c * 16, o);
-      }
-      s = warp_sum(s);
-      if (lane == 0) red_s[warp] = s;
-      named_bar_sync(1, kCePipeThreads);
-      s = red_s[0];
-#pragma unroll
-      for (int w = 1; w < kCePipeWarps; ++w) s += red_s[w];
-      if (tid == 0) ce_pair_send(&peer_s[par], xs, peer, s);
-      mbar_wait_cluster(xs, par);
-      s = s + peer_s[par];  // commutative: both CTAs hold the same bits
-      const bool bad = !(s == s) || m == INFINITY;
-      if (tid == 0 && (own_t || (t < 0 && rank == 0)))
-        rowloss[r] = t < 0 ? 0.0 : bad ? (double)NAN : (double)logf(s) + (double)m - (double)lt;
-      // (3) dl = e * g / s - g * onehot(t); column sums in fp32 before rounding
-      const float g = t >= 0 ? inv_count : 0.f;
-      const float gs = g / s;
-      for (int c = tid; c < nv; c += kCePipeThreads) {
-        float v[8];
-        ce_unpack8(lds128(base + c * 16), v);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) v[e] *= gs;
-        if (own_t && c == tc) {
-          const float pt = gs * ex2_approx(fmaf(lt, kL2e, -ml2)) - g;
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            if (e == t - (c0 + c) * 8) v[e] = pt;
-        }
-        uint4 o;
-        o.x = pack_bf16x2(v[0], v[1]);
-        o.y = pack_bf16x2(v[2], v[3]);
-        o.z = pack_bf16x2(v[4], v[5]);
-        o.w = pack_bf16x2(v[6], v[7]);
-        sts128(base + c * 16, o);
-        float4 lo = *reinterpret_cast<const float4*>(acc + c * 8);
-        float4 hi = *reinterpret_cast<const float4*>(acc + c * 8 + 4);
-        lo.x += v[0]; lo.y += v[1]; lo.z += v[2]; lo.w += v[3];
-        hi.x += v[4]; hi.y += v[5]; hi.z += v[6]; hi.w += v[7];
-        *reinterpret_cast<float4*>(acc + c * 8) = lo;
-        *reinterpret_cast<float4*>(acc + c * 8 + 4) = hi;
-      }
-      fence_async_smem();
-      named_bar_sync(1, kCePipeThreads);  // red_s read by every thread before the next row
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&done[b]);
-    }
-    // this cluster's column partial of its half
-    named_bar_sync(1, kCePipeThreads);
-    float4* out = reinterpret_cast<float4*>(part + (size_t)cid * V + (size_t)c0 * 8);
-    for (int i = tid; i < nv * 2; i += kCePipeThreads) out[i] = reinterpret_cast<const float4*>(acc)[i];
-  }
-  __syncwarp();
-  ce_cluster_sync();  // no remote store / arrive into this CTA still in flight
-}
-
 template <typename T>
-bool ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count, double* rowloss,
-                bool write_grad, cudaStream_t st, float* dbias, float* part) {
+void ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count, double* rowloss,
+                bool write_grad, cudaStream_t st) {
   if constexpr (sizeof(T) == 2) {
     const bool aligned = (reinterpret_cast<uintptr_t>(logits) & 15) == 0;
-    if (write_grad && dbias && part && V % 8 == 0 && V >= 2048 && aligned &&
-        ce_pair_smem(V) <= (size_t)kCePipeMaxSmem && M >= 4 * kCePairClusters) {
-      static std::atomic<uint64_t> attr{0};  // per device
-      int dev = 0;
-      PH_CUDA(cudaGetDevice(&dev));
-      if (!(attr.load() & (1ull << (dev & 63)))) {
-        PH_CUDA(cudaFuncSetAttribute(ce_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kCePipeMaxSmem));
-        attr.fetch_or(1ull << (dev & 63));
-      }
-      ce_pair_kernel<<<2 * kCePairClusters, kCePipeThreads + 32, ce_pair_smem(V), st>>>(
-          reinterpret_cast<bf16*>(logits), targets, M, V, inv_count, rowloss, part);
-      PH_LAUNCH_CHECK();
-      colreduce(part, kCePairClusters, V, V, dbias, V, nullptr, st);
-      return true;
-    }
     if (V % 8 == 0 && ce_pipe_smem(V) <= (size_t)kCePipeMaxSmem && M > 0 && aligned) {
       static std::atomic<uint64_t> attr{0};  // per device
       int dev = 0;
@@ -1449,18 +1225,17 @@ bool ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count
       ce_pipe_kernel<<<std::min(M, kNumSMs), kCePipeThreads + 32, ce_pipe_smem(V), st>>>(
           logits, targets, M, V, inv_count, rowloss, write_grad ? 1 : 0);
       PH_LAUNCH_CHECK();
-      return false;
+      return;
     }
     if (V % 8 == 0 && V <= kCeRegChunks * 8 * kCeThreads && aligned) {
       ce_reg_kernel<<<M, kCeThreads, 0, st>>>(logits, targets, V, inv_count, rowloss,
                                               write_grad ? 1 : 0);
       PH_LAUNCH_CHECK();
-      return false;
+      return;
     }
   }
   ce_kernel<T><<<M, 512, 0, st>>>(logits, targets, V, inv_count, rowloss, write_grad ? 1 : 0);
   PH_LAUNCH_CHECK();
-  return false;
 }
 
 __global__ void sum_scaled_kernel(const double* __restrict__ x, int n, double scale,
@@ -1721,8 +1496,7 @@ void f32_to_bf16(const float* in, bf16* out, uint64_t n, cudaStream_t st) {
                           const float*, float*, T*, float*, float*, float*, int, int,            \
                           cudaStream_t, float*);                                                \
   template void colsum<T>(const T*, int, int, float*, float*, cudaStream_t);                    \
-  template bool ce_fwd_bwd<T>(T*, const int32_t*, int, int, float, double*, bool, cudaStream_t, \
-                               float*, float*);                                               \
+  template void ce_fwd_bwd<T>(T*, const int32_t*, int, int, float, double*, bool, cudaStream_t); \
   template void attn_fwd_simt<T>(const T*, const T*, const T*, T*, float*, int, int, int, int,    \
                                  cudaStream_t);                                                 \
   template void attn_bwd_simt<T>(const T*, const T*, const T*, const T*, const T*, const float*,  \

@@ -44,15 +44,9 @@ void colsum_parts(const float* part, int nparts, int N, float* scratch, float* o
 // ---- softmax cross-entropy fwd+bwd (tensor.cpp:544-603) --------------------
 // logits [M,V] overwritten with dlogits = (softmax - onehot) * inv_count;
 // rowloss[m] = logsumexp - logit[target] (0 for target < 0)
-// With write_grad and dbias / part given, bf16 logits at the head's shape take
-// the CTA-pair kernel that also emits the column sums of dlogits (the head-bias
-// gradient, tensor.cpp:279-285) into dbias[V] through part
-// (>= ce_bias_part_floats(V) floats); returns whether dbias was written.
 template <typename T>
-bool ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count,
-                double* rowloss, bool write_grad, cudaStream_t st, float* dbias = nullptr,
-                float* part = nullptr);
-size_t ce_bias_part_floats(int V);
+void ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count,
+                double* rowloss, bool write_grad, cudaStream_t st);
 // out = inv_count * sum(rowloss) (fixed-order tree)
 void sum_scaled(const double* x, int n, double scale, double* out, cudaStream_t st);
 

@@ -2,9 +2,10 @@
 against a plain PyTorch fp32/f64 reference of the same op (through the C ABI's
 debug hooks, which call exactly what the engine calls):
 
-  * softmax cross-entropy at V = 50,368 (tensor.cpp:544-603) with the head-bias
-    column sums fused into the CTA-pair kernel, plus the single-CTA pipelined
-    kernel (eval / no bias) and the small-M fallback;
+  * softmax cross-entropy at V = 50,368 (tensor.cpp:544-603): the persistent
+    pipelined kernel (two 100 KB shared-memory row buffers, refills when
+    M > 148), forward-only, target padding, NaN rows, plus the head-bias
+    column sums over the written dlogits (the whole-row kernel);
   * LayerNorm forward / backward at d = 768 (the register-resident NV = 6
     kernels) and d = 4,096 (the row-split WPR = 8 kernels of the 7B config)
     (tensor.cpp:322-394);
@@ -13,8 +14,9 @@ debug hooks, which call exactly what the engine calls):
     over every band (tensor.cpp:152-207).
 
 Tolerances (stated per check below): fp32 outputs rel 1e-4 of the output
-scale; bf16 outputs one bf16 rounding (rel 1e-2 of the scale); row losses and
-fp32 column sums rel 1e-5 / 1e-4.
+scale; bf16 outputs one bf16 rounding (rel 1e-2 of the scale); row losses rel
+1e-5; fp32 column sums of fp32 inputs rel 1e-4, of bf16-rounded gradients
+(the head bias) rel 2e-3 of the largest column sum.
 """
 import ctypes as C
 
@@ -84,15 +86,16 @@ def _ce_case(M, V, write_grad, with_bias, seed=0, pad_rows=(), nan_row=None):
     # one bf16 rounding of each gradient value (rel 2^-8), abs floor for p ~ 0
     d = (got - ref_g)[ok].abs()
     assert (d <= 8e-3 * ref_g[ok].abs() + 1e-6 * scale).all(), d.max().item()
-    if with_bias:
+    if with_bias and nan_row is None:  # (a NaN row makes every column sum NaN, as in f64)
+        # sums of the bf16-rounded gradient values (rel 2^-9 each), fp32 accumulate
         ref_b = ref_g[ok].sum(0)
         eb = (dbias.double() - ref_b).abs().max().item() / (ref_b.abs().max().item() + 1e-30)
-        assert eb <= 1e-4, eb
+        assert eb <= 2e-3, eb
     return ms.value
 
 
-def test_ce_head_shape_fused_bias():
-    # M = 1,024 > 4 x 74 pairs: the CTA-pair kernel (refills, both halves)
+def test_ce_head_shape_with_bias():
+    # M = 1,024 > 148: every persistent CTA refills its row buffers
     _ce_case(1024, V125, True, True)
 
 
@@ -104,12 +107,12 @@ def test_ce_head_shape_padding_and_nan():
 
 @pytest.mark.parametrize("M", [1024, 150])
 def test_ce_head_shape_pipe_kernel(M):
-    # no bias requested: the single-CTA pipelined kernel (M < 2 x 148 included)
+    # M < 2 x 148 included (some CTAs get one row, none a refill)
     _ce_case(M, V125, True, False, seed=1)
 
 
 def test_ce_head_shape_small_m_with_bias():
-    # M below the pair kernel's minimum: CE kernel + separate column sums
+    # M below the whole-row column-sum kernel's minimum: the strip kernel
     _ce_case(200, V125, True, True, seed=2)
 
 
@@ -118,7 +121,7 @@ def test_ce_forward_only():
 
 
 def test_ce_odd_vocab_with_bias():
-    # V / 8 odd: the two halves of the pair differ by one 8-column chunk
+    # V / 8 odd
     _ce_case(640, 8 * 1001, True, True, seed=5)
 
 
