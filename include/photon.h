@@ -176,6 +176,14 @@ int photon_plan_iid(const uint16_t* tokens, uint64_t n_tokens, uint64_t n_shards
 int photon_plan_by_source(const uint16_t* const* corpora, const uint64_t* lens,
                           uint64_t n_sources, uint64_t clients_per_source, uint64_t seq_len,
                           photon_plan** out, photon_err* err);     /* data.cpp:166-199 */
+/* ShardPlan import (data.h:33-62): an existing plan's corpora and per-client
+ * block lists -- e.g. a fedsim::ShardPlan handed over by the C++ adapter.
+ * Client c owns n_blocks[c] blocks of seq_len + 1 tokens; its i-th block is
+ * (sources[j], offsets[j]) with j = n_blocks[0] + ... + n_blocks[c-1] + i. */
+int photon_plan_from_blocks(const uint16_t* const* corpora, const uint64_t* lens,
+                            uint64_t n_sources, uint64_t seq_len, const uint64_t* n_blocks,
+                            uint64_t n_clients, const uint32_t* sources, const uint64_t* offsets,
+                            photon_plan** out, photon_err* err);
 void photon_plan_free(photon_plan* p);
 uint64_t photon_plan_n_clients(const photon_plan* p);
 uint64_t photon_plan_client_blocks(const photon_plan* p, uint64_t client);

@@ -112,6 +112,8 @@ _SIGS = {
     "photon_aggregate_device_f32": (i32, [C.c_void_p, P(C.c_void_p), u64, u64, C.c_void_p,
                                           C.c_void_p, P(photon_server_cfg), P(dbl),
                                           P(photon_err)]),
+    "photon_plan_from_blocks": (i32, [P(C.c_void_p), P(u64), u64, u64, P(u64), u64,
+                                      P(C.c_uint32), P(u64), P(C.c_void_p), P(photon_err)]),
     "photon_debug_gemm": (i32, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int64,
                                 C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p,
                                 C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,

@@ -175,6 +175,33 @@ int photon_plan_by_source(const uint16_t* const* corpora, const uint64_t* lens, 
   });
 }
 
+int photon_plan_from_blocks(const uint16_t* const* corpora, const uint64_t* lens,
+                            uint64_t n_sources, uint64_t seq_len, const uint64_t* n_blocks,
+                            uint64_t n_clients, const uint32_t* sources, const uint64_t* offsets,
+                            photon_plan** out, photon_err* err) {
+  return guarded(err, [&] {
+    need(corpora && lens && n_blocks && sources && offsets && out, PHOTON_ERR_USAGE,
+         "plan_from_blocks: null argument");
+    need(n_sources >= 1 && n_sources < (1u << 15), PHOTON_ERR_CONFIG,
+         "plan_from_blocks: bad source count");
+    need(seq_len >= 1 && n_clients >= 1, PHOTON_ERR_CONFIG, "plan_from_blocks: empty plan");
+    Plan p;
+    p.seq_len = seq_len;
+    for (uint64_t s = 0; s < n_sources; ++s) p.corpora.emplace_back(corpora[s], corpora[s] + lens[s]);
+    p.blocks.assign(n_clients, {});
+    uint64_t j = 0;
+    for (uint64_t c = 0; c < n_clients; ++c) {
+      for (uint64_t i = 0; i < n_blocks[c]; ++i, ++j) {
+        need(sources[j] < n_sources, PHOTON_ERR_INDEX, "plan_from_blocks: source out of range");
+        need(offsets[j] + seq_len + 1 <= lens[sources[j]] && offsets[j] < (1ull << 48),
+             PHOTON_ERR_INDEX, "plan_from_blocks: block past the end of its corpus");
+        p.blocks[c].push_back((uint64_t)sources[j] << 48 | offsets[j]);
+      }
+    }
+    *out = new photon_plan{std::move(p)};
+  });
+}
+
 void photon_plan_free(photon_plan* p) { delete p; }
 uint64_t photon_plan_n_clients(const photon_plan* p) { return p->p.blocks.size(); }
 uint64_t photon_plan_client_blocks(const photon_plan* p, uint64_t c) {

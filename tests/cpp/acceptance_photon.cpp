@@ -1,0 +1,230 @@
+// acceptance_photon.cpp -- the reference's acceptance criteria c3 and c4
+// (proj/tests/acceptance/acceptance_main.cpp:237-337) re-run with the photon
+// drop-in substituted for the client update, the mean and the server step
+// (include/photon_fedsim.hpp over libphoton.so), against the UNMODIFIED
+// reference's run_centralized as the oracle.
+//
+// Built by oracle/Makefile (target _ref/acceptance_photon) against the
+// reference's headers and objects; run by tests/test_gpu_acceptance_cpp.py.
+// Prints one "[cN<variant>] ..." line per check, exits non-zero on failure.
+//
+//   c3  tau = 1, full participation, plain SGD, FedAvg == the union-batch
+//       centralized run (reference bound: <= 1e-9 per coordinate over 50 rounds)
+//     c3a  reference client + photon mean / server_step (f64, bit-exact entry
+//          points): <= 1e-9, as the reference
+//     c3b  photon device client round (fp32 engine) + photon mean / server_step
+//     c3c  photon FederationRunner (device-resident round)
+//   c4  one-client federation (tau = 20, AdamW, 10 rounds) == centralized with
+//       opt_reset_interval = tau (reference: bitwise)
+//     c4a  reference client + photon mean / server_step: bitwise
+//     c4b  photon FederationRunner vs photon run_centralized (both on the
+//          device): bitwise
+//     c4c  photon FederationRunner vs the reference centralized run (f64)
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "fedsim/aggregator.h"
+#include "fedsim/baselines.h"
+#include "fedsim/client.h"
+#include "fedsim/data.h"
+#include "fedsim/model.h"
+#include "fedsim/optim.h"
+#include "photon_fedsim.hpp"
+
+using namespace fedsim;
+
+namespace {
+
+// device-round tolerances (fp32 engine vs the f64 reference), stated here and
+// in DESIGN.md section 5
+constexpr double kC3Device = 2e-6;   // SGD, 50 rounds of tau = 1
+constexpr double kC4Device = 2e-4;   // AdamW, 200 steps (AdamW amplifies ulp noise)
+
+double worst_gap(const ParamVector& a, const ParamVector& b) {
+  const std::vector<double> x = a.flatten(), y = b.flatten();
+  double w = 0.0;
+  for (std::size_t i = 0; i < x.size(); ++i) w = std::max(w, std::fabs(x[i] - y[i]));
+  return w;
+}
+
+bool same_bits(const ParamVector& a, const ParamVector& b) {
+  const std::vector<double> x = a.flatten(), y = b.flatten();
+  return x.size() == y.size() && std::memcmp(x.data(), y.data(), x.size() * 8) == 0;
+}
+
+enum class ClientImpl { kReference, kPhoton };
+
+// One federated round as aggregator.cpp:93-220 composes it (ascending clients,
+// anchored mean, pseudo-gradient, server step) with the photon entry points in
+// place of the reference's mean / server_step, and either client update.
+struct Federation {
+  FederationConfig fed;
+  LocalTrainConfig local;
+  std::shared_ptr<const ShardPlan> plan;
+  ParamVector theta;
+  ServerOptState state;
+  std::vector<std::uint64_t> cursors;
+  std::size_t round = 0;
+
+  Federation(FederationConfig f, LocalTrainConfig l, ServerOptConfig s,
+             std::shared_ptr<const ShardPlan> p, ParamVector th0)
+      : fed(f), local(std::move(l)), plan(std::move(p)), theta(std::move(th0)),
+        state(ServerOptState::init(s, theta)), cursors(f.population, 0) {}
+
+  void run_round(photon_fedsim::Device& dev, ClientImpl impl) {
+    const auto ids = sample_clients(fed.population, fed.clients_per_round, fed.seed, round);
+    std::vector<ParamVector> models;
+    for (std::size_t id : ids) {
+      BatchStream stream(plan, id, local.batch_size, local.model.seq_len,
+                         stream_seed(fed.seed, id), cursors[id]);
+      const std::size_t step_base = round * local.local_steps;
+      ClientResult r = impl == ClientImpl::kReference
+                           ? run_local_round(theta, stream, local, round, id, step_base)
+                           : photon_fedsim::run_local_round(dev, theta, stream, local, round, id,
+                                                            step_base);
+      cursors[id] = r.cursor;
+      models.push_back(std::move(r.theta));
+    }
+    std::vector<const ParamVector*> ptrs;
+    for (const auto& m : models) ptrs.push_back(&m);
+    const ParamVector mean = photon_fedsim::mean(dev, ptrs);
+    const ParamVector delta = ParamVector::sub(theta, mean);
+    theta = photon_fedsim::server_step(dev, state, theta, delta, mean);
+    ++round;
+  }
+};
+
+int failures = 0;
+
+void report(const char* tag, bool ok, const char* fmt, double v) {
+  std::printf("[%s] %s ", tag, ok ? "PASS" : "FAIL");
+  std::printf(fmt, v);
+  std::printf("\n");
+  std::fflush(stdout);
+  if (!ok) ++failures;
+}
+
+// ---- c3 ------------------------------------------------------------------------
+void criterion3() {
+  ModelConfig m;
+  TransformerModel model(m);
+  auto plan = std::make_shared<const ShardPlan>(
+      partition_iid(generate_corpus("web", 40000, 7), 2, m.seq_len, 99));
+  const ParamVector theta0 = model.init_params(1);
+  LrSchedule sched;
+  sched.eta_max = 0.01;
+  sched.warmup_steps = 5;
+  sched.decay_steps = 50;
+  sched.alpha = 0.1;
+  LocalTrainConfig local;
+  local.model = m;
+  local.schedule = sched;
+  local.opt = ClientOptKind::kSgd;
+  local.sgd_clip_norm = 0.0;
+  local.local_steps = 1;
+  local.batch_size = 8;
+  FederationConfig fed;
+  fed.population = 2;
+  fed.clients_per_round = 2;
+  fed.rounds = 50;
+  fed.seed = 5;
+
+  CentralizedConfig cc;
+  cc.model = m;
+  cc.schedule = sched;
+  cc.opt = ClientOptKind::kSgd;
+  cc.sgd_clip_norm = 0.0;
+  cc.n_workers = 2;
+  cc.global_batch = 16;
+  cc.total_steps = 50;
+  std::vector<ParamVector> traj;
+  run_centralized(cc, plan, fed.seed, theta0, 1,
+                  [&](std::size_t, const ParamVector& th) { traj.push_back(th.clone()); });
+
+  photon_fedsim::Device dev64(0, m, local.batch_size, PHOTON_PREC_F32);
+  for (ClientImpl impl : {ClientImpl::kReference, ClientImpl::kPhoton}) {
+    Federation f(fed, local, ServerOptConfig{}, plan, theta0.clone());
+    double worst = 0.0;
+    for (std::size_t r = 0; r < fed.rounds; ++r) {
+      f.run_round(dev64, impl);
+      worst = std::max(worst, worst_gap(f.theta, traj[r]));
+    }
+    if (impl == ClientImpl::kReference)
+      report("c3a", worst < 1e-9, "worst per-coordinate gap %.3e (bound 1e-9)", worst);
+    else
+      report("c3b", worst < kC3Device, "worst per-coordinate gap %.3e (bound 2e-6)", worst);
+  }
+  {
+    photon_fedsim::FederationRunner runner(dev64, fed, local, ServerOptConfig{}, CostModelParams{},
+                                           plan, theta0.clone(), RunnerOptions{});
+    double worst = 0.0;
+    for (std::size_t r = 0; r < fed.rounds; ++r) {
+      runner.run_round();
+      worst = std::max(worst, worst_gap(runner.theta(), traj[r]));
+    }
+    report("c3c", worst < kC3Device && runner.done(),
+           "worst per-coordinate gap %.3e (bound 2e-6)", worst);
+  }
+}
+
+// ---- c4 ------------------------------------------------------------------------
+void criterion4() {
+  ModelConfig m;
+  TransformerModel model(m);
+  auto plan = std::make_shared<const ShardPlan>(
+      partition_iid(generate_corpus("web", 40000, 11), 1, m.seq_len, 3));
+  const ParamVector theta0 = model.init_params(1);
+  LocalTrainConfig local;
+  local.model = m;
+  local.local_steps = 20;
+  local.batch_size = 8;
+  FederationConfig fed;
+  fed.population = 1;
+  fed.clients_per_round = 1;
+  fed.rounds = 10;
+  fed.seed = 77;
+  CentralizedConfig cc;
+  cc.model = m;
+  cc.n_workers = 1;
+  cc.global_batch = 8;
+  cc.total_steps = 200;
+  cc.opt_reset_interval = 20;
+  const CentralizedResult ref = run_centralized(cc, plan, fed.seed, theta0);
+
+  photon_fedsim::Device dev(0, m, local.batch_size, PHOTON_PREC_F32);
+  {
+    Federation f(fed, local, ServerOptConfig{}, plan, theta0.clone());
+    for (std::size_t r = 0; r < fed.rounds; ++r) f.run_round(dev, ClientImpl::kReference);
+    report("c4a", same_bits(f.theta, ref.theta), "bitwise (max abs %.3e)",
+           worst_gap(f.theta, ref.theta));
+  }
+  photon_fedsim::FederationRunner runner(dev, fed, local, ServerOptConfig{}, CostModelParams{},
+                                         plan, theta0.clone(), RunnerOptions{});
+  while (!runner.done()) runner.run_round();
+  const CentralizedResult dc = photon_fedsim::run_centralized(dev, cc, plan, fed.seed, theta0);
+  report("c4b", same_bits(runner.theta(), dc.theta), "bitwise (max abs %.3e)",
+         worst_gap(runner.theta(), dc.theta));
+  const double gap = worst_gap(runner.theta(), ref.theta);
+  report("c4c", gap < kC4Device, "max abs vs the reference %.3e (bound 2e-4)", gap);
+  // the adapter's bookkeeping matches the reference runner's
+  report("c4d", runner.client_cursor(0) == ref.cursors[0] && dc.cursors[0] == ref.cursors[0],
+         "cursor %.0f", (double)runner.client_cursor(0));
+}
+
+}  // namespace
+
+int main() {
+  try {
+    criterion3();
+    criterion4();
+  } catch (const std::exception& e) {
+    std::printf("[error] %s\n", e.what());
+    return 2;
+  }
+  std::printf("%s\n", failures ? "FAILED" : "ALL PASS");
+  return failures ? 1 : 0;
+}
