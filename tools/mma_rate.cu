@@ -18,7 +18,8 @@ __device__ __forceinline__ uint64_t sw128(uint32_t saddr, uint32_t lbo, uint32_t
   return d;
 }
 
-template <int N, int FORM>  // FORM 0: SS K-major B, 1: SS MN-major B, 2: TS (A in TMEM), MN-major B
+template <int N, int FORM, int NACC = 1>  // FORM 0: SS K-major B, 1: SS MN-major B, 2: TS (A in TMEM), MN-major B
+// NACC: independent accumulators issued round-robin (1 = one dependent chain)
 __global__ void mma_kernel(int n_mma, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -56,7 +57,7 @@ __global__ void mma_kernel(int n_mma, unsigned long long* out) {
         const uint64_t ad = sw128(a + kk * 32, 16, 1024);
         asm volatile(
             "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (i % NACC) * N),
             "l"(ad), "l"(bd), "r"(idesc), "r"(1));
       }
     }
@@ -76,15 +77,16 @@ __global__ void mma_kernel(int n_mma, unsigned long long* out) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-template <int N, int FORM>
+template <int N, int FORM, int NACC = 1>
 void run(const char* name) {
   unsigned long long* d;
   unsigned long long h[2];
   cudaMalloc(&d, 16);
   const int smem = 65536 + 1024;
-  cudaFuncSetAttribute(mma_kernel<N, FORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(mma_kernel<N, FORM, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (NACC > 1) printf("(%d independent accumulators)\n", NACC);
   for (int n : {8, 64, 512}) {
-    mma_kernel<N, FORM><<<148, 128, smem>>>(n, d);
+    mma_kernel<N, FORM, NACC><<<148, 128, smem>>>(n, d);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("%s: %s\n", name, cudaGetErrorString(e)); return; }
     cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
@@ -185,5 +187,9 @@ int main() {
   run<128, 0>("SS Kmaj");
   run<128, 2>("TS MNmaj");
   run<256, 0>("SS Kmaj");
+  run<64, 0, 2>("SS Kmaj");
+  run<64, 0, 4>("SS Kmaj");
+  run<64, 1, 2>("SS MNmaj");
+  run<128, 0, 2>("SS Kmaj");
   return 0;
 }

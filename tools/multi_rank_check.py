@@ -34,6 +34,7 @@ drop = server.endswith("_drop")  # parameter server with a simulated dropout in 
 # rank holds more local models than the peer path takes: every rank
 # must agree on the NCCL path.
 POP, K = {"diloco_k8": (12, 8), "diloco_many": (40, 36)}.get(server, (6, 4))
+plan = F.partition_iid(F.generate_corpus("web", 10000 * POP, 7, 64), POP, 16, 7)
 if server == "central":  # DDP baseline: 6 workers, per-step gradient all-reduce
     ccfg = F.CentralizedConfig(model=cfg, schedule=F.LrSchedule(2e-3, 16, 160, 0.1), n_workers=6,
                                global_batch=12, total_steps=4, opt_reset_interval=2)
@@ -45,7 +46,6 @@ if server == "central":  # DDP baseline: 6 workers, per-step gradient all-reduce
         dist.barrier()
         dist.destroy_process_group()
     sys.exit(0)
-plan = F.partition_iid(F.generate_corpus("web", 10000 * POP, 7, 64), POP, 16, 7)
 es = F.EvalSet(["web"], 40, 7, cfg, 8)  # 5 batches: uneven over 2 or 4 ranks
 many = server == "diloco_many"
 topo = F.Topology.kParameterServer if (drop or many) else F.Topology.kRingAllReduce
