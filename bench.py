@@ -304,7 +304,7 @@ def run_reference_arm(args):
 def _config(args):
     shape, name, params = MODELS[args.model]
     L, d, H, e, V, S = shape
-    per_gpu = RUN[args.model][2]
+    per_gpu = args.clients_per_gpu
     server = "nesterov eta=0.1 mu=0.9"
     return {"workload": f"{name} federated round (reference architecture, {params} params)",
             "model": f"L{L} d{d} H{H} e{e} V{V} S{S}", "clients": args.gpus * per_gpu,
@@ -356,7 +356,7 @@ def run_ours(args):
     hbm, bf16_burst, bf16_sus, peak_src = _peaks()
     L, d, H, e, V, S = MODELS[args.model][0]
     model = F.ModelConfig(L, d, H, e, V, S)
-    per_gpu = RUN[args.model][2]
+    per_gpu = args.clients_per_gpu
     K = world * per_gpu  # weak scaling: clients per GPU fixed
     rounds = args.warmup + args.steps + 1
     tau, B = args.tau, args.batch
@@ -505,6 +505,8 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tau", type=int, default=None, help="local steps (default per model)")
     ap.add_argument("--batch", type=int, default=None, help="local batch (default per model)")
+    ap.add_argument("--clients-per-gpu", type=int, default=None,
+                    help="sampled clients trained per GPU each round (default per model)")
     ap.add_argument("--precision", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--agg-k", type=int, default=8)
     ap.add_argument("--no-agg", action="store_true")
@@ -517,6 +519,8 @@ def main(argv=None):
         args.tau = int(os.environ.get("PHOTON_BENCH_TAU", RUN[args.model][0]))
     if args.batch is None:
         args.batch = RUN[args.model][1]
+    if args.clients_per_gpu is None:
+        args.clients_per_gpu = RUN[args.model][2]
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

@@ -194,7 +194,10 @@ int photon_stream_next(const photon_plan* p, uint64_t client, uint64_t batch_siz
 
 /* ---- device context ------------------------------------------------------------ */
 /* One GPU's client engine for `model` at `precision`, activations sized for
- * max_batch rows of model->seq_len tokens. */
+ * max_batch rows of model->seq_len tokens.  A larger batch (a client's local
+ * batch, an eval batch) runs as micro-batches of max_batch rows whose
+ * gradients and losses accumulate into the step's (the loss stays the mean
+ * over all of the batch's targets, client.cpp:135-154). */
 int photon_ctx_create(int device, const photon_model_cfg* model, int precision,
                       uint64_t max_batch, photon_ctx** out, photon_err* err);
 void photon_ctx_destroy(photon_ctx* ctx);

@@ -84,7 +84,6 @@ void load_params(Ctx& c, const double* params) {
 void check_batch(const Ctx& c, uint64_t B, uint64_t S) {
   need(B > 0 && S > 0, PHOTON_ERR_SHAPE, "forward: inconsistent batch");
   need(S <= c.cfg.seq_len, PHOTON_ERR_SHAPE, "forward: batch seq_len exceeds model seq_len");
-  need(B <= c.max_batch, PHOTON_ERR_CAPACITY, "batch exceeds the context's max_batch");
 }
 
 }  // namespace

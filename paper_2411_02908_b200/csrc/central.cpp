@@ -57,8 +57,6 @@ Central::Central(Ctx* c, const photon_central_cfg& cf, const Plan* p, uint64_t s
     throw Error(PHOTON_ERR_USAGE, "stream: seq_len does not match the plan's block size");
   if (ws < 1 || rk < 0 || rk >= ws) throw Error(PHOTON_ERR_USAGE, "centralized: bad rank/world");
   per_worker = cf.global_batch / cf.n_workers;
-  if (per_worker > c->max_batch)
-    throw Error(PHOTON_ERR_CONFIG, "centralized: per-worker batch exceeds the context's max_batch");
   P = c->eng->P;
   shard = ((P + ws - 1) / ws + 3) / 4 * 4;
   Ppad = shard * ws;

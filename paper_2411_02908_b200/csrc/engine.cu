@@ -77,6 +77,9 @@ class EngineT final : public Engine {
   }
 
   void forward_backward(const StepBatch& b, double* loss_dev, bool backward) override;
+  // one micro-batch: rows [row0, row0 + bt.B * S) of the step's batch; acc adds
+  // every gradient (and the loss) onto the previous micro-batches'
+  void micro(const StepBatch& bt, double* loss_dev, bool backward, bool acc, int row0);
 
  private:
   ModelOffsets off_;
@@ -282,12 +285,32 @@ class EngineT final : public Engine {
   }
 };
 
+// A step's batch larger than the activation capacity (max_batch rows) runs as
+// micro-batches of at most max_batch rows: every gradient write of the later
+// micro-batches adds onto the earlier ones (GEMM Accum epilogues, accumulating
+// column reductions), the cross-entropy scale stays 1 / #targets of the whole
+// batch, so the step's loss and gradient are those of the full batch
+// (client.cpp:135-154: one mean over all local-batch targets).
 template <typename T>
 void EngineT<T>::forward_backward(const StepBatch& bt, double* loss_dev, bool backward) {
+  if ((uint64_t)bt.S > Smax_)
+    throw Error(PHOTON_ERR_SHAPE, "sequence exceeds the context's seq_len");
+  const int mb = (int)max_batch;
+  for (int r0 = 0, j = 0; r0 < bt.B; r0 += mb, ++j) {
+    StepBatch sb = bt;
+    sb.B = std::min(mb, bt.B - r0);
+    sb.tokens = bt.tokens + (size_t)r0 * bt.S;
+    sb.targets = bt.targets + (size_t)r0 * bt.S;
+    micro(sb, loss_dev, backward, j > 0, r0 * bt.S);
+  }
+}
+
+template <typename T>
+void EngineT<T>::micro(const StepBatch& bt, double* loss_dev, bool backward, bool acc, int row0) {
   const int B = bt.B, S = bt.S, M = B * S;
   const int d = (int)d_, hid = (int)hid_, V = (int)V_, H = (int)H_, L = (int)L_;
-  if ((uint64_t)B > max_batch || (uint64_t)S > Smax_)
-    throw Error(PHOTON_ERR_SHAPE, "batch exceeds the context's activation capacity");
+  // weight gradients: stored by the first micro-batch, accumulated by the rest
+  const Epi WG = acc ? Epi::Accum : Epi::Store;
   const size_t Md = (size_t)M * d, Mh = (size_t)M * hid;
   const double attn_fwd_flops = 4.0 * B * H * (d / H) * (double)S * (S + 1) / 2.0;
   const DT TT = dt_of<T>();
@@ -335,7 +358,7 @@ void EngineT<T>::forward_backward(const StepBatch& bt, double* loss_dev, bool ba
   {
     Scope sc(this, 2, 0);
     k::ce_fwd_bwd<T>(logits_, bt.targets, M, V, bt.inv_count, rowloss_, backward, stream);
-    k::sum_scaled(rowloss_, M, (double)bt.inv_count, loss_dev, stream);
+    k::sum_scaled(rowloss_, M, (double)bt.inv_count, loss_dev, stream, acc);
   }
   if (!backward) {
     collect_times();
@@ -346,21 +369,21 @@ void EngineT<T>::forward_backward(const StepBatch& bt, double* loss_dev, bool ba
   // every gradient entry is written (stored, never accumulated) by exactly one
   // kernel below -- except the position embeddings of positions this batch
   // does not reach (S < seq_len), which are zero
-  if ((uint64_t)S < Smax_)
+  if ((uint64_t)S < Smax_ && !acc)
     PH_CUDA(cudaMemsetAsync(G(off_.pos) + (size_t)S * d, 0, (Smax_ - S) * d * sizeof(float),
                             stream));
   // logits = add_bias(xf W_head, b_head)
   {
     Scope sc(this, 2, 0);
-    k::colsum<T>(logits_, M, V, part_, G(off_.head_b), stream);
+    k::colsum<T>(logits_, M, V, part_, G(off_.head_b), stream, acc);
   }
   mm(M, d, V, logits_, V, true, W(off_.head_w), V, true, dy_, d, DT::F32, Epi::Store);
-  mm(d, V, M, xf_, d, false, logits_, V, false, G(off_.head_w), V, DT::F32, Epi::Store);
+  mm(d, V, M, xf_, d, false, logits_, V, false, G(off_.head_w), V, DT::F32, WG);
   {
     Scope sc(this, 2, 0);
     // the column sums of its output are the last block's b2 gradient
     k::ln_bwd<T>(dy_, xL, meanf_, rstdf_, Pm(off_.lnfg), nullptr, dx_, dxT_, part_, G(off_.lnfg),
-                 G(off_.lnfb), M, d, stream, G(off_.blocks[L - 1].b2));
+                 G(off_.lnfb), M, d, stream, G(off_.blocks[L - 1].b2), acc);
   }
   for (int l = L - 1; l >= 0; --l) {
     const BlockOffsets& o = off_.blocks[l];
@@ -383,24 +406,24 @@ void EngineT<T>::forward_backward(const StepBatch& bt, double* loss_dev, bool ba
     }
     mm(M, hid, d, dxT_, d, true, W(o.w2), d, true, dpre_, hid, TT, Epi::GeluBwd, nullptr, nullptr,
        pre, fuse_b1 ? part_ : nullptr);
-    mm(hid, d, M, u, hid, false, dxT_, d, false, G(o.w2), d, DT::F32, Epi::Store);
+    mm(hid, d, M, u, hid, false, dxT_, d, false, G(o.w2), d, DT::F32, WG);
     {
       Scope sc(this, 2, 0);
       if (fuse_b1)
-        k::colsum_parts(part_, M / 32, hid, part_ + (size_t)(M / 32) * hid, G(o.b1), stream);
+        k::colsum_parts(part_, M / 32, hid, part_ + (size_t)(M / 32) * hid, G(o.b1), stream, acc);
       else
-        k::colsum<T>(dpre_, M, hid, part_, G(o.b1), stream);
+        k::colsum<T>(dpre_, M, hid, part_, G(o.b1), stream, acc);
     }
     mm(M, d, hid, dpre_, hid, true, W(o.w1), hid, true, dy_, d, DT::F32, Epi::Store);
-    mm(d, hid, M, h2, d, false, dpre_, hid, false, G(o.w1), hid, DT::F32, Epi::Store);
+    mm(d, hid, M, h2, d, false, dpre_, hid, false, G(o.w1), hid, DT::F32, WG);
     {
       Scope sc(this, 2, 0);
       // x_mid = x + (o Wo + bo): dbo = column sums of this output
       k::ln_bwd<T>(dy_, xm, mean2_ + (size_t)l * M, rstd2_ + (size_t)l * M, Pm(o.ln2g), dx_, dx_,
-                   dxT_, part_, G(o.ln2g), G(o.ln2b), M, d, stream, G(o.bo));
+                   dxT_, part_, G(o.ln2g), G(o.ln2b), M, d, stream, G(o.bo), acc);
     }
     mm(M, d, d, dxT_, d, true, W(o.wo), d, true, dO_, d, TT, Epi::Store);
-    mm(d, d, M, ao, d, false, dxT_, d, false, G(o.wo), d, DT::F32, Epi::Store);
+    mm(d, d, M, ao, d, false, dxT_, d, false, G(o.wo), d, DT::F32, WG);
     bool qkv_sums;
     {
       Scope sc(this, 1, 2.5 * attn_fwd_flops);
@@ -413,13 +436,13 @@ void EngineT<T>::forward_backward(const StepBatch& bt, double* loss_dev, bool ba
         const int np = B * ((S + 31) / 32);
         const size_t P = (size_t)np * d;
         float* scr = part_ + 3 * P;
-        k::colsum_parts(part_ + 2 * P, np, d, scr, G(o.bv), stream);
-        k::colsum_parts(part_ + P, np, d, scr, G(o.bk), stream);
-        k::colsum_parts(part_, np, d, scr, G(o.bq), stream);
+        k::colsum_parts(part_ + 2 * P, np, d, scr, G(o.bv), stream, acc);
+        k::colsum_parts(part_ + P, np, d, scr, G(o.bk), stream, acc);
+        k::colsum_parts(part_, np, d, scr, G(o.bq), stream, acc);
       } else {
-        k::colsum<T>(dv_, M, d, part_, G(o.bv), stream);
-        k::colsum<T>(dk_, M, d, part_, G(o.bk), stream);
-        k::colsum<T>(dq_, M, d, part_, G(o.bq), stream);
+        k::colsum<T>(dv_, M, d, part_, G(o.bv), stream, acc);
+        k::colsum<T>(dk_, M, d, part_, G(o.bk), stream, acc);
+        k::colsum<T>(dq_, M, d, part_, G(o.bq), stream, acc);
       }
     }
     // dy = dv Wv^T + dk Wk^T + dq Wq^T: one K-concatenated contraction on the
@@ -443,20 +466,21 @@ void EngineT<T>::forward_backward(const StepBatch& bt, double* loss_dev, bool ba
       mm(M, d, d, dk_, d, true, W(o.wk), d, true, dy_, d, DT::F32, Epi::Accum);
       mm(M, d, d, dq_, d, true, W(o.wq), d, true, dy_, d, DT::F32, Epi::Accum);
     }
-    mm(d, d, M, h, d, false, dv_, d, false, G(o.wv), d, DT::F32, Epi::Store);
-    mm(d, d, M, h, d, false, dk_, d, false, G(o.wk), d, DT::F32, Epi::Store);
-    mm(d, d, M, h, d, false, dq_, d, false, G(o.wq), d, DT::F32, Epi::Store);
+    mm(d, d, M, h, d, false, dv_, d, false, G(o.wv), d, DT::F32, WG);
+    mm(d, d, M, h, d, false, dk_, d, false, G(o.wk), d, DT::F32, WG);
+    mm(d, d, M, h, d, false, dq_, d, false, G(o.wq), d, DT::F32, WG);
     {
       Scope sc(this, 2, 0);
       // the output is block l-1's x_out gradient: its column sums are db2 of l-1
       k::ln_bwd<T>(dy_, x, mean1_ + (size_t)l * M, rstd1_ + (size_t)l * M, Pm(o.ln1g), dx_, dx_,
                    dxT_, part_, G(o.ln1g), G(o.ln1b), M, d, stream,
-                   l > 0 ? G(off_.blocks[l - 1].b2) : nullptr);
+                   l > 0 ? G(off_.blocks[l - 1].b2) : nullptr, acc);
     }
   }
   {
     Scope sc(this, 2, 0);
-    k::embed_bwd(dx_, bt.csr_off, bt.csr_rows, G(off_.tok), G(off_.pos), V, M, S, d, stream);
+    k::embed_bwd(dx_, bt.csr_off, bt.csr_rows, G(off_.tok), G(off_.pos), V, M, S, d, stream, row0,
+                 acc);
   }
   collect_times();
 }

@@ -43,37 +43,40 @@ void embed_fwd(const int32_t* tokens, const float* tok, const float* pos, float*
 // row), so the sum order is fixed and no atomics are needed.
 __global__ void embed_bwd_tok_kernel(const float* __restrict__ dx, const int32_t* __restrict__ off,
                                      const int32_t* __restrict__ rows, float* __restrict__ dtok,
-                                     int V, int d) {
+                                     int V, int d, int row0, int M, int acc) {
   const int warps = blockDim.x / 32, lane = threadIdx.x & 31;
   for (int v = blockIdx.x * warps + threadIdx.x / 32; v < V; v += gridDim.x * warps) {
     const int b = off[v], e = off[v + 1];
     float* out = dtok + (size_t)v * d;
     for (int j = lane; j < d; j += 32) {
-      float acc = 0.f;
-      for (int r = b; r < e; ++r) acc += dx[(size_t)rows[r] * d + j];
-      out[j] = acc;
+      float a = 0.f;
+      for (int r = b; r < e; ++r) {
+        const int m = rows[r] - row0;  // this micro-batch's rows only
+        if ((unsigned)m < (unsigned)M) a += dx[(size_t)m * d + j];
+      }
+      out[j] = acc ? out[j] + a : a;
     }
   }
 }
 __global__ void embed_bwd_pos_kernel(const float* __restrict__ dx, float* __restrict__ dpos,
-                                     int M, int S, int d) {
+                                     int M, int S, int d, int acc) {
   const size_t total = (size_t)S * d;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
     const int s = (int)(i / d), j = (int)(i % d);
-    float acc = 0.f;
-    for (int m = s; m < M; m += S) acc += dx[(size_t)m * d + j];
-    dpos[i] = acc;
+    float a = 0.f;
+    for (int m = s; m < M; m += S) a += dx[(size_t)m * d + j];
+    dpos[i] = acc ? dpos[i] + a : a;
   }
 }
 
 void embed_bwd(const float* dx, const int32_t* csr_off, const int32_t* csr_rows, float* dtok,
-               float* dpos, int V, int M, int S, int d, cudaStream_t st) {
+               float* dpos, int V, int M, int S, int d, cudaStream_t st, int row0, bool acc) {
   embed_bwd_tok_kernel<<<std::min<int>(cdiv(V, 8), kNumSMs * 16), 256, 0, st>>>(
-      dx, csr_off, csr_rows, dtok, V, d);
+      dx, csr_off, csr_rows, dtok, V, d, row0, M, acc ? 1 : 0);
   PH_LAUNCH_CHECK();
   embed_bwd_pos_kernel<<<std::min<int>(cdiv((uint64_t)S * d, 256), kNumSMs * 8), 256, 0, st>>>(
-      dx, dpos, M, S, d);
+      dx, dpos, M, S, d, acc ? 1 : 0);
   PH_LAUNCH_CHECK();
 }
 
@@ -313,7 +316,8 @@ ln_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ x,
 // ascending p, then the 8 slices are added in ascending s.  32 columns per CTA.
 __global__ void __launch_bounds__(256) colreduce_kernel(const float* __restrict__ part, int nparts,
                                                         int n, int stride, float* __restrict__ out,
-                                                        int split, float* __restrict__ out1) {
+                                                        int split, float* __restrict__ out1,
+                                                        int acc_out) {
   __shared__ float red[8][33];
   const int cl = threadIdx.x & 31, s = threadIdx.x >> 5;
   const int j = blockIdx.x * 32 + cl;
@@ -333,13 +337,14 @@ __global__ void __launch_bounds__(256) colreduce_kernel(const float* __restrict_
     float t = 0.f;
 #pragma unroll
     for (int w = 0; w < 8; ++w) t += red[w][cl];
-    if (j < split) out[j] = t;
-    else out1[j - split] = t;
+    float* o = j < split ? out + j : out1 + (j - split);
+    *o = acc_out ? *o + t : t;  // micro-batches after the first add onto the gradient
   }
 }
 static void colreduce(const float* part, int nparts, int n, int stride, float* out, int split,
-                      float* out1, cudaStream_t st) {
-  colreduce_kernel<<<cdiv(n, 32), 256, 0, st>>>(part, nparts, n, stride, out, split, out1);
+                      float* out1, cudaStream_t st, bool acc = false) {
+  colreduce_kernel<<<cdiv(n, 32), 256, 0, st>>>(part, nparts, n, stride, out, split, out1,
+                                                acc ? 1 : 0);
   PH_LAUNCH_CHECK();
 }
 
@@ -373,13 +378,14 @@ __global__ void __launch_bounds__(256) colreduce_rows_kernel(const float* __rest
 
 size_t colsum_parts_scratch_floats(int N) { return (size_t)kColsumPartGroups * N; }
 
-void colsum_parts(const float* part, int nparts, int N, float* scratch, float* out, cudaStream_t st) {
+void colsum_parts(const float* part, int nparts, int N, float* scratch, float* out, cudaStream_t st,
+                  bool acc) {
   const int groups = std::min(kColsumPartGroups, nparts);
   const int per = cdiv(nparts, groups);
   const int used = cdiv(nparts, per);
   colreduce_rows_kernel<<<dim3(cdiv(N, 32), used), 256, 0, st>>>(part, nparts, per, N, scratch);
   PH_LAUNCH_CHECK();
-  colreduce(scratch, used, N, N, out, N, nullptr, st);
+  colreduce(scratch, used, N, N, out, N, nullptr, st, acc);
 }
 
 // Register-resident variant for d = 128 * NV: one warp per row, x, dy and the
@@ -589,7 +595,7 @@ ln_bwd_split_kernel(const float* __restrict__ dy, const float* __restrict__ x,
 template <typename T>
 void ln_bwd(const float* dy, const float* x, const float* mean, const float* rstd,
             const float* gain, const float* dres, float* dx_out, T* dx_T, float* part,
-            float* dgain, float* dbias, int M, int d, cudaStream_t st, float* dsum) {
+            float* dgain, float* dbias, int M, int d, cudaStream_t st, float* dsum, bool acc) {
   const int nsum = dsum ? 3 : 2;
   switch (d) {
 #define PH_LNB(NV)                                                                         \
@@ -632,8 +638,8 @@ void ln_bwd(const float* dy, const float* x, const float* mean, const float* rst
     }
   }
   PH_LAUNCH_CHECK();
-  colreduce(part, kLnBwdBlocks, 2 * d, 3 * d, dgain, d, dbias, st);
-  if (dsum) colreduce(part + 2 * d, kLnBwdBlocks, d, 3 * d, dsum, d, nullptr, st);
+  colreduce(part, kLnBwdBlocks, 2 * d, 3 * d, dgain, d, dbias, st, acc);
+  if (dsum) colreduce(part + 2 * d, kLnBwdBlocks, d, 3 * d, dsum, d, nullptr, st, acc);
 }
 
 // ============================================================================
@@ -812,7 +818,7 @@ __global__ void __launch_bounds__(1024, 2)
 }
 
 template <typename T>
-void colsum(const T* x, int M, int N, float* part, float* out, cudaStream_t st) {
+void colsum(const T* x, int M, int N, float* part, float* out, cudaStream_t st, bool acc) {
   if constexpr (sizeof(T) == 2) {
     if (colsum_wide_ok(N, sizeof(T)) && M >= 4 * kNumSMs &&
         (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
@@ -828,7 +834,7 @@ void colsum(const T* x, int M, int N, float* part, float* out, cudaStream_t st) 
       colsum_wide_kernel<<<kNumSMs, kColsumWideThreads, smem, st>>>(
           reinterpret_cast<const bf16*>(x), M, N, part);
       PH_LAUNCH_CHECK();
-      colreduce(part, kNumSMs, N, N, out, N, nullptr, st);
+      colreduce(part, kNumSMs, N, N, out, N, nullptr, st, acc);
       return;
     }
     if (colsum_rows_ok(N, sizeof(T)) && M >= 4 * kColsumRowsCtas &&
@@ -848,7 +854,7 @@ void colsum(const T* x, int M, int N, float* part, float* out, cudaStream_t st) 
       colsum_rows_kernel<<<kColsumRowsCtas, 1024, smem, st>>>(reinterpret_cast<const bf16*>(x), M, N,
                                                               slots, part);
       PH_LAUNCH_CHECK();
-      colreduce(part, kColsumRowsCtas, N, N, out, N, nullptr, st);
+      colreduce(part, kColsumRowsCtas, N, N, out, N, nullptr, st, acc);
       return;
     }
   }
@@ -858,7 +864,7 @@ void colsum(const T* x, int M, int N, float* part, float* out, cudaStream_t st) 
   const int used = (M + rows - 1) / rows;
   colsum_part_kernel<T><<<dim3(cdiv(N, STRIP), used), 256, 0, st>>>(x, M, N, rows, part);
   PH_LAUNCH_CHECK();
-  colreduce(part, used, N, N, out, N, nullptr, st);
+  colreduce(part, used, N, N, out, N, nullptr, st, acc);
 }
 
 // ============================================================================
@@ -1239,7 +1245,7 @@ void ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count
 }
 
 __global__ void sum_scaled_kernel(const double* __restrict__ x, int n, double scale,
-                                  double* __restrict__ out) {
+                                  double* __restrict__ out, int acc_out) {
   __shared__ double sm[32];
   double acc = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) acc += x[i];
@@ -1249,12 +1255,12 @@ __global__ void sum_scaled_kernel(const double* __restrict__ x, int n, double sc
   if (threadIdx.x < 32) {
     acc = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
     acc = warp_sum(acc);
-    if (threadIdx.x == 0) *out = acc * scale;
+    if (threadIdx.x == 0) *out = acc_out ? *out + acc * scale : acc * scale;
   }
 }
 
-void sum_scaled(const double* x, int n, double scale, double* out, cudaStream_t st) {
-  sum_scaled_kernel<<<1, 1024, 0, st>>>(x, n, scale, out);
+void sum_scaled(const double* x, int n, double scale, double* out, cudaStream_t st, bool acc) {
+  sum_scaled_kernel<<<1, 1024, 0, st>>>(x, n, scale, out, acc ? 1 : 0);
   PH_LAUNCH_CHECK();
 }
 
@@ -1494,8 +1500,8 @@ void f32_to_bf16(const float* in, bf16* out, uint64_t n, cudaStream_t st) {
                           cudaStream_t);                                                        \
   template void ln_bwd<T>(const float*, const float*, const float*, const float*, const float*,   \
                           const float*, float*, T*, float*, float*, float*, int, int,            \
-                          cudaStream_t, float*);                                                \
-  template void colsum<T>(const T*, int, int, float*, float*, cudaStream_t);                    \
+                          cudaStream_t, float*, bool);                                          \
+  template void colsum<T>(const T*, int, int, float*, float*, cudaStream_t, bool);              \
   template void ce_fwd_bwd<T>(T*, const int32_t*, int, int, float, double*, bool, cudaStream_t); \
   template void attn_fwd_simt<T>(const T*, const T*, const T*, T*, float*, int, int, int, int,    \
                                  cudaStream_t);                                                 \

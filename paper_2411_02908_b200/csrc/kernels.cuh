@@ -11,9 +11,12 @@ namespace k {
 // ---- embedding (gather_rows + add, tensor.cpp:209-223, 290-320) ------------
 void embed_fwd(const int32_t* tokens, const float* tok, const float* pos, float* x, int M, int S,
                int d, cudaStream_t st);
-// deterministic scatter-add: rows sorted by token (CSR), ascending row order
+// deterministic scatter-add: rows sorted by token (CSR), ascending row order.
+// dx holds rows [row0, row0 + M) of the CSR's batch (one micro-batch); acc adds
+// onto dtok / dpos instead of overwriting them (micro-batches after the first).
 void embed_bwd(const float* dx, const int32_t* csr_off, const int32_t* csr_rows, float* dtok,
-               float* dpos, int V, int M, int S, int d, cudaStream_t st);
+               float* dpos, int V, int M, int S, int d, cudaStream_t st, int row0 = 0,
+               bool acc = false);
 
 // ---- layer norm (tensor.cpp:322-394) ---------------------------------------
 template <typename T>
@@ -27,19 +30,21 @@ void ln_fwd(const float* x, const float* gain, const float* bias, T* y, float* m
 template <typename T>
 void ln_bwd(const float* dy, const float* x, const float* mean, const float* rstd,
             const float* gain, const float* dres, float* dx_out, T* dx_T, float* part,
-            float* dgain, float* dbias, int M, int d, cudaStream_t st, float* dsum = nullptr);
+            float* dgain, float* dbias, int M, int d, cudaStream_t st, float* dsum = nullptr,
+            bool acc = false);  // acc: add dgain / dbias / dsum onto the existing values
 int ln_bwd_parts();
 
 // ---- column sums (add_bias backward, tensor.cpp:279-285) -------------------
 template <typename T>
-void colsum(const T* x, int M, int N, float* part, float* out, cudaStream_t st);
+void colsum(const T* x, int M, int N, float* part, float* out, cudaStream_t st, bool acc = false);
 size_t colsum_part_floats(int M, int N);
 // Column sums from caller-written partials part[nparts][N] (e.g. the per-32-row
 // sums a GEMM epilogue emits): fixed-order two-level reduction through
 // `scratch` (colsum_parts_scratch_floats(N) floats) into out[N].
 constexpr int kColsumPartGroups = 64;
 size_t colsum_parts_scratch_floats(int N);
-void colsum_parts(const float* part, int nparts, int N, float* scratch, float* out, cudaStream_t st);
+void colsum_parts(const float* part, int nparts, int N, float* scratch, float* out, cudaStream_t st,
+                  bool acc = false);
 
 // ---- softmax cross-entropy fwd+bwd (tensor.cpp:544-603) --------------------
 // logits [M,V] overwritten with dlogits = (softmax - onehot) * inv_count;
@@ -47,8 +52,9 @@ void colsum_parts(const float* part, int nparts, int N, float* scratch, float* o
 template <typename T>
 void ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count,
                 double* rowloss, bool write_grad, cudaStream_t st);
-// out = inv_count * sum(rowloss) (fixed-order tree)
-void sum_scaled(const double* x, int n, double scale, double* out, cudaStream_t st);
+// out = inv_count * sum(rowloss) (fixed-order tree); acc: out += ...
+void sum_scaled(const double* x, int n, double scale, double* out, cudaStream_t st,
+                bool acc = false);
 
 // ---- causal attention (tensor.cpp:436-542), SIMT fp32 math ------------------
 template <typename T>

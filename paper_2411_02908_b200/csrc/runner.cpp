@@ -67,8 +67,6 @@ Runner::Runner(Ctx* c, const photon_fed_cfg& f, const photon_train_cfg& t,
     throw Error(PHOTON_ERR_USAGE, "stream: seq_len does not match the plan's block size");
   if (std::memcmp(&t.model, &c->cfg, sizeof(photon_model_cfg)) != 0)
     throw Error(PHOTON_ERR_CONFIG, "runner: train model differs from the context's model");
-  if (t.batch_size > c->max_batch)
-    throw Error(PHOTON_ERR_CONFIG, "runner: batch_size exceeds the context's max_batch");
   if (ws < 1 || rk < 0 || rk >= ws) throw Error(PHOTON_ERR_USAGE, "runner: bad rank/world");
   check_train_cfg(t);
   validate_server(s);
@@ -375,8 +373,6 @@ void Runner::set_eval(const EvalSet& es, uint64_t every) {
   uint64_t row = 0;
   for (uint64_t b = 0; b < eval_n; ++b) {
     const uint64_t B = es.batch_sizes[b];
-    if (B > ctx->max_batch)
-      throw Error(PHOTON_ERR_CONFIG, "eval set: batch exceeds the context's max_batch");
     const int32_t* in = es.inputs.data() + row * S;
     const int32_t* tg = es.targets.data() + row * S;
     for (uint64_t i = 0; i < B * S; ++i) eval_valid[b] += tg[i] >= 0;

@@ -496,9 +496,12 @@ def _util_ctx(device: int = 0) -> Context:
 
 class TransformerModel:
     def __init__(self, cfg: ModelConfig, device: int = 0, precision: str = "f32",
-                 max_batch: int = 8):
+                 max_batch: int = 8, micro_batch: Optional[int] = None):
+        """micro_batch: activation capacity in rows -- larger batches run as
+        accumulated micro-batches; None: sized for the batch (>= max_batch)."""
         cfg.validate()
         self.cfg, self.device, self.precision, self.max_batch = cfg, device, precision, max_batch
+        self.micro_batch = micro_batch
 
     def config(self) -> ModelConfig:
         return self.cfg
@@ -523,7 +526,8 @@ class TransformerModel:
         return out
 
     def _ctx(self, batch: int) -> Context:
-        return context(self.cfg, self.device, self.precision, max(self.max_batch, batch))
+        cap = self.micro_batch or max(self.max_batch, batch)
+        return context(self.cfg, self.device, self.precision, cap)
 
     def forward_loss(self, params: np.ndarray, batch: Batch, build_grad: bool = True):
         """(loss, grads-or-None): forward_loss + backward + collect_grads."""
@@ -680,7 +684,7 @@ def sgd_step(params: np.ndarray, grads: np.ndarray, lr: float, clip_norm: float 
 
 def run_local_round(theta_t: np.ndarray, stream: BatchStream, cfg: LocalTrainConfig,
                     round: int, client_id: int, step_base: int, device: int = 0,  # noqa: A002
-                    precision: str = "f32") -> ClientResult:
+                    precision: str = "f32", micro_batch: Optional[int] = None) -> ClientResult:
     theta = _f64(theta_t)
     if len(theta) != cfg.model.param_count():
         raise ShapeError("forward: params do not match model layout")
@@ -689,7 +693,7 @@ def run_local_round(theta_t: np.ndarray, stream: BatchStream, cfg: LocalTrainCon
     inp, tgt = stream.take(tau)
     out = np.zeros_like(theta)
     metrics = (A.photon_step_metric * max(tau, 1))()
-    ctx = context(cfg.model, device, precision, cfg.batch_size)
+    ctx = context(cfg.model, device, precision, micro_batch or cfg.batch_size)
     t = cfg.c()
     try:
         _call(A.lib().photon_client_round, ctx.handle, C.byref(t), _dp(theta),
@@ -724,10 +728,15 @@ class FederationRunner:
                  plan: ShardPlan, theta0: np.ndarray, device: int = 0, precision: str = "f32",
                  rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
                  dropouts: Sequence[Tuple[int, int]] = (), eval_set: "Optional[EvalSet]" = None,
-                 eval_every: int = 0):
+                 eval_every: int = 0, micro_batch: Optional[int] = None):
+        """micro_batch: activation capacity in rows; a local batch (or eval
+        batch) above it runs as accumulated micro-batches of that many rows
+        (same loss and gradient as the whole batch).  None: the whole batch."""
         self.fed, self.local, self.server, self.plan = fed, local, server, plan
-        # the context's activations must also hold the largest eval batch
-        max_batch = max([local.batch_size] + ([eval_set.max_batch()] if eval_set else []))
+        if micro_batch:
+            max_batch = micro_batch
+        else:  # the context's activations hold the whole batch and the largest eval batch
+            max_batch = max([local.batch_size] + ([eval_set.max_batch()] if eval_set else []))
         self.ctx = context(local.model, device, precision, max_batch)
         theta0 = _f64(theta0)
         self._P = len(theta0)
@@ -815,10 +824,10 @@ class CentralizedTrainer:
 
     def __init__(self, cfg: CentralizedConfig, plan: ShardPlan, seed: int, theta0: np.ndarray,
                  device: int = 0, precision: str = "f32", rank: int = 0, world: int = 1,
-                 nccl_id: Optional[bytes] = None):
+                 nccl_id: Optional[bytes] = None, micro_batch: Optional[int] = None):
         self.cfg, self.plan = cfg, plan
         per_worker = cfg.global_batch // max(cfg.n_workers, 1)
-        self.ctx = context(cfg.model, device, precision, max(per_worker, 1))
+        self.ctx = context(cfg.model, device, precision, micro_batch or max(per_worker, 1))
         theta0 = _f64(theta0)
         self._P = len(theta0)
         h = C.c_void_p()

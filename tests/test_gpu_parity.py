@@ -413,3 +413,56 @@ def test_f64_mean_more_models_than_smem_table(F, oracle):
     st = F.ServerOptState(F.ServerOptConfig(1, 0.1, 0.9, True), np.zeros(n))
     assert np.array_equal(F.aggregate(models, theta, st), out_ref)
     assert np.array_equal(st.velocity, v_ref)
+
+
+@pytest.mark.parametrize("precision,cfg_t,B,mb", [("f32", HETERO4, 5, 2), ("f32", DEFAULT, 4, 1),
+                                                  ("bf16", WIDE256, 4, 1), ("bf16", HETERO4, 6, 4)])
+def test_micro_batched_step_matches_whole_batch(F, oracle, precision, cfg_t, B, mb):
+    """A batch above the context's activation capacity runs as accumulated
+    micro-batches (GEMM Accum epilogues, accumulating column reductions and
+    embedding scatter, one loss scale 1/#targets): same loss and gradient as
+    the whole batch (client.cpp:135-154) -- f32 within the oracle tolerances,
+    and micro vs whole within fp32 summation-order noise."""
+    mc = ModelCfg(*cfg_t)
+    params = oracle.init_params(mc, 3)
+    inp, tgt = _batch(oracle, cfg_t, B)
+    whole = F.TransformerModel(_mc(F, cfg_t), precision=precision, max_batch=B)
+    micro = F.TransformerModel(_mc(F, cfg_t), precision=precision, micro_batch=mb)
+    batch = F.Batch(inp, tgt, B, cfg_t[5])
+    lw, gw = whole.forward_loss(params, batch)
+    lm, gm = micro.forward_loss(params, batch)
+    assert abs(lm - lw) / abs(lw) <= (1e-6 if precision == "f32" else 2e-3)
+    assert _rel_l2(gm, gw) <= (1e-5 if precision == "f32" else 2e-2)
+    if precision == "f32":
+        l_ref, g_ref = oracle.forward_backward(mc, params, inp, tgt, B, cfg_t[5])
+        assert abs(lm - l_ref) / abs(l_ref) <= 1e-5
+        for name, off, shape in micro.layout():
+            n = int(np.prod(shape))
+            gr = g_ref[off:off + n]
+            if np.linalg.norm(gr) > 1e-8:
+                assert _rel_l2(gm[off:off + n], gr) <= 5e-4, name
+        # forward-only / eval through micro-batches
+        assert abs(micro.forward_loss(params, batch, build_grad=False)[0] - l_ref) / l_ref <= 1e-5
+
+
+def test_micro_batched_runner_vs_oracle(F, oracle):
+    """FederationRunner with micro_batch=1 (B=4): 3 DiLoCo rounds vs the oracle,
+    tolerances of test_runner_vs_oracle_f32."""
+    server = (1, 0.1, 0.9, 1)
+    mc = ModelCfg(*HETERO4)
+    theta0 = oracle.init_params(mc, 1)
+    corpus = oracle.generate_corpus("web", 200000, 7, 64)
+    oplan = oracle.plan_iid(corpus, 2, 16, 7)
+    t = TrainCfg(eta_max=2e-3, warmup_steps=16, decay_steps=160, alpha=0.1, local_steps=16,
+                 batch_size=4)
+    th_ref, vel_ref = theta0.copy(), np.zeros_like(theta0)
+    cursors = np.zeros(2, np.uint64)
+    for r in range(3):
+        oracle.run_round(mc, t, ServerCfg(*server), oplan, 2, 2, 42, r, th_ref, vel_ref, cursors)
+    runner = F.FederationRunner(F.FederationConfig(2, 2, 3, F.Topology.kRingAllReduce, 42),
+                                _hetero4_train(F), F.ServerOptConfig(1, 0.1, 0.9, True),
+                                F.partition_iid(corpus, 2, 16, 7), theta0, micro_batch=1)
+    for _ in range(3):
+        runner.run_round()
+    assert np.max(np.abs(runner.theta() - th_ref)) <= 5e-4
+    assert np.max(np.abs(runner.velocity() - vel_ref)) <= 5e-4
