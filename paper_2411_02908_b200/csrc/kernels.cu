@@ -312,39 +312,42 @@ ln_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ x,
 }
 
 // out[j] = sum_p part[p*stride + j] for j < n, with columns j >= split going to
-// out1[j - split].  Fixed order: slice s of 8 sums parts p = s (mod 8) in
-// ascending p, then the 8 slices are added in ascending s.  32 columns per CTA.
-__global__ void __launch_bounds__(256) colreduce_kernel(const float* __restrict__ part, int nparts,
-                                                        int n, int stride, float* __restrict__ out,
-                                                        int split, float* __restrict__ out1,
-                                                        int acc_out) {
-  __shared__ float red[8][33];
+// out1[j - split].  Fixed order: slice s of 32 sums parts p = s (mod 32) in
+// ascending p, then the 32 slices are added in ascending s.  32 columns per
+// CTA of 1024 threads, so each thread has only ~nparts/32 partials to read,
+// all issued before the first add (the partials were just written: L2 hits;
+// the kernel is latency-, not bandwidth-bound).
+__global__ void __launch_bounds__(1024) colreduce_kernel(const float* __restrict__ part, int nparts,
+                                                         int n, int stride, float* __restrict__ out,
+                                                         int split, float* __restrict__ out1,
+                                                         int acc_out) {
+  __shared__ float red[32][33];
   const int cl = threadIdx.x & 31, s = threadIdx.x >> 5;
   const int j = blockIdx.x * 32 + cl;
   float acc = 0.f;
   if (j < n) {
     int p = s;
-    for (; p + 24 < nparts; p += 32) {  // four independent loads in flight
-      const float a = part[(size_t)p * stride + j], b = part[(size_t)(p + 8) * stride + j];
-      const float c2 = part[(size_t)(p + 16) * stride + j], d2 = part[(size_t)(p + 24) * stride + j];
+    for (; p + 96 < nparts; p += 128) {  // four independent loads in flight
+      const float a = part[(size_t)p * stride + j], b = part[(size_t)(p + 32) * stride + j];
+      const float c2 = part[(size_t)(p + 64) * stride + j], d2 = part[(size_t)(p + 96) * stride + j];
       acc = (((acc + a) + b) + c2) + d2;
     }
-    for (; p < nparts; p += 8) acc += part[(size_t)p * stride + j];
+    for (; p < nparts; p += 32) acc += part[(size_t)p * stride + j];
   }
   red[s][cl] = acc;
   __syncthreads();
   if (s == 0 && j < n) {
     float t = 0.f;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) t += red[w][cl];
+    for (int w = 0; w < 32; ++w) t += red[w][cl];
     float* o = j < split ? out + j : out1 + (j - split);
     *o = acc_out ? *o + t : t;  // micro-batches after the first add onto the gradient
   }
 }
 static void colreduce(const float* part, int nparts, int n, int stride, float* out, int split,
                       float* out1, cudaStream_t st, bool acc = false) {
-  colreduce_kernel<<<cdiv(n, 32), 256, 0, st>>>(part, nparts, n, stride, out, split, out1,
-                                                acc ? 1 : 0);
+  colreduce_kernel<<<cdiv(n, 32), 1024, 0, st>>>(part, nparts, n, stride, out, split, out1,
+                                                 acc ? 1 : 0);
   PH_LAUNCH_CHECK();
 }
 
