@@ -391,21 +391,11 @@ __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
         m = mx;
       }
       if (warp == 2 && lane == 0) ATTN_TRACE(6, j);
-      // P = exp2(s*sl2 - m) as bf16 pairs, in registers (the first 64 of s[]),
-      // BEFORE waiting for PV_{j-1}: the exponentials overlap that product
-      float rs = 0.f;
-#pragma unroll
-      for (int i = 0; i < TK / 2; ++i) {
-        const float p0 = ex2(fmaf(__uint_as_float(s[2 * i]), sl2, -m));
-        const float p1 = ex2(fmaf(__uint_as_float(s[2 * i + 1]), sl2, -m));
-        rs += p0 + p1;
-        s[i] = pk(p0, p1);
-      }
       // P and O are free once PV_{j-1} retired
       if (j >= 1) mbar_wait(o_done, (j - 1) & 1);
       if (warp == 2 && lane == 0) ATTN_TRACE(7, j);
       fence_after();
-      if (__any_sync(0xffffffffu, rescale)) {  // 8 columns at a time
+      if (__any_sync(0xffffffffu, rescale)) {  // 8 columns at a time: s[] stays in registers
 #pragma unroll 1
         for (int c = 0; c < HD / 8; ++c) {
           uint32_t u[8];
@@ -417,9 +407,20 @@ __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
         }
       }
       l *= scale;
-      // -> TMEM columns [128, 192)
+      // P = exp2(s*sl2 - m) -> bf16 pairs into TMEM columns [128, 192)
+      float rs = 0.f;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) TMEM_ST16(tmem + lane_off + kColP + c * 16, (s + c * 16));
+      for (int c = 0; c < 4; ++c) {
+        uint32_t pp[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float p0 = ex2(fmaf(__uint_as_float(s[c * 32 + 2 * i]), sl2, -m));
+          const float p1 = ex2(fmaf(__uint_as_float(s[c * 32 + 2 * i + 1]), sl2, -m));
+          rs += p0 + p1;
+          pp[i] = pk(p0, p1);
+        }
+        TMEM_ST16(tmem + lane_off + kColP + c * 16, pp);
+      }
       l += rs;
       tmem_wait_st();
       fence_before();
