@@ -65,21 +65,22 @@ MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 METRIC = "tokens/s/round at 1-8 B200 (125M); FedAvg aggregate GB/s vs roofline"
 
 
-NCU_GEMM = os.path.join(ROOT, "profiles", "r01_ncu_gemm_dram.json")
+NCU_STEP = os.path.join(ROOT, "profiles", "r02_step.json")
 
 
-def _gemm_traffic():
-    """Mean DRAM bytes (read + write) per gemm_tc launch over the GEMM launches
-    of one 125M client step, from the committed ncu capture
-    (tools/capture_profiles.sh -> profiles/r01_ncu_gemm_dram.json), or None."""
+def _gemm_ncu():
+    """ncu evidence for the roofline kernel class: mean DRAM bytes (read + write)
+    per tcgen05 GEMM launch over ALL 195 GEMM launches of one 125M client step,
+    their algorithmic bytes, and the time-weighted tensor-pipe utilisation
+    (tools/capture_r02.sh -> tools/step_table.py -> profiles/r02_step.json)."""
     try:
-        with open(NCU_GEMM) as f:
-            ks = json.load(f)["kernels"]
-        n = sum(v["launches"] for k, v in ks.items() if "gemm_tc" in k)
-        b = sum(v["launches"] * v["dram_bytes_per_launch"] for k, v in ks.items() if "gemm_tc" in k)
-        return b / n if n else None
+        with open(NCU_STEP) as f:
+            g = json.load(f)["ALL GEMMs"]
+        return {"traffic": g["dram_bytes_per_launch"],
+                "algorithmic_bytes_per_launch": g["alg_bytes_per_launch"],
+                "tensor_pipe_pct_ncu": g["tensor_pipe_pct"], "launches_per_step": g["launches"]}
     except Exception:
-        return None
+        return {"traffic": None}
 
 
 def _boundary_path(n_params: int) -> str:
@@ -448,12 +449,13 @@ def run_ours(args):
     }
     if prof:
         ach = prof["gemm_flops"] / (prof["gemm_ms"] * 1e-3) / 1e12 if prof["gemm_ms"] else 0.0
-        line["roofline"] = {"kernel": "gemm_tc (tcgen05, all client-step contractions)",
-                            "bound": "tensor", "achieved": ach, "peak": bf16_sus,
-                            "unit": "TFLOP/s", "frac": ach / bf16_sus,
-                            "traffic": _gemm_traffic() if args.model == "125m" else None,
-                            "traffic_unit": "DRAM bytes per launch (ncu, mean over one step's GEMMs)",
-                            "peak_source": f"{peak_src} bf16 sustained"}
+        ncu = _gemm_ncu() if args.model == "125m" else {"traffic": None}
+        line["roofline"] = dict({"kernel": "gemm_tc (tcgen05, all client-step contractions)",
+                                 "bound": "tensor", "achieved": ach, "peak": bf16_sus,
+                                 "unit": "TFLOP/s", "frac": ach / bf16_sus},
+                                **ncu, traffic_unit="DRAM bytes per launch (ncu, mean over all "
+                                                    "195 GEMM launches of one step)",
+                                peak_source=f"{peak_src} bf16 sustained")
         line["kernel_ms_per_round"] = prof
         if prof["attn_ms"]:
             att = prof["attn_flops"] / (prof["attn_ms"] * 1e-3) / 1e12
