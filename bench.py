@@ -312,6 +312,7 @@ def _config(args):
             "clients_per_gpu": per_gpu, "local_steps": args.tau, "batch": args.batch,
             "seq_len": S, "global_batch": args.gpus * per_gpu * args.batch,
             "server_opt": server, "parallelism": f"fed{args.gpus}", "precision": args.precision,
+            "micro_batch": args.micro_batch or args.batch,
             "l2": "inputs larger than L2 (weights+activations >> 126 MB)"
             if args.model != "small" else "model and batch fit in L2 (config 1 is tiny)"}
 
@@ -375,7 +376,7 @@ def run_ours(args):
     runner = F.FederationRunner(F.FederationConfig(K, K, rounds, F.Topology.kRingAllReduce, 42),
                                 local_cfg, server, plan, theta0, device=local,
                                 precision=args.precision, rank=rank, world=world,
-                                nccl_id=nccl_id)
+                                nccl_id=nccl_id, micro_batch=args.micro_batch)
     for _ in range(args.warmup):
         runner.run_round()
 
@@ -507,6 +508,8 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tau", type=int, default=None, help="local steps (default per model)")
     ap.add_argument("--batch", type=int, default=None, help="local batch (default per model)")
+    ap.add_argument("--micro-batch", type=int, default=None,
+                    help="activation rows per micro-batch (default: the whole local batch)")
     ap.add_argument("--clients-per-gpu", type=int, default=None,
                     help="sampled clients trained per GPU each round (default per model)")
     ap.add_argument("--precision", default="bf16", choices=["bf16", "f32"])
