@@ -274,8 +274,8 @@ int photon_debug_colsum(const void* x, int x_bf16, int M, int N, float* out, dou
  * (tensor.cpp:544-603): rowloss[M] (f64) = logsumexp - logit[target]; with
  * write_grad the logits are overwritten by (softmax - onehot) * inv_count and,
  * when dbias != NULL, dbias[V] receives their column sums (the head-bias
- * gradient, tensor.cpp:279-285, the engine's column-sum pass).  *ms = device
- * time of the call. */
+ * gradient, tensor.cpp:279-285) exactly as the engine produces them.  *ms =
+ * device time of the call. */
 int photon_debug_ce(void* logits, int logits_bf16, const int32_t* targets, int M, int V,
                     float inv_count, double* rowloss, int write_grad, float* dbias, double* ms,
                     photon_err* err);

@@ -576,7 +576,8 @@ int photon_debug_colsum(const void* x, int x_bf16, int M, int N, float* out, dou
 
 // Cross-entropy forward+backward exactly as the engine runs it (tensor.cpp:544-603)
 // plus the head-bias gradient (the column sums of dlogits, tensor.cpp:279-285)
-// when dbias != NULL: the engine's column-sum pass over the written dlogits.
+// when dbias != NULL: accumulated inside the cross-entropy pass where the
+// kernel supports the shape, else the column-sum pass over the written dlogits.
 int photon_debug_ce(void* logits, int logits_bf16, const int32_t* targets, int M, int V,
                     float inv_count, double* rowloss, int write_grad, float* dbias, double* ms,
                     photon_err* err) {
@@ -584,7 +585,7 @@ int photon_debug_ce(void* logits, int logits_bf16, const int32_t* targets, int M
     need(logits && targets && rowloss && M > 0 && V > 1, PHOTON_ERR_USAGE,
          "debug_ce: bad arguments");
     DevBuf<float> part;
-    part.reserve(k::colsum_part_floats(M, V));
+    part.reserve(std::max(k::colsum_part_floats(M, V), k::ce_bias_part_floats(V)));
     cudaStream_t st;
     cudaEvent_t e0, e1;
     PH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -595,8 +596,9 @@ int photon_debug_ce(void* logits, int logits_bf16, const int32_t* targets, int M
     PH_CUDA(cudaEventRecord(e0, st));
     if (logits_bf16) {
       auto* l = static_cast<bf16*>(logits);
-      k::ce_fwd_bwd<bf16>(l, targets, M, V, inv_count, rowloss, write_grad != 0, st);
-      if (dbias && write_grad) k::colsum<bf16>(l, M, V, part.ptr, dbias, st);
+      const bool fused = k::ce_fwd_bwd<bf16>(l, targets, M, V, inv_count, rowloss, write_grad != 0,
+                                             st, write_grad ? dbias : nullptr, part.ptr);
+      if (dbias && write_grad && !fused) k::colsum<bf16>(l, M, V, part.ptr, dbias, st);
     } else {
       auto* l = static_cast<float*>(logits);
       k::ce_fwd_bwd<float>(l, targets, M, V, inv_count, rowloss, write_grad != 0, st);

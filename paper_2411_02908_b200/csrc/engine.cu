@@ -120,6 +120,7 @@ class EngineT final : public Engine {
     const uint64_t rows_bhs = max_batch * H_ * Smax_;
     size_t part_floats = std::max<size_t>((size_t)k::ln_bwd_parts() * 3 * d,
                                           std::max({k::colsum_part_floats((int)M, (int)V_),
+                                                    k::ce_bias_part_floats((int)V_),
                                                     k::colsum_part_floats((int)M, (int)hid),
                                                     k::colsum_part_floats((int)M, (int)d),
                                                     // b1 partials of the GeluBwd epilogue
@@ -311,6 +312,7 @@ void EngineT<T>::micro(const StepBatch& bt, double* loss_dev, bool backward, boo
   const int d = (int)d_, hid = (int)hid_, V = (int)V_, H = (int)H_, L = (int)L_;
   // weight gradients: stored by the first micro-batch, accumulated by the rest
   const Epi WG = acc ? Epi::Accum : Epi::Store;
+  bool head_b_done = false;
   const size_t Md = (size_t)M * d, Mh = (size_t)M * hid;
   const double attn_fwd_flops = 4.0 * B * H * (d / H) * (double)S * (S + 1) / 2.0;
   const DT TT = dt_of<T>();
@@ -357,7 +359,10 @@ void EngineT<T>::micro(const StepBatch& bt, double* loss_dev, bool backward, boo
   mm(M, V, d, xf_, d, true, W(off_.head_w), V, false, logits_, V, TT, Epi::Bias, Pm(off_.head_b));
   {
     Scope sc(this, 2, 0);
-    k::ce_fwd_bwd<T>(logits_, bt.targets, M, V, bt.inv_count, rowloss_, backward, stream);
+    // the head-bias gradient (column sums of dlogits) comes out of the
+    // cross-entropy pass where the kernel supports the shape
+    head_b_done = k::ce_fwd_bwd<T>(logits_, bt.targets, M, V, bt.inv_count, rowloss_, backward,
+                                   stream, backward ? G(off_.head_b) : nullptr, part_, acc);
     k::sum_scaled(rowloss_, M, (double)bt.inv_count, loss_dev, stream, acc);
   }
   if (!backward) {
@@ -373,7 +378,7 @@ void EngineT<T>::micro(const StepBatch& bt, double* loss_dev, bool backward, boo
     PH_CUDA(cudaMemsetAsync(G(off_.pos) + (size_t)S * d, 0, (Smax_ - S) * d * sizeof(float),
                             stream));
   // logits = add_bias(xf W_head, b_head)
-  {
+  if (!head_b_done) {
     Scope sc(this, 2, 0);
     k::colsum<T>(logits_, M, V, part_, G(off_.head_b), stream, acc);
   }

@@ -1076,12 +1076,23 @@ __device__ __forceinline__ void ce_combine(float& m, float& s, float m2, float s
   m = mm;
 }
 
+// bias_part != nullptr (backward): the head-bias gradient -- the column sums of
+// dlogits (add_bias backward, tensor.cpp:279-285) -- accumulates in TENSOR
+// memory, the one on-chip store this kernel leaves free (shared memory holds
+// the two row buffers): thread t owns the 8-column chunks t + 512 j of every
+// row, kept in its own TMEM lane (lane quarter w % 4 of warp w, columns
+// 128 (w / 4) + 8 j), so the sums need no atomics and no second pass over the
+// 6.6 GB of bf16 dlogits.  Summed in fp32 before the bf16 rounding, rows in a
+// fixed order per CTA; bias_part[blockIdx.x][V] is reduced in CTA order.
+constexpr int kCeBiasMaxChunks = 16;  // per thread: V <= 512 * 16 * 8
 __global__ void __launch_bounds__(kCePipeThreads + 32, 1)
     ce_pipe_kernel(bf16* __restrict__ logits, const int32_t* __restrict__ targets, int M, int V,
-                   float inv_count, double* __restrict__ rowloss, int write_grad) {
+                   float inv_count, double* __restrict__ rowloss, int write_grad,
+                   float* __restrict__ bias_part) {
   using namespace sm100;
   extern __shared__ __align__(128) uint8_t ce_sm[];
   __shared__ float red_m[kCePipeWarps], red_s[kCePipeWarps];
+  __shared__ uint32_t tmem_slot;
   const uint32_t row_bytes = (uint32_t)V * 2, stride = ce_pipe_buf_stride(V);
   uint64_t* full = reinterpret_cast<uint64_t*>(ce_sm + 2 * stride);
   uint64_t* done = full + 2;
@@ -1094,7 +1105,21 @@ __global__ void __launch_bounds__(kCePipeThreads + 32, 1)
     mbar_init(&done[1], kCePipeWarps);
     mbar_init_fence();
   }
+  const bool bias = bias_part != nullptr;
+  if (bias && warp == 0) tmem_alloc(&tmem_slot, 512);
+  tmem_fence_before();
   __syncthreads();
+  tmem_fence_after();
+  const int nvec = V / 8;
+  // this thread's TMEM accumulator columns (chunk j at tacc + 8 j); the chunk
+  // loops are warp-uniform because tcgen05.ld / st are .sync.aligned
+  const uint32_t tacc = bias ? tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + 128 * (warp >> 2) : 0;
+  const int warp_chunks = (nvec - warp * 32 + kCePipeThreads - 1) / kCePipeThreads;  // j range
+  if (bias && warp < kCePipeWarps) {
+    const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int j = 0; j < warp_chunks; ++j) tmem_st8(tacc + 8 * j, z);
+    tmem_wait_st();
+  }
 
   if (warp == kCePipeWarps) {  // ---------------- producer ----------------
     if (lane == 0) {
@@ -1123,11 +1148,10 @@ __global__ void __launch_bounds__(kCePipeThreads + 32, 1)
       }
       bulk_wait_all();
     }
-    return;
-  }
-
+    if (!bias) return;
+    __syncwarp();
+  } else {
   // ---------------- compute warps ----------------
-  const int nvec = V / 8;
   constexpr float kL2e = 1.4426950408889634f;
   for (int i = 0;; ++i) {
     const int r = blockIdx.x + i * G;
@@ -1190,36 +1214,70 @@ __global__ void __launch_bounds__(kCePipeThreads + 32, 1)
     if (write_grad) {
       const float g = t >= 0 ? inv_count : 0.f;
       const float gs = g / s;
-      for (int c = tid; c < nvec; c += kCePipeThreads) {
-        float v[8];
-        ce_unpack8(lds128(base + c * 16), v);
+      for (int j = 0; j < warp_chunks; ++j) {
+        const int c = tid + j * kCePipeThreads;
+        float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (c < nvec) {
+          ce_unpack8(lds128(base + c * 16), v);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) v[e] *= gs;
-        const int te = t - c * 8;  // target column within this chunk (if any)
-        if ((unsigned)te < 8u) {
-          const float pt = gs * ex2_approx(fmaf(lt, kL2e, -ml2)) - g;
+          for (int e = 0; e < 8; ++e) v[e] *= gs;
+          const int te = t - c * 8;  // target column within this chunk (if any)
+          if ((unsigned)te < 8u) {
+            const float pt = gs * ex2_approx(fmaf(lt, kL2e, -ml2)) - g;
 #pragma unroll
-          for (int e = 0; e < 8; ++e)
-            if (e == te) v[e] = pt;
+            for (int e = 0; e < 8; ++e)
+              if (e == te) v[e] = pt;
+          }
+          uint4 o;
+          o.x = pack_bf16x2(v[0], v[1]);
+          o.y = pack_bf16x2(v[2], v[3]);
+          o.z = pack_bf16x2(v[4], v[5]);
+          o.w = pack_bf16x2(v[6], v[7]);
+          sts128(base + c * 16, o);
         }
-        uint4 o;
-        o.x = pack_bf16x2(v[0], v[1]);
-        o.y = pack_bf16x2(v[2], v[3]);
-        o.z = pack_bf16x2(v[4], v[5]);
-        o.w = pack_bf16x2(v[6], v[7]);
-        sts128(base + c * 16, o);
+        if (bias) {  // column sums in fp32, before the bf16 rounding
+          float a[8];
+          tmem_ld8_wait(tacc + 8 * j, a);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) a[e] += v[e];
+          tmem_st8(tacc + 8 * j, a);
+        }
       }
+      if (bias) tmem_wait_st();  // this row's sums land before the next row reads them
       fence_async_smem();
     }
     named_bar_sync(1, kCePipeThreads);  // red_s read by every thread before the next row
     __syncwarp();
     if (lane == 0) mbar_arrive(&done[b]);
   }
+  if (bias) {  // this CTA's column partial
+    for (int j = 0; j < warp_chunks; ++j) {
+      const int c = tid + j * kCePipeThreads;
+      float a[8];
+      tmem_ld8_wait(tacc + 8 * j, a);
+      if (c < nvec) {
+        float4* o = reinterpret_cast<float4*>(bias_part + (size_t)blockIdx.x * V + (size_t)c * 8);
+        o[0] = make_float4(a[0], a[1], a[2], a[3]);
+        o[1] = make_float4(a[4], a[5], a[6], a[7]);
+      }
+    }
+  }
+  }  // compute warps
+  if (bias) {
+    tmem_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+      tmem_fence_after();
+      tmem_dealloc(tmem_slot, 512);
+    }
+  }
 }
 
+size_t ce_bias_part_floats(int V) { return (size_t)kNumSMs * V; }
+
 template <typename T>
-void ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count, double* rowloss,
-                bool write_grad, cudaStream_t st) {
+bool ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count, double* rowloss,
+                bool write_grad, cudaStream_t st, float* dbias, float* part, bool acc) {
   if constexpr (sizeof(T) == 2) {
     const bool aligned = (reinterpret_cast<uintptr_t>(logits) & 15) == 0;
     if (V % 8 == 0 && ce_pipe_smem(V) <= (size_t)kCePipeMaxSmem && M > 0 && aligned) {
@@ -1231,20 +1289,24 @@ void ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count
                                      kCePipeMaxSmem));
         attr.fetch_or(1ull << (dev & 63));
       }
-      ce_pipe_kernel<<<std::min(M, kNumSMs), kCePipeThreads + 32, ce_pipe_smem(V), st>>>(
-          logits, targets, M, V, inv_count, rowloss, write_grad ? 1 : 0);
+      const bool fuse = write_grad && dbias && part && V / 8 <= kCePipeThreads * kCeBiasMaxChunks;
+      const int grid = std::min(M, kNumSMs);
+      ce_pipe_kernel<<<grid, kCePipeThreads + 32, ce_pipe_smem(V), st>>>(
+          logits, targets, M, V, inv_count, rowloss, write_grad ? 1 : 0, fuse ? part : nullptr);
       PH_LAUNCH_CHECK();
-      return;
+      if (fuse) colreduce(part, grid, V, V, dbias, V, nullptr, st, acc);
+      return fuse;
     }
     if (V % 8 == 0 && V <= kCeRegChunks * 8 * kCeThreads && aligned) {
       ce_reg_kernel<<<M, kCeThreads, 0, st>>>(logits, targets, V, inv_count, rowloss,
                                               write_grad ? 1 : 0);
       PH_LAUNCH_CHECK();
-      return;
+      return false;
     }
   }
   ce_kernel<T><<<M, 512, 0, st>>>(logits, targets, V, inv_count, rowloss, write_grad ? 1 : 0);
   PH_LAUNCH_CHECK();
+  return false;
 }
 
 __global__ void sum_scaled_kernel(const double* __restrict__ x, int n, double scale,
@@ -1505,7 +1567,8 @@ void f32_to_bf16(const float* in, bf16* out, uint64_t n, cudaStream_t st) {
                           const float*, float*, T*, float*, float*, float*, int, int,            \
                           cudaStream_t, float*, bool);                                          \
   template void colsum<T>(const T*, int, int, float*, float*, cudaStream_t, bool);              \
-  template void ce_fwd_bwd<T>(T*, const int32_t*, int, int, float, double*, bool, cudaStream_t); \
+  template bool ce_fwd_bwd<T>(T*, const int32_t*, int, int, float, double*, bool, cudaStream_t, \
+                               float*, float*, bool);                                         \
   template void attn_fwd_simt<T>(const T*, const T*, const T*, T*, float*, int, int, int, int,    \
                                  cudaStream_t);                                                 \
   template void attn_bwd_simt<T>(const T*, const T*, const T*, const T*, const T*, const float*,  \

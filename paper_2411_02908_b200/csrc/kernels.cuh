@@ -49,9 +49,15 @@ void colsum_parts(const float* part, int nparts, int N, float* scratch, float* o
 // ---- softmax cross-entropy fwd+bwd (tensor.cpp:544-603) --------------------
 // logits [M,V] overwritten with dlogits = (softmax - onehot) * inv_count;
 // rowloss[m] = logsumexp - logit[target] (0 for target < 0)
+// With write_grad and dbias / part (>= ce_bias_part_floats(V) floats), the
+// bf16 pipelined kernel also produces the head-bias gradient dbias[V] (the
+// column sums of dlogits; acc adds onto dbias) and returns true; false: the
+// caller takes the column sums itself.
 template <typename T>
-void ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count,
-                double* rowloss, bool write_grad, cudaStream_t st);
+bool ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count,
+                double* rowloss, bool write_grad, cudaStream_t st, float* dbias = nullptr,
+                float* part = nullptr, bool acc = false);
+size_t ce_bias_part_floats(int V);
 // out = inv_count * sum(rowloss) (fixed-order tree); acc: out += ...
 void sum_scaled(const double* x, int n, double scale, double* out, cudaStream_t st,
                 bool acc = false);

@@ -4,8 +4,9 @@ debug hooks, which call exactly what the engine calls):
 
   * softmax cross-entropy at V = 50,368 (tensor.cpp:544-603): the persistent
     pipelined kernel (two 100 KB shared-memory row buffers, refills when
-    M > 148), forward-only, target padding, NaN rows, plus the head-bias
-    column sums over the written dlogits (the whole-row kernel);
+    M > 148), forward-only, target padding, NaN rows, with the head-bias
+    column sums accumulated in tensor memory inside the same pass (fp32, before
+    the bf16 rounding) and, where that does not apply, the column-sum kernels;
   * LayerNorm forward / backward at d = 768 (the register-resident NV = 6
     kernels) and d = 4,096 (the row-split WPR = 8 kernels of the 7B config)
     (tensor.cpp:322-394);
@@ -38,7 +39,7 @@ def _A():
 # ---------------------------------------------------------------------------
 # cross-entropy (+ fused head-bias gradient)
 # ---------------------------------------------------------------------------
-def _ce_case(M, V, write_grad, with_bias, seed=0, pad_rows=(), nan_row=None):
+def _ce_case(M, V, write_grad, with_bias, seed=0, pad_rows=(), nan_row=None, fused_bias=True):
     A = _A()
     g = torch.Generator(device="cuda").manual_seed(seed)
     logits = (torch.randn(M, V, device="cuda", generator=g) * 2.0).bfloat16()
@@ -87,10 +88,11 @@ def _ce_case(M, V, write_grad, with_bias, seed=0, pad_rows=(), nan_row=None):
     d = (got - ref_g)[ok].abs()
     assert (d <= 8e-3 * ref_g[ok].abs() + 1e-6 * scale).all(), d.max().item()
     if with_bias and nan_row is None:  # (a NaN row makes every column sum NaN, as in f64)
-        # sums of the bf16-rounded gradient values (rel 2^-9 each), fp32 accumulate
+        # fused: fp32 sums of the unrounded values (rel 1e-4); the separate
+        # column-sum pass adds the bf16-rounded values (rel 2^-9 each)
         ref_b = ref_g[ok].sum(0)
         eb = (dbias.double() - ref_b).abs().max().item() / (ref_b.abs().max().item() + 1e-30)
-        assert eb <= 2e-3, eb
+        assert eb <= (1e-4 if fused_bias else 2e-3), eb
     return ms.value
 
 
@@ -112,7 +114,7 @@ def test_ce_head_shape_pipe_kernel(M):
 
 
 def test_ce_head_shape_small_m_with_bias():
-    # M below the whole-row column-sum kernel's minimum: the strip kernel
+    # M = 200: some persistent CTAs own two rows, most one
     _ce_case(200, V125, True, True, seed=2)
 
 

@@ -1,6 +1,6 @@
 """Time the cross-entropy pass at the 125M head shape (M = 65,536, V = 50,368):
-the CTA-pair kernel with the fused head-bias column sums vs the single-CTA
-pipelined kernel followed by the separate column-sum pass (photon_debug_ce /
+with the head-bias column sums accumulated inside it (tensor memory) vs the
+pass without them followed by the separate column-sum kernel (photon_debug_ce /
 photon_debug_colsum, device time per call, median of 5)."""
 import ctypes as C
 import os
@@ -45,5 +45,5 @@ def run(fused):
 a = run(False)
 b = run(True)
 gb = 2 * M * V * 2 / 1e9
-print(f"pipe + colsum: {a:.3f} ms   pair (fused bias): {b:.3f} ms   "
+print(f"CE + column-sum pass: {a:.3f} ms   CE with fused bias sums: {b:.3f} ms   "
       f"(CE algorithmic {gb:.1f} GB -> {gb / b:.0f} GB/s fused)")
