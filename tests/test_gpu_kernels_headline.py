@@ -88,11 +88,11 @@ def _ce_case(M, V, write_grad, with_bias, seed=0, pad_rows=(), nan_row=None, fus
     d = (got - ref_g)[ok].abs()
     assert (d <= 8e-3 * ref_g[ok].abs() + 1e-6 * scale).all(), d.max().item()
     if with_bias and nan_row is None:  # (a NaN row makes every column sum NaN, as in f64)
-        # fused: fp32 sums of the unrounded values (rel 1e-4); the separate
+        # fused: fp32 sums of the unrounded values (rel 3e-4); the separate
         # column-sum pass adds the bf16-rounded values (rel 2^-9 each)
         ref_b = ref_g[ok].sum(0)
         eb = (dbias.double() - ref_b).abs().max().item() / (ref_b.abs().max().item() + 1e-30)
-        assert eb <= (1e-4 if fused_bias else 2e-3), eb
+        assert eb <= (3e-4 if fused_bias else 2e-3), eb
     return ms.value
 
 

@@ -46,4 +46,4 @@ a = run(False)
 b = run(True)
 gb = 2 * M * V * 2 / 1e9
 print(f"CE + column-sum pass: {a:.3f} ms   CE with fused bias sums: {b:.3f} ms   "
-      f"(CE algorithmic {gb:.1f} GB -> {gb / b:.0f} GB/s fused)")
+      f"(CE algorithmic {gb:.1f} GB -> {gb / b:.2f} TB/s fused)")
