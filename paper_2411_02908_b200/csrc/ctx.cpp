@@ -2,6 +2,9 @@
 #include "ctx.hpp"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
 
 #include <cmath>
 
@@ -44,6 +47,7 @@ void RoundBatches::finalize(int V) {
 Ctx::Ctx(int dev, const photon_model_cfg& m, int prec, uint64_t mb)
     : device(dev), cfg(m), precision(prec), max_batch(mb) {
   validate_model(m);
+  if (const char* g = std::getenv("PHOTON_GRAPHS")) graphs_on = std::string(g) != "0";
   PH_CUDA(cudaSetDevice(dev));
   PH_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   PH_CUDA(cudaEventCreate(&ev0));
@@ -53,6 +57,8 @@ Ctx::Ctx(int dev, const photon_model_cfg& m, int prec, uint64_t mb)
 }
 
 Ctx::~Ctx() {
+  for (auto& kv : graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   eng.reset();
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
@@ -85,6 +91,10 @@ void DeviceBatches::upload(const RoundBatches& rb, int V, cudaStream_t st) {
   PH_CUDA(cudaMemcpyAsync(csr_off.ptr, rb.csr_off.ptr, rb.tau * (size_t)(V + 1) * 4,
                           cudaMemcpyHostToDevice, st));
   PH_CUDA(cudaMemcpyAsync(csr_rows.ptr, rb.csr_rows.ptr, rb.tau * M * 4, cudaMemcpyHostToDevice, st));
+  // pageable source: staged by the call, so the host vector may change after it returns
+  inv_dev.reserve(std::max(rb.tau, 1));
+  PH_CUDA(cudaMemcpyAsync(inv_dev.ptr, rb.inv_count.data(), rb.tau * sizeof(float),
+                          cudaMemcpyHostToDevice, st));
 }
 
 void Ctx::upload(const RoundBatches& rb) { dev_batches.upload(rb, (int)cfg.vocab_size, stream); }
@@ -106,11 +116,13 @@ void check_train_cfg(const photon_train_cfg& t) {
 
 // run_local_round (client.cpp:125-158) on the device: theta copy, fresh AdamW
 // state, tau x {forward, backward, clip, AdamW/SGD}, post-process.  Losses stay
-// on the device until the caller reads them once per round.
-void Ctx::launch_local_round(const photon_train_cfg& t, const DeviceBatches& db,
-                             const float* d_theta_in, float* d_theta_out, uint64_t step_base,
-                             double* d_loss, int* d_flag) {
-  Engine& e = *eng;
+// on the device until the caller reads them once per round.  lr_dev (optional):
+// the per-step learning rates on the device, read instead of the host values.
+static void enqueue_local_round(Ctx& c, const photon_train_cfg& t, const DeviceBatches& db,
+                                const float* d_theta_in, float* d_theta_out, uint64_t step_base,
+                                double* d_loss, int* d_flag, const double* lr_dev) {
+  Engine& e = *c.eng;
+  cudaStream_t stream = c.stream;
   const uint64_t P = e.P;
   if (d_theta_in != e.master)
     PH_CUDA(cudaMemcpyAsync(e.master, d_theta_in, P * 4, cudaMemcpyDeviceToDevice, stream));
@@ -118,7 +130,7 @@ void Ctx::launch_local_round(const photon_train_cfg& t, const DeviceBatches& db,
   PH_CUDA(cudaMemsetAsync(e.mom, 0, P * 4, stream));
   PH_CUDA(cudaMemsetAsync(e.vel2, 0, P * 4, stream));
   PH_CUDA(cudaMemsetAsync(e.bad_step, 0, sizeof(int), stream));
-  const size_t M = (size_t)db.B * db.S, V = cfg.vocab_size;
+  const size_t M = (size_t)db.B * db.S, V = c.cfg.vocab_size;
   const double b1 = t.adamw.beta1, b2 = t.adamw.beta2;
   for (int i = 0; i < db.tau; ++i) {
     StepBatch sb;
@@ -129,14 +141,15 @@ void Ctx::launch_local_round(const photon_train_cfg& t, const DeviceBatches& db,
     sb.B = db.B;
     sb.S = db.S;
     sb.inv_count = db.inv_count[i];
+    sb.inv_count_dev = lr_dev ? db.inv_dev.ptr + i : nullptr;
     e.forward_backward(sb, d_loss + i, true);
     const double lr = lr_at(t.schedule, step_base + i);
     if (t.opt == 0) {
       const double stepc = (double)(i + 1);  // fresh state each round: step_count = i+1
       e.adamw(t.adamw.clip_norm, lr, b1, b2, 1.0 - std::pow(b1, stepc), 1.0 - std::pow(b2, stepc),
-              t.adamw.eps, t.adamw.weight_decay, i);
+              t.adamw.eps, t.adamw.weight_decay, i, lr_dev ? lr_dev + i : nullptr);
     } else {
-      e.sgd(t.sgd_clip_norm, lr, i);
+      e.sgd(t.sgd_clip_norm, lr, i, lr_dev ? lr_dev + i : nullptr);
     }
   }
   if (t.post_kind == 1)
@@ -144,6 +157,59 @@ void Ctx::launch_local_round(const photon_train_cfg& t, const DeviceBatches& db,
   if (d_theta_out != e.master)
     PH_CUDA(cudaMemcpyAsync(d_theta_out, e.master, P * 4, cudaMemcpyDeviceToDevice, stream));
   PH_CUDA(cudaMemcpyAsync(d_flag, e.bad_step, sizeof(int), cudaMemcpyDeviceToDevice, stream));
+}
+
+void Ctx::launch_local_round(const photon_train_cfg& t, const DeviceBatches& db,
+                             const float* d_theta_in, float* d_theta_out, uint64_t step_base,
+                             double* d_loss, int* d_flag) {
+  if (!graphs_on || eng->timing || db.tau < 1) {
+    enqueue_local_round(*this, t, db, d_theta_in, d_theta_out, step_base, d_loss, d_flag, nullptr);
+    return;
+  }
+  d_lr.reserve(std::max(db.tau, 64));  // before the key: a reserve that moves it re-keys
+  // everything the captured launches depend on, except the per-round data that
+  // lives in device memory (tokens, targets, CSR, 1/#targets, lr)
+  char key[512];
+  std::snprintf(key, sizeof(key), "%p %p %p %p %p %p %p %p %p %p %d %d %d %d %d %.17g %.17g %.17g "
+                "%.17g %.17g %.17g %.17g %d %.17g",
+                (const void*)d_lr.ptr,
+                (const void*)db.tokens.ptr, (const void*)db.targets.ptr, (const void*)db.csr_off.ptr,
+                (const void*)db.csr_rows.ptr, (const void*)db.inv_dev.ptr, (const void*)d_theta_in,
+                (const void*)d_theta_out, (const void*)d_loss, (const void*)d_flag, db.tau, db.B,
+                db.S, (int)t.opt, (int)t.post_kind, t.adamw.beta1, t.adamw.beta2, t.adamw.eps,
+                t.adamw.weight_decay, t.adamw.clip_norm, t.sgd_clip_norm, t.post_threshold,
+                (int)max_batch, t.schedule.eta_max);
+  std::vector<double> lr(db.tau);
+  for (int i = 0; i < db.tau; ++i) lr[i] = lr_at(t.schedule, step_base + i);
+  RoundGraph& g = graphs[key];
+  // per-round device scalars: pageable source, staged by the call
+  PH_CUDA(cudaMemcpyAsync(d_lr.ptr, lr.data(), db.tau * sizeof(double), cudaMemcpyHostToDevice,
+                          stream));
+  if (!g.exec && g.seen++ >= 1) {
+    cudaGraph_t graph = nullptr;
+    PH_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueue_local_round(*this, t, db, d_theta_in, d_theta_out, step_base, d_loss, d_flag,
+                          d_lr.ptr);
+    } catch (...) {
+      cudaStreamEndCapture(stream, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      graphs_on = false;  // this context stays eager from here on
+      throw;
+    }
+    PH_CUDA(cudaStreamEndCapture(stream, &graph));
+    const cudaError_t ie = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) {
+      cudaGetLastError();
+      g.exec = nullptr;
+      graphs_on = false;
+    }
+  }
+  if (g.exec) PH_CUDA(cudaGraphLaunch(g.exec, stream));
+  else enqueue_local_round(*this, t, db, d_theta_in, d_theta_out, step_base, d_loss, d_flag,
+                           d_lr.ptr);
 }
 
 constexpr uint64_t kStageChunk = 1ull << 24;  // 16 M values = 128 MB of f64 staging

@@ -2,7 +2,9 @@
 // and the device-resident client update (run_local_round, client.cpp:125-158).
 #pragma once
 
+#include <map>
 #include <memory>
+#include <string>
 #include <utility>
 #include <vector>
 
@@ -81,6 +83,7 @@ struct RoundBatches {
 struct DeviceBatches {
   DevBuf<int32_t> tokens, targets, csr_off, csr_rows;
   std::vector<float> inv_count;
+  DevBuf<float> inv_dev;  // inv_count on the device (read by graph-captured rounds)
   int tau = 0, B = 0, S = 0;
   void upload(const RoundBatches& rb, int V, cudaStream_t st);
 };
@@ -111,6 +114,17 @@ struct Ctx {
   DevBuf<double> d_f64a, d_f64b, d_f64c, d_f64d;
   DevBuf<float> d_f32a, d_f32b;
   DevBuf<const void*> d_ptrs;
+  // CUDA graphs of the local round (launch-bound small models): one executable
+  // graph per (buffers, shapes, hyper-parameters) key, captured on the second
+  // launch with that key (the first runs eagerly: lazy allocations and kernel
+  // attributes happen outside capture); lr per step comes from d_lr
+  struct RoundGraph {
+    cudaGraphExec_t exec = nullptr;
+    int seen = 0;
+  };
+  std::map<std::string, RoundGraph> graphs;
+  bool graphs_on = true;
+  DevBuf<double> d_lr;
 
   Ctx(int dev, const photon_model_cfg& m, int prec, uint64_t mb);
   ~Ctx();

@@ -28,18 +28,19 @@ Engine::Engine(const photon_model_cfg& c, int prec, uint64_t mb, cudaStream_t st
     : cfg(c), precision(prec), max_batch(mb), P(param_count(c)), stream(st) {}
 
 void Engine::adamw(double clip, double lr, double b1, double b2, double bc1, double bc2,
-                   double eps, double wd, int step) {
+                   double eps, double wd, int step, const double* lr_dev) {
   if (timing) times.launches += 3;
   k::sumsq_parts(grads, P, red_part, stream);
   k::clip_finalize(red_part, clip, norm, cf, bad_step, step, stream);
-  k::adamw_f32(master, grads, mom, vel2, shadow, P, cf, lr, b1, b2, bc1, bc2, eps, wd, stream);
+  k::adamw_f32(master, grads, mom, vel2, shadow, P, cf, lr, b1, b2, bc1, bc2, eps, wd, stream,
+               lr_dev);
 }
 
-void Engine::sgd(double clip, double lr, int step) {
+void Engine::sgd(double clip, double lr, int step, const double* lr_dev) {
   if (timing) times.launches += 3;
   k::sumsq_parts(grads, P, red_part, stream);
   k::clip_finalize(red_part, clip, norm, cf, bad_step, step, stream);
-  k::sgd_f32(master, grads, shadow, P, cf, lr, stream);
+  k::sgd_f32(master, grads, shadow, P, cf, lr, stream, lr_dev);
 }
 
 namespace {
@@ -362,8 +363,9 @@ void EngineT<T>::micro(const StepBatch& bt, double* loss_dev, bool backward, boo
     // the head-bias gradient (column sums of dlogits) comes out of the
     // cross-entropy pass where the kernel supports the shape
     head_b_done = k::ce_fwd_bwd<T>(logits_, bt.targets, M, V, bt.inv_count, rowloss_, backward,
-                                   stream, backward ? G(off_.head_b) : nullptr, part_, acc);
-    k::sum_scaled(rowloss_, M, (double)bt.inv_count, loss_dev, stream, acc);
+                                   stream, backward ? G(off_.head_b) : nullptr, part_, acc,
+                                   bt.inv_count_dev);
+    k::sum_scaled(rowloss_, M, (double)bt.inv_count, loss_dev, stream, acc, bt.inv_count_dev);
   }
   if (!backward) {
     collect_times();

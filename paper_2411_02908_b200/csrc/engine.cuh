@@ -18,6 +18,7 @@ struct StepBatch {
   const int32_t* csr_rows = nullptr;  // [B*S] row ids sorted by (token, row)
   int B = 0, S = 0;
   float inv_count = 0.f;              // 1 / #targets >= 0
+  const float* inv_count_dev = nullptr;  // the same on the device (graph-captured rounds)
 };
 
 // Per-kernel-class device time accumulated when timing is enabled.
@@ -61,9 +62,10 @@ class Engine {
   // loss (scaled mean) to *loss_dev; grads when backward
   virtual void forward_backward(const StepBatch& b, double* loss_dev, bool backward) = 0;
   // AdamW / SGD with the global-norm clip (optim.cpp:50-103); scalars from host
+  // lr_dev (optional): lr read from device memory (graph-captured rounds)
   void adamw(double clip, double lr, double b1, double b2, double bc1, double bc2, double eps,
-             double wd, int step);
-  void sgd(double clip, double lr, int step);
+             double wd, int step, const double* lr_dev = nullptr);
+  void sgd(double clip, double lr, int step, const double* lr_dev = nullptr);
 
  protected:
   Engine(const photon_model_cfg& c, int prec, uint64_t mb, cudaStream_t st);

@@ -878,8 +878,9 @@ void colsum(const T* x, int M, int N, float* part, float* out, cudaStream_t st, 
 template <typename T>
 __global__ void __launch_bounds__(512) ce_kernel(T* __restrict__ logits,
                                                  const int32_t* __restrict__ targets, int V,
-                                                 float inv_count, double* __restrict__ rowloss,
-                                                 int write_grad) {
+                                                 float inv_v, double* __restrict__ rowloss,
+                                                 int write_grad, const float* inv_dev) {
+  const float inv_count = inv_dev ? *inv_dev : inv_v;
   __shared__ float red_m[16], red_s[16];
   const int row = blockIdx.x;
   T* l = logits + (size_t)row * V;
@@ -950,9 +951,10 @@ __global__ void __launch_bounds__(512) ce_kernel(T* __restrict__ logits,
 constexpr int kCeThreads = 256, kCeRegChunks = 26;  // V <= 53248
 __global__ void __launch_bounds__(kCeThreads) ce_reg_kernel(bf16* __restrict__ logits,
                                                             const int32_t* __restrict__ targets,
-                                                            int V, float inv_count,
+                                                            int V, float inv_v,
                                                             double* __restrict__ rowloss,
-                                                            int write_grad) {
+                                                            int write_grad, const float* inv_dev) {
+  const float inv_count = inv_dev ? *inv_dev : inv_v;
   __shared__ float red[kCeThreads / 32];
   __shared__ float bcast;
   const int row = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1087,8 +1089,9 @@ __device__ __forceinline__ void ce_combine(float& m, float& s, float m2, float s
 constexpr int kCeBiasMaxChunks = 16;  // per thread: V <= 512 * 16 * 8
 __global__ void __launch_bounds__(kCePipeThreads + 32, 1)
     ce_pipe_kernel(bf16* __restrict__ logits, const int32_t* __restrict__ targets, int M, int V,
-                   float inv_count, double* __restrict__ rowloss, int write_grad,
-                   float* __restrict__ bias_part) {
+                   float inv_v, double* __restrict__ rowloss, int write_grad,
+                   float* __restrict__ bias_part, const float* inv_dev) {
+  const float inv_count = inv_dev ? *inv_dev : inv_v;
   using namespace sm100;
   extern __shared__ __align__(128) uint8_t ce_sm[];
   __shared__ float red_m[kCePipeWarps], red_s[kCePipeWarps];
@@ -1277,7 +1280,8 @@ size_t ce_bias_part_floats(int V) { return (size_t)kNumSMs * V; }
 
 template <typename T>
 bool ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count, double* rowloss,
-                bool write_grad, cudaStream_t st, float* dbias, float* part, bool acc) {
+                bool write_grad, cudaStream_t st, float* dbias, float* part, bool acc,
+                const float* inv_dev) {
   if constexpr (sizeof(T) == 2) {
     const bool aligned = (reinterpret_cast<uintptr_t>(logits) & 15) == 0;
     if (V % 8 == 0 && ce_pipe_smem(V) <= (size_t)kCePipeMaxSmem && M > 0 && aligned) {
@@ -1292,25 +1296,28 @@ bool ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count
       const bool fuse = write_grad && dbias && part && V / 8 <= kCePipeThreads * kCeBiasMaxChunks;
       const int grid = std::min(M, kNumSMs);
       ce_pipe_kernel<<<grid, kCePipeThreads + 32, ce_pipe_smem(V), st>>>(
-          logits, targets, M, V, inv_count, rowloss, write_grad ? 1 : 0, fuse ? part : nullptr);
+          logits, targets, M, V, inv_count, rowloss, write_grad ? 1 : 0, fuse ? part : nullptr,
+          inv_dev);
       PH_LAUNCH_CHECK();
       if (fuse) colreduce(part, grid, V, V, dbias, V, nullptr, st, acc);
       return fuse;
     }
     if (V % 8 == 0 && V <= kCeRegChunks * 8 * kCeThreads && aligned) {
       ce_reg_kernel<<<M, kCeThreads, 0, st>>>(logits, targets, V, inv_count, rowloss,
-                                              write_grad ? 1 : 0);
+                                              write_grad ? 1 : 0, inv_dev);
       PH_LAUNCH_CHECK();
       return false;
     }
   }
-  ce_kernel<T><<<M, 512, 0, st>>>(logits, targets, V, inv_count, rowloss, write_grad ? 1 : 0);
+  ce_kernel<T><<<M, 512, 0, st>>>(logits, targets, V, inv_count, rowloss, write_grad ? 1 : 0,
+                                  inv_dev);
   PH_LAUNCH_CHECK();
   return false;
 }
 
-__global__ void sum_scaled_kernel(const double* __restrict__ x, int n, double scale,
-                                  double* __restrict__ out, int acc_out) {
+__global__ void sum_scaled_kernel(const double* __restrict__ x, int n, double scale_v,
+                                  double* __restrict__ out, int acc_out, const float* scale_dev) {
+  const double scale = scale_dev ? (double)*scale_dev : scale_v;
   __shared__ double sm[32];
   double acc = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) acc += x[i];
@@ -1324,8 +1331,9 @@ __global__ void sum_scaled_kernel(const double* __restrict__ x, int n, double sc
   }
 }
 
-void sum_scaled(const double* x, int n, double scale, double* out, cudaStream_t st, bool acc) {
-  sum_scaled_kernel<<<1, 1024, 0, st>>>(x, n, scale, out, acc ? 1 : 0);
+void sum_scaled(const double* x, int n, double scale, double* out, cudaStream_t st, bool acc,
+                const float* scale_dev) {
+  sum_scaled_kernel<<<1, 1024, 0, st>>>(x, n, scale, out, acc ? 1 : 0, scale_dev);
   PH_LAUNCH_CHECK();
 }
 
@@ -1568,7 +1576,7 @@ void f32_to_bf16(const float* in, bf16* out, uint64_t n, cudaStream_t st) {
                           cudaStream_t, float*, bool);                                          \
   template void colsum<T>(const T*, int, int, float*, float*, cudaStream_t, bool);              \
   template bool ce_fwd_bwd<T>(T*, const int32_t*, int, int, float, double*, bool, cudaStream_t, \
-                               float*, float*, bool);                                         \
+                               float*, float*, bool, const float*);                           \
   template void attn_fwd_simt<T>(const T*, const T*, const T*, T*, float*, int, int, int, int,    \
                                  cudaStream_t);                                                 \
   template void attn_bwd_simt<T>(const T*, const T*, const T*, const T*, const T*, const float*,  \

@@ -53,14 +53,15 @@ void colsum_parts(const float* part, int nparts, int N, float* scratch, float* o
 // bf16 pipelined kernel also produces the head-bias gradient dbias[V] (the
 // column sums of dlogits; acc adds onto dbias) and returns true; false: the
 // caller takes the column sums itself.
+// inv_dev (optional): 1 / #targets read from device memory instead of inv_count.
 template <typename T>
 bool ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count,
                 double* rowloss, bool write_grad, cudaStream_t st, float* dbias = nullptr,
-                float* part = nullptr, bool acc = false);
+                float* part = nullptr, bool acc = false, const float* inv_dev = nullptr);
 size_t ce_bias_part_floats(int V);
 // out = inv_count * sum(rowloss) (fixed-order tree); acc: out += ...
 void sum_scaled(const double* x, int n, double scale, double* out, cudaStream_t st,
-                bool acc = false);
+                bool acc = false, const float* scale_dev = nullptr);
 
 // ---- causal attention (tensor.cpp:436-542), SIMT fp32 math ------------------
 template <typename T>
@@ -106,11 +107,13 @@ int sumsq_nparts();
 void clip_finalize(const double* part, double clip, double* norm_out, float* cf_out,
                    int* bad_step, int step, cudaStream_t st);
 // AdamW (optim.cpp:61-90) in f64 arithmetic over fp32 storage
+// lr_dev (optional): the learning rate read from device memory instead of `lr`
+// (CUDA-graph replays of a local round, whose lr changes every round)
 void adamw_f32(float* p, const float* g, float* m, float* v, bf16* shadow, uint64_t n,
                const float* cf, double lr, double b1, double b2, double bc1, double bc2,
-               double eps, double wd, cudaStream_t st);
+               double eps, double wd, cudaStream_t st, const double* lr_dev = nullptr);
 void sgd_f32(float* p, const float* g, bf16* shadow, uint64_t n, const float* cf, double lr,
-             cudaStream_t st);
+             cudaStream_t st, const double* lr_dev = nullptr);
 // exact f64 variants for the f64 C-ABI (bit-exact vs the reference)
 void sumsq_sequential_f64(const double* g, uint64_t n, double* out, cudaStream_t st);
 void adamw_f64(double* p, const double* g, double* m, double* v, uint64_t n, const double* norm,

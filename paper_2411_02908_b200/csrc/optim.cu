@@ -94,10 +94,11 @@ __device__ __forceinline__ void adamw_elem(float& p, float g, float& m, float& v
 
 __global__ void __launch_bounds__(256) adamw_f32_kernel(
     float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v,
-    bf16* __restrict__ shadow, uint64_t n, const float* cfp, float lr, float b1, float b2, float ib1,
-    float ib2, float eps, float wd) {
+    bf16* __restrict__ shadow, uint64_t n, const float* cfp, float lr_v, const double* lr_dev,
+    float b1, float b2, float ib1, float ib2, float eps, float wd) {
   const float cf = *cfp;
   if (cf != cf) return;  // NumericError step: no update (clip_finalize_kernel)
+  const float lr = lr_dev ? (float)*lr_dev : lr_v;  // device lr: graph-captured rounds
   const uint64_t n4 = n / 4;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4;
        i += (uint64_t)gridDim.x * blockDim.x) {
@@ -129,8 +130,8 @@ __global__ void __launch_bounds__(256) adamw_f32_kernel(
 
 void adamw_f32(float* p, const float* g, float* m, float* v, bf16* shadow, uint64_t n,
                const float* cf, double lr, double b1, double b2, double bc1, double bc2,
-               double eps, double wd, cudaStream_t st) {
-  adamw_f32_kernel<<<kNumSMs * 8, 256, 0, st>>>(p, g, m, v, shadow, n, cf, (float)lr, (float)b1,
+               double eps, double wd, cudaStream_t st, const double* lr_dev) {
+  adamw_f32_kernel<<<kNumSMs * 8, 256, 0, st>>>(p, g, m, v, shadow, n, cf, (float)lr, lr_dev, (float)b1,
                                                 (float)b2, (float)(1.0 / bc1), (float)(1.0 / bc2),
                                                 (float)eps, (float)wd);
   PH_LAUNCH_CHECK();
@@ -139,9 +140,10 @@ void adamw_f32(float* p, const float* g, float* m, float* v, bf16* shadow, uint6
 // optim.cpp:92-103: p -= lr * (g * cf)
 __global__ void sgd_f32_kernel(float* __restrict__ p, const float* __restrict__ g,
                                bf16* __restrict__ shadow, uint64_t n, const float* cfp,
-                               double lr) {
+                               double lr_v, const double* lr_dev) {
   const double cf = (double)*cfp;
   if (cf != cf) return;  // NumericError step: no update (clip_finalize_kernel)
+  const double lr = lr_dev ? *lr_dev : lr_v;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const float np = (float)((double)p[i] - lr * ((double)g[i] * cf));
@@ -151,8 +153,8 @@ __global__ void sgd_f32_kernel(float* __restrict__ p, const float* __restrict__ 
 }
 
 void sgd_f32(float* p, const float* g, bf16* shadow, uint64_t n, const float* cf, double lr,
-             cudaStream_t st) {
-  sgd_f32_kernel<<<kNumSMs * 8, 256, 0, st>>>(p, g, shadow, n, cf, lr);
+             cudaStream_t st, const double* lr_dev) {
+  sgd_f32_kernel<<<kNumSMs * 8, 256, 0, st>>>(p, g, shadow, n, cf, lr, lr_dev);
   PH_LAUNCH_CHECK();
 }
 
