@@ -930,6 +930,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int j = 0; j <= qt; ++j, ++gj) {
           const int st = gj % NRQ;
           mbar_wait(&kv_empty[st], ((gj / NRQ) & 1) ^ 1);
+          ATTN_TRACE_P(10, gj);
           mbar_expect_tx(&kv_full[st], 2 * KB);
           for (int t = 0; t < NA; ++t) {
             tma_load_2d(sK + st * KB + t * 16384, &tk, &kv_full[st], h * HD + 64 * t, row_base + j * TK);
@@ -947,6 +948,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                                ((uint32_t)(HD >> 3) << 17) | ((uint32_t)(TQ >> 4) << 24);
       auto issue_dq = [&](int g, int st, bool first, int t) {
         mbar_wait(p_full, g & 1);
+        ATTN_TRACE_P(13, g);
         if (first && t > 0) mbar_wait(acc_empty, (t - 1) & 1);  // previous dQ drained
         fence_after();
         const uint32_t bk = su32(sK + st * KB);
@@ -968,7 +970,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int j = 0; j <= qt; ++j, ++gj) {
           const int st = gj % NRQ;
           mbar_wait(&kv_full[st], (gj / NRQ) & 1);
+          ATTN_TRACE_P(11, gj);
           mbar_wait(s_empty, (gj & 1) ^ 1);
+          ATTN_TRACE_P(12, gj);
           fence_after();
           const uint32_t bk = su32(sK + st * KB), bv = su32(sV + st * KB);
 #pragma unroll
@@ -1006,6 +1010,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const float D = a.Dp[(int64_t)bh * a.Spad + qrow];
       for (int j = 0; j <= qt; ++j, ++gj) {
         mbar_wait(s_full, gj & 1);
+        if (warp == 2 && lane == 0) ATTN_TRACE_P(15, gj);
         fence_after();
         uint32_t s[CPT], dp[CPT];
         tmem_ld_cols<CPT>(tmem + lane_off + cg * CPT, s);
@@ -1014,6 +1019,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(s_empty);
+        if (warp == 2 && lane == 0) ATTN_TRACE_P(16, gj);
         const int k0 = j * TK + cg * CPT;
         const bool masked = (j * TK + TK > q0) || (j * TK + TK > a.S);
         uint32_t dd[CPT / 2];  // dS unscaled (the softmax scale is applied to dQ at the store)
@@ -1027,13 +1033,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
           dd[i] = pk(p0 * (__uint_as_float(dp[2 * i]) - D), p1 * (__uint_as_float(dp[2 * i + 1]) - D));
         }
+        if (warp == 2 && lane == 0) ATTN_TRACE_P(17, gj);
         if (gj >= 1) mbar_wait(g_done, (gj - 1) & 1);
+        if (warp == 2 && lane == 0) ATTN_TRACE_P(18, gj);
         fence_after();
         tmem_st_cols<CPT / 2>(tmem + lane_off + 256 + cg * (CPT / 2), dd);
         tmem_wait_st();
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full);
+        if (warp == 2 && lane == 0) ATTN_TRACE_P(19, gj);
       }
       mbar_wait(g_done, (gj - 1) & 1);
       fence_after();
