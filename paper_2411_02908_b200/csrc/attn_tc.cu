@@ -192,21 +192,6 @@ __device__ __forceinline__ float ex2(float x) {  // MUFU.EX2 without range fix-u
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// 2^x on the FMA / ALU pipes (x <= 0): round-to-nearest split x = j + f via the
-// 1.5 * 2^23 shifter, 2^f on [-1/2, 1/2] by a degree-3 polynomial (rel. error
-// 7.5e-5, far below the bf16 rounding its result goes through), j added to the
-// exponent field.  Offloads part of the exponentials from MUFU, which bounds
-// the dQ pass's softmax phase.
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -125.f);  // keeps the exponent field normal (2^-125 is 0 in bf16 terms)
-  const float t = x + 12582912.f;
-  const float j = t - 12582912.f;
-  const float f = x - j;
-  float p = fmaf(5.517132e-2f, f, 2.4261054e-1f);  // minimax (relative) on [-1/2, 1/2]
-  p = fmaf(p, f, 6.9326099e-1f);
-  p = fmaf(p, f, 0.99992811f);
-  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
-}
 __device__ __forceinline__ float4 lds_f4(const float* p) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -556,10 +541,6 @@ struct BwdArgs {
 constexpr int SWB = PHOTON_ATTN_SWB;
 constexpr int NCG = SWB / 4;       // column groups
 constexpr int CPT = 128 / NCG;     // score columns per thread
-#ifndef PHOTON_DQ_POLY_EVERY
-#define PHOTON_DQ_POLY_EVERY 3
-#endif
-constexpr int kDqPolyEvery = PHOTON_DQ_POLY_EVERY;  // dQ pass: 1 in N exponentials by polynomial
 constexpr int kBwdThreads = 64 + SWB * 32;
 // Ring depth of the streamed operand (Q/dO/L/D in dK/dV, K/V in dQ).  A stage is
 // held until the tile's gradient MMAs retire, and a TMA load under the full
@@ -1044,11 +1025,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         uint32_t dd[CPT / 2];  // dS unscaled (the softmax scale is applied to dQ at the store)
 #pragma unroll
         for (int i = 0; i < CPT / 2; ++i) {
-          // every third exponential on the FMA pipe (kDqPolyEvery), the rest on MUFU
-          const float x0 = fmaf(__uint_as_float(s[2 * i]), a.sl2, -L);
-          const float x1 = fmaf(__uint_as_float(s[2 * i + 1]), a.sl2, -L);
-          float p0 = (2 * i) % kDqPolyEvery == kDqPolyEvery - 1 ? ex2_poly(x0) : ex2(x0);
-          float p1 = (2 * i + 1) % kDqPolyEvery == kDqPolyEvery - 1 ? ex2_poly(x1) : ex2(x1);
+          float p0 = ex2(fmaf(__uint_as_float(s[2 * i]), a.sl2, -L));
+          float p1 = ex2(fmaf(__uint_as_float(s[2 * i + 1]), a.sl2, -L));
           if (masked) {
             p0 = (k0 + 2 * i <= qrow && k0 + 2 * i < a.S) ? p0 : 0.f;
             p1 = (k0 + 2 * i + 1 <= qrow && k0 + 2 * i + 1 < a.S) ? p1 : 0.f;
