@@ -225,6 +225,10 @@ constexpr uint32_t kColS = 0, kColP = 128, kColO = 192;
 // forward K ring depth: a TMA load under the forward's traffic takes up to ~5k
 // cycles (clock64 trace), more than two tiles of softmax
 constexpr int NKF = 3;
+#ifndef PHOTON_FWD_PRE
+#define PHOTON_FWD_PRE 1
+#endif
+constexpr int kFwdPre = PHOTON_FWD_PRE;  // 32-score chunks of P computed before the PV wait
 
 template <int HD>
 __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
@@ -376,9 +380,15 @@ __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
         for (int i = 0; i < TK; ++i)
           if (k0 + i > qrow || k0 + i >= a.S) s[i] = __float_as_uint(-INFINITY);
       }
-      float mx = -INFINITY;  // raw-score max (scale > 0 keeps the order)
+      // raw-score max (scale > 0 keeps the order): eight independent chains
+      // instead of one 128-deep dependent chain on the softmax's critical path
+      float mxs[8];
 #pragma unroll
-      for (int i = 0; i < TK; ++i) mx = fmaxf(mx, __uint_as_float(s[i]));
+      for (int u = 0; u < 8; ++u) mxs[u] = __uint_as_float(s[u]);
+#pragma unroll
+      for (int i = 8; i < TK; ++i) mxs[i & 7] = fmaxf(mxs[i & 7], __uint_as_float(s[i]));
+      float mx = fmaxf(fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3])),
+                       fmaxf(fmaxf(mxs[4], mxs[5]), fmaxf(mxs[6], mxs[7])));
       mx *= sl2;
       // lazy rescale: keep the stale max unless it grew by > 2^8
       float scale = 1.f;
@@ -391,6 +401,19 @@ __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
         m = mx;
       }
       if (warp == 2 && lane == 0) ATTN_TRACE(6, j);
+      // the first kFwdPre 32-score chunks of P are computed before waiting for
+      // PV_{j-1}, so their exponentials overlap that product
+      float rs = 0.f;
+      uint32_t pre[kFwdPre * 16 + 1];
+#pragma unroll
+      for (int c = 0; c < kFwdPre; ++c)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float p0 = ex2(fmaf(__uint_as_float(s[c * 32 + 2 * i]), sl2, -m));
+          const float p1 = ex2(fmaf(__uint_as_float(s[c * 32 + 2 * i + 1]), sl2, -m));
+          rs += p0 + p1;
+          pre[c * 16 + i] = pk(p0, p1);
+        }
       // P and O are free once PV_{j-1} retired
       if (j >= 1) mbar_wait(o_done, (j - 1) & 1);
       if (warp == 2 && lane == 0) ATTN_TRACE(7, j);
@@ -408,9 +431,10 @@ __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
       }
       l *= scale;
       // P = exp2(s*sl2 - m) -> bf16 pairs into TMEM columns [128, 192)
-      float rs = 0.f;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < kFwdPre; ++c) TMEM_ST16(tmem + lane_off + kColP + c * 16, (pre + c * 16));
+#pragma unroll
+      for (int c = kFwdPre; c < 4; ++c) {
         uint32_t pp[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
