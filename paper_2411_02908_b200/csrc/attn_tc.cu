@@ -44,9 +44,18 @@ __device__ unsigned long long g_attn_trace[64 * 64];
   do {                                                                                \
     if (blockIdx.x == 0 && (g) < 64) g_attn_trace[(e) * 64 + (g)] = clock64();        \
   } while (0)
+// the latest of all callers (e.g. every softmax warp's lane 0)
+#define ATTN_TRACE_MAX(e, g)                                                          \
+  do {                                                                                \
+    if (blockIdx.x == 0 && (g) < 64)                                                  \
+      atomicMax(&g_attn_trace[(e) * 64 + (g)], (unsigned long long)clock64());        \
+  } while (0)
 #else
 #define ATTN_TRACE_P(e, g) \
   do {                     \
+  } while (0)
+#define ATTN_TRACE_MAX(e, g) \
+  do {                       \
   } while (0)
 #define ATTN_TRACE(e, it) \
   do {                    \
@@ -574,6 +583,24 @@ constexpr int kBwdThreads = 64 + SWB * 32;
 #define PHOTON_ATTN_NR 4
 #endif
 constexpr int NR = PHOTON_ATTN_NR;
+// dQ pass (HD = 64): K/V ring depth (32 KB stages; up to 5 fit).  clock64
+// traces show a K/V load taking ~4.5 k cycles under the backward's L2 traffic,
+// but 5 stages (and, in dK/dV, one K/V buffer with 5 Q/dO stages) measured the
+// same as 4 -- the loads are not what paces the passes.
+#ifndef PHOTON_ATTN_NRQ
+#define PHOTON_ATTN_NRQ 4
+#endif
+constexpr int NRQ64 = PHOTON_ATTN_NRQ;
+// dK/dV pass (HD = 64): K/V buffers (2 = the next key tile prefetched) and the
+// Q/dO ring depth that fits beside them
+#ifndef PHOTON_ATTN_NKV
+#define PHOTON_ATTN_NKV 2
+#endif
+constexpr int NKV64 = PHOTON_ATTN_NKV;
+#ifndef PHOTON_ATTN_NR64
+#define PHOTON_ATTN_NR64 NR
+#endif
+constexpr int NR64 = PHOTON_ATTN_NR64;
 
 // Store N columns of a row of a 64-column fp32 TMEM accumulator (thread = row)
 // as bf16 into the head slice.
@@ -648,21 +675,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   constexpr int NA = HD / 64, KB = 16384 * NA;  // swizzle atoms per row, K/V tile bytes
   constexpr int TQB = HD == 64 ? 128 : 64, QB = TQB * 128 * NA, QA = TQB * 128;  // Q tile, atom
   constexpr int CPQ = TQB / NCG, GPH = HD / NCG;  // score / accumulator columns per thread
-  constexpr int NKV = HD == 64 ? 2 : 1;           // K/V buffers (the next tile's prefetch)
+  constexpr int NKV = HD == 64 ? NKV64 : 1;       // K/V buffers (the next tile's prefetch)
+  constexpr int NRK = HD == 64 ? NR64 : NR;       // Q/dO/L/D ring depth
   constexpr uint32_t colDP = TQB, colP = 2 * TQB, colDS = colP + TQB / 2, colDV = 512 - 2 * HD,
                      colDK = 512 - HD;
   uint8_t* sK = sm;               // [NKV]
   uint8_t* sV = sK + NKV * KB;    // [NKV]
-  uint8_t* sQ = sV + NKV * KB;    // [NR]
-  uint8_t* sO = sQ + NR * QB;     // [NR] dO
-  float* sL = reinterpret_cast<float*>(sO + NR * QB);  // [NR][TQB]
-  float* sD = sL + NR * TQB;                           // [NR][TQB]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sD + NR * TQB);
+  uint8_t* sQ = sV + NKV * KB;    // [NRK]
+  uint8_t* sO = sQ + NRK * QB;     // [NRK] dO
+  float* sL = reinterpret_cast<float*>(sO + NRK * QB);  // [NRK][TQB]
+  float* sD = sL + NRK * TQB;                           // [NRK][TQB]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sD + NRK * TQB);
   uint64_t* kv_full = bar;                 // [NKV]
   uint64_t* kv_empty = bar + NKV;          // [NKV]
-  uint64_t* q_full = bar + 2 * NKV;        // [NR]
-  uint64_t* q_empty = q_full + NR;         // [NR]
-  uint64_t* s_full = q_empty + NR;
+  uint64_t* q_full = bar + 2 * NKV;        // [NRK]
+  uint64_t* q_empty = q_full + NRK;         // [NRK]
+  uint64_t* s_full = q_empty + NRK;
   uint64_t* s_empty = s_full + 1;
   uint64_t* p_full = s_full + 2;
   uint64_t* g_done = s_full + 3;
@@ -677,7 +705,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
-    for (int i = 0; i < NR; ++i) {
+    for (int i = 0; i < NRK; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
     }
@@ -712,8 +740,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           tma_load_2d(sV + kb * KB + t * 16384, &tv, &kv_full[kb], h * HD + 64 * t, row_base + kt * TK);
         }
         for (int it = 0; it < n_it; ++it, ++gi) {
-          const int st = gi % NR, qt = qt0 + it;
-          mbar_wait(&q_empty[st], ((gi / NR) & 1) ^ 1);
+          const int st = gi % NRK, qt = qt0 + it;
+          mbar_wait(&q_empty[st], ((gi / NRK) & 1) ^ 1);
           ATTN_TRACE_P(0, gi);
           mbar_expect_tx(&q_full[st], 2 * QB + 8 * TQB);
           for (int t = 0; t < NA; ++t) {
@@ -760,8 +788,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         mbar_wait(&kv_full[kb], (ti / NKV) & 1);
         const uint32_t ak = su32(sK + kb * KB), av = su32(sV + kb * KB);
         for (int it = 0; it < n_it; ++it, ++gi) {
-          const int st = gi % NR;
-          mbar_wait(&q_full[st], (gi / NR) & 1);
+          const int st = gi % NRK;
+          mbar_wait(&q_full[st], (gi / NRK) & 1);
           ATTN_TRACE_P(1, gi);
           mbar_wait(s_empty, (gi & 1) ^ 1);
           ATTN_TRACE_P(2, gi);
@@ -801,8 +829,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int key = kt * TK + r;
       const bool key_live = key < a.S;
       for (int it = 0; it < n_it; ++it, ++gi) {
-        const int st = gi % NR, q0 = (qt0 + it) * TQB;
-        mbar_wait(&q_full[st], (gi / NR) & 1);  // L, D of this query tile visible
+        const int st = gi % NRK, q0 = (qt0 + it) * TQB;
+        mbar_wait(&q_full[st], (gi / NRK) & 1);  // L, D of this query tile visible
         mbar_wait(s_full, gi & 1);
         if (warp == 2 && lane == 0) ATTN_TRACE_P(5, gi);
         fence_after();
@@ -814,6 +842,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(s_empty);
         if (warp == 2 && lane == 0) ATTN_TRACE_P(6, gi);
+        if (lane == 0) ATTN_TRACE_MAX(4, gi);
         const float* L = sL + st * TQB + cg * CPQ;
         const float* D = sD + st * TQB + cg * CPQ;
         // masking only where this key tile meets the diagonal or the sequence end
@@ -891,7 +920,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
   constexpr int NA = HD / 64, KB = 16384 * NA;  // swizzle atoms per row, tile bytes
-  constexpr int NRQ = HD == 64 ? NR : 2;         // K/V ring depth within 227 KB
+  constexpr int NRQ = HD == 64 ? NRQ64 : 2;      // K/V ring depth within 227 KB
   constexpr int NQO = HD == 64 ? 2 : 1;          // Q/dO buffers (the next tile's prefetch)
   constexpr int GPH = HD / NCG;
   uint8_t* sQ = sm;                // [NQO]
@@ -1044,6 +1073,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(s_empty);
         if (warp == 2 && lane == 0) ATTN_TRACE_P(16, gj);
+        if (lane == 0) ATTN_TRACE_MAX(14, gj);
         const int k0 = j * TK + cg * CPT;
         const bool masked = (j * TK + TK > q0) || (j * TK + TK > a.S);
         uint32_t dd[CPT / 2];  // dS unscaled (the softmax scale is applied to dQ at the store)
@@ -1186,8 +1216,9 @@ void attn_bwd_hd(const bf16* q, const bf16* k, const bf16* v, const bf16* o, con
   BwdArgs a{S,  H,  d,  Spad, B * H, rsqrtf((float)HD) * kLog2e, rsqrtf((float)HD), Lp, Dp, dk, dv,
             sums ? sums + P : nullptr, sums ? sums + 2 * P : nullptr, nblk};
   constexpr int NA = HD / 64;
-  constexpr int NKV = HD == 64 ? 2 : 1, NRQ = HD == 64 ? NR : 2, NQO = HD == 64 ? 2 : 1;
-  constexpr int SMEM1 = 1024 + 2 * NKV * 16384 * NA + NR * 2 * TQB * 128 * NA + NR * 8 * TQB + 512;
+  constexpr int NKV = HD == 64 ? NKV64 : 1, NRQ = HD == 64 ? NRQ64 : 2, NQO = HD == 64 ? 2 : 1;
+  constexpr int NRK = HD == 64 ? NR64 : NR;
+  constexpr int SMEM1 = 1024 + 2 * NKV * 16384 * NA + NRK * 2 * TQB * 128 * NA + NRK * 8 * TQB + 512;
   constexpr int SMEM2 = 1024 + (2 * NQO + 2 * NRQ) * 16384 * NA + 512;
   static_assert(SMEM1 <= 232448 && SMEM2 <= 232448, "attention backward: shared memory");
   static std::atomic<uint64_t> cfg1{0}, cfg2{0};

@@ -26,9 +26,10 @@ for bwd in (False, True, True):
 torch.cuda.synchronize()
 print(f"backward {ms.value:.3f} ms")
 buf = (C.c_ulonglong * (64 * 64))()
+# (the trace buffer is not reset between launches: events 4 / 14 keep the max)
 assert A.lib().photon_debug_attn_trace(buf, 64 * 64) == 0
-for base, names in ((0, "prod_q,mma_qfull,mma_sissue,mma_pready,-,sm_sready,sm_loaded,sm_computed,sm_gdone,sm_pfull"),
-                    (10, "prod_kv,mma_kvfull,mma_sissue,mma_pready,-,sm_sready,sm_loaded,sm_computed,sm_gdone,sm_pfull")):
+for base, names in ((0, "prod_q,mma_qfull,mma_sissue,mma_pready,last_loaded,sm_sready,sm_loaded,sm_computed,sm_gdone,sm_pfull"),
+                    (10, "prod_kv,mma_kvfull,mma_sissue,mma_pready,last_loaded,sm_sready,sm_loaded,sm_computed,sm_gdone,sm_pfull")):
     names = names.split(",")
     t0 = min(buf[(base + e) * 64] for e in range(len(names)) if buf[(base + e) * 64])
     print("dK/dV" if base == 0 else "dQ")
