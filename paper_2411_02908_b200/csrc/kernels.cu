@@ -134,11 +134,24 @@ __global__ void __launch_bounds__(256) ln_fwd_vec_kernel(const float* __restrict
   constexpr int D = NV * 128;
   const int lane = threadIdx.x & 31;
   const float inv_d = 1.0f / (float)D;
-  for (int m = blockIdx.x * 8 + (threadIdx.x >> 5); m < M; m += gridDim.x * 8) {
-    const float4* xr = reinterpret_cast<const float4*>(x + (size_t)m * D);
+  const int step = gridDim.x * 8;
+  // the next row's loads are issued before this row's reductions and stores, so
+  // every warp keeps a row in flight through its arithmetic
+  float4 nx[NV];
+  int m = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (m < M) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) nx[i] = reinterpret_cast<const float4*>(x + (size_t)m * D)[lane + 32 * i];
+  }
+  for (; m < M; m += step) {
     float4 v[NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) v[i] = xr[lane + 32 * i];
+    for (int i = 0; i < NV; ++i) v[i] = nx[i];
+    if (m + step < M) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i)
+        nx[i] = reinterpret_cast<const float4*>(x + (size_t)(m + step) * D)[lane + 32 * i];
+    }
     float s = 0.f;
 #pragma unroll
     for (int i = 0; i < NV; ++i) s += ((v[i].x + v[i].y) + v[i].z) + v[i].w;
