@@ -305,6 +305,19 @@ int photon_debug_attention(int impl, int B, int S, int H, int d, const void* q, 
 int photon_ctx_set_timing(photon_ctx* ctx, int on);
 int photon_ctx_kernel_times(photon_ctx* ctx, double* times8);
 
+/* ---- the multi-GPU round boundary's plan (host logic, no GPU) -------------------
+ * What every rank of the runner derives identically: the flat parameter
+ * vector is cut into `world` shards of photon_shard_len elements (a multiple
+ * of 4; world * shard_len >= n_params); sampled slot si (ascending client ids;
+ * worker w of the centralized baseline) trains on rank photon_slot_owner(si);
+ * photon_boundary_peer says whether a round with n_survivors of k sampled
+ * clients runs on the NVLink peer-memory kernel (1) or the NCCL send/recv +
+ * all-gather path (0), honouring PHOTON_BOUNDARY.  The runner uses the same
+ * functions; tests drive them over gloo. */
+uint64_t photon_shard_len(uint64_t n_params, int world);
+int photon_slot_owner(uint64_t slot, int world);
+int photon_boundary_peer(uint64_t n_params, uint64_t k, uint64_t n_survivors, int world);
+
 /* ---- federated round runner (FederationRunner, aggregator.h:70-102) ------------ */
 /* Device-resident: theta_t, velocity and client state live in HBM.  With
  * world > 1 each rank runs the sampled clients with slot % world == rank and

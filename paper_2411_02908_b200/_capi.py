@@ -114,6 +114,9 @@ _SIGS = {
                                           P(photon_err)]),
     "photon_plan_from_blocks": (i32, [P(C.c_void_p), P(u64), u64, u64, P(u64), u64,
                                       P(C.c_uint32), P(u64), P(C.c_void_p), P(photon_err)]),
+    "photon_shard_len": (u64, [u64, C.c_int]),
+    "photon_slot_owner": (C.c_int, [u64, C.c_int]),
+    "photon_boundary_peer": (C.c_int, [u64, u64, u64, C.c_int]),
     "photon_debug_gemm": (i32, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int64,
                                 C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p,
                                 C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,

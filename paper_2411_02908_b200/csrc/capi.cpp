@@ -720,6 +720,19 @@ int photon_ctx_kernel_times(photon_ctx* ctx, double* t) {
   return PHOTON_OK;
 }
 
+// ---- the boundary plan (host.hpp) ----------------------------------------------------------
+uint64_t photon_shard_len(uint64_t n_params, int world) {
+  return world >= 1 ? shard_len(n_params, world) : 0;
+}
+int photon_slot_owner(uint64_t slot, int world) { return world >= 1 ? slot_owner(slot, world) : -1; }
+int photon_boundary_peer(uint64_t n_params, uint64_t k, uint64_t n_survivors, int world) {
+  if (world <= 1) return 0;
+  return boundary_prefers_peer(shard_len(n_params, world) * (uint64_t)world * 4) &&
+                 peer_round_ok(n_survivors, k, world)
+             ? 1
+             : 0;
+}
+
 // ---- runner ------------------------------------------------------------------------------
 int photon_nccl_unique_id(uint8_t* out, photon_err* err) {
   return guarded(err, [&] {
@@ -783,7 +796,7 @@ int photon_debug_boundary(int device, uint64_t n_params, int rank, int world,
     validate_server(*server);
     PH_CUDA(cudaSetDevice(device));
     const uint64_t P = n_params;
-    const uint64_t shard = ((P + world - 1) / world + 3) / 4 * 4, Ppad = shard * world;
+    const uint64_t shard = shard_len(P, world), Ppad = shard * world;
     cudaStream_t st;
     PH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     DevBuf<float> theta, vel, model, recv;

@@ -58,7 +58,7 @@ Central::Central(Ctx* c, const photon_central_cfg& cf, const Plan* p, uint64_t s
   if (ws < 1 || rk < 0 || rk >= ws) throw Error(PHOTON_ERR_USAGE, "centralized: bad rank/world");
   per_worker = cf.global_batch / cf.n_workers;
   P = c->eng->P;
-  shard = ((P + ws - 1) / ws + 3) / 4 * 4;
+  shard = shard_len(P, ws);
   Ppad = shard * ws;
   cursors.assign(cf.n_workers, 0);
   for (uint64_t w = 0; w < cf.n_workers; ++w)
@@ -137,7 +137,7 @@ void Central::step(photon_step_metric* out) {
   } else {
     PH_NCCL(nccl().GroupStart());
     for (int w = 0; w < nw; ++w) {
-      const int owner = w % world;
+      const int owner = slot_owner(w, world);
       if (owner == rank) {
         const float* g = d_grads.ptr + (size_t)(w / world) * Ppad;
         for (int q = 0; q < world; ++q)

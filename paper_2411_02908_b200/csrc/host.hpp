@@ -135,4 +135,33 @@ struct ResumeState {  // PersistedState (harness.cpp:527-535), federated fields
 void write_state_json(const std::string& path, const ResumeState& st);
 ResumeState read_state_json(const std::string& path);
 
+// ---- the multi-GPU round boundary's plan (runner.cpp, central.cpp, p2p.cpp) ----
+// The flat parameter vector is cut into `world` contiguous shards of
+// shard_len elements (a multiple of 4 for 128-bit access; world * shard_len >=
+// P).  Slot si of a round's ascending sampled clients (worker w of the
+// centralized baseline) trains on rank si % world, so each shard owner sees its
+// shard of every model in the canonical ascending order (aggregator.cpp:177).
+inline uint64_t shard_len(uint64_t P, int world) {
+  return ((P + (uint64_t)world - 1) / (uint64_t)world + 3) / 4 * 4;
+}
+inline int slot_owner(uint64_t si, int world) { return (int)(si % (uint64_t)world); }
+// The NVLink peer-memory boundary kernel takes at most this many surviving
+// models and ranks (its pointer tables), and replicas up to kPeerMaxBytes: on
+// 4 B200s 27.5 GB replicas (6.87B fp32) collapse to ~200 GB/s once remote loads
+// and stores run together (remote address translation over very large
+// mappings), where the NCCL path keeps ~500 GB/s.
+constexpr int kMaxPeerModels = 16;
+constexpr int kMaxPeerWorld = 16;
+constexpr uint64_t kPeerMaxBytes = 24000000000ull;
+// Whether a runner sets the peer boundary up at all (PHOTON_BOUNDARY=nccl|p2p
+// forces either), from the padded fp32 replica size.
+bool boundary_prefers_peer(uint64_t replica_bytes);
+// Whether a round of k sampled clients with n_surv survivors takes it: decided
+// from quantities every rank shares -- the survivor count and the busiest
+// rank's local model count ceil(k / world) -- so all ranks take the same path.
+inline bool peer_round_ok(uint64_t n_surv, uint64_t k, int world) {
+  return n_surv <= (uint64_t)kMaxPeerModels && world <= kMaxPeerWorld &&
+         (k + (uint64_t)world - 1) / (uint64_t)world <= (uint64_t)kMaxPeerModels;
+}
+
 }  // namespace photon

@@ -127,8 +127,8 @@ void sgd_f64(double* p, const double* g, uint64_t n, const double* norm, double 
 // Round boundary over peer memory (optim.cu): models[c] = surviving client c's
 // full model (ascending slot, IPC-mapped or local), replicas[g] = rank g's
 // theta buffer; this rank updates [off, off+len) of every replica.
-constexpr int kMaxPeerModels = 16;
-constexpr int kMaxPeerWorld = 16;
+using photon::kMaxPeerModels;  // host.hpp: the boundary plan
+using photon::kMaxPeerWorld;
 struct PeerBoundaryArgs {
   const float* models[kMaxPeerModels];
   float* replicas[kMaxPeerWorld];

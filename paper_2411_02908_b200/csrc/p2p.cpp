@@ -173,7 +173,7 @@ void PeerBoundary::run(const std::vector<int>& surv, uint64_t shard, float* vel,
   k::PeerBoundaryArgs a;
   std::memset(&a, 0, sizeof(a));
   for (int r = 0; r < n; ++r) {
-    const int si = surv[r], owner = si % world_, j = si / world_;
+    const int si = surv[r], owner = slot_owner(si, world_), j = si / world_;
     if (j >= (int)models_[owner].size())
       throw Error(PHOTON_ERR_USAGE, "peer boundary: slot not published by its rank");
     a.models[r] = models_[owner][j];

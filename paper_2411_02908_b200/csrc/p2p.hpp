@@ -36,15 +36,8 @@ struct PeerBoundary {
   void run(const std::vector<int>& surv, uint64_t shard, float* vel,
            const photon_server_cfg& server, cudaStream_t st);
   static bool supported(int n_survivors, int world) {
-    return n_survivors <= k::kMaxPeerModels && world <= k::kMaxPeerWorld;
+    return n_survivors <= kMaxPeerModels && world <= kMaxPeerWorld;
   }
-  // Whether the peer path should carry a model of `bytes` per replica.  Measured
-  // on 4 B200s (profiles/r01_aggregation_p2p_*): 628-673 GB/s busbw up to 22 GB
-  // (5.5B fp32 params) per buffer, but 27.5 GB buffers (6.87B) collapse to ~200
-  // GB/s once remote loads and remote stores run together (each alone is fine:
-  // 520 / 605 GB/s) -- remote address translation over very large mappings.
-  // Beyond the bound the NCCL path (staging through small FIFOs) is faster.
-  static bool fits(uint64_t bytes) { return bytes <= (uint64_t)24e9; }
   // device ms of the last run()'s fused kernel (after the opening barrier)
   float last_kernel_ms() const;
   // after run() has completed on the stream: throws if a peer never arrived

@@ -32,12 +32,13 @@ namespace photon {
       throw Error(PHOTON_ERR_NCCL, std::string(#call) + ": " + nccl().GetErrorString(r_)); \
   } while (0)
 
-bool use_peer_boundary(uint64_t replica_bytes) {
+bool boundary_prefers_peer(uint64_t replica_bytes) {
   const char* e = std::getenv("PHOTON_BOUNDARY");
   if (e && std::string(e) == "nccl") return false;
   if (e && std::string(e) == "p2p") return true;
-  return PeerBoundary::fits(replica_bytes);
+  return replica_bytes <= kPeerMaxBytes;
 }
+bool use_peer_boundary(uint64_t replica_bytes) { return boundary_prefers_peer(replica_bytes); }
 
 // optim.cpp:105-113
 void validate_server(const photon_server_cfg& s) {
@@ -71,7 +72,7 @@ Runner::Runner(Ctx* c, const photon_fed_cfg& f, const photon_train_cfg& t,
   check_train_cfg(t);
   validate_server(s);
   P = c->eng->P;
-  shard = ((P + ws - 1) / ws + 3) / 4 * 4;
+  shard = shard_len(P, ws);
   Ppad = shard * ws;
   cursors.assign(f.population, 0);
   PH_CUDA(cudaSetDevice(c->device));
@@ -125,7 +126,7 @@ double Runner::stage(uint64_t round, int set, const std::vector<uint64_t>& cur) 
   const int V = (int)train.model.vocab_size;
   std::vector<int> mine;
   for (int si = 0; si < K; ++si)
-    if (si % world == rank) mine.push_back(si);
+    if (slot_owner(si, world) == rank) mine.push_back(si);
   if (host_batches[set].size() < mine.size()) {
     host_batches[set].resize(mine.size());
     dev_batches[set].resize(mine.size());
@@ -158,7 +159,7 @@ void Runner::run_round(photon_round_record* rec) {
 
   std::vector<int> mine;
   for (int si = 0; si < K; ++si)
-    if (si % world == rank) mine.push_back(si);
+    if (slot_owner(si, world) == rank) mine.push_back(si);
   // one local client trains in (and is aggregated from) the engine's master;
   // several keep their results in dedicated slots
   const bool in_master = mine.size() == 1;
@@ -268,10 +269,8 @@ void Runner::run_round(photon_round_record* rec) {
       recv = d_recv.ptr;
     }
   }
-  // every rank must take the same path: the local model count of the busiest
-  // rank (slot si lives on rank si % world) is known to all ranks from K
-  const int max_local = (K + world - 1) / world;
-  const bool peer = p2p && PeerBoundary::supported(n, world) && max_local <= k::kMaxPeerModels;
+  // every rank must take the same path (host.hpp peer_round_ok)
+  const bool peer = p2p && peer_round_ok((uint64_t)n, (uint64_t)K, world);
   if (peer) {
     p2p->publish(local_models.data(), (int)local_models.size(), d_theta.ptr, st);
     p2p->run(surv, shard, d_vel.ptr, server, st);
@@ -340,7 +339,7 @@ void round_boundary(ncclComm_t comm, int rank, int world, uint64_t P, uint64_t s
   } else {
     PH_NCCL(nccl().GroupStart());
     for (int r = 0; r < n; ++r) {
-      const int si = surv[r], owner = si % world;
+      const int si = surv[r], owner = slot_owner(si, world);
       if (owner == rank) {
         const float* model = local_models[si / world];
         for (int q = 0; q < world; ++q)

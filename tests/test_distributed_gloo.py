@@ -126,3 +126,61 @@ def test_slot_ownership_and_volume():
     covered = sum(hi - lo for lo, hi in (shard_range(r, 1001, 3) for r in range(3)))
     assert covered == 1001
     assert wire_bytes_per_gpu(164044480, 8) == pytest.approx(2 * 7 / 8 * 164044480 * 4)
+
+
+def test_peer_boundary_decision(monkeypatch):
+    """The NVLink peer-memory boundary vs the NCCL path (runner.cpp, host.hpp
+    peer_round_ok): decided from quantities every rank shares, so a rank that
+    holds more local models than the peer kernel takes sends every rank down
+    the NCCL path together (K = 33 on 2 GPUs, 17 dropouts)."""
+    from paper_2411_02908_b200.sharding import peer_boundary
+
+    P = 164044480
+    assert peer_boundary(P, 8, 8, 8)
+    assert peer_boundary(P, 2, 2, 2)
+    assert not peer_boundary(P, 33, 16, 2)   # busiest rank holds 17 > 16 models
+    assert not peer_boundary(P, 20, 17, 4)   # 17 survivors > 16
+    assert not peer_boundary(6865216704, 4, 4, 4)  # 27.5 GB replicas: NCCL path
+    assert not peer_boundary(P, 1, 1, 1)     # one GPU: no boundary exchange
+    monkeypatch.setenv("PHOTON_BOUNDARY", "nccl")
+    assert not peer_boundary(P, 8, 8, 8)
+    monkeypatch.setenv("PHOTON_BOUNDARY", "p2p")
+    assert peer_boundary(6865216704, 4, 4, 4)
+
+
+def _decision_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2411_02908_b200.sharding import owned_slots, peer_boundary
+
+    rng = np.random.default_rng(rank)  # each rank draws its own dropout pattern ...
+    cases = [(k, n) for k in (2, 16, 33, 40) for n in range(1, k + 1, 3)]
+    mine = torch.tensor([int(peer_boundary(164044480, k, n, world)) for k, n in cases])
+    local = torch.tensor([len(owned_slots(k, rank, world)) for k, _ in cases])
+    del rng  # ... but the decision only reads shared quantities
+    allm = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(allm, mine)
+    alll = [torch.zeros_like(local) for _ in range(world)]
+    dist.all_gather(alll, local)
+    if rank == 0:
+        out_q.put(([a.tolist() for a in allm], [a.tolist() for a in alll], cases))
+    dist.destroy_process_group()
+
+
+def test_peer_boundary_decision_agrees_across_ranks():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_decision_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    decisions, local_counts, cases = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert decisions[0] == decisions[1]
+    for (k, n), d, l0, l1 in zip(cases, decisions[0], local_counts[0], local_counts[1]):
+        # the peer path only when the busiest rank's models fit its tables
+        assert d == int(n <= 16 and max(l0, l1) <= 16), (k, n)
