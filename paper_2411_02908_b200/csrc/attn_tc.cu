@@ -412,15 +412,18 @@ __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
       if (warp == 2 && lane == 0) ATTN_TRACE(6, j);
       // the first kFwdPre 32-score chunks of P are computed before waiting for
       // PV_{j-1}, so their exponentials overlap that product
-      float rs = 0.f;
+      float2 rs2 = make_float2(0.f, 0.f);
       uint32_t pre[kFwdPre * 16 + 1];
 #pragma unroll
       for (int c = 0; c < kFwdPre; ++c)
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float p0 = ex2(fmaf(__uint_as_float(s[c * 32 + 2 * i]), sl2, -m));
-          const float p1 = ex2(fmaf(__uint_as_float(s[c * 32 + 2 * i + 1]), sl2, -m));
-          rs += p0 + p1;
+          // packed FFMA2 / FADD2: half the issue slots of the scale and the sum
+          const float2 x = __ffma2_rn(make_float2(__uint_as_float(s[c * 32 + 2 * i]),
+                                                  __uint_as_float(s[c * 32 + 2 * i + 1])),
+                                      make_float2(sl2, sl2), make_float2(-m, -m));
+          const float p0 = ex2(x.x), p1 = ex2(x.y);
+          rs2 = __fadd2_rn(rs2, make_float2(p0, p1));
           pre[c * 16 + i] = pk(p0, p1);
         }
       // P and O are free once PV_{j-1} retired
@@ -447,14 +450,17 @@ __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
         uint32_t pp[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float p0 = ex2(fmaf(__uint_as_float(s[c * 32 + 2 * i]), sl2, -m));
-          const float p1 = ex2(fmaf(__uint_as_float(s[c * 32 + 2 * i + 1]), sl2, -m));
-          rs += p0 + p1;
+          // packed FFMA2 / FADD2: half the issue slots of the scale and the sum
+          const float2 x = __ffma2_rn(make_float2(__uint_as_float(s[c * 32 + 2 * i]),
+                                                  __uint_as_float(s[c * 32 + 2 * i + 1])),
+                                      make_float2(sl2, sl2), make_float2(-m, -m));
+          const float p0 = ex2(x.x), p1 = ex2(x.y);
+          rs2 = __fadd2_rn(rs2, make_float2(p0, p1));
           pp[i] = pk(p0, p1);
         }
         TMEM_ST16(tmem + lane_off + kColP + c * 16, pp);
       }
-      l += rs;
+      l += rs2.x + rs2.y;
       tmem_wait_st();
       fence_before();
       __syncwarp();

@@ -130,7 +130,7 @@ class EngineT final : public Engine {
                                                     // q / k / v partials of the attention backward
                                                     k::attn_bwd_sums_floats((int)max_batch,
                                                                             (int)Smax_, (int)d) +
-                                                        k::colsum_parts_scratch_floats((int)d)}));
+                                                        3 * k::colsum_parts_scratch_floats((int)d)}));
     auto plan = [&](char* p) {
       char* s = p;
       // master: separate allocation (see master_alloc_)
@@ -443,9 +443,7 @@ void EngineT<T>::micro(const StepBatch& bt, double* loss_dev, bool backward, boo
         const int np = B * ((S + 31) / 32);
         const size_t P = (size_t)np * d;
         float* scr = part_ + 3 * P;
-        k::colsum_parts(part_ + 2 * P, np, d, scr, G(o.bv), stream, acc);
-        k::colsum_parts(part_ + P, np, d, scr, G(o.bk), stream, acc);
-        k::colsum_parts(part_, np, d, scr, G(o.bq), stream, acc);
+        k::colsum_parts3(part_, P, np, d, scr, G(o.bq), G(o.bk), G(o.bv), stream, acc);
       } else {
         k::colsum<T>(dv_, M, d, part_, G(o.bv), stream, acc);
         k::colsum<T>(dk_, M, d, part_, G(o.bk), stream, acc);

@@ -333,7 +333,8 @@ ln_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ x,
 __global__ void __launch_bounds__(1024) colreduce_kernel(const float* __restrict__ part, int nparts,
                                                          int n, int stride, float* __restrict__ out,
                                                          int split, float* __restrict__ out1,
-                                                         int acc_out) {
+                                                         int acc_out, int split2,
+                                                         float* __restrict__ out2) {
   __shared__ float red[32][33];
   const int cl = threadIdx.x & 31, s = threadIdx.x >> 5;
   const int j = blockIdx.x * 32 + cl;
@@ -353,42 +354,49 @@ __global__ void __launch_bounds__(1024) colreduce_kernel(const float* __restrict
     float t = 0.f;
 #pragma unroll
     for (int w = 0; w < 32; ++w) t += red[w][cl];
-    float* o = j < split ? out + j : out1 + (j - split);
+    float* o = j < split ? out + j : j < split2 ? out1 + (j - split) : out2 + (j - split2);
     *o = acc_out ? *o + t : t;  // micro-batches after the first add onto the gradient
   }
 }
+// columns [0, split) -> out, [split, split2) -> out1, [split2, n) -> out2
 static void colreduce(const float* part, int nparts, int n, int stride, float* out, int split,
-                      float* out1, cudaStream_t st, bool acc = false) {
+                      float* out1, cudaStream_t st, bool acc = false, int split2 = -1,
+                      float* out2 = nullptr) {
   colreduce_kernel<<<cdiv(n, 32), 1024, 0, st>>>(part, nparts, n, stride, out, split, out1,
-                                                 acc ? 1 : 0);
+                                                 acc ? 1 : 0, split2 < 0 ? n : split2, out2);
   PH_LAUNCH_CHECK();
 }
 
 // First level of a many-part column reduction: CTA (x, y) sums parts
 // [y * per, (y + 1) * per) of 32 columns in the colreduce order and writes
 // row y of `out` ([gridDim.y][n]).
+// Several same-shaped partial arrays at once: column J of the combined
+// [nseg * n] row is column J % n of segment J / n (segments seg_stride apart).
 __global__ void __launch_bounds__(256) colreduce_rows_kernel(const float* __restrict__ part, int nparts,
-                                                             int per, int n, float* __restrict__ out) {
+                                                             int per, int n, float* __restrict__ out,
+                                                             int nseg, size_t seg_stride) {
   __shared__ float red[8][33];
   const int cl = threadIdx.x & 31, s = threadIdx.x >> 5;
-  const int j = blockIdx.x * 32 + cl;
+  const int J = blockIdx.x * 32 + cl, nn = n * nseg;
+  const int seg = J / n, j = J - seg * n;
+  const float* ps = part + (size_t)seg * seg_stride;
   const int p0 = blockIdx.y * per, p1 = min(nparts, p0 + per);
   float acc = 0.f;
-  if (j < n) {
+  if (J < nn) {
     int p = p0 + s;
     for (; p + 8 < p1; p += 16) {
-      const float a = part[(size_t)p * n + j], b = part[(size_t)(p + 8) * n + j];
+      const float a = ps[(size_t)p * n + j], b = ps[(size_t)(p + 8) * n + j];
       acc = (acc + a) + b;
     }
-    for (; p < p1; p += 8) acc += part[(size_t)p * n + j];
+    for (; p < p1; p += 8) acc += ps[(size_t)p * n + j];
   }
   red[s][cl] = acc;
   __syncthreads();
-  if (s == 0 && j < n) {
+  if (s == 0 && J < nn) {
     float t = 0.f;
 #pragma unroll
     for (int w = 0; w < 8; ++w) t += red[w][cl];
-    out[(size_t)blockIdx.y * n + j] = t;
+    out[(size_t)blockIdx.y * nn + J] = t;
   }
 }
 
@@ -399,9 +407,20 @@ void colsum_parts(const float* part, int nparts, int N, float* scratch, float* o
   const int groups = std::min(kColsumPartGroups, nparts);
   const int per = cdiv(nparts, groups);
   const int used = cdiv(nparts, per);
-  colreduce_rows_kernel<<<dim3(cdiv(N, 32), used), 256, 0, st>>>(part, nparts, per, N, scratch);
+  colreduce_rows_kernel<<<dim3(cdiv(N, 32), used), 256, 0, st>>>(part, nparts, per, N, scratch, 1, 0);
   PH_LAUNCH_CHECK();
   colreduce(scratch, used, N, N, out, N, nullptr, st, acc);
+}
+
+void colsum_parts3(const float* part, size_t seg_stride, int nparts, int N, float* scratch,
+                   float* out0, float* out1, float* out2, cudaStream_t st, bool acc) {
+  const int groups = std::min(kColsumPartGroups, nparts);
+  const int per = cdiv(nparts, groups);
+  const int used = cdiv(nparts, per);
+  colreduce_rows_kernel<<<dim3(cdiv(3 * N, 32), used), 256, 0, st>>>(part, nparts, per, N, scratch,
+                                                                      3, seg_stride);
+  PH_LAUNCH_CHECK();
+  colreduce(scratch, used, 3 * N, 3 * N, out0, N, out1, st, acc, 2 * N, out2);
 }
 
 // Register-resident variant for d = 128 * NV: one warp per row, x, dy and the
@@ -654,8 +673,9 @@ void ln_bwd(const float* dy, const float* x, const float* mean, const float* rst
     }
   }
   PH_LAUNCH_CHECK();
-  colreduce(part, kLnBwdBlocks, 2 * d, 3 * d, dgain, d, dbias, st, acc);
-  if (dsum) colreduce(part + 2 * d, kLnBwdBlocks, d, 3 * d, dsum, d, nullptr, st, acc);
+  // gain, bias and (optionally) the output's column sums in one launch
+  colreduce(part, kLnBwdBlocks, dsum ? 3 * d : 2 * d, 3 * d, dgain, d, dbias, st, acc, 2 * d,
+            dsum);
 }
 
 // ============================================================================

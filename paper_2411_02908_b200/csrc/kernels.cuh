@@ -45,6 +45,10 @@ constexpr int kColsumPartGroups = 64;
 size_t colsum_parts_scratch_floats(int N);
 void colsum_parts(const float* part, int nparts, int N, float* scratch, float* out, cudaStream_t st,
                   bool acc = false);
+// three same-shaped partial arrays (part + i * seg_stride) into out0..out2 in
+// two launches (the q / k / v bias gradients); scratch >= 3 x colsum_parts_scratch_floats(N)
+void colsum_parts3(const float* part, size_t seg_stride, int nparts, int N, float* scratch,
+                   float* out0, float* out1, float* out2, cudaStream_t st, bool acc = false);
 
 // ---- softmax cross-entropy fwd+bwd (tensor.cpp:544-603) --------------------
 // logits [M,V] overwritten with dlogits = (softmax - onehot) * inv_count;
