@@ -304,6 +304,9 @@ int photon_debug_attention(int impl, int B, int S, int H, int d, const void* q, 
  * launches}, accumulated since the last reset (set_timing resets). */
 int photon_ctx_set_timing(photon_ctx* ctx, int on);
 int photon_ctx_kernel_times(photon_ctx* ctx, double* times8);
+/* Kernels this library has launched in this process (every launch site, plus
+ * the kernel nodes of each CUDA-graph replay of a local round). */
+uint64_t photon_launch_count(void);
 
 /* ---- the multi-GPU round boundary's plan (host logic, no GPU) -------------------
  * What every rank of the runner derives identically: the flat parameter

@@ -133,6 +133,7 @@ _SIGS = {
                                      P(dbl), P(photon_err)]),
     "photon_ctx_set_timing": (i32, [C.c_void_p, C.c_int]),
     "photon_ctx_kernel_times": (i32, [C.c_void_p, P(dbl)]),
+    "photon_launch_count": (C.c_uint64, []),
     "photon_nccl_unique_id": (i32, [P(u8), P(photon_err)]),
     "photon_runner_create": (i32, [C.c_void_p, P(photon_fed_cfg), P(photon_train_cfg),
                                    P(photon_server_cfg), C.c_void_p, P(dbl), C.c_int, C.c_int,

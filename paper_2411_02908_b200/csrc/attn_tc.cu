@@ -570,6 +570,11 @@ struct BwdArgs {
   float* s0;
   float* s1;
   int nblk;
+  // fused backward: g0 = dq, g1 = dk, g2 = dv (sums s0 / s1 / s2), and the fp32
+  // dQ accumulator [BH][ntq][HD/4][128] float4
+  bf16* g2;
+  float* s2;
+  float* dqa;
 };
 
 // producer, MMA, SWB softmax warps: SWB/4 warps per TMEM lane quarter, each on
@@ -1126,6 +1131,418 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 }
 #undef PH_FOR_TILES
 
+// ---- fused backward at HD = 64: dK, dV and dQ in one pass -------------------------
+// The two-pass backward computes every P tile twice (once per pass): 2 x 1,024
+// MUFU cycles and 2,196 MMA cycles per 128 x 128 tile pair, against 1,024 and
+// 1,685 for one pass.  One pass needs dQ_i = sum_j dS_ij K_j summed across the
+// key tiles j, which the two-pass design got from a query-major second pass.
+// Here a CTA owns a whole (batch, head): key tiles j ascending (outer), query
+// tiles i = j..n-1 (inner), and dQ_i's per-tile partials (an M = 128-query MMA
+// with A = dS read from shared memory) are drained by the softmax warps into an
+// fp32 accumulator in global memory, each (row, column) always by the same
+// thread, in the order j = 0, 1, ..., i: j = 0 stores, 0 < j < i adds
+// (red.add), j = i reads back, adds, scales and writes the bf16 dq row and the
+// bias partials.  Same-thread same-address operations are ordered, and no other
+// CTA touches the head: deterministic, no atomics across CTAs.
+// dS^T goes to shared memory only (two 32 KB buffers, [2 query halves][128 keys]
+// [64 queries] with the 128B swizzle), read as the K-major A of dK = dS^T Q and
+// as the MN-major A of dQ = dS K.  The gradient products of a tile are split
+// over two completions (pv_done: dV, which frees P^T; gq_done: dK and dQ), so
+// the next tile's P^T store waits only for the dV product.  Clock64 timelines
+// (tools/attn_trace_fused.py) and ncu (L2 hit rate 44 %) show the pass paced by
+// the per-tile hand-offs and by L2 misses on the re-streamed Q/dO (a head's
+// Q/dO and dQ accumulator are ~1 MB, 128 heads in flight): odd CTAs walk the
+// key tiles in descending order to halve that footprint, and the grid keeps the
+// waves of heads even (384 heads: 128 CTAs x 3).
+// TMEM: S^T [0,128) dP^T [128,256) P^T [256,320) dV [320,384) dK [384,448) dQ [448,512)
+#ifndef PHOTON_ATTN_FUSED
+#define PHOTON_ATTN_FUSED 1
+#endif
+// Q/dO/L/D ring depth and K buffers (2: the next key tile's K streams in while
+// the last tile's dQ product still reads K; V is read by dP^T only, one buffer)
+#ifndef PHOTON_ATTN_NRF
+#define PHOTON_ATTN_NRF 3
+#endif
+#ifndef PHOTON_ATTN_NKF
+#define PHOTON_ATTN_NKF 2
+#endif
+constexpr int NRF = PHOTON_ATTN_NRF, NKF2 = PHOTON_ATTN_NKF;
+#ifndef PHOTON_FUSED_ALT
+#define PHOTON_FUSED_ALT 1
+#endif
+#ifndef PHOTON_FUSED_GRID
+#define PHOTON_FUSED_GRID 1
+#endif
+constexpr int kFusedSmem = 1024 + 2 * 32768 + (NKF2 + 1) * 16384 + NRF * (2 * 16384 + 8 * 128) + 512;
+static_assert(kFusedSmem <= 232448, "fused attention backward: shared memory");
+
+__device__ __forceinline__ void st_relaxed_f4(float* p, float4 v) {
+  asm volatile("st.relaxed.gpu.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void red_add_f4(float* p, float4 v) {
+  asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ float4 ld_relaxed_f4(const float* p) {
+  float4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    attn_bwd_fused64_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                               const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
+                               const BwdArgs a) {
+  static_assert(SWB == 16, "fused backward: 16 softmax warps (4 column groups of 32 queries)");
+  constexpr int HD = 64, KB = 16384, QB = 16384, T = 128;  // tiles: 128 rows x 64 bf16
+  constexpr int CPQ = 32, GPH = 16;                          // per-thread score / accumulator columns
+  constexpr uint32_t colDP = 128, colP = 256, colDV = 320, colDK = 384, colDQ = 448;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint8_t* sDS = sm;                    // dS^T [2], 32 KB each
+  uint8_t* sK = sDS + 2 * 32768;        // [NKF2]
+  uint8_t* sV = sK + NKF2 * KB;         // [1]
+  uint8_t* sQ = sV + KB;                // [NRF]
+  uint8_t* sO = sQ + NRF * QB;          // [NRF] dO
+  float* sL = reinterpret_cast<float*>(sO + NRF * QB);  // [NRF][128]
+  float* sD = sL + NRF * T;                             // [NRF][128]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sD + NRF * T);
+  uint64_t* k_full = bar;                   // [NKF2]
+  uint64_t* k_empty = bar + NKF2;           // [NKF2]
+  uint64_t* v_full = bar + 2 * NKF2;
+  uint64_t* v_empty = v_full + 1;
+  uint64_t* q_full = v_full + 2;            // [NRF]
+  uint64_t* q_empty = q_full + NRF;         // [NRF]
+  uint64_t* s_full = q_empty + NRF;
+  uint64_t* s_empty = s_full + 1;
+  uint64_t* p_full = s_full + 2;            // P^T and dS^T of the tile stored
+  uint64_t* pv_done = s_full + 3;           // dV product retired (P^T free)
+  uint64_t* gq_done = s_full + 4;           // dK, dQ products retired (dS^T buffer free, dQ ready)
+  uint64_t* dq_free = s_full + 5;           // dQ drained from TMEM by the softmax warps
+  uint64_t* acc_empty = s_full + 6;         // dK / dV drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 7);
+
+  const int nt = (a.S + T - 1) / T;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  // odd CTAs walk the key tiles in descending order: the live set of an
+  // ascending head (Q/dO tiles j..n-1 and the accumulators of dQ_{j+1..n-1})
+  // shrinks while a descending one's grows, so the L2 footprint of all heads in
+  // flight stays near half of its peak
+  const bool desc = PHOTON_FUSED_ALT && (blockIdx.x & 1);
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < NKF2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+    }
+    mbar_init(v_full, 1);
+    mbar_init(v_empty, 1);
+    for (int i = 0; i < NRF; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_empty, SWB);
+    mbar_init(p_full, SWB);
+    mbar_init(pv_done, 1);
+    mbar_init(gq_done, 1);
+    mbar_init(dq_free, SWB);
+    mbar_init(acc_empty, SWB);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        su32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ===== producer: K, V per key tile, the Q / dO / L / D ring =====
+      int ti = 0, gi = 0;
+      for (int bh = blockIdx.x; bh < a.BH; bh += gridDim.x) {
+        const int b = bh / a.H, h = bh % a.H, row_base = b * a.S;
+        for (int kk = 0; kk < nt; ++kk, ++ti) {
+          const int kt = desc ? nt - 1 - kk : kk;
+          const int kb = ti % NKF2;
+          mbar_wait(&k_empty[kb], ((ti / NKF2) & 1) ^ 1);
+          mbar_expect_tx(&k_full[kb], KB);
+          tma_load_2d(sK + kb * KB, &tk, &k_full[kb], h * HD, row_base + kt * T);
+          mbar_wait(v_empty, (ti & 1) ^ 1);
+          mbar_expect_tx(v_full, KB);
+          tma_load_2d(sV, &tv, v_full, h * HD, row_base + kt * T);
+          for (int qt = kt; qt < nt; ++qt, ++gi) {
+            const int st = gi % NRF;
+            mbar_wait(&q_empty[st], ((gi / NRF) & 1) ^ 1);
+            ATTN_TRACE_P(20, gi);
+            mbar_expect_tx(&q_full[st], 2 * QB + 8 * T);
+            tma_load_2d(sQ + st * QB, &tq, &q_full[st], h * HD, row_base + qt * T);
+            tma_load_2d(sO + st * QB, &tdo, &q_full[st], h * HD, row_base + qt * T);
+            bulk_load(sL + st * T, a.Lp + (int64_t)bh * a.Spad + qt * T, 4 * T, &q_full[st]);
+            bulk_load(sD + st * T, a.Dp + (int64_t)bh * a.Spad + qt * T, 4 * T, &q_full[st]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ===== MMA issuer =====
+      // S^T, dP^T: M = 128 keys, N = 128 queries, both operands K-major
+      constexpr uint32_t IDS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(T >> 3) << 17) |
+                               ((uint32_t)(T >> 4) << 24);
+      // dV, dK: M = 128 keys, N = 64, B (dO / Q) MN-major
+      constexpr uint32_t IDG = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
+                               ((uint32_t)(HD >> 3) << 17) | ((uint32_t)(T >> 4) << 24);
+      // dQ: M = 128 queries, N = 64, A (dS) and B (K) MN-major
+      constexpr uint32_t IDQ = IDG | (1u << 15);
+      auto issue_grads = [&](int g, int st, bool first, int t, int kb, bool last) {
+        mbar_wait(p_full, g & 1);
+        if (first && t > 0) mbar_wait(acc_empty, (t - 1) & 1);  // previous dK/dV drained
+        ATTN_TRACE_P(23, g);
+        fence_after();
+        const uint32_t bo = su32(sO + st * QB), bq = su32(sQ + st * QB), bk = su32(sK + kb * KB);
+        const uint32_t ads = su32(sDS + (g & 1) * 32768);
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk)  // dV += P^T dO (P^T from TMEM)
+          mma_ts(tmem + colDV, tmem + colP + kk * 8, sw128(bo + kk * 2048, QB, 1024), IDG,
+                 (!first || kk > 0) ? 1u : 0u);
+        commit(pv_done);
+        if (g > 0) mbar_wait(dq_free, (g - 1) & 1);  // the previous tile's dQ drained
+        fence_after();
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk)  // dK += dS^T Q (dS^T K-major in smem)
+          mma(tmem + colDK, sw128(ads + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+              sw128(bq + kk * 2048, QB, 1024), IDG, (!first || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk)  // dQ_tile = dS K (dS MN-major in smem, K MN-major)
+          mma(tmem + colDQ, sw128(ads + kk * 2048, 16384, 1024), sw128(bk + kk * 2048, KB, 1024),
+              IDQ, kk > 0 ? 1u : 0u);
+        commit(gq_done);
+        commit(&q_empty[st]);
+        if (last) commit(&k_empty[kb]);  // this key tile's K no longer read
+      };
+      int ti = 0, gi = 0;
+      int pend = -1, pend_st = 0, pend_t = 0, pend_kb = 0;
+      bool pend_first = false, pend_last = false;
+      for (int bh = blockIdx.x; bh < a.BH; bh += gridDim.x) {
+        for (int kk = 0; kk < nt; ++kk, ++ti) {
+          const int kt = desc ? nt - 1 - kk : kk;
+          const int kb = ti % NKF2;
+          mbar_wait(&k_full[kb], (ti / NKF2) & 1);
+          mbar_wait(v_full, ti & 1);
+          const uint32_t ak = su32(sK + kb * KB), av = su32(sV);
+          for (int qt = kt; qt < nt; ++qt, ++gi) {
+            const int st = gi % NRF;
+            mbar_wait(&q_full[st], (gi / NRF) & 1);
+            ATTN_TRACE_P(21, gi);
+            mbar_wait(s_empty, (gi & 1) ^ 1);
+            ATTN_TRACE_P(22, gi);
+            fence_after();
+            const uint32_t bq = su32(sQ + st * QB), bo = su32(sO + st * QB);
+#pragma unroll
+            for (int k4 = 0; k4 < HD / 16; ++k4)  // S^T = K Q^T
+              mma(tmem + 0, sw128(ak + k4 * 32, 16, 1024), sw128(bq + k4 * 32, 16, 1024), IDS,
+                  k4 > 0 ? 1u : 0u);
+#pragma unroll
+            for (int k4 = 0; k4 < HD / 16; ++k4)  // dP^T = V dO^T
+              mma(tmem + colDP, sw128(av + k4 * 32, 16, 1024), sw128(bo + k4 * 32, 16, 1024), IDS,
+                  k4 > 0 ? 1u : 0u);
+            commit(s_full);
+            if (qt == nt - 1) commit(v_empty);  // the key tile's V no longer read
+            if (pend >= 0) issue_grads(pend, pend_st, pend_first, pend_t, pend_kb, pend_last);
+            pend = gi;
+            pend_st = st;
+            pend_first = qt == kt;
+            pend_t = ti;
+            pend_kb = kb;
+            pend_last = qt == nt - 1;
+          }
+        }
+      }
+      if (pend >= 0) issue_grads(pend, pend_st, pend_first, pend_t, pend_kb, pend_last);
+    }
+  } else {
+    // ===== softmax: thread = key row r (TMEM lane) x 32 query columns (group cg) =====
+    const int q = warp & 3, cg = (warp - 2) >> 2;
+    const int r = q * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    // this thread's 16-byte chunks of the dS^T row r (queries cg*32 + 8t .. +7)
+    const uint32_t ds_row = su32(sDS) + (cg >> 1) * 16384 + r * 128;
+    // dQ of the previous tile (drained one tile late: its MMA runs under this
+    // tile's softmax) and where it goes
+    auto emit_dq = [&](const uint32_t (&u)[GPH], int p_bh, int p_qt, int p_kt) {
+      float* acc = a.dqa + (((int64_t)p_bh * nt + p_qt) * (HD / 4) + cg * (GPH / 4)) * (4 * T) + 4 * r;
+      const bool first = desc ? p_kt == p_qt : p_kt == 0, fin = desc ? p_kt == 0 : p_kt == p_qt;
+      if (!fin) {
+#pragma unroll
+        for (int c = 0; c < GPH / 4; ++c) {
+          const float4 v = make_float4(__uint_as_float(u[4 * c]), __uint_as_float(u[4 * c + 1]),
+                                       __uint_as_float(u[4 * c + 2]), __uint_as_float(u[4 * c + 3]));
+          if (first) st_relaxed_f4(acc + c * 4 * T, v);
+          else red_add_f4(acc + c * 4 * T, v);
+        }
+        return;
+      }
+      // dQ_i's last contribution: finish the row
+      const int b = p_bh / a.H, h = p_bh % a.H, qrow = p_qt * T + r;
+      const bool live = qrow < a.S;
+      float f[GPH];
+#pragma unroll
+      for (int c = 0; c < GPH / 4; ++c) {
+        float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (!first) s = ld_relaxed_f4(acc + c * 4 * T);
+        f[4 * c] = live ? (s.x + __uint_as_float(u[4 * c])) * a.scale : 0.f;
+        f[4 * c + 1] = live ? (s.y + __uint_as_float(u[4 * c + 1])) * a.scale : 0.f;
+        f[4 * c + 2] = live ? (s.z + __uint_as_float(u[4 * c + 2])) * a.scale : 0.f;
+        f[4 * c + 3] = live ? (s.w + __uint_as_float(u[4 * c + 3])) * a.scale : 0.f;
+      }
+      if (live) {
+        bf16* row = a.g0 + (int64_t)(b * a.S + qrow) * a.d + h * HD + cg * GPH;
+#pragma unroll
+        for (int i = 0; i < GPH; i += 8)
+          *reinterpret_cast<uint4*>(row + i) = make_uint4(pk(f[i], f[i + 1]), pk(f[i + 2], f[i + 3]),
+                                                          pk(f[i + 4], f[i + 5]), pk(f[i + 6], f[i + 7]));
+      }
+      if (a.s0 && p_qt * T + q * 32 < a.S)
+        warp_colsum<GPH>(f, a.s0 + ((int64_t)b * a.nblk + p_qt * (T / 32) + q) * a.d + h * HD + cg * GPH);
+    };
+    // drain the dQ of tile g (its products retired) and let the issuer reuse it
+    auto drain_dq = [&](int g, uint32_t (&u)[GPH]) {
+      mbar_wait(gq_done, g & 1);
+      fence_after();
+      TMEM_LD16(tmem + lane_off + colDQ + cg * GPH, u);
+      tmem_wait_ld();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dq_free);
+    };
+    int gi = 0;
+    int p_bh = 0, p_qt = 0, p_kt = 0;
+    for (int bh = blockIdx.x; bh < a.BH; bh += gridDim.x) {
+      const int b = bh / a.H, h = bh % a.H, row_base = b * a.S;
+      for (int kk = 0; kk < nt; ++kk) {
+        const int kt = desc ? nt - 1 - kk : kk;
+        const int key = kt * T + r;
+        const bool key_live = key < a.S;
+        for (int qt = kt; qt < nt; ++qt, ++gi) {
+          const int st = gi % NRF, q0 = qt * T;
+          mbar_wait(&q_full[st], (gi / NRF) & 1);  // L, D of this query tile visible
+          mbar_wait(s_full, gi & 1);
+          if (warp == 2 && lane == 0) ATTN_TRACE_P(25, gi);
+          fence_after();
+          const float* L = sL + st * T + cg * CPQ;
+          const float* D = sD + st * T + cg * CPQ;
+          const bool masked = (kt * T + T > q0) || (kt * T + T > a.S);
+          uint32_t pp[CPQ / 2], dd[CPQ / 2];
+          // two halves of 16 columns (96 registers at 576 threads): the second
+          // half's scores are loaded after the first half's exponentials
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            uint32_t s[CPQ / 2], dp[CPQ / 2];
+            TMEM_LD16(tmem + lane_off + cg * CPQ + hf * 16, s);
+            TMEM_LD16(tmem + lane_off + colDP + cg * CPQ + hf * 16, dp);
+            tmem_wait_ld();
+            if (hf == 1) {
+              fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(s_empty);
+              if (lane == 0) ATTN_TRACE_MAX(24, gi);
+            }
+#pragma unroll
+            for (int i4 = 0; i4 < CPQ / 8; ++i4) {
+              const int i = hf * (CPQ / 8) + i4;
+              const float4 l4 = lds_f4(L + 4 * i), d4 = lds_f4(D + 4 * i);
+              float p0 = ex2(fmaf(__uint_as_float(s[4 * i4]), a.sl2, -l4.x));
+              float p1 = ex2(fmaf(__uint_as_float(s[4 * i4 + 1]), a.sl2, -l4.y));
+              float p2 = ex2(fmaf(__uint_as_float(s[4 * i4 + 2]), a.sl2, -l4.z));
+              float p3 = ex2(fmaf(__uint_as_float(s[4 * i4 + 3]), a.sl2, -l4.w));
+              if (masked) {
+                const int qc = q0 + cg * CPQ + 4 * i;
+                p0 = (key_live && key <= qc) ? p0 : 0.f;
+                p1 = (key_live && key <= qc + 1) ? p1 : 0.f;
+                p2 = (key_live && key <= qc + 2) ? p2 : 0.f;
+                p3 = (key_live && key <= qc + 3) ? p3 : 0.f;
+              }
+              pp[2 * i] = pk(p0, p1);
+              pp[2 * i + 1] = pk(p2, p3);
+              dd[2 * i] = pk(p0 * (__uint_as_float(dp[4 * i4]) - d4.x),
+                             p1 * (__uint_as_float(dp[4 * i4 + 1]) - d4.y));
+              dd[2 * i + 1] = pk(p2 * (__uint_as_float(dp[4 * i4 + 2]) - d4.z),
+                                 p3 * (__uint_as_float(dp[4 * i4 + 3]) - d4.w));
+            }
+          }
+          if (warp == 2 && lane == 0) ATTN_TRACE_P(26, gi);
+          if (lane == 0) ATTN_TRACE_MAX(30, gi);
+          // dS^T into buffer gi & 1 (its last readers, tile gi-2's dK / dQ
+          // products, retired before tile gi-1 drained their dQ)
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            sts128(ds_row + (gi & 1) * 32768 + ((((cg & 1) * 4 + t) ^ (r & 7)) << 4), dd[4 * t],
+                   dd[4 * t + 1], dd[4 * t + 2], dd[4 * t + 3]);
+          // P^T is free once the previous tile's dV product retired
+          if (gi >= 1) mbar_wait(pv_done, (gi - 1) & 1);
+          if (warp == 2 && lane == 0) ATTN_TRACE_P(27, gi);
+          fence_after();
+          tmem_st_cols<CPQ / 2>(tmem + lane_off + colP + cg * (CPQ / 2), pp);
+          tmem_wait_st();
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(p_full);
+          if (warp == 2 && lane == 0) ATTN_TRACE_P(28, gi);
+          if (gi >= 1) {
+            uint32_t dqv[GPH];
+            drain_dq(gi - 1, dqv);
+            emit_dq(dqv, p_bh, p_qt, p_kt);
+          }
+          if (warp == 2 && lane == 0) ATTN_TRACE_P(29, gi);
+          if (lane == 0) ATTN_TRACE_MAX(31, gi);
+          p_bh = bh;
+          p_qt = qt;
+          p_kt = kt;
+        }
+        // the key tile's dK / dV are complete once its last products retire
+        mbar_wait(pv_done, (gi - 1) & 1);
+        mbar_wait(gq_done, (gi - 1) & 1);
+        fence_after();
+        const int64_t row = (int64_t)(row_base + key) * a.d + h * HD + cg * GPH;
+        const bool sums = a.s1 && kt * T + q * 32 < a.S;
+        const int64_t prow = ((int64_t)b * a.nblk + kt * (T / 32) + q) * a.d + h * HD + cg * GPH;
+        float fk[GPH], fv[GPH];
+        store_acc_rows<GPH>(tmem + lane_off + colDK + cg * GPH, a.g1 + row, a.scale, key_live, fk);
+        store_acc_rows<GPH>(tmem + lane_off + colDV + cg * GPH, a.g2 + row, 1.f, key_live, fv);
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty);
+        if (sums) {
+          warp_colsum<GPH>(fk, a.s1 + prow);
+          warp_colsum<GPH>(fv, a.s2 + prow);
+        }
+      }
+    }
+    if (gi >= 1) {  // the last tile's dQ
+      uint32_t dqv[GPH];
+      drain_dq(gi - 1, dqv);
+      emit_dq(dqv, p_bh, p_qt, p_kt);
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -1194,9 +1611,10 @@ extern "C" int photon_debug_attn_trace(unsigned long long* out, int n) {
 
 bool attn_tc_supported(int dh, int d) { return (dh == 64 || dh == 128) && (d % 8) == 0; }
 
-size_t attn_bwd_tc_ws_floats(int B, int S, int H) {
+size_t attn_bwd_tc_ws_floats(int B, int S, int H, int d) {
   const size_t Spad = (size_t)(S + TQ - 1) / TQ * TQ;
-  return (size_t)2 * B * H * Spad;
+  // L, D; at head dim 64 the fused pass's fp32 dQ accumulator
+  return (size_t)2 * B * H * Spad + (PHOTON_ATTN_FUSED && d == 64 * H ? (size_t)B * H * Spad * 64 : 0);
 }
 
 namespace {
@@ -1206,7 +1624,7 @@ void attn_bwd_hd(const bf16* q, const bf16* k, const bf16* v, const bf16* o, con
                  const float* lse, bf16* dq, bf16* dk, bf16* dv, int B, int S, int H, int d,
                  float* ws, float* sums, cudaStream_t st) {
   const int nt = (S + TQ - 1) / TQ, Spad = nt * TQ, rows = B * S;
-  if (!ws) ws = scratch(attn_bwd_tc_ws_floats(B, S, H));
+  if (!ws) ws = scratch(attn_bwd_tc_ws_floats(B, S, H, d));
   float* Lp = ws;
   float* Dp = Lp + (size_t)B * H * Spad;
   attn_bwd_prep_kernel<HD><<<std::min<int64_t>(((int64_t)B * S + 7) / 8, kNumSMs * 16), 256, 0,
@@ -1221,6 +1639,24 @@ void attn_bwd_hd(const bf16* q, const bf16* k, const bf16* v, const bf16* o, con
   const size_t P = (size_t)B * nblk * d;  // sums: dq, dk, dv partials
   BwdArgs a{S,  H,  d,  Spad, B * H, rsqrtf((float)HD) * kLog2e, rsqrtf((float)HD), Lp, Dp, dk, dv,
             sums ? sums + P : nullptr, sums ? sums + 2 * P : nullptr, nblk};
+  if constexpr (HD == 64 && PHOTON_ATTN_FUSED) {
+    a.g0 = dq;
+    a.g1 = dk;
+    a.g2 = dv;
+    a.s0 = sums;
+    a.s1 = sums ? sums + P : nullptr;
+    a.s2 = sums ? sums + 2 * P : nullptr;
+    a.dqa = Dp + (size_t)B * H * Spad;
+    static std::atomic<uint64_t> cfgf{0};
+    set_smem_once(cfgf, attn_bwd_fused64_tc_kernel, kFusedSmem);
+    // as many CTAs as keep the waves of heads even (e.g. 384 heads: 128 x 3)
+    const int waves = (B * H + kNumSMs - 1) / kNumSMs;
+    const int grid = PHOTON_FUSED_GRID ? std::min(kNumSMs, (B * H + waves - 1) / waves)
+                                       : std::min(kNumSMs, B * H);
+    attn_bwd_fused64_tc_kernel<<<grid, kBwdThreads, kFusedSmem, st>>>(mq, mk, mv, mo, a);
+    PH_LAUNCH_CHECK();
+    return;
+  }
   constexpr int NA = HD / 64;
   constexpr int NKV = HD == 64 ? NKV64 : 1, NRQ = HD == 64 ? NRQ64 : 2, NQO = HD == 64 ? 2 : 1;
   constexpr int NRK = HD == 64 ? NR64 : NR;

@@ -707,6 +707,8 @@ int photon_ctx_set_timing(photon_ctx* ctx, int on) {
   return PHOTON_OK;
 }
 
+uint64_t photon_launch_count(void) { return launch_counter().load(); }
+
 int photon_ctx_kernel_times(photon_ctx* ctx, double* t) {
   const KernelTimes& k = ctx->c.eng->times;
   t[0] = k.gemm_ms;

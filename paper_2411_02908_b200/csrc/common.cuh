@@ -21,7 +21,18 @@ namespace photon {
                                                  __FILE__ + ":" + std::to_string(__LINE__)); \
   } while (0)
 
-#define PH_LAUNCH_CHECK() PH_CUDA(cudaGetLastError())
+// Every kernel launch site is followed by exactly one PH_LAUNCH_CHECK, which
+// also counts the launch (photon_launch_count; a CUDA graph replay adds the
+// kernel nodes it holds, see Ctx::launch_local_round).
+inline std::atomic<uint64_t>& launch_counter() {
+  static std::atomic<uint64_t> n{0};
+  return n;
+}
+#define PH_LAUNCH_CHECK()                                                  \
+  do {                                                                     \
+    PH_CUDA(cudaGetLastError());                                           \
+    ::photon::launch_counter().fetch_add(1, std::memory_order_relaxed);    \
+  } while (0)
 
 using bf16 = __nv_bfloat16;
 

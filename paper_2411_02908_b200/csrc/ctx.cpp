@@ -187,6 +187,7 @@ void Ctx::launch_local_round(const photon_train_cfg& t, const DeviceBatches& db,
                           stream));
   if (!g.exec && g.seen++ >= 1) {
     cudaGraph_t graph = nullptr;
+    const uint64_t n0 = launch_counter().load();
     PH_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
     try {
       enqueue_local_round(*this, t, db, d_theta_in, d_theta_out, step_base, d_loss, d_flag,
@@ -199,6 +200,18 @@ void Ctx::launch_local_round(const photon_train_cfg& t, const DeviceBatches& db,
       throw;
     }
     PH_CUDA(cudaStreamEndCapture(stream, &graph));
+    // captured launches did not run: count the graph's kernel nodes per replay
+    launch_counter().fetch_sub(launch_counter().load() - n0);
+    size_t nn = 0;
+    PH_CUDA(cudaGraphGetNodes(graph, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    if (nn) PH_CUDA(cudaGraphGetNodes(graph, nodes.data(), &nn));
+    g.kernels = 0;
+    for (auto nd : nodes) {
+      cudaGraphNodeType ty;
+      PH_CUDA(cudaGraphNodeGetType(nd, &ty));
+      g.kernels += ty == cudaGraphNodeTypeKernel;
+    }
     const cudaError_t ie = cudaGraphInstantiate(&g.exec, graph, 0);
     cudaGraphDestroy(graph);
     if (ie != cudaSuccess) {
@@ -207,8 +220,11 @@ void Ctx::launch_local_round(const photon_train_cfg& t, const DeviceBatches& db,
       graphs_on = false;
     }
   }
-  if (g.exec) PH_CUDA(cudaGraphLaunch(g.exec, stream));
-  else enqueue_local_round(*this, t, db, d_theta_in, d_theta_out, step_base, d_loss, d_flag,
+  if (g.exec) {
+    PH_CUDA(cudaGraphLaunch(g.exec, stream));
+    launch_counter().fetch_add(g.kernels);
+  } else
+    enqueue_local_round(*this, t, db, d_theta_in, d_theta_out, step_base, d_loss, d_flag,
                            d_lr.ptr);
 }
 

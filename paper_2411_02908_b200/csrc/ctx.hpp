@@ -121,6 +121,7 @@ struct Ctx {
   struct RoundGraph {
     cudaGraphExec_t exec = nullptr;
     int seen = 0;
+    uint64_t kernels = 0;  // kernel nodes (added to launch_counter per replay)
   };
   std::map<std::string, RoundGraph> graphs;
   bool graphs_on = true;

@@ -166,7 +166,7 @@ class EngineT final : public Engine {
       Dvec_ = carve<float>(p, rows_bhs);
       gemm_ws_ = sizeof(T) == 2 ? carve<float>(p, kGemmWsFloats) : nullptr;
       attn_ws_ = sizeof(T) == 2 && k::attn_tc_supported((int)(d_ / H_), (int)d_)
-                     ? carve<float>(p, k::attn_bwd_tc_ws_floats((int)max_batch, (int)Smax_, (int)H_))
+                     ? carve<float>(p, k::attn_bwd_tc_ws_floats((int)max_batch, (int)Smax_, (int)H_, (int)d_))
                      : nullptr;
       part_ = carve<float>(p, part_floats);
       dxT_ = carve<T>(p, M * d);

@@ -89,7 +89,7 @@ void attn_fwd_tc(const bf16* q, const bf16* k, const bf16* v, bf16* o, float* ls
                  int H, int d, cudaStream_t st);
 // Fused deterministic backward; ws = attn_bwd_tc_ws_floats() floats of device
 // workspace owned by the caller (nullptr: a per-device scratch, debug use only).
-size_t attn_bwd_tc_ws_floats(int B, int S, int H);
+size_t attn_bwd_tc_ws_floats(int B, int S, int H, int d);
 void attn_bwd_tc(const bf16* q, const bf16* k, const bf16* v, const bf16* o, const bf16* dO,
                  const float* lse, bf16* dq, bf16* dk, bf16* dv, int B, int S, int H, int d,
                  float* ws, cudaStream_t st, float* sums = nullptr);
