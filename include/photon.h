@@ -281,11 +281,11 @@ int photon_debug_ce(void* logits, int logits_bf16, const int32_t* targets, int M
                     photon_err* err);
 
 /* LayerNorm forward (+ backward when dy != NULL) on device pointers, as the
- * engine runs them (tensor.cpp:322-394): x, gain, bias, dy, dres fp32; y and
+ * engine runs them (tensor.cpp:322-394): x, gain, bias, dres fp32; y, dy and
  * dxT bf16 when y_bf16 else fp32; mean / rstd fp32 [M]; dx = dres + LN'(dy);
  * dgain / dbias [d]; dsum (optional) = column sums of dx. */
 int photon_debug_layernorm(int y_bf16, int M, int d, const float* x, const float* gain,
-                           const float* bias, void* y, float* mean, float* rstd, const float* dy,
+                           const float* bias, void* y, float* mean, float* rstd, const void* dy,
                            const float* dres, float* dx, void* dxT, float* dgain, float* dbias,
                            float* dsum, double* ms, photon_err* err);
 

@@ -95,6 +95,30 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
       : "memory");
 }
+// L2 eviction-priority policies for TMA loads / stores (createpolicy)
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                 int c0, int c1, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void st_hint_u4(void* p, uint4 v, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w), "l"(policy)
+               : "memory");
+}
 __device__ __forceinline__ void fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
@@ -620,7 +644,7 @@ constexpr int NR64 = PHOTON_ATTN_NR64;
 // a dead row) for warp_colsum.
 template <int N>
 __device__ __forceinline__ void store_acc_rows(uint32_t taddr, bf16* row_ptr, float mul, bool live,
-                                               float (&f)[N]) {
+                                               float (&f)[N], uint64_t policy = 0) {
   uint32_t u[N];
   if constexpr (N == 32) TMEM_LD32(taddr, u);
   else TMEM_LD16(taddr, u);
@@ -629,9 +653,12 @@ __device__ __forceinline__ void store_acc_rows(uint32_t taddr, bf16* row_ptr, fl
   for (int i = 0; i < N; ++i) f[i] = live ? __uint_as_float(u[i]) * mul : 0.f;
   if (live) {
 #pragma unroll
-    for (int i = 0; i < N; i += 8)
-      *reinterpret_cast<uint4*>(row_ptr + i) = make_uint4(pk(f[i], f[i + 1]), pk(f[i + 2], f[i + 3]),
-                                                          pk(f[i + 4], f[i + 5]), pk(f[i + 6], f[i + 7]));
+    for (int i = 0; i < N; i += 8) {
+      const uint4 w = make_uint4(pk(f[i], f[i + 1]), pk(f[i + 2], f[i + 3]), pk(f[i + 4], f[i + 5]),
+                                 pk(f[i + 6], f[i + 7]));
+      if (policy) st_hint_u4(row_ptr + i, w, policy);
+      else *reinterpret_cast<uint4*>(row_ptr + i) = w;
+    }
   }
 }
 // Column sums of the warp's 32 rows of f (the bias gradients' partials): a
@@ -1170,6 +1197,9 @@ constexpr int NRF = PHOTON_ATTN_NRF, NKF2 = PHOTON_ATTN_NKF;
 #ifndef PHOTON_FUSED_ALT
 #define PHOTON_FUSED_ALT 1
 #endif
+#ifndef PHOTON_FUSED_HINTS
+#define PHOTON_FUSED_HINTS 1
+#endif
 #ifndef PHOTON_FUSED_GRID
 #define PHOTON_FUSED_GRID 1
 #endif
@@ -1269,6 +1299,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ===== producer: K, V per key tile, the Q / dO / L / D ring =====
+      // K / V are read once per head (evict first); a head's Q / dO are re-read
+      // by every key tile (evict last)
+      const uint64_t pol_once = PHOTON_FUSED_HINTS ? policy_evict_first() : 0;
+      const uint64_t pol_keep = PHOTON_FUSED_HINTS ? policy_evict_last() : 0;
       int ti = 0, gi = 0;
       for (int bh = blockIdx.x; bh < a.BH; bh += gridDim.x) {
         const int b = bh / a.H, h = bh % a.H, row_base = b * a.S;
@@ -1277,17 +1311,28 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           const int kb = ti % NKF2;
           mbar_wait(&k_empty[kb], ((ti / NKF2) & 1) ^ 1);
           mbar_expect_tx(&k_full[kb], KB);
-          tma_load_2d(sK + kb * KB, &tk, &k_full[kb], h * HD, row_base + kt * T);
+          if (PHOTON_FUSED_HINTS)
+            tma_load_2d_hint(sK + kb * KB, &tk, &k_full[kb], h * HD, row_base + kt * T, pol_once);
+          else
+            tma_load_2d(sK + kb * KB, &tk, &k_full[kb], h * HD, row_base + kt * T);
           mbar_wait(v_empty, (ti & 1) ^ 1);
           mbar_expect_tx(v_full, KB);
-          tma_load_2d(sV, &tv, v_full, h * HD, row_base + kt * T);
+          if (PHOTON_FUSED_HINTS)
+            tma_load_2d_hint(sV, &tv, v_full, h * HD, row_base + kt * T, pol_once);
+          else
+            tma_load_2d(sV, &tv, v_full, h * HD, row_base + kt * T);
           for (int qt = kt; qt < nt; ++qt, ++gi) {
             const int st = gi % NRF;
             mbar_wait(&q_empty[st], ((gi / NRF) & 1) ^ 1);
             ATTN_TRACE_P(20, gi);
             mbar_expect_tx(&q_full[st], 2 * QB + 8 * T);
-            tma_load_2d(sQ + st * QB, &tq, &q_full[st], h * HD, row_base + qt * T);
-            tma_load_2d(sO + st * QB, &tdo, &q_full[st], h * HD, row_base + qt * T);
+            if (PHOTON_FUSED_HINTS) {
+              tma_load_2d_hint(sQ + st * QB, &tq, &q_full[st], h * HD, row_base + qt * T, pol_keep);
+              tma_load_2d_hint(sO + st * QB, &tdo, &q_full[st], h * HD, row_base + qt * T, pol_keep);
+            } else {
+              tma_load_2d(sQ + st * QB, &tq, &q_full[st], h * HD, row_base + qt * T);
+              tma_load_2d(sO + st * QB, &tdo, &q_full[st], h * HD, row_base + qt * T);
+            }
             bulk_load(sL + st * T, a.Lp + (int64_t)bh * a.Spad + qt * T, 4 * T, &q_full[st]);
             bulk_load(sD + st * T, a.Dp + (int64_t)bh * a.Spad + qt * T, 4 * T, &q_full[st]);
           }
@@ -1374,6 +1419,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // ===== softmax: thread = key row r (TMEM lane) x 32 query columns (group cg) =====
     const int q = warp & 3, cg = (warp - 2) >> 2;
     const int r = q * 32 + lane;
+    const uint64_t pol_out = PHOTON_FUSED_HINTS ? policy_evict_first() : 0;  // dq / dk / dv rows
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     // this thread's 16-byte chunks of the dS^T row r (queries cg*32 + 8t .. +7)
     const uint32_t ds_row = su32(sDS) + (cg >> 1) * 16384 + r * 128;
@@ -1408,9 +1454,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (live) {
         bf16* row = a.g0 + (int64_t)(b * a.S + qrow) * a.d + h * HD + cg * GPH;
 #pragma unroll
-        for (int i = 0; i < GPH; i += 8)
-          *reinterpret_cast<uint4*>(row + i) = make_uint4(pk(f[i], f[i + 1]), pk(f[i + 2], f[i + 3]),
-                                                          pk(f[i + 4], f[i + 5]), pk(f[i + 6], f[i + 7]));
+        for (int i = 0; i < GPH; i += 8) {
+          const uint4 w = make_uint4(pk(f[i], f[i + 1]), pk(f[i + 2], f[i + 3]), pk(f[i + 4], f[i + 5]),
+                                     pk(f[i + 6], f[i + 7]));
+          if (pol_out) st_hint_u4(row + i, w, pol_out);
+          else *reinterpret_cast<uint4*>(row + i) = w;
+        }
       }
       if (a.s0 && p_qt * T + q * 32 < a.S)
         warp_colsum<GPH>(f, a.s0 + ((int64_t)b * a.nblk + p_qt * (T / 32) + q) * a.d + h * HD + cg * GPH);
@@ -1518,8 +1567,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const bool sums = a.s1 && kt * T + q * 32 < a.S;
         const int64_t prow = ((int64_t)b * a.nblk + kt * (T / 32) + q) * a.d + h * HD + cg * GPH;
         float fk[GPH], fv[GPH];
-        store_acc_rows<GPH>(tmem + lane_off + colDK + cg * GPH, a.g1 + row, a.scale, key_live, fk);
-        store_acc_rows<GPH>(tmem + lane_off + colDV + cg * GPH, a.g2 + row, 1.f, key_live, fv);
+        store_acc_rows<GPH>(tmem + lane_off + colDK + cg * GPH, a.g1 + row, a.scale, key_live, fk, pol_out);
+        store_acc_rows<GPH>(tmem + lane_off + colDV + cg * GPH, a.g2 + row, 1.f, key_live, fv, pol_out);
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty);

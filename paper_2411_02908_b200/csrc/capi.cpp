@@ -616,11 +616,11 @@ int photon_debug_ce(void* logits, int logits_bf16, const int32_t* targets, int M
 }
 
 // LayerNorm forward (and, with dy != NULL, backward) exactly as the engine runs
-// them (tensor.cpp:322-394): y in bf16 when y_bf16 else fp32; the backward
+// them (tensor.cpp:322-394): y, dy and dxT in bf16 when y_bf16 else fp32; the backward
 // writes dx = dres + LN'(dy) (dres may be NULL), its bf16/fp32 copy dxT, the
 // gain / bias gradients and (dsum != NULL) the column sums of dx.
 int photon_debug_layernorm(int y_bf16, int M, int d, const float* x, const float* gain,
-                           const float* bias, void* y, float* mean, float* rstd, const float* dy,
+                           const float* bias, void* y, float* mean, float* rstd, const void* dy,
                            const float* dres, float* dx, void* dxT, float* dgain, float* dbias,
                            float* dsum, double* ms, photon_err* err) {
   return guarded(err, [&] {
@@ -641,12 +641,14 @@ int photon_debug_layernorm(int y_bf16, int M, int d, const float* x, const float
     if (y_bf16) {
       k::ln_fwd<bf16>(x, gain, bias, static_cast<bf16*>(y), mean, rstd, M, d, st);
       if (dy)
-        k::ln_bwd<bf16>(dy, x, mean, rstd, gain, dres, dx, static_cast<bf16*>(dxT), part.ptr,
+        k::ln_bwd<bf16>(static_cast<const bf16*>(dy), x, mean, rstd, gain, dres, dx,
+                        static_cast<bf16*>(dxT), part.ptr,
                         dgain, dbias, M, d, st, dsum);
     } else {
       k::ln_fwd<float>(x, gain, bias, static_cast<float*>(y), mean, rstd, M, d, st);
       if (dy)
-        k::ln_bwd<float>(dy, x, mean, rstd, gain, dres, dx, static_cast<float*>(dxT), part.ptr,
+        k::ln_bwd<float>(static_cast<const float*>(dy), x, mean, rstd, gain, dres, dx,
+                         static_cast<float*>(dxT), part.ptr,
                          dgain, dbias, M, d, st, dsum);
     }
     PH_CUDA(cudaEventRecord(e1, st));

@@ -94,6 +94,9 @@ class EngineT final : public Engine {
   T *h_, *q_, *k_, *v_, *o_, *h2_, *pre_, *u_, *xf_, *logits_;
   // backward scratch
   float *dx_, *dy_, *Dvec_, *part_, *attn_ws_, *gemm_ws_;
+  // the LayerNorm backwards' input gradient in the activation type (bf16 on the
+  // tensor-core path: the dX GEMMs write it directly; fp32 mode: dy_ itself)
+  T* dyT_;
   T *dxT_, *dpre_, *dq_, *dk_, *dv_, *dO_;
   double* rowloss_;
   // timing
@@ -163,6 +166,7 @@ class EngineT final : public Engine {
       logits_ = carve<T>(p, M * V_);
       dx_ = carve<float>(p, M * d);
       dy_ = carve<float>(p, M * d);
+      dyT_ = sizeof(T) == 4 ? reinterpret_cast<T*>(dy_) : carve<T>(p, M * d);
       Dvec_ = carve<float>(p, rows_bhs);
       gemm_ws_ = sizeof(T) == 2 ? carve<float>(p, kGemmWsFloats) : nullptr;
       attn_ws_ = sizeof(T) == 2 && k::attn_tc_supported((int)(d_ / H_), (int)d_)
@@ -384,12 +388,12 @@ void EngineT<T>::micro(const StepBatch& bt, double* loss_dev, bool backward, boo
     Scope sc(this, 2, 0);
     k::colsum<T>(logits_, M, V, part_, G(off_.head_b), stream, acc);
   }
-  mm(M, d, V, logits_, V, true, W(off_.head_w), V, true, dy_, d, DT::F32, Epi::Store);
+  mm(M, d, V, logits_, V, true, W(off_.head_w), V, true, dyT_, d, TT, Epi::Store);
   mm(d, V, M, xf_, d, false, logits_, V, false, G(off_.head_w), V, DT::F32, WG);
   {
     Scope sc(this, 2, 0);
     // the column sums of its output are the last block's b2 gradient
-    k::ln_bwd<T>(dy_, xL, meanf_, rstdf_, Pm(off_.lnfg), nullptr, dx_, dxT_, part_, G(off_.lnfg),
+    k::ln_bwd<T>(dyT_, xL, meanf_, rstdf_, Pm(off_.lnfg), nullptr, dx_, dxT_, part_, G(off_.lnfg),
                  G(off_.lnfb), M, d, stream, G(off_.blocks[L - 1].b2), acc);
   }
   for (int l = L - 1; l >= 0; --l) {
@@ -421,12 +425,12 @@ void EngineT<T>::micro(const StepBatch& bt, double* loss_dev, bool backward, boo
       else
         k::colsum<T>(dpre_, M, hid, part_, G(o.b1), stream, acc);
     }
-    mm(M, d, hid, dpre_, hid, true, W(o.w1), hid, true, dy_, d, DT::F32, Epi::Store);
+    mm(M, d, hid, dpre_, hid, true, W(o.w1), hid, true, dyT_, d, TT, Epi::Store);
     mm(d, hid, M, h2, d, false, dpre_, hid, false, G(o.w1), hid, DT::F32, WG);
     {
       Scope sc(this, 2, 0);
       // x_mid = x + (o Wo + bo): dbo = column sums of this output
-      k::ln_bwd<T>(dy_, xm, mean2_ + (size_t)l * M, rstd2_ + (size_t)l * M, Pm(o.ln2g), dx_, dx_,
+      k::ln_bwd<T>(dyT_, xm, mean2_ + (size_t)l * M, rstd2_ + (size_t)l * M, Pm(o.ln2g), dx_, dx_,
                    dxT_, part_, G(o.ln2g), G(o.ln2b), M, d, stream, G(o.bo), acc);
     }
     mm(M, d, d, dxT_, d, true, W(o.wo), d, true, dO_, d, TT, Epi::Store);
@@ -458,7 +462,7 @@ void EngineT<T>::micro(const StepBatch& bt, double* loss_dev, bool backward, boo
       g.A = dv_; g.lda = d; g.a_kmajor = true;
       g.B = W(o.wv); g.ldb = d; g.b_kmajor = true;
       g.ab = dt_of<T>();
-      g.C = dy_; g.ldc = d; g.c = DT::F32;
+      g.C = dyT_; g.ldc = d; g.c = dt_of<T>();
       g.epi = Epi::Store;
       g.nseg = 3;
       g.A_seg[1] = dk_; g.B_seg[1] = W(o.wk);
@@ -470,6 +474,7 @@ void EngineT<T>::micro(const StepBatch& bt, double* loss_dev, bool backward, boo
       mm(M, d, d, dv_, d, true, W(o.wv), d, true, dy_, d, DT::F32, Epi::Store);
       mm(M, d, d, dk_, d, true, W(o.wk), d, true, dy_, d, DT::F32, Epi::Accum);
       mm(M, d, d, dq_, d, true, W(o.wq), d, true, dy_, d, DT::F32, Epi::Accum);
+      if (sizeof(T) == 2) k::f32_to_bf16(dy_, reinterpret_cast<bf16*>(dyT_), (uint64_t)M * d, stream);
     }
     mm(d, d, M, h, d, false, dv_, d, false, G(o.wv), d, DT::F32, WG);
     mm(d, d, M, h, d, false, dk_, d, false, G(o.wk), d, DT::F32, WG);
@@ -477,7 +482,7 @@ void EngineT<T>::micro(const StepBatch& bt, double* loss_dev, bool backward, boo
     {
       Scope sc(this, 2, 0);
       // the output is block l-1's x_out gradient: its column sums are db2 of l-1
-      k::ln_bwd<T>(dy_, x, mean1_ + (size_t)l * M, rstd1_ + (size_t)l * M, Pm(o.ln1g), dx_, dx_,
+      k::ln_bwd<T>(dyT_, x, mean1_ + (size_t)l * M, rstd1_ + (size_t)l * M, Pm(o.ln1g), dx_, dx_,
                    dxT_, part_, G(o.ln1g), G(o.ln1b), M, d, stream,
                    l > 0 ? G(off_.blocks[l - 1].b2) : nullptr, acc);
     }

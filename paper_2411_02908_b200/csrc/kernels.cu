@@ -277,7 +277,7 @@ int ln_bwd_parts() { return kLnBwdBlocks; }
 
 template <typename T>
 __global__ void __launch_bounds__(kLnBwdWarps * 32)
-ln_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ x,
+ln_bwd_kernel(const T* __restrict__ dy, const float* __restrict__ x,
               const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
               const float* __restrict__ gain, const float* dres, float* dx_out,
               T* __restrict__ dx_T, float* __restrict__ part, int M, int d, int nsum) {
@@ -288,13 +288,13 @@ ln_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ x,
   for (int j = lane; j < nsum * d; j += 32) my[j] = 0.f;
   const float inv_d = 1.0f / (float)d;
   for (int m = blockIdx.x * warps + warp; m < M; m += gridDim.x * warps) {
-    const float* dyr = dy + (size_t)m * d;
+    const T* dyr = dy + (size_t)m * d;
     const float* xr = x + (size_t)m * d;
     const float mean = mean_in[m], rstd = rstd_in[m];
     float s1 = 0.f, s2 = 0.f;
     for (int j = lane; j < d; j += 32) {
       const float xh = (xr[j] - mean) * rstd;
-      const float g = dyr[j];
+      const float g = to_f<T>(dyr[j]);
       const float dxh = g * gain[j];
       s1 += dxh;
       s2 += dxh * xh;
@@ -308,7 +308,7 @@ ln_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ x,
     T* outT = dx_T ? dx_T + (size_t)m * d : nullptr;
     for (int j = lane; j < d; j += 32) {
       const float xh = (xr[j] - mean) * rstd;
-      float g = rstd * (dyr[j] * gain[j] - s1 - xh * s2);
+      float g = rstd * (to_f<T>(dyr[j]) * gain[j] - s1 - xh * s2);
       if (rr) g += rr[j];
       out[j] = g;
       if (outT) outT[j] = from_f<T>(g);
@@ -435,7 +435,7 @@ constexpr int kLnBwdVecSmem(int D) { return (D / 4) * 16 + 3 * kLnBwdWarps * D *
 
 template <typename T, int NV>
 __global__ void __launch_bounds__(256, 2)
-ln_bwd_vec_kernel(const float* __restrict__ dy, const float* __restrict__ x,
+ln_bwd_vec_kernel(const T* __restrict__ dy, const float* __restrict__ x,
                   const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
                   const float* __restrict__ gain, const float* dres, float* dx_out,
                   T* __restrict__ dx_T, float* __restrict__ part, int M, int osum) {
@@ -459,13 +459,13 @@ ln_bwd_vec_kernel(const float* __restrict__ dy, const float* __restrict__ x,
   const float inv_d = 1.0f / (float)D;
   for (int m = blockIdx.x * kLnBwdWarps + warp; m < M; m += gridDim.x * kLnBwdWarps) {
     const float4* xr = reinterpret_cast<const float4*>(x + (size_t)m * D);
-    const float4* gr = reinterpret_cast<const float4*>(dy + (size_t)m * D);
+    const T* gr = dy + (size_t)m * D;
     const float4* rr = dres ? reinterpret_cast<const float4*>(dres + (size_t)m * D) : nullptr;
     float4 xv[NV], gv[NV], rv[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       xv[i] = xr[lane + 32 * i];
-      gv[i] = gr[lane + 32 * i];
+      gv[i] = ld4f(gr + 4 * (lane + 32 * i));
       rv[i] = rr ? rr[lane + 32 * i] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     const float mean = mean_in[m], rstd = rstd_in[m];
@@ -532,7 +532,7 @@ ln_bwd_vec_kernel(const float* __restrict__ dy, const float* __restrict__ x,
 // registers; row groups are reduced through shared memory in a fixed order.
 template <typename T, int WPR>
 __global__ void __launch_bounds__(256, 1)
-ln_bwd_split_kernel(const float* __restrict__ dy, const float* __restrict__ x,
+ln_bwd_split_kernel(const T* __restrict__ dy, const float* __restrict__ x,
                     const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
                     const float* __restrict__ gain, const float* dres, float* dx_out,
                     T* __restrict__ dx_T, float* __restrict__ part, int M, int osum) {
@@ -548,13 +548,13 @@ ln_bwd_split_kernel(const float* __restrict__ dy, const float* __restrict__ x,
   int it = 0;
   for (int m = blockIdx.x * G + grp; m < M; m += gridDim.x * G, ++it) {
     const float4* xr = reinterpret_cast<const float4*>(x + (size_t)m * D) + c4base;
-    const float4* gr = reinterpret_cast<const float4*>(dy + (size_t)m * D) + c4base;
+    const T* gr = dy + (size_t)m * D + 4 * c4base;
     const float4* rr = dres ? reinterpret_cast<const float4*>(dres + (size_t)m * D) + c4base : nullptr;
     float4 xv[NV], gv[NV], rv[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       xv[i] = xr[lane + 32 * i];
-      gv[i] = gr[lane + 32 * i];
+      gv[i] = ld4f(gr + 4 * (lane + 32 * i));
       rv[i] = rr ? rr[lane + 32 * i] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     const float mean = mean_in[m], rstd = rstd_in[m];
@@ -628,7 +628,7 @@ ln_bwd_split_kernel(const float* __restrict__ dy, const float* __restrict__ x,
 }
 
 template <typename T>
-void ln_bwd(const float* dy, const float* x, const float* mean, const float* rstd,
+void ln_bwd(const T* dy, const float* x, const float* mean, const float* rstd,
             const float* gain, const float* dres, float* dx_out, T* dx_T, float* part,
             float* dgain, float* dbias, int M, int d, cudaStream_t st, float* dsum, bool acc) {
   const int nsum = dsum ? 3 : 2;
@@ -1604,7 +1604,7 @@ void f32_to_bf16(const float* in, bf16* out, uint64_t n, cudaStream_t st) {
 #define INST(T)                                                                                 \
   template void ln_fwd<T>(const float*, const float*, const float*, T*, float*, float*, int, int, \
                           cudaStream_t);                                                        \
-  template void ln_bwd<T>(const float*, const float*, const float*, const float*, const float*,   \
+  template void ln_bwd<T>(const T*, const float*, const float*, const float*, const float*,       \
                           const float*, float*, T*, float*, float*, float*, int, int,            \
                           cudaStream_t, float*, bool);                                          \
   template void colsum<T>(const T*, int, int, float*, float*, cudaStream_t, bool);              \

@@ -22,13 +22,14 @@ void embed_bwd(const float* dx, const int32_t* csr_off, const int32_t* csr_rows,
 template <typename T>
 void ln_fwd(const float* x, const float* gain, const float* bias, T* y, float* mean, float* rstd,
             int M, int d, cudaStream_t st);
-// dx_out = dres + LN'(dy); dx_T = bf16/f32 copy (optional); gain/bias grads
+// dx_out = dres + LN'(dy) (dy in the activation type T: bf16 on the tensor-core
+// path, where the dX GEMMs write it); dx_T = bf16/f32 copy (optional); gain/bias grads
 // written to dgain/dbias via per-block partials in `part` (>= ln_bwd_parts()*3*d
 // floats).  dsum (optional) receives the column sums of dx_out: the bias
 // gradient of the linear layer whose output is this residual-stream gradient
 // (add_bias backward, tensor.cpp:279-285), without a second pass over dx_out.
 template <typename T>
-void ln_bwd(const float* dy, const float* x, const float* mean, const float* rstd,
+void ln_bwd(const T* dy, const float* x, const float* mean, const float* rstd,
             const float* gain, const float* dres, float* dx_out, T* dx_T, float* part,
             float* dgain, float* dbias, int M, int d, cudaStream_t st, float* dsum = nullptr,
             bool acc = false);  // acc: add dgain / dbias / dsum onto the existing values

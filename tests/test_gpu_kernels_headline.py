@@ -140,9 +140,9 @@ def test_layernorm_headline_widths(d, y_bf16):
     x = torch.randn(M, d, device="cuda", generator=g) * 1.5 + 0.3
     gain = 1.0 + 0.1 * torch.randn(d, device="cuda", generator=g)
     bias = 0.1 * torch.randn(d, device="cuda", generator=g)
-    dy = torch.randn(M, d, device="cuda", generator=g)
-    dres = torch.randn(M, d, device="cuda", generator=g)
     tdt = torch.bfloat16 if y_bf16 else torch.float32
+    dy = torch.randn(M, d, device="cuda", generator=g).to(tdt)  # the dX GEMMs' output type
+    dres = torch.randn(M, d, device="cuda", generator=g)
     y = torch.empty(M, d, device="cuda", dtype=tdt)
     mean = torch.empty(M, device="cuda")
     rstd = torch.empty(M, device="cuda")

@@ -10,7 +10,8 @@ import torch  # noqa: E402
 from paper_2411_02908_b200 import _capi as A  # noqa: E402
 
 M, d = 65536, int(os.environ.get("LN_D", "768"))
-x, dy, dres = (torch.randn(M, d, device="cuda") for _ in range(3))
+x, dres = (torch.randn(M, d, device="cuda") for _ in range(2))
+dy = torch.randn(M, d, device="cuda").bfloat16()  # the dX GEMMs write bf16
 g, b = torch.randn(d, device="cuda"), torch.randn(d, device="cuda")
 y = torch.empty(M, d, device="cuda", dtype=torch.bfloat16)
 mean, rstd = torch.empty(M, device="cuda"), torch.empty(M, device="cuda")

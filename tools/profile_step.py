@@ -3,6 +3,7 @@
 import sys
 
 sys.path.insert(0, "/root/repo")
+from paper_2411_02908_b200 import _capi as A  # noqa: E402
 from paper_2411_02908_b200 import fedsim as F  # noqa: E402
 
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 32
@@ -16,5 +17,7 @@ local = F.LocalTrainConfig(model=m, local_steps=1, batch_size=B)
 r = F.FederationRunner(F.FederationConfig(1, 1, 2, 2, 42), local, F.ServerOptConfig(1, 0.1, 0.9, True),
                        plan, theta0, precision="bf16")
 for _ in range(2):
+    n0 = A.lib().photon_launch_count()
     rec = r.run_round()
-    print("round_ms", rec.round_ms, "loss", rec.mean_client_loss, flush=True)
+    print("round_ms", rec.round_ms, "loss", rec.mean_client_loss, "kernel launches",
+          A.lib().photon_launch_count() - n0, flush=True)
