@@ -160,6 +160,34 @@ __device__ __forceinline__ void gelu_pair2(float2 x, float2& g, float2& gp) {
   gp = __ffma2_rn(__fmul2_rn(x, make_float2(0.39894228040143267794f, 0.39894228040143267794f)), e,
                   Phi);
 }
+// The same pair with one MUFU operation per element (ex2) instead of two: the
+// tail of the normal distribution as 0.5 * exp(-x^2/2) * R(|x| / 6.5), R a
+// degree-10 polynomial fit of erfcx(|x| / sqrt 2) weighted by exp(-x^2/2)
+// (|Phi - Phi_exact| <= 3.1e-7 in fp32, far below the bf16 rounding of the
+// epilogue's outputs; |x| > 6.5 clamps, where Phi is 0 or 1 in fp32).  The
+// tensor-core GEMM's GeluBias epilogue is MUFU-bound with the A&S form.
+__device__ __forceinline__ void gelu_pair2_poly(float2 x, float2& g, float2& gp) {
+  constexpr float c[11] = {0.999999463558197f,  -5.186119079589844f, 21.11585235595703f,
+                           -72.7467269897461f,  217.98768615722656f, -562.3059692382812f,
+                           1190.892822265625f,  -1921.429443359375f, 2145.36767578125f,
+                           -1443.036376953125f, 433.9256286621094f};
+  const float2 t = make_float2(fminf(fabsf(x.x) * (1.0f / 6.5f), 1.0f), fminf(fabsf(x.y) * (1.0f / 6.5f), 1.0f));
+  float2 p = make_float2(c[10], c[10]);
+#pragma unroll
+  for (int k = 9; k >= 0; --k) p = __ffma2_rn(p, t, make_float2(c[k], c[k]));
+  const float2 q = __fmul2_rn(x, __fmul2_rn(x, make_float2(-0.72134752044448170f, -0.72134752044448170f)));
+  float2 e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(q.x));  // exp(-x^2/2)
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(q.y));
+  const float2 w = __fmul2_rn(__fmul2_rn(p, e), make_float2(0.5f, 0.5f));  // Phi(-|x|)
+  float2 h = __ffma2_rn(w, make_float2(-1.0f, -1.0f), make_float2(0.5f, 0.5f));
+  h.x = copysignf(h.x, x.x);
+  h.y = copysignf(h.y, x.y);
+  const float2 Phi = __fadd2_rn(h, make_float2(0.5f, 0.5f));
+  g = __fmul2_rn(x, Phi);
+  gp = __ffma2_rn(__fmul2_rn(x, make_float2(0.39894228040143267794f, 0.39894228040143267794f)), e,
+                  Phi);
+}
 __device__ __forceinline__ float gelu_fast(float x) {
   float Phi, phi;
   phi_Phi(x, Phi, phi);

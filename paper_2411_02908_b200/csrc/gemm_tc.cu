@@ -575,7 +575,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           const uint32_t oa = su32(sbuf);
           if (epi == Epi::GeluBias && !splitk) {
-            // one Phi / phi evaluation per element: gelu'(u) = Phi + u phi -> aux box
+            // one Phi / phi evaluation per element (one MUFU op): gelu'(u) = Phi + u phi -> aux box
             // (second 2 KB, the backward's factor), v <- gelu(u) = u Phi
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int e = 0; e < 8; e += 2) {
                 float2 g2, gp2;
-                gelu_pair2(make_float2(v[8 * j + e], v[8 * j + e + 1]), g2, gp2);
+                gelu_pair2_poly(make_float2(v[8 * j + e], v[8 * j + e + 1]), g2, gp2);
                 v[8 * j + e] = g2.x;
                 v[8 * j + e + 1] = g2.y;
                 gp[e] = gp2.x;
