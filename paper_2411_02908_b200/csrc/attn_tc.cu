@@ -220,6 +220,11 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
                "r"(d)
                : "memory");
 }
+__device__ __forceinline__ float fmax3(float a, float b, float c) {  // FMNMX3 (sm_100)
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
 __device__ __forceinline__ float ex2(float x) {  // MUFU.EX2 without range fix-up
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -415,13 +420,15 @@ __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
       }
       // raw-score max (scale > 0 keeps the order): eight independent chains
       // instead of one 128-deep dependent chain on the softmax's critical path
+      // (three-input FMNMX3: two new scores per instruction)
       float mxs[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) mxs[u] = __uint_as_float(s[u]);
 #pragma unroll
-      for (int i = 8; i < TK; ++i) mxs[i & 7] = fmaxf(mxs[i & 7], __uint_as_float(s[i]));
-      float mx = fmaxf(fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3])),
-                       fmaxf(fmaxf(mxs[4], mxs[5]), fmaxf(mxs[6], mxs[7])));
+      for (int i = 8; i < TK; i += 2)
+        mxs[(i >> 1) & 7] = fmax3(mxs[(i >> 1) & 7], __uint_as_float(s[i]), __uint_as_float(s[i + 1]));
+      float mx = fmax3(fmax3(mxs[0], mxs[1], mxs[2]), fmax3(mxs[3], mxs[4], mxs[5]),
+                       fmaxf(mxs[6], mxs[7]));
       mx *= sl2;
       // lazy rescale: keep the stale max unless it grew by > 2^8
       float scale = 1.f;
