@@ -165,7 +165,8 @@ __device__ __forceinline__ void gelu_pair2(float2 x, float2& g, float2& gp) {
 // degree-10 polynomial fit of erfcx(|x| / sqrt 2) weighted by exp(-x^2/2)
 // (|Phi - Phi_exact| <= 3.1e-7 in fp32, far below the bf16 rounding of the
 // epilogue's outputs; |x| > 6.5 clamps, where Phi is 0 or 1 in fp32).  The
-// tensor-core GEMM's GeluBias epilogue is MUFU-bound with the A&S form.
+// tensor-core GEMM measured it slower in the step than the A&S form (its FMA
+// work costs more than the MUFU op it saves), so it is off by default.
 __device__ __forceinline__ void gelu_pair2_poly(float2 x, float2& g, float2& gp) {
   constexpr float c[11] = {0.999999463558197f,  -5.186119079589844f, 21.11585235595703f,
                            -72.7467269897461f,  217.98768615722656f, -562.3059692382812f,

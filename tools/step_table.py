@@ -112,7 +112,8 @@ def main(src, stem):
     out.append(f"mean DRAM bytes per GEMM launch (bench.py roofline.traffic): "
                f"{allrow['dram_bytes_per_launch']:.4g}; algorithmic {allrow['alg_bytes_per_launch']:.4g}")
 
-    # attention: fwd FLOPs 4*B*H*dh*S(S+1)/2 per layer, backward 2.5x (two recomputing passes)
+    # attention: fwd FLOPs 4*B*H*dh*S(S+1)/2 per layer, backward 2.5x (the fused pass, or
+    # 1.25x for each of the two recomputing passes)
     p = os.path.join(src, "r02_attn_step.csv")
     if os.path.exists(p):
         at = collections.OrderedDict()
@@ -135,7 +136,9 @@ def main(src, stem):
         out.append("kernel | launches | ms | tensor pipe % | FMA pipe % | ALU pipe % | "
                    "XU (MUFU) warp-inst per launch | DRAM GB | TFLOP/s (fwd convention)")
         for name, e in at.items():
-            fl = fwd * e["n"] if "fwd" in name else (1.25 * fwd * e["n"] if ("dkdv" in name or "dq" in name) else 0.0)
+            fl = (fwd * e["n"] if "fwd" in name else
+                  2.5 * fwd * e["n"] if "fused" in name else
+                  1.25 * fwd * e["n"] if ("dkdv" in name or "dq" in name) else 0.0)
             row = {"launches": int(e["n"]), "ms": e["us"] / 1e3,
                    "tensor_pipe_pct": e["tensor"] / e["us"], "fma_pipe_pct": e["fma"] / e["us"],
                    "alu_pipe_pct": e["alu"] / e["us"], "xu_inst_per_launch": e["xu_inst"] / e["n"],
