@@ -466,3 +466,29 @@ def test_micro_batched_runner_vs_oracle(F, oracle):
         runner.run_round()
     assert np.max(np.abs(runner.theta() - th_ref)) <= 5e-4
     assert np.max(np.abs(runner.velocity() - vel_ref)) <= 5e-4
+
+
+@pytest.mark.parametrize("precision", ["f32", "bf16"])
+def test_launch_count_graph_replay_matches_eager(F, oracle, precision):
+    # photon_launch_count (bench.py's gpu_launches) counts every launch site and,
+    # for a CUDA-graph replay of a local round, the graph's kernel nodes: the
+    # first round runs eager, the second is captured and replayed, later ones
+    # replay -- every round must add the same number of kernels
+    from paper_2411_02908_b200 import _capi as A
+
+    cfg_t = WIDE256
+    mc = ModelCfg(*cfg_t)
+    theta0 = oracle.init_params(mc, 3)
+    corpus = oracle.generate_corpus("web", 60000, 5, cfg_t[4])
+    plan = F.partition_iid(corpus, 2, cfg_t[5], 3)
+    local = F.LocalTrainConfig(model=F.ModelConfig(*cfg_t), local_steps=3, batch_size=2)
+    runner = F.FederationRunner(F.FederationConfig(2, 2, 4, F.Topology.kRingAllReduce, 5), local,
+                                F.ServerOptConfig(1, 0.1, 0.9, True), plan, theta0,
+                                precision=precision)
+    counts = []
+    for _ in range(4):
+        n0 = A.lib().photon_launch_count()
+        runner.run_round()
+        counts.append(A.lib().photon_launch_count() - n0)
+    assert counts[0] > 0
+    assert counts == [counts[0]] * 4, counts
