@@ -83,6 +83,12 @@ def test_attention_tcgen05_dh128_long():
     _run(2, 1, 2048, 2, 256)
 
 
+def test_attention_tcgen05_many_heads():
+    # B * H = 192 > 148: the fused dh-64 backward runs several heads per CTA
+    # (96 CTAs x 2), odd CTAs walking the key tiles in descending order
+    _run(2, 16, 256, 12, 768)
+
+
 def test_attention_tcgen05_backward_deterministic():
     # the fused backward adds dQ partial sums in a fixed key-tile order: two runs
     # are bit-identical, and the result does not depend on CTA scheduling
