@@ -94,6 +94,12 @@ class EngineT final : public Engine {
   T *h_, *q_, *k_, *v_, *o_, *h2_, *pre_, *u_, *xf_, *logits_;
   // backward scratch
   float *dx_, *dy_, *Dvec_, *part_, *attn_ws_, *gemm_ws_;
+  // deferred column reductions: every bias / LayerNorm-gain partial of a
+  // backward pass in its own slice of defer_, reduced by two batched launches
+  // at the end of the pass (k::run_reduce_jobs)
+  float* defer_ = nullptr;
+  size_t defer_ln_ = 0, defer_b1_ = 0, defer_qkv_ = 0, defer_head_ = 0;
+  k::ReduceJobs jobs_;
   // the LayerNorm backwards' input gradient in the activation type (bf16 on the
   // tensor-core path: the dX GEMMs write it directly; fp32 mode: dy_ itself)
   T* dyT_;
@@ -134,6 +140,12 @@ class EngineT final : public Engine {
                                                     k::attn_bwd_sums_floats((int)max_batch,
                                                                             (int)Smax_, (int)d) +
                                                         3 * k::colsum_parts_scratch_floats((int)d)}));
+    defer_ln_ = (size_t)k::ln_bwd_parts() * 3 * d;
+    defer_b1_ = (size_t)(M / 32) * hid + k::colsum_parts_scratch_floats((int)hid);
+    defer_qkv_ = k::attn_bwd_sums_floats((int)max_batch, (int)Smax_, (int)d) +
+                 3 * k::colsum_parts_scratch_floats((int)d);
+    defer_head_ = k::ce_bias_part_floats((int)V_);
+    const size_t defer_floats = L * (2 * defer_ln_ + defer_b1_ + defer_qkv_) + defer_ln_ + defer_head_;
     auto plan = [&](char* p) {
       char* s = p;
       // master: separate allocation (see master_alloc_)
@@ -173,6 +185,7 @@ class EngineT final : public Engine {
                      ? carve<float>(p, k::attn_bwd_tc_ws_floats((int)max_batch, (int)Smax_, (int)H_, (int)d_))
                      : nullptr;
       part_ = carve<float>(p, part_floats);
+      defer_ = carve<float>(p, defer_floats);
       dxT_ = carve<T>(p, M * d);
       dpre_ = carve<T>(p, M * hid);
       dq_ = carve<T>(p, M * d);
@@ -252,12 +265,12 @@ class EngineT final : public Engine {
     }
     k::attn_fwd_simt<T>(q, k, v, o, lse, B, S, H, d, stream);
   }
-  // true when the q / k / v column sums came with it (attn_bwd_sums_floats in part_)
+  // true when the q / k / v column sums came with it (attn_bwd_sums_floats in sums)
   bool attn_bwd(const T* q, const T* k, const T* v, const T* o, const T* dO, const float* lse,
-                int B, int S, int H, int d) {
+                int B, int S, int H, int d, float* sums) {
     if constexpr (sizeof(T) == 2) {
       if (attn_mode == 1 && k::attn_tc_supported((int)(d_ / H_), d)) {
-        k::attn_bwd_tc(q, k, v, o, dO, lse, dq_, dk_, dv_, B, S, H, d, attn_ws_, stream, part_);
+        k::attn_bwd_tc(q, k, v, o, dO, lse, dq_, dk_, dv_, B, S, H, d, attn_ws_, stream, sums);
         return true;
       }
       if (use_mma_attn()) {
@@ -313,6 +326,8 @@ void EngineT<T>::forward_backward(const StepBatch& bt, double* loss_dev, bool ba
 
 template <typename T>
 void EngineT<T>::micro(const StepBatch& bt, double* loss_dev, bool backward, bool acc, int row0) {
+  jobs_.rows.clear();  // (a pass that threw left its jobs behind)
+  jobs_.cols.clear();
   const int B = bt.B, S = bt.S, M = B * S;
   const int d = (int)d_, hid = (int)hid_, V = (int)V_, H = (int)H_, L = (int)L_;
   // weight gradients: stored by the first micro-batch, accumulated by the rest
@@ -367,8 +382,9 @@ void EngineT<T>::micro(const StepBatch& bt, double* loss_dev, bool backward, boo
     // the head-bias gradient (column sums of dlogits) comes out of the
     // cross-entropy pass where the kernel supports the shape
     head_b_done = k::ce_fwd_bwd<T>(logits_, bt.targets, M, V, bt.inv_count, rowloss_, backward,
-                                   stream, backward ? G(off_.head_b) : nullptr, part_, acc,
-                                   bt.inv_count_dev);
+                                   stream, backward ? G(off_.head_b) : nullptr,
+                                   defer_ + L_ * (2 * defer_ln_ + defer_b1_ + defer_qkv_) + defer_ln_,
+                                   acc, bt.inv_count_dev, &jobs_);
     k::sum_scaled(rowloss_, M, (double)bt.inv_count, loss_dev, stream, acc, bt.inv_count_dev);
   }
   if (!backward) {
@@ -393,11 +409,15 @@ void EngineT<T>::micro(const StepBatch& bt, double* loss_dev, bool backward, boo
   {
     Scope sc(this, 2, 0);
     // the column sums of its output are the last block's b2 gradient
-    k::ln_bwd<T>(dyT_, xL, meanf_, rstdf_, Pm(off_.lnfg), nullptr, dx_, dxT_, part_, G(off_.lnfg),
-                 G(off_.lnfb), M, d, stream, G(off_.blocks[L - 1].b2), acc);
+    k::ln_bwd<T>(dyT_, xL, meanf_, rstdf_, Pm(off_.lnfg), nullptr, dx_, dxT_,
+                 defer_ + L_ * (2 * defer_ln_ + defer_b1_ + defer_qkv_), G(off_.lnfg),
+                 G(off_.lnfb), M, d, stream, G(off_.blocks[L - 1].b2), acc, &jobs_);
   }
   for (int l = L - 1; l >= 0; --l) {
     const BlockOffsets& o = off_.blocks[l];
+    // this layer's slices of the deferred-reduction partials
+    float* pl = defer_ + (size_t)l * (2 * defer_ln_ + defer_b1_ + defer_qkv_);
+    float *p_ln2 = pl, *p_b1 = pl + defer_ln_, *p_qkv = p_b1 + defer_b1_, *p_ln1 = p_qkv + defer_qkv_;
     float* x = x_ + (size_t)l * Md;
     float* xm = xmid_ + (size_t)l * Md;
     T *h = h_ + l * Md, *q = q_ + l * Md, *kk = k_ + l * Md, *v = v_ + l * Md, *ao = o_ + l * Md;
@@ -416,12 +436,13 @@ void EngineT<T>::micro(const StepBatch& bt, double* loss_dev, bool backward, boo
       fuse_b1 = gemm_tc_single_pass(ga);
     }
     mm(M, hid, d, dxT_, d, true, W(o.w2), d, true, dpre_, hid, TT, Epi::GeluBwd, nullptr, nullptr,
-       pre, fuse_b1 ? part_ : nullptr);
+       pre, fuse_b1 ? p_b1 : nullptr);
     mm(hid, d, M, u, hid, false, dxT_, d, false, G(o.w2), d, DT::F32, WG);
     {
       Scope sc(this, 2, 0);
       if (fuse_b1)
-        k::colsum_parts(part_, M / 32, hid, part_ + (size_t)(M / 32) * hid, G(o.b1), stream, acc);
+        k::colsum_parts(p_b1, M / 32, hid, p_b1 + (size_t)(M / 32) * hid, G(o.b1), stream, acc,
+                        &jobs_);
       else
         k::colsum<T>(dpre_, M, hid, part_, G(o.b1), stream, acc);
     }
@@ -431,14 +452,14 @@ void EngineT<T>::micro(const StepBatch& bt, double* loss_dev, bool backward, boo
       Scope sc(this, 2, 0);
       // x_mid = x + (o Wo + bo): dbo = column sums of this output
       k::ln_bwd<T>(dyT_, xm, mean2_ + (size_t)l * M, rstd2_ + (size_t)l * M, Pm(o.ln2g), dx_, dx_,
-                   dxT_, part_, G(o.ln2g), G(o.ln2b), M, d, stream, G(o.bo), acc);
+                   dxT_, p_ln2, G(o.ln2g), G(o.ln2b), M, d, stream, G(o.bo), acc, &jobs_);
     }
     mm(M, d, d, dxT_, d, true, W(o.wo), d, true, dO_, d, TT, Epi::Store);
     mm(d, d, M, ao, d, false, dxT_, d, false, G(o.wo), d, DT::F32, WG);
     bool qkv_sums;
     {
       Scope sc(this, 1, 2.5 * attn_fwd_flops);
-      qkv_sums = attn_bwd(q, kk, v, ao, dO_, lse_ + (size_t)l * B * H * S, B, S, H, d);
+      qkv_sums = attn_bwd(q, kk, v, ao, dO_, lse_ + (size_t)l * B * H * S, B, S, H, d, p_qkv);
     }
     // q,k,v = h W{q,k,v} + b{q,k,v}; LN1's output grad sums v, k, q in that order
     {
@@ -446,8 +467,8 @@ void EngineT<T>::micro(const StepBatch& bt, double* loss_dev, bool backward, boo
       if (qkv_sums) {  // partials from the attention backward's stores
         const int np = B * ((S + 31) / 32);
         const size_t P = (size_t)np * d;
-        float* scr = part_ + 3 * P;
-        k::colsum_parts3(part_, P, np, d, scr, G(o.bq), G(o.bk), G(o.bv), stream, acc);
+        float* scr = p_qkv + 3 * P;
+        k::colsum_parts3(p_qkv, P, np, d, scr, G(o.bq), G(o.bk), G(o.bv), stream, acc, &jobs_);
       } else {
         k::colsum<T>(dv_, M, d, part_, G(o.bv), stream, acc);
         k::colsum<T>(dk_, M, d, part_, G(o.bk), stream, acc);
@@ -483,12 +504,14 @@ void EngineT<T>::micro(const StepBatch& bt, double* loss_dev, bool backward, boo
       Scope sc(this, 2, 0);
       // the output is block l-1's x_out gradient: its column sums are db2 of l-1
       k::ln_bwd<T>(dyT_, x, mean1_ + (size_t)l * M, rstd1_ + (size_t)l * M, Pm(o.ln1g), dx_, dx_,
-                   dxT_, part_, G(o.ln1g), G(o.ln1b), M, d, stream,
-                   l > 0 ? G(off_.blocks[l - 1].b2) : nullptr, acc);
+                   dxT_, p_ln1, G(o.ln1g), G(o.ln1b), M, d, stream,
+                   l > 0 ? G(off_.blocks[l - 1].b2) : nullptr, acc, &jobs_);
     }
   }
   {
     Scope sc(this, 2, 0);
+    // every deferred bias / LayerNorm-gain reduction of the pass: two launches
+    k::run_reduce_jobs(jobs_, stream);
     k::embed_bwd(dx_, bt.csr_off, bt.csr_rows, G(off_.tok), G(off_.pos), V, M, S, d, stream, row0,
                  acc);
   }

@@ -330,14 +330,13 @@ ln_bwd_kernel(const T* __restrict__ dy, const float* __restrict__ x,
 // CTA of 1024 threads, so each thread has only ~nparts/32 partials to read,
 // all issued before the first add (the partials were just written: L2 hits;
 // the kernel is latency-, not bandwidth-bound).
-__global__ void __launch_bounds__(1024) colreduce_kernel(const float* __restrict__ part, int nparts,
-                                                         int n, int stride, float* __restrict__ out,
-                                                         int split, float* __restrict__ out1,
-                                                         int acc_out, int split2,
-                                                         float* __restrict__ out2) {
+__device__ __forceinline__ void colreduce_body(const float* __restrict__ part, int nparts, int n,
+                                               int stride, float* __restrict__ out, int split,
+                                               float* __restrict__ out1, int acc_out, int split2,
+                                               float* __restrict__ out2, int bx) {
   __shared__ float red[32][33];
   const int cl = threadIdx.x & 31, s = threadIdx.x >> 5;
-  const int j = blockIdx.x * 32 + cl;
+  const int j = bx * 32 + cl;
   float acc = 0.f;
   if (j < n) {
     int p = s;
@@ -358,10 +357,22 @@ __global__ void __launch_bounds__(1024) colreduce_kernel(const float* __restrict
     *o = acc_out ? *o + t : t;  // micro-batches after the first add onto the gradient
   }
 }
+__global__ void __launch_bounds__(1024) colreduce_kernel(const float* __restrict__ part, int nparts,
+                                                         int n, int stride, float* __restrict__ out,
+                                                         int split, float* __restrict__ out1,
+                                                         int acc_out, int split2,
+                                                         float* __restrict__ out2) {
+  colreduce_body(part, nparts, n, stride, out, split, out1, acc_out, split2, out2, blockIdx.x);
+}
 // columns [0, split) -> out, [split, split2) -> out1, [split2, n) -> out2
 static void colreduce(const float* part, int nparts, int n, int stride, float* out, int split,
                       float* out1, cudaStream_t st, bool acc = false, int split2 = -1,
-                      float* out2 = nullptr) {
+                      float* out2 = nullptr, ReduceJobs* defer = nullptr) {
+  if (defer) {
+    defer->cols.push_back(ColJob{part, nparts, n, stride, split, split2 < 0 ? n : split2, out, out1,
+                                 out2, acc ? 1 : 0});
+    return;
+  }
   colreduce_kernel<<<cdiv(n, 32), 1024, 0, st>>>(part, nparts, n, stride, out, split, out1,
                                                  acc ? 1 : 0, split2 < 0 ? n : split2, out2);
   PH_LAUNCH_CHECK();
@@ -372,15 +383,15 @@ static void colreduce(const float* part, int nparts, int n, int stride, float* o
 // row y of `out` ([gridDim.y][n]).
 // Several same-shaped partial arrays at once: column J of the combined
 // [nseg * n] row is column J % n of segment J / n (segments seg_stride apart).
-__global__ void __launch_bounds__(256) colreduce_rows_kernel(const float* __restrict__ part, int nparts,
-                                                             int per, int n, float* __restrict__ out,
-                                                             int nseg, size_t seg_stride) {
+__device__ __forceinline__ void colreduce_rows_body(const float* __restrict__ part, int nparts,
+                                                    int per, int n, float* __restrict__ out,
+                                                    int nseg, size_t seg_stride, int bx, int by) {
   __shared__ float red[8][33];
   const int cl = threadIdx.x & 31, s = threadIdx.x >> 5;
-  const int J = blockIdx.x * 32 + cl, nn = n * nseg;
+  const int J = bx * 32 + cl, nn = n * nseg;
   const int seg = J / n, j = J - seg * n;
   const float* ps = part + (size_t)seg * seg_stride;
-  const int p0 = blockIdx.y * per, p1 = min(nparts, p0 + per);
+  const int p0 = by * per, p1 = min(nparts, p0 + per);
   float acc = 0.f;
   if (J < nn) {
     int p = p0 + s;
@@ -396,31 +407,113 @@ __global__ void __launch_bounds__(256) colreduce_rows_kernel(const float* __rest
     float t = 0.f;
 #pragma unroll
     for (int w = 0; w < 8; ++w) t += red[w][cl];
-    out[(size_t)blockIdx.y * nn + J] = t;
+    out[(size_t)by * nn + J] = t;
   }
+}
+__global__ void __launch_bounds__(256) colreduce_rows_kernel(const float* __restrict__ part, int nparts,
+                                                             int per, int n, float* __restrict__ out,
+                                                             int nseg, size_t seg_stride) {
+  colreduce_rows_body(part, nparts, per, n, out, nseg, seg_stride, blockIdx.x, blockIdx.y);
+}
+
+// ---- deferred column reductions, batched ------------------------------------------
+// A job table travels as a kernel parameter; CTA b runs the job whose CTA range
+// holds b, with exactly the body (and so the summation order) of the one-job
+// kernels above.
+constexpr int kReduceBatch = 160;
+struct RowTable {
+  int njobs;
+  int start[kReduceBatch + 1];
+  RowJob job[kReduceBatch];
+};
+struct ColTable {
+  int njobs;
+  int start[kReduceBatch + 1];
+  ColJob job[kReduceBatch];
+};
+__device__ __forceinline__ int find_job(const int* start, int njobs, int b) {
+  int lo = 0, hi = njobs - 1;  // largest j with start[j] <= b
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (start[mid] <= b) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+__global__ void __launch_bounds__(256) reduce_rows_batch_kernel(const __grid_constant__ RowTable t) {
+  const int j = find_job(t.start, t.njobs, blockIdx.x);
+  const RowJob& r = t.job[j];
+  const int local = blockIdx.x - t.start[j], nx = (r.n * r.nseg + 31) / 32;
+  colreduce_rows_body(r.part, r.nparts, r.per, r.n, r.out, r.nseg, r.seg_stride, local % nx,
+                      local / nx);
+}
+__global__ void __launch_bounds__(1024) reduce_cols_batch_kernel(const __grid_constant__ ColTable t) {
+  const int j = find_job(t.start, t.njobs, blockIdx.x);
+  const ColJob& c = t.job[j];
+  colreduce_body(c.part, c.nparts, c.n, c.stride, c.out, c.split, c.out1, c.acc, c.split2, c.out2,
+                 blockIdx.x - t.start[j]);
+}
+void run_reduce_jobs(ReduceJobs& jobs, cudaStream_t st) {
+  for (size_t b = 0; b < jobs.rows.size(); b += kReduceBatch) {
+    RowTable t{};
+    t.njobs = (int)std::min<size_t>(kReduceBatch, jobs.rows.size() - b);
+    int n = 0;
+    for (int i = 0; i < t.njobs; ++i) {
+      t.job[i] = jobs.rows[b + i];
+      t.start[i] = n;
+      n += cdiv(t.job[i].n * t.job[i].nseg, 32) * t.job[i].used;
+    }
+    t.start[t.njobs] = n;
+    reduce_rows_batch_kernel<<<n, 256, 0, st>>>(t);
+    PH_LAUNCH_CHECK();
+  }
+  for (size_t b = 0; b < jobs.cols.size(); b += kReduceBatch) {
+    ColTable t{};
+    t.njobs = (int)std::min<size_t>(kReduceBatch, jobs.cols.size() - b);
+    int n = 0;
+    for (int i = 0; i < t.njobs; ++i) {
+      t.job[i] = jobs.cols[b + i];
+      t.start[i] = n;
+      n += cdiv(t.job[i].n, 32);
+    }
+    t.start[t.njobs] = n;
+    reduce_cols_batch_kernel<<<n, 1024, 0, st>>>(t);
+    PH_LAUNCH_CHECK();
+  }
+  jobs.rows.clear();
+  jobs.cols.clear();
 }
 
 size_t colsum_parts_scratch_floats(int N) { return (size_t)kColsumPartGroups * N; }
 
 void colsum_parts(const float* part, int nparts, int N, float* scratch, float* out, cudaStream_t st,
-                  bool acc) {
+                  bool acc, ReduceJobs* defer) {
   const int groups = std::min(kColsumPartGroups, nparts);
   const int per = cdiv(nparts, groups);
   const int used = cdiv(nparts, per);
-  colreduce_rows_kernel<<<dim3(cdiv(N, 32), used), 256, 0, st>>>(part, nparts, per, N, scratch, 1, 0);
-  PH_LAUNCH_CHECK();
-  colreduce(scratch, used, N, N, out, N, nullptr, st, acc);
+  if (defer) {
+    defer->rows.push_back(RowJob{part, nparts, per, N, 1, 0, scratch, used});
+  } else {
+    colreduce_rows_kernel<<<dim3(cdiv(N, 32), used), 256, 0, st>>>(part, nparts, per, N, scratch, 1, 0);
+    PH_LAUNCH_CHECK();
+  }
+  colreduce(scratch, used, N, N, out, N, nullptr, st, acc, -1, nullptr, defer);
 }
 
 void colsum_parts3(const float* part, size_t seg_stride, int nparts, int N, float* scratch,
-                   float* out0, float* out1, float* out2, cudaStream_t st, bool acc) {
+                   float* out0, float* out1, float* out2, cudaStream_t st, bool acc,
+                   ReduceJobs* defer) {
   const int groups = std::min(kColsumPartGroups, nparts);
   const int per = cdiv(nparts, groups);
   const int used = cdiv(nparts, per);
-  colreduce_rows_kernel<<<dim3(cdiv(3 * N, 32), used), 256, 0, st>>>(part, nparts, per, N, scratch,
-                                                                      3, seg_stride);
-  PH_LAUNCH_CHECK();
-  colreduce(scratch, used, 3 * N, 3 * N, out0, N, out1, st, acc, 2 * N, out2);
+  if (defer) {
+    defer->rows.push_back(RowJob{part, nparts, per, N, 3, seg_stride, scratch, used});
+  } else {
+    colreduce_rows_kernel<<<dim3(cdiv(3 * N, 32), used), 256, 0, st>>>(part, nparts, per, N, scratch,
+                                                                        3, seg_stride);
+    PH_LAUNCH_CHECK();
+  }
+  colreduce(scratch, used, 3 * N, 3 * N, out0, N, out1, st, acc, 2 * N, out2, defer);
 }
 
 // Register-resident variant for d = 128 * NV: one warp per row, x, dy and the
@@ -630,7 +723,8 @@ ln_bwd_split_kernel(const T* __restrict__ dy, const float* __restrict__ x,
 template <typename T>
 void ln_bwd(const T* dy, const float* x, const float* mean, const float* rstd,
             const float* gain, const float* dres, float* dx_out, T* dx_T, float* part,
-            float* dgain, float* dbias, int M, int d, cudaStream_t st, float* dsum, bool acc) {
+            float* dgain, float* dbias, int M, int d, cudaStream_t st, float* dsum, bool acc,
+            ReduceJobs* defer) {
   const int nsum = dsum ? 3 : 2;
   switch (d) {
 #define PH_LNB(NV)                                                                         \
@@ -675,7 +769,7 @@ void ln_bwd(const T* dy, const float* x, const float* mean, const float* rstd,
   PH_LAUNCH_CHECK();
   // gain, bias and (optionally) the output's column sums in one launch
   colreduce(part, kLnBwdBlocks, dsum ? 3 * d : 2 * d, 3 * d, dgain, d, dbias, st, acc, 2 * d,
-            dsum);
+            dsum, defer);
 }
 
 // ============================================================================
@@ -1314,7 +1408,7 @@ size_t ce_bias_part_floats(int V) { return (size_t)kNumSMs * V; }
 template <typename T>
 bool ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count, double* rowloss,
                 bool write_grad, cudaStream_t st, float* dbias, float* part, bool acc,
-                const float* inv_dev) {
+                const float* inv_dev, ReduceJobs* defer) {
   if constexpr (sizeof(T) == 2) {
     const bool aligned = (reinterpret_cast<uintptr_t>(logits) & 15) == 0;
     if (V % 8 == 0 && ce_pipe_smem(V) <= (size_t)kCePipeMaxSmem && M > 0 && aligned) {
@@ -1332,7 +1426,7 @@ bool ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count
           logits, targets, M, V, inv_count, rowloss, write_grad ? 1 : 0, fuse ? part : nullptr,
           inv_dev);
       PH_LAUNCH_CHECK();
-      if (fuse) colreduce(part, grid, V, V, dbias, V, nullptr, st, acc);
+      if (fuse) colreduce(part, grid, V, V, dbias, V, nullptr, st, acc, -1, nullptr, defer);
       return fuse;
     }
     if (V % 8 == 0 && V <= kCeRegChunks * 8 * kCeThreads && aligned) {
@@ -1606,10 +1700,10 @@ void f32_to_bf16(const float* in, bf16* out, uint64_t n, cudaStream_t st) {
                           cudaStream_t);                                                        \
   template void ln_bwd<T>(const T*, const float*, const float*, const float*, const float*,       \
                           const float*, float*, T*, float*, float*, float*, int, int,            \
-                          cudaStream_t, float*, bool);                                          \
+                          cudaStream_t, float*, bool, ReduceJobs*);                             \
   template void colsum<T>(const T*, int, int, float*, float*, cudaStream_t, bool);              \
   template bool ce_fwd_bwd<T>(T*, const int32_t*, int, int, float, double*, bool, cudaStream_t, \
-                               float*, float*, bool, const float*);                           \
+                               float*, float*, bool, const float*, ReduceJobs*);              \
   template void attn_fwd_simt<T>(const T*, const T*, const T*, T*, float*, int, int, int, int,    \
                                  cudaStream_t);                                                 \
   template void attn_bwd_simt<T>(const T*, const T*, const T*, const T*, const T*, const float*,  \

@@ -3,10 +3,39 @@
 // optim.cu next to each kernel.
 #pragma once
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace photon {
 namespace k {
+
+// ---- deferred column reductions -------------------------------------------------
+// The bias / LayerNorm-gain gradients are column sums of per-block partials.
+// With a ReduceJobs list the producers below write their partials and append a
+// job instead of launching the reduction; run_reduce_jobs then runs every
+// first-level row reduction in ONE launch and every final column reduction in
+// a second, each element summed in exactly the order of the one-job kernels
+// (the gradients are bitwise those of the immediate path).  The partial
+// buffers must stay distinct until run_reduce_jobs.
+struct RowJob {
+  const float* part;
+  int nparts, per, n, nseg;
+  size_t seg_stride;
+  float* out;
+  int used;
+};
+struct ColJob {
+  const float* part;
+  int nparts, n, stride, split, split2;
+  float *out, *out1, *out2;
+  int acc;
+};
+struct ReduceJobs {
+  std::vector<RowJob> rows;
+  std::vector<ColJob> cols;
+};
+void run_reduce_jobs(ReduceJobs& jobs, cudaStream_t st);
 
 // ---- embedding (gather_rows + add, tensor.cpp:209-223, 290-320) ------------
 void embed_fwd(const int32_t* tokens, const float* tok, const float* pos, float* x, int M, int S,
@@ -32,7 +61,8 @@ template <typename T>
 void ln_bwd(const T* dy, const float* x, const float* mean, const float* rstd,
             const float* gain, const float* dres, float* dx_out, T* dx_T, float* part,
             float* dgain, float* dbias, int M, int d, cudaStream_t st, float* dsum = nullptr,
-            bool acc = false);  // acc: add dgain / dbias / dsum onto the existing values
+            bool acc = false,  // acc: add dgain / dbias / dsum onto the existing values
+            ReduceJobs* defer = nullptr);
 int ln_bwd_parts();
 
 // ---- column sums (add_bias backward, tensor.cpp:279-285) -------------------
@@ -45,11 +75,12 @@ size_t colsum_part_floats(int M, int N);
 constexpr int kColsumPartGroups = 64;
 size_t colsum_parts_scratch_floats(int N);
 void colsum_parts(const float* part, int nparts, int N, float* scratch, float* out, cudaStream_t st,
-                  bool acc = false);
+                  bool acc = false, ReduceJobs* defer = nullptr);
 // three same-shaped partial arrays (part + i * seg_stride) into out0..out2 in
 // two launches (the q / k / v bias gradients); scratch >= 3 x colsum_parts_scratch_floats(N)
 void colsum_parts3(const float* part, size_t seg_stride, int nparts, int N, float* scratch,
-                   float* out0, float* out1, float* out2, cudaStream_t st, bool acc = false);
+                   float* out0, float* out1, float* out2, cudaStream_t st, bool acc = false,
+                   ReduceJobs* defer = nullptr);
 
 // ---- softmax cross-entropy fwd+bwd (tensor.cpp:544-603) --------------------
 // logits [M,V] overwritten with dlogits = (softmax - onehot) * inv_count;
@@ -62,7 +93,8 @@ void colsum_parts3(const float* part, size_t seg_stride, int nparts, int N, floa
 template <typename T>
 bool ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count,
                 double* rowloss, bool write_grad, cudaStream_t st, float* dbias = nullptr,
-                float* part = nullptr, bool acc = false, const float* inv_dev = nullptr);
+                float* part = nullptr, bool acc = false, const float* inv_dev = nullptr,
+                ReduceJobs* defer = nullptr);
 size_t ce_bias_part_floats(int V);
 // out = inv_count * sum(rowloss) (fixed-order tree); acc: out += ...
 void sum_scaled(const double* x, int n, double scale, double* out, cudaStream_t st,
