@@ -272,6 +272,7 @@ template <int HD>
 __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                        const __grid_constant__ CUtensorMap tv, const FwdArgs a) {
+  pdl_launch_dependents();
   // smem: Q | K[2] | V[2] | barriers; 16 KB tiles at HD = 64 (two CTAs per SM),
   // 32 KB at HD = 128 (one CTA per SM, 512 TMEM columns)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -329,6 +330,7 @@ __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // inputs of the previous kernel visible from here
 
   if (warp == 0) {
     if (lane == 0) {  // ===== producer: Q, then the K ring =====
@@ -549,6 +551,8 @@ template <int HD>
 __global__ void attn_bwd_prep_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dO,
                                      const float* __restrict__ lse, float* __restrict__ Lp,
                                      float* __restrict__ Dp, int B, int S, int H, int d, int Spad) {
+  pdl_launch_dependents();
+  pdl_wait();
   constexpr int VPH = HD / 8;  // 16-byte vectors per head
   const int nvec = d / 8, lane = threadIdx.x & 31;
   const int warps = blockDim.x / 32;
@@ -713,6 +717,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                             const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
                             const BwdArgs a) {
+  pdl_launch_dependents();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
@@ -770,6 +775,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // inputs of the previous kernel visible from here
 
   if (warp == 0) {
     if (lane == 0) {
@@ -961,6 +967,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                           const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
                           const BwdArgs a) {
+  pdl_launch_dependents();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
@@ -1012,6 +1019,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // inputs of the previous kernel visible from here
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1236,6 +1244,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_fused64_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                                const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
                                const BwdArgs a) {
+  pdl_launch_dependents();
   static_assert(SWB == 16, "fused backward: 16 softmax warps (4 column groups of 32 queries)");
   constexpr int HD = 64, KB = 16384, QB = 16384, T = 128;  // tiles: 128 rows x 64 bf16
   constexpr int CPQ = 32, GPH = 16;                          // per-thread score / accumulator columns
@@ -1303,6 +1312,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // inputs of the previous kernel visible from here
 
   if (warp == 0) {
     if (lane == 0) {  // ===== producer: K, V per key tile, the Q / dO / L / D ring =====
@@ -1683,8 +1693,7 @@ void attn_bwd_hd(const bf16* q, const bf16* k, const bf16* v, const bf16* o, con
   if (!ws) ws = scratch(attn_bwd_tc_ws_floats(B, S, H, d));
   float* Lp = ws;
   float* Dp = Lp + (size_t)B * H * Spad;
-  attn_bwd_prep_kernel<HD><<<std::min<int64_t>(((int64_t)B * S + 7) / 8, kNumSMs * 16), 256, 0,
-                             st>>>(o, dO, lse, Lp, Dp, B, S, H, d, Spad);
+  launch_pdl(attn_bwd_prep_kernel<HD>, std::min<int64_t>(((int64_t)B * S + 7) / 8, kNumSMs * 16), 256, 0, st, o, dO, lse, Lp, Dp, B, S, H, d, Spad);
   PH_LAUNCH_CHECK();
   constexpr int TQB = HD == 64 ? 128 : 64;  // dK/dV kernel's query tile
   const CUtensorMap mq = head_map(q, rows, d), mk = head_map(k, rows, d), mv = head_map(v, rows, d),
@@ -1709,7 +1718,7 @@ void attn_bwd_hd(const bf16* q, const bf16* k, const bf16* v, const bf16* o, con
     const int waves = (B * H + kNumSMs - 1) / kNumSMs;
     const int grid = PHOTON_FUSED_GRID ? std::min(kNumSMs, (B * H + waves - 1) / waves)
                                        : std::min(kNumSMs, B * H);
-    attn_bwd_fused64_tc_kernel<<<grid, kBwdThreads, kFusedSmem, st>>>(mq, mk, mv, mo, a);
+    launch_pdl(attn_bwd_fused64_tc_kernel, grid, kBwdThreads, kFusedSmem, st, mq, mk, mv, mo, a);
     PH_LAUNCH_CHECK();
     return;
   }
@@ -1724,13 +1733,13 @@ void attn_bwd_hd(const bf16* q, const bf16* k, const bf16* v, const bf16* o, con
   set_smem_once(cfg2, attn_bwd_dq_tc_kernel<HD>, SMEM2);
   // persistent: one CTA per SM over the units (tile pairs) of both kernels
   const int grid = std::min(kNumSMs, B * H * ((nt + 1) / 2));
-  attn_bwd_dkdv_tc_kernel<HD><<<grid, kBwdThreads, SMEM1, st>>>(mqb, mk, mv, mob, a);
+  launch_pdl(attn_bwd_dkdv_tc_kernel<HD>, grid, kBwdThreads, SMEM1, st, mqb, mk, mv, mob, a);
   PH_LAUNCH_CHECK();
   a.g0 = dq;
   a.g1 = nullptr;
   a.s0 = sums;
   a.s1 = nullptr;
-  attn_bwd_dq_tc_kernel<HD><<<grid, kBwdThreads, SMEM2, st>>>(mq, mk, mv, mo, a);
+  launch_pdl(attn_bwd_dq_tc_kernel<HD>, grid, kBwdThreads, SMEM2, st, mq, mk, mv, mo, a);
   PH_LAUNCH_CHECK();
 }
 
@@ -1744,7 +1753,7 @@ void attn_fwd_hd(const bf16* q, const bf16* k, const bf16* v, bf16* o, float* ls
   static std::atomic<uint64_t> cfg{0};
   set_smem_once(cfg, attn_fwd_tc_kernel<HD>, SMEM);
   dim3 grid((S + TQ - 1) / TQ, B * H);
-  attn_fwd_tc_kernel<HD><<<grid, kThreads, SMEM, st>>>(mq, mk, mv, a);
+  launch_pdl(attn_fwd_tc_kernel<HD>, grid, kThreads, SMEM, st, mq, mk, mv, a);
   PH_LAUNCH_CHECK();
 }
 

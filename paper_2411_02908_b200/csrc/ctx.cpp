@@ -162,6 +162,7 @@ static void enqueue_local_round(Ctx& c, const photon_train_cfg& t, const DeviceB
 void Ctx::launch_local_round(const photon_train_cfg& t, const DeviceBatches& db,
                              const float* d_theta_in, float* d_theta_out, uint64_t step_base,
                              double* d_loss, int* d_flag) {
+  PdlScope pdl(cfg.d_model <= kPdlMaxWidth);  // launch-bound small models only (common.cuh)
   if (!graphs_on || eng->timing || db.tau < 1) {
     enqueue_local_round(*this, t, db, d_theta_in, d_theta_out, step_base, d_loss, d_flag, nullptr);
     return;

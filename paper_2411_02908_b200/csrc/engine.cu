@@ -312,6 +312,7 @@ class EngineT final : public Engine {
 // (client.cpp:135-154: one mean over all local-batch targets).
 template <typename T>
 void EngineT<T>::forward_backward(const StepBatch& bt, double* loss_dev, bool backward) {
+  PdlScope pdl(d_ <= kPdlMaxWidth);  // launch-bound small models only (common.cuh)
   if ((uint64_t)bt.S > Smax_)
     throw Error(PHOTON_ERR_SHAPE, "sequence exceeds the context's seq_len");
   const int mb = (int)max_batch;

@@ -279,6 +279,7 @@ template <int BN, bool A_MN, bool B_MN, int NCTA>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ OperandMaps om,
                    const __grid_constant__ EpiMaps em, const TcParams p) {
+  pdl_launch_dependents();
   constexpr int BNL = BN / NCTA;  // B rows (N) staged by this CTA
   constexpr int A_BYTES = BM * BK * 2;
   constexpr int B_BYTES = BNL * BK * 2;
@@ -341,6 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // inputs of the previous kernel visible from here
 
   if (warp == 0) {
     if (lane == 0) {
@@ -679,6 +681,8 @@ struct ReduceArgs {
   void* aux;
 };
 __global__ void splitk_reduce_kernel(const ReduceArgs r) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int64_t total = (int64_t)r.M * r.N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -711,6 +715,8 @@ __global__ void splitk_reduce_kernel(const ReduceArgs r) {
 // same order as splitk_reduce_kernel, so the result is unchanged).
 __global__ void splitk_reduce_store4_kernel(const float* __restrict__ ws, int M, int N, int splits,
                                             float* __restrict__ C, int64_t ldc) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int n4 = N / 4;
   const int64_t total4 = (int64_t)M * n4, total = (int64_t)M * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total4;
@@ -804,20 +810,22 @@ void launch(const OperandMaps& om, const EpiMaps& em, const TcParams& p, int gri
     configured.fetch_or(1ull << (dev & 63));
   }
   if (NCTA == 1) {
-    kern<<<grid, kThreads, SMEM, st>>>(om, em, p);
+    launch_pdl(kern, grid, kThreads, SMEM, st, om, em, p);
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = SMEM;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // see launch_pdl
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_on() ? 2 : 1;
     PH_CUDA(cudaLaunchKernelEx(&cfg, kern, om, em, p));
   }
   PH_LAUNCH_CHECK();
@@ -981,11 +989,11 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
   }
   if (p.splits > 1) {
     if (g.epi == Epi::Store && !p.c_bf16 && g.N % 4 == 0 && g.ldc % 4 == 0 && aligned16(g.C)) {
-      splitk_reduce_store4_kernel<<<kNumSMs * 4, 256, 0, st>>>(ws, g.M, g.N, p.splits,
+      launch_pdl(splitk_reduce_store4_kernel, kNumSMs * 4, 256, 0, st, ws, g.M, g.N, p.splits,
                                                                static_cast<float*>(g.C), g.ldc);
     } else {
       ReduceArgs r{g.M, g.N, p.splits, p.epi, p.c_bf16, g.ldc, ws, g.C, g.bias, g.resid, g.aux};
-      splitk_reduce_kernel<<<kNumSMs * 4, 256, 0, st>>>(r);
+      launch_pdl(splitk_reduce_kernel, kNumSMs * 4, 256, 0, st, r);
     }
     PH_LAUNCH_CHECK();
   }

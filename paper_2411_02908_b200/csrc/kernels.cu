@@ -14,6 +14,8 @@ namespace k {
 __global__ void embed_fwd_kernel(const int32_t* __restrict__ tokens, const float* __restrict__ tok,
                                  const float* __restrict__ pos, float* __restrict__ x, int M,
                                  int S, int d) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int warps = blockDim.x / 32, lane = threadIdx.x & 31;
   for (int m = blockIdx.x * warps + threadIdx.x / 32; m < M; m += gridDim.x * warps) {
     const float* te = tok + (size_t)tokens[m] * d;
@@ -34,7 +36,7 @@ __global__ void embed_fwd_kernel(const int32_t* __restrict__ tokens, const float
 void embed_fwd(const int32_t* tokens, const float* tok, const float* pos, float* x, int M, int S,
                int d, cudaStream_t st) {
   const int blocks = std::min<int>(cdiv(M, 8), kNumSMs * 16);
-  embed_fwd_kernel<<<blocks, 256, 0, st>>>(tokens, tok, pos, x, M, S, d);
+  launch_pdl(embed_fwd_kernel, blocks, 256, 0, st, tokens, tok, pos, x, M, S, d);
   PH_LAUNCH_CHECK();
 }
 
@@ -44,6 +46,8 @@ void embed_fwd(const int32_t* tokens, const float* tok, const float* pos, float*
 __global__ void embed_bwd_tok_kernel(const float* __restrict__ dx, const int32_t* __restrict__ off,
                                      const int32_t* __restrict__ rows, float* __restrict__ dtok,
                                      int V, int d, int row0, int M, int acc) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int warps = blockDim.x / 32, lane = threadIdx.x & 31;
   for (int v = blockIdx.x * warps + threadIdx.x / 32; v < V; v += gridDim.x * warps) {
     const int b = off[v], e = off[v + 1];
@@ -60,6 +64,8 @@ __global__ void embed_bwd_tok_kernel(const float* __restrict__ dx, const int32_t
 }
 __global__ void embed_bwd_pos_kernel(const float* __restrict__ dx, float* __restrict__ dpos,
                                      int M, int S, int d, int acc) {
+  pdl_launch_dependents();
+  pdl_wait();
   const size_t total = (size_t)S * d;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
@@ -72,10 +78,10 @@ __global__ void embed_bwd_pos_kernel(const float* __restrict__ dx, float* __rest
 
 void embed_bwd(const float* dx, const int32_t* csr_off, const int32_t* csr_rows, float* dtok,
                float* dpos, int V, int M, int S, int d, cudaStream_t st, int row0, bool acc) {
-  embed_bwd_tok_kernel<<<std::min<int>(cdiv(V, 8), kNumSMs * 16), 256, 0, st>>>(
+  launch_pdl(embed_bwd_tok_kernel, std::min<int>(cdiv(V, 8), kNumSMs * 16), 256, 0, st, 
       dx, csr_off, csr_rows, dtok, V, d, row0, M, acc ? 1 : 0);
   PH_LAUNCH_CHECK();
-  embed_bwd_pos_kernel<<<std::min<int>(cdiv((uint64_t)S * d, 256), kNumSMs * 8), 256, 0, st>>>(
+  launch_pdl(embed_bwd_pos_kernel, std::min<int>(cdiv((uint64_t)S * d, 256), kNumSMs * 8), 256, 0, st, 
       dx, dpos, M, S, d, acc ? 1 : 0);
   PH_LAUNCH_CHECK();
 }
@@ -131,6 +137,8 @@ __global__ void __launch_bounds__(256) ln_fwd_vec_kernel(const float* __restrict
                                                          T* __restrict__ y,
                                                          float* __restrict__ mean_out,
                                                          float* __restrict__ rstd_out, int M) {
+  pdl_launch_dependents();
+  pdl_wait();
   constexpr int D = NV * 128;
   const int lane = threadIdx.x & 31;
   const float inv_d = 1.0f / (float)D;
@@ -191,6 +199,8 @@ __global__ void __launch_bounds__(256) ln_fwd_split_kernel(const float* __restri
                                                            T* __restrict__ y,
                                                            float* __restrict__ mean_out,
                                                            float* __restrict__ rstd_out, int M) {
+  pdl_launch_dependents();
+  pdl_wait();
   constexpr int NV = 4, D = NV * 128 * WPR, G = 8 / WPR;
   __shared__ float red[2][2][8];  // [row parity][sum][warp]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, grp = warp / WPR, wi = warp % WPR;
@@ -250,13 +260,13 @@ void ln_fwd(const float* x, const float* gain, const float* bias, T* y, float* m
   switch (d) {
 #define PH_LNF(NV)                                                                       \
   case NV * 128:                                                                         \
-    ln_fwd_vec_kernel<T, NV><<<grid, 256, 0, st>>>(x, gain, bias, y, mean, rstd, M);      \
+    launch_pdl(ln_fwd_vec_kernel<T, NV>, grid, 256, 0, st, x, gain, bias, y, mean, rstd, M);      \
     break;
     PH_LNF(1) PH_LNF(2) PH_LNF(3) PH_LNF(4) PH_LNF(5) PH_LNF(6)
 #undef PH_LNF
 #define PH_LNFS(WPR)                                                                      \
   case 512 * WPR:                                                                          \
-    ln_fwd_split_kernel<T, WPR><<<std::min<int>(cdiv(M, 8 / WPR), kNumSMs * 8), 256, 0, st>>>( \
+    launch_pdl(ln_fwd_split_kernel<T, WPR>, std::min<int>(cdiv(M, 8 / WPR), kNumSMs * 8), 256, 0, st,  \
         x, gain, bias, y, mean, rstd, M);                                                  \
     break;
     PH_LNFS(2) PH_LNFS(4) PH_LNFS(8)
@@ -441,6 +451,8 @@ __device__ __forceinline__ int find_job(const int* start, int njobs, int b) {
   return lo;
 }
 __global__ void __launch_bounds__(256) reduce_rows_batch_kernel(const __grid_constant__ RowTable t) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int j = find_job(t.start, t.njobs, blockIdx.x);
   const RowJob& r = t.job[j];
   const int local = blockIdx.x - t.start[j], nx = (r.n * r.nseg + 31) / 32;
@@ -448,6 +460,8 @@ __global__ void __launch_bounds__(256) reduce_rows_batch_kernel(const __grid_con
                       local / nx);
 }
 __global__ void __launch_bounds__(1024) reduce_cols_batch_kernel(const __grid_constant__ ColTable t) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int j = find_job(t.start, t.njobs, blockIdx.x);
   const ColJob& c = t.job[j];
   colreduce_body(c.part, c.nparts, c.n, c.stride, c.out, c.split, c.out1, c.acc, c.split2, c.out2,
@@ -464,7 +478,7 @@ void run_reduce_jobs(ReduceJobs& jobs, cudaStream_t st) {
       n += cdiv(t.job[i].n * t.job[i].nseg, 32) * t.job[i].used;
     }
     t.start[t.njobs] = n;
-    reduce_rows_batch_kernel<<<n, 256, 0, st>>>(t);
+    launch_pdl(reduce_rows_batch_kernel, n, 256, 0, st, t);
     PH_LAUNCH_CHECK();
   }
   for (size_t b = 0; b < jobs.cols.size(); b += kReduceBatch) {
@@ -477,7 +491,7 @@ void run_reduce_jobs(ReduceJobs& jobs, cudaStream_t st) {
       n += cdiv(t.job[i].n, 32);
     }
     t.start[t.njobs] = n;
-    reduce_cols_batch_kernel<<<n, 1024, 0, st>>>(t);
+    launch_pdl(reduce_cols_batch_kernel, n, 1024, 0, st, t);
     PH_LAUNCH_CHECK();
   }
   jobs.rows.clear();
@@ -532,6 +546,8 @@ ln_bwd_vec_kernel(const T* __restrict__ dy, const float* __restrict__ x,
                   const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
                   const float* __restrict__ gain, const float* dres, float* dx_out,
                   T* __restrict__ dx_T, float* __restrict__ part, int M, int osum) {
+  pdl_launch_dependents();
+  pdl_wait();
   constexpr int D = NV * 128;
   extern __shared__ float4 lnb_sm[];
   float4* gs = lnb_sm;                                      // [D/4] gain
@@ -629,6 +645,8 @@ ln_bwd_split_kernel(const T* __restrict__ dy, const float* __restrict__ x,
                     const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
                     const float* __restrict__ gain, const float* dres, float* dx_out,
                     T* __restrict__ dx_T, float* __restrict__ part, int M, int osum) {
+  pdl_launch_dependents();
+  pdl_wait();
   constexpr int NV = 4, D = NV * 128 * WPR, G = 8 / WPR;
   extern __shared__ float lnbs_sm[];          // [G][D] final reduction
   __shared__ float red[2][2][8];              // [row parity][sum][warp]
@@ -738,7 +756,7 @@ void ln_bwd(const T* dy, const float* x, const float* mean, const float* rstd,
                                    kLnBwdVecSmem(NV * 128)));                              \
       attr.fetch_or(1ull << (dev & 63));                                                   \
     }                                                                                      \
-    ln_bwd_vec_kernel<T, NV><<<kLnBwdBlocks, kLnBwdWarps * 32, kLnBwdVecSmem(NV * 128), st>>>( \
+    launch_pdl(ln_bwd_vec_kernel<T, NV>, kLnBwdBlocks, kLnBwdWarps * 32, kLnBwdVecSmem(NV * 128), st,  \
         dy, x, mean, rstd, gain, dres, dx_out, dx_T, part, M, dsum ? 1 : 0);               \
     break;                                                                                 \
   }
@@ -747,7 +765,7 @@ void ln_bwd(const T* dy, const float* x, const float* mean, const float* rstd,
 #define PH_LNBS(WPR)                                                                       \
   case 512 * WPR: {                                                                        \
     constexpr int smem = (8 / WPR) * 512 * WPR * 4;                                        \
-    ln_bwd_split_kernel<T, WPR><<<kLnBwdBlocks, 256, smem, st>>>(                          \
+    launch_pdl(ln_bwd_split_kernel<T, WPR>, kLnBwdBlocks, 256, smem, st,                           \
         dy, x, mean, rstd, gain, dres, dx_out, dx_T, part, M, dsum ? 1 : 0);               \
     break;                                                                                 \
   }
@@ -1218,6 +1236,8 @@ __global__ void __launch_bounds__(kCePipeThreads + 32, 1)
     ce_pipe_kernel(bf16* __restrict__ logits, const int32_t* __restrict__ targets, int M, int V,
                    float inv_v, double* __restrict__ rowloss, int write_grad,
                    float* __restrict__ bias_part, const float* inv_dev) {
+  pdl_launch_dependents();
+  pdl_wait();
   const float inv_count = inv_dev ? *inv_dev : inv_v;
   using namespace sm100;
   extern __shared__ __align__(128) uint8_t ce_sm[];
@@ -1422,7 +1442,7 @@ bool ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count
       }
       const bool fuse = write_grad && dbias && part && V / 8 <= kCePipeThreads * kCeBiasMaxChunks;
       const int grid = std::min(M, kNumSMs);
-      ce_pipe_kernel<<<grid, kCePipeThreads + 32, ce_pipe_smem(V), st>>>(
+      launch_pdl(ce_pipe_kernel, grid, kCePipeThreads + 32, ce_pipe_smem(V), st, 
           logits, targets, M, V, inv_count, rowloss, write_grad ? 1 : 0, fuse ? part : nullptr,
           inv_dev);
       PH_LAUNCH_CHECK();
@@ -1444,6 +1464,8 @@ bool ce_fwd_bwd(T* logits, const int32_t* targets, int M, int V, float inv_count
 
 __global__ void sum_scaled_kernel(const double* __restrict__ x, int n, double scale_v,
                                   double* __restrict__ out, int acc_out, const float* scale_dev) {
+  pdl_launch_dependents();
+  pdl_wait();
   const double scale = scale_dev ? (double)*scale_dev : scale_v;
   __shared__ double sm[32];
   double acc = 0.0;
@@ -1460,7 +1482,7 @@ __global__ void sum_scaled_kernel(const double* __restrict__ x, int n, double sc
 
 void sum_scaled(const double* x, int n, double scale, double* out, cudaStream_t st, bool acc,
                 const float* scale_dev) {
-  sum_scaled_kernel<<<1, 1024, 0, st>>>(x, n, scale, out, acc ? 1 : 0, scale_dev);
+  launch_pdl(sum_scaled_kernel, 1, 1024, 0, st, x, n, scale, out, acc ? 1 : 0, scale_dev);
   PH_LAUNCH_CHECK();
 }
 
@@ -1677,6 +1699,8 @@ __global__ void f32_to_f64_kernel(const float* __restrict__ in, double* __restri
 }
 __global__ void f32_to_bf16_kernel(const float* __restrict__ in, bf16* __restrict__ out,
                                    uint64_t n) {
+  pdl_launch_dependents();
+  pdl_wait();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
     out[i] = __float2bfloat16_rn(in[i]);
@@ -1690,7 +1714,7 @@ void f32_to_f64(const float* in, double* out, uint64_t n, cudaStream_t st) {
   PH_LAUNCH_CHECK();
 }
 void f32_to_bf16(const float* in, bf16* out, uint64_t n, cudaStream_t st) {
-  f32_to_bf16_kernel<<<std::min<unsigned>(cdiv(n, 256), kNumSMs * 8), 256, 0, st>>>(in, out, n);
+  launch_pdl(f32_to_bf16_kernel, std::min<unsigned>(cdiv(n, 256), kNumSMs * 8), 256, 0, st, in, out, n);
   PH_LAUNCH_CHECK();
 }
 

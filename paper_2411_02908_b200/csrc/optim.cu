@@ -30,6 +30,8 @@ __device__ __forceinline__ double block_sum(double v, T* /*tag*/) {
 
 // ---- global norm (param_vector.cpp:105-110), fast path: fixed-shape tree ------
 __global__ void sumsq_kernel(const float* __restrict__ g, uint64_t n, double* __restrict__ part) {
+  pdl_launch_dependents();
+  pdl_wait();
   double acc = 0.0;
   const uint64_t n4 = n / 4;
   const float4* g4 = reinterpret_cast<const float4*>(g);
@@ -46,7 +48,7 @@ __global__ void sumsq_kernel(const float* __restrict__ g, uint64_t n, double* __
 }
 
 void sumsq_parts(const float* g, uint64_t n, double* part, cudaStream_t st) {
-  sumsq_kernel<<<kRedBlocks, 256, 0, st>>>(g, n, part);
+  launch_pdl(sumsq_kernel, kRedBlocks, 256, 0, st, g, n, part);
   PH_LAUNCH_CHECK();
 }
 
@@ -54,6 +56,8 @@ void sumsq_parts(const float* g, uint64_t n, double* part, cudaStream_t st) {
 // norm is recorded (NumericError surfaces at the round boundary).
 __global__ void clip_finalize_kernel(const double* __restrict__ part, int nparts, double clip,
                                      double* norm_out, float* cf_out, int* bad_step, int step) {
+  pdl_launch_dependents();
+  pdl_wait();
   double acc = 0.0;
   for (int i = threadIdx.x; i < nparts; i += blockDim.x) acc += part[i];
   const double s = block_sum(acc, (float*)nullptr);
@@ -71,7 +75,7 @@ __global__ void clip_finalize_kernel(const double* __restrict__ part, int nparts
 
 void clip_finalize(const double* part, double clip, double* norm_out, float* cf_out,
                    int* bad_step, int step, cudaStream_t st) {
-  clip_finalize_kernel<<<1, 1024, 0, st>>>(part, kRedBlocks, clip, norm_out, cf_out, bad_step,
+  launch_pdl(clip_finalize_kernel, 1, 1024, 0, st, part, kRedBlocks, clip, norm_out, cf_out, bad_step,
                                           step);
   PH_LAUNCH_CHECK();
 }
@@ -96,6 +100,8 @@ __global__ void __launch_bounds__(256) adamw_f32_kernel(
     float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v,
     bf16* __restrict__ shadow, uint64_t n, const float* cfp, float lr_v, const double* lr_dev,
     float b1, float b2, float ib1, float ib2, float eps, float wd) {
+  pdl_launch_dependents();
+  pdl_wait();
   const float cf = *cfp;
   if (cf != cf) return;  // NumericError step: no update (clip_finalize_kernel)
   const float lr = lr_dev ? (float)*lr_dev : lr_v;  // device lr: graph-captured rounds
@@ -131,7 +137,7 @@ __global__ void __launch_bounds__(256) adamw_f32_kernel(
 void adamw_f32(float* p, const float* g, float* m, float* v, bf16* shadow, uint64_t n,
                const float* cf, double lr, double b1, double b2, double bc1, double bc2,
                double eps, double wd, cudaStream_t st, const double* lr_dev) {
-  adamw_f32_kernel<<<kNumSMs * 8, 256, 0, st>>>(p, g, m, v, shadow, n, cf, (float)lr, lr_dev, (float)b1,
+  launch_pdl(adamw_f32_kernel, kNumSMs * 8, 256, 0, st, p, g, m, v, shadow, n, cf, (float)lr, lr_dev, (float)b1,
                                                 (float)b2, (float)(1.0 / bc1), (float)(1.0 / bc2),
                                                 (float)eps, (float)wd);
   PH_LAUNCH_CHECK();
@@ -141,6 +147,8 @@ void adamw_f32(float* p, const float* g, float* m, float* v, bf16* shadow, uint6
 __global__ void sgd_f32_kernel(float* __restrict__ p, const float* __restrict__ g,
                                bf16* __restrict__ shadow, uint64_t n, const float* cfp,
                                double lr_v, const double* lr_dev) {
+  pdl_launch_dependents();
+  pdl_wait();
   const double cf = (double)*cfp;
   if (cf != cf) return;  // NumericError step: no update (clip_finalize_kernel)
   const double lr = lr_dev ? *lr_dev : lr_v;
@@ -154,7 +162,7 @@ __global__ void sgd_f32_kernel(float* __restrict__ p, const float* __restrict__ 
 
 void sgd_f32(float* p, const float* g, bf16* shadow, uint64_t n, const float* cf, double lr,
              cudaStream_t st, const double* lr_dev) {
-  sgd_f32_kernel<<<kNumSMs * 8, 256, 0, st>>>(p, g, shadow, n, cf, lr, lr_dev);
+  launch_pdl(sgd_f32_kernel, kNumSMs * 8, 256, 0, st, p, g, shadow, n, cf, lr, lr_dev);
   PH_LAUNCH_CHECK();
 }
 
