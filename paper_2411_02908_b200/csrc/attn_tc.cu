@@ -1693,7 +1693,7 @@ void attn_bwd_hd(const bf16* q, const bf16* k, const bf16* v, const bf16* o, con
   if (!ws) ws = scratch(attn_bwd_tc_ws_floats(B, S, H, d));
   float* Lp = ws;
   float* Dp = Lp + (size_t)B * H * Spad;
-  launch_pdl(attn_bwd_prep_kernel<HD>, std::min<int64_t>(((int64_t)B * S + 7) / 8, kNumSMs * 16), 256, 0, st, o, dO, lse, Lp, Dp, B, S, H, d, Spad);
+  launch_pdl_cls(kPdlAttn, attn_bwd_prep_kernel<HD>, std::min<int64_t>(((int64_t)B * S + 7) / 8, kNumSMs * 16), 256, 0, st, o, dO, lse, Lp, Dp, B, S, H, d, Spad);
   PH_LAUNCH_CHECK();
   constexpr int TQB = HD == 64 ? 128 : 64;  // dK/dV kernel's query tile
   const CUtensorMap mq = head_map(q, rows, d), mk = head_map(k, rows, d), mv = head_map(v, rows, d),
@@ -1718,7 +1718,7 @@ void attn_bwd_hd(const bf16* q, const bf16* k, const bf16* v, const bf16* o, con
     const int waves = (B * H + kNumSMs - 1) / kNumSMs;
     const int grid = PHOTON_FUSED_GRID ? std::min(kNumSMs, (B * H + waves - 1) / waves)
                                        : std::min(kNumSMs, B * H);
-    launch_pdl(attn_bwd_fused64_tc_kernel, grid, kBwdThreads, kFusedSmem, st, mq, mk, mv, mo, a);
+    launch_pdl_cls(kPdlAttn, attn_bwd_fused64_tc_kernel, grid, kBwdThreads, kFusedSmem, st, mq, mk, mv, mo, a);
     PH_LAUNCH_CHECK();
     return;
   }
@@ -1733,13 +1733,13 @@ void attn_bwd_hd(const bf16* q, const bf16* k, const bf16* v, const bf16* o, con
   set_smem_once(cfg2, attn_bwd_dq_tc_kernel<HD>, SMEM2);
   // persistent: one CTA per SM over the units (tile pairs) of both kernels
   const int grid = std::min(kNumSMs, B * H * ((nt + 1) / 2));
-  launch_pdl(attn_bwd_dkdv_tc_kernel<HD>, grid, kBwdThreads, SMEM1, st, mqb, mk, mv, mob, a);
+  launch_pdl_cls(kPdlAttn, attn_bwd_dkdv_tc_kernel<HD>, grid, kBwdThreads, SMEM1, st, mqb, mk, mv, mob, a);
   PH_LAUNCH_CHECK();
   a.g0 = dq;
   a.g1 = nullptr;
   a.s0 = sums;
   a.s1 = nullptr;
-  launch_pdl(attn_bwd_dq_tc_kernel<HD>, grid, kBwdThreads, SMEM2, st, mq, mk, mv, mo, a);
+  launch_pdl_cls(kPdlAttn, attn_bwd_dq_tc_kernel<HD>, grid, kBwdThreads, SMEM2, st, mq, mk, mv, mo, a);
   PH_LAUNCH_CHECK();
 }
 
@@ -1753,7 +1753,7 @@ void attn_fwd_hd(const bf16* q, const bf16* k, const bf16* v, bf16* o, float* ls
   static std::atomic<uint64_t> cfg{0};
   set_smem_once(cfg, attn_fwd_tc_kernel<HD>, SMEM);
   dim3 grid((S + TQ - 1) / TQ, B * H);
-  launch_pdl(attn_fwd_tc_kernel<HD>, grid, kThreads, SMEM, st, mq, mk, mv, a);
+  launch_pdl_cls(kPdlAttn, attn_fwd_tc_kernel<HD>, grid, kThreads, SMEM, st, mq, mk, mv, a);
   PH_LAUNCH_CHECK();
 }
 

@@ -74,6 +74,32 @@ struct PdlScope {
   PdlScope& operator=(const PdlScope&) = delete;
 };
 constexpr uint64_t kPdlMaxWidth = 512;
+// kernel classes for PHOTON_PDL_MASK (experiments): 1 GEMM, 2 attention, 4 the rest.
+// On the 125M step (PHOTON_PDL=1), per MHz: off 537.6, GEMM only 532, attention
+// only 538, the rest only 513-519, all 519 tokens/s/MHz.
+enum PdlClass : int { kPdlGemm = 1, kPdlAttn = 2, kPdlOther = 4 };
+inline bool pdl_class_on(int cls) {
+  static const int mask = [] {
+    const char* e = std::getenv("PHOTON_PDL_MASK");
+    return e ? std::atoi(e) : 7;
+  }();
+  return pdl_on() && (mask & cls);
+}
+template <typename... KArgs, typename... Args>
+inline void launch_pdl_cls(int cls, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                           cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_class_on(cls) ? 1 : 0;
+  PH_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                        Args&&... args) {
@@ -86,7 +112,7 @@ inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_on() ? 1 : 0;
+  cfg.numAttrs = pdl_class_on(kPdlOther) ? 1 : 0;
   PH_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 

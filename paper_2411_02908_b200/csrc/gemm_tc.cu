@@ -810,7 +810,7 @@ void launch(const OperandMaps& om, const EpiMaps& em, const TcParams& p, int gri
     configured.fetch_or(1ull << (dev & 63));
   }
   if (NCTA == 1) {
-    launch_pdl(kern, grid, kThreads, SMEM, st, om, em, p);
+    launch_pdl_cls(kPdlGemm, kern, grid, kThreads, SMEM, st, om, em, p);
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -825,7 +825,7 @@ void launch(const OperandMaps& om, const EpiMaps& em, const TcParams& p, int gri
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // see launch_pdl
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_on() ? 2 : 1;
+    cfg.numAttrs = pdl_class_on(kPdlGemm) ? 2 : 1;
     PH_CUDA(cudaLaunchKernelEx(&cfg, kern, om, em, p));
   }
   PH_LAUNCH_CHECK();
