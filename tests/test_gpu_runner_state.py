@@ -113,3 +113,20 @@ def test_token_pipeline_prefetch(F, oracle):
                    [runner.client_cursor(c) for c in range(3)])
     assert runner.run_round().host_ms > 0  # the restore dropped the prefetch
     assert runner.run_round().host_ms == 0
+
+
+@pytest.mark.parametrize("precision", ["f32", "bf16"])
+def test_topology_invariance(F, oracle, precision):
+    # acceptance c6 (acceptance_main.cpp:390-463): the topology only changes the
+    # reference's cost model, so theta, velocity and cursors after the rounds
+    # are bit-identical for parameter-server, all-reduce and ring all-reduce
+    mc, theta0, plan, local, _, srv, _ = _setup(F, oracle, 3, precision=precision)
+    out = []
+    for topo in (F.Topology.kParameterServer, F.Topology.kAllReduce, F.Topology.kRingAllReduce):
+        r = F.FederationRunner(F.FederationConfig(3, 2, 3, topo, 42), local, srv, plan, theta0,
+                               precision=precision)
+        losses = [r.run_round().mean_client_loss for _ in range(3)]
+        out.append((losses, r.theta().tobytes(), r.velocity().tobytes(),
+                    [r.client_cursor(c) for c in range(3)]))
+    for o in out[1:]:
+        assert o == out[0]
