@@ -230,6 +230,34 @@ __device__ __forceinline__ float ex2(float x) {  // MUFU.EX2 without range fix-u
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x for a pair on the FMA / ALU pipes (no MUFU): round-to-nearest split via
+// the 1.5 * 2^23 magic constant, degree-3 minimax polynomial of 2^f on
+// [-1/2, 1/2] (relative error 1.9e-4, far below the bf16 rounding of P), the
+// exponent added to the bits; x <= -126 gives 0.
+__device__ __forceinline__ float2 ex2_fma2(float2 x) {
+  constexpr float M = 12582912.0f;
+  const float2 j = __fadd2_rn(make_float2(fmaxf(x.x, -126.f), fmaxf(x.y, -126.f)), make_float2(M, M));
+  const float2 r = __fadd2_rn(j, make_float2(-M, -M));
+  const float2 f = __fadd2_rn(x, make_float2(-r.x, -r.y));
+  float2 p = __ffma2_rn(make_float2(0.054898735135793686f, 0.054898735135793686f), f,
+                        make_float2(0.24193310737609863f, 0.24193310737609863f));
+  p = __ffma2_rn(p, f, make_float2(0.6932485103607178f, 0.6932485103607178f));
+  p = __ffma2_rn(p, f, make_float2(0.9999765157699585f, 0.9999765157699585f));
+  const int ex = __float_as_int(j.x) - __float_as_int(M), ey = __float_as_int(j.y) - __float_as_int(M);
+  return make_float2(x.x > -126.f ? __int_as_float(__float_as_int(p.x) + (ex << 23)) : 0.f,
+                     x.y > -126.f ? __int_as_float(__float_as_int(p.y) + (ey << 23)) : 0.f);
+}
+#ifndef PHOTON_FWD_FMA_PRE
+#define PHOTON_FWD_FMA_PRE 0  // the same for the pre-wait chunk (0: none)
+#endif
+#ifndef PHOTON_FWD_FMA_EXP
+#define PHOTON_FWD_FMA_EXP 8  // every 8th pair of the P loops on the FMA pipe (0: none)
+#endif
+// (measured at the 125M shape: 1/8 of the main loop's pairs 0.357-0.367 ms vs
+// 0.365-0.381 with none, 1/4 0.359, 1/2 0.372, 1/16 0.369; also in the pre-wait
+// chunk: no better)
+constexpr int kFmaExp = PHOTON_FWD_FMA_EXP, kFmaExpMod = kFmaExp > 0 ? kFmaExp : 1;
+constexpr int kFmaPre = PHOTON_FWD_FMA_PRE, kFmaPreMod = kFmaPre > 0 ? kFmaPre : 1;
 __device__ __forceinline__ float4 lds_f4(const float* p) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -455,9 +483,13 @@ __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
           const float2 x = __ffma2_rn(make_float2(__uint_as_float(s[c * 32 + 2 * i]),
                                                   __uint_as_float(s[c * 32 + 2 * i + 1])),
                                       make_float2(sl2, sl2), make_float2(-m, -m));
-          const float p0 = ex2(x.x), p1 = ex2(x.y);
-          rs2 = __fadd2_rn(rs2, make_float2(p0, p1));
-          pre[c * 16 + i] = pk(p0, p1);
+          float2 e2;
+          if (kFmaPre > 0 && i % kFmaPreMod == kFmaPreMod - 1)
+            e2 = ex2_fma2(x);
+          else
+            e2 = make_float2(ex2(x.x), ex2(x.y));
+          rs2 = __fadd2_rn(rs2, e2);
+          pre[c * 16 + i] = pk(e2.x, e2.y);
         }
       // P and O are free once PV_{j-1} retired
       if (j >= 1) mbar_wait(o_done, (j - 1) & 1);
@@ -487,9 +519,13 @@ __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
           const float2 x = __ffma2_rn(make_float2(__uint_as_float(s[c * 32 + 2 * i]),
                                                   __uint_as_float(s[c * 32 + 2 * i + 1])),
                                       make_float2(sl2, sl2), make_float2(-m, -m));
-          const float p0 = ex2(x.x), p1 = ex2(x.y);
-          rs2 = __fadd2_rn(rs2, make_float2(p0, p1));
-          pp[i] = pk(p0, p1);
+          float2 e2;
+          if (kFmaExp > 0 && i % kFmaExpMod == kFmaExpMod - 1)
+            e2 = ex2_fma2(x);  // part of the exponentials off the MUFU pipe
+          else
+            e2 = make_float2(ex2(x.x), ex2(x.y));
+          rs2 = __fadd2_rn(rs2, e2);
+          pp[i] = pk(e2.x, e2.y);
         }
         TMEM_ST16(tmem + lane_off + kColP + c * 16, pp);
       }
