@@ -230,23 +230,6 @@ __device__ __forceinline__ float ex2(float x) {  // MUFU.EX2 without range fix-u
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// 2^x for a pair on the FMA / ALU pipes (no MUFU): round-to-nearest split via
-// the 1.5 * 2^23 magic constant, degree-3 minimax polynomial of 2^f on
-// [-1/2, 1/2] (relative error 1.9e-4, far below the bf16 rounding of P), the
-// exponent added to the bits; x <= -126 gives 0.
-__device__ __forceinline__ float2 ex2_fma2(float2 x) {
-  constexpr float M = 12582912.0f;
-  const float2 j = __fadd2_rn(make_float2(fmaxf(x.x, -126.f), fmaxf(x.y, -126.f)), make_float2(M, M));
-  const float2 r = __fadd2_rn(j, make_float2(-M, -M));
-  const float2 f = __fadd2_rn(x, make_float2(-r.x, -r.y));
-  float2 p = __ffma2_rn(make_float2(0.054898735135793686f, 0.054898735135793686f), f,
-                        make_float2(0.24193310737609863f, 0.24193310737609863f));
-  p = __ffma2_rn(p, f, make_float2(0.6932485103607178f, 0.6932485103607178f));
-  p = __ffma2_rn(p, f, make_float2(0.9999765157699585f, 0.9999765157699585f));
-  const int ex = __float_as_int(j.x) - __float_as_int(M), ey = __float_as_int(j.y) - __float_as_int(M);
-  return make_float2(x.x > -126.f ? __int_as_float(__float_as_int(p.x) + (ex << 23)) : 0.f,
-                     x.y > -126.f ? __int_as_float(__float_as_int(p.y) + (ey << 23)) : 0.f);
-}
 #ifndef PHOTON_FWD_FMA_PRE
 #define PHOTON_FWD_FMA_PRE 0  // the same for the pre-wait chunk (0: none)
 #endif
