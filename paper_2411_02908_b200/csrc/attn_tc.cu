@@ -562,43 +562,58 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
-// D = dO . O per (row, head), warp per row: lane l streams the 16-byte vectors
-// l, l + 32, ... of the row (contiguous 512 B per instruction), the HD / 8
-// lanes of a head sum their partial dot products with butterfly shuffles, and
-// the head's first lane writes D and lse (log2 units) into the padded arrays.
+// D = dO . O per (row, head).  A warp takes RPW rows of one head at a time
+// (lane = row within the group x 16-byte vector of the head's columns, so each
+// load instruction reads whole 128-byte lines), four groups per iteration with
+// all loads issued before the first product; the VPH lanes of a row sum their
+// partial dot products with butterfly shuffles and the row's first lane writes
+// D and lse (log2 units) -- consecutive rows of one head, so the writes into the
+// [B*H][Spad] arrays and the lse reads are contiguous.
 template <int HD>
 __global__ void attn_bwd_prep_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dO,
                                      const float* __restrict__ lse, float* __restrict__ Lp,
                                      float* __restrict__ Dp, int B, int S, int H, int d, int Spad) {
   pdl_launch_dependents();
   pdl_wait();
-  constexpr int VPH = HD / 8;  // 16-byte vectors per head
-  const int nvec = d / 8, lane = threadIdx.x & 31;
+  constexpr int VPH = HD / 8;     // 16-byte vectors per head row
+  constexpr int RPW = 32 / VPH;   // rows per warp instruction
+  constexpr int U = 4;            // row groups in flight per lane
+  const int lane = threadIdx.x & 31, vec = lane % VPH, rsub = lane / VPH;
   const int warps = blockDim.x / 32;
-  const int64_t rows = (int64_t)B * S;
-  for (int64_t row = (int64_t)blockIdx.x * warps + threadIdx.x / 32; row < rows;
-       row += (int64_t)gridDim.x * warps) {
-    const uint4* po = reinterpret_cast<const uint4*>(o + row * d);
-    const uint4* pd = reinterpret_cast<const uint4*>(dO + row * d);
-    const int b = (int)(row / S), i = (int)(row % S);
-    for (int v0 = 0; v0 < nvec; v0 += 32) {
-      const int v = v0 + lane;
-      float acc = 0.f;
-      if (v < nvec) {
-        const uint4 x = po[v], y = pd[v];
-        const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+  const int groups = (S + RPW * U - 1) / (RPW * U);  // per head
+  const int64_t items = (int64_t)B * H * groups;
+  for (int64_t it = (int64_t)blockIdx.x * warps + threadIdx.x / 32; it < items;
+       it += (int64_t)gridDim.x * warps) {
+    const int bh = (int)(it / groups), g = (int)(it % groups);
+    const int b = bh / H, h = bh % H;
+    uint4 xs[U], ys[U];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          acc = fmaf(__uint_as_float(xs[e] << 16), __uint_as_float(ys[e] << 16), acc);
-          acc = fmaf(__uint_as_float(xs[e] & 0xffff0000u), __uint_as_float(ys[e] & 0xffff0000u), acc);
-        }
+    for (int u = 0; u < U; ++u) {
+      const int i = (g * U + u) * RPW + rsub;
+      if (i < S) {
+        const int64_t off = ((int64_t)(b * S + i) * d + h * HD) / 8 + vec;
+        xs[u] = reinterpret_cast<const uint4*>(o)[off];
+        ys[u] = reinterpret_cast<const uint4*>(dO)[off];
+      } else {
+        xs[u] = ys[u] = make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t xw[4] = {xs[u].x, xs[u].y, xs[u].z, xs[u].w};
+      const uint32_t yw[4] = {ys[u].x, ys[u].y, ys[u].z, ys[u].w};
+      float acc = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        acc = fmaf(__uint_as_float(xw[e] << 16), __uint_as_float(yw[e] << 16), acc);
+        acc = fmaf(__uint_as_float(xw[e] & 0xffff0000u), __uint_as_float(yw[e] & 0xffff0000u), acc);
       }
 #pragma unroll
       for (int off = 1; off < VPH; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-      if (v < nvec && v % VPH == 0) {
-        const int64_t bh = (int64_t)b * H + v / VPH;
-        Dp[bh * Spad + i] = acc;
-        Lp[bh * Spad + i] = lse[bh * S + i] * kLog2e;
+      const int i = (g * U + u) * RPW + rsub;
+      if (vec == 0 && i < S) {
+        Dp[(int64_t)bh * Spad + i] = acc;
+        Lp[(int64_t)bh * Spad + i] = lse[(int64_t)bh * S + i] * kLog2e;
       }
     }
   }
