@@ -42,7 +42,48 @@ void embed_fwd(const int32_t* tokens, const float* tok, const float* pos, float*
 
 // gather_rows backward (tensor.cpp:305-318): duplicates accumulate in ascending
 // row order.  One warp per vocab row walks that token's rows (CSR sorted by
-// row), so the sum order is fixed and no atomics are needed.
+// row), so the sum order is fixed and no atomics are needed.  With d % 128 == 0
+// each lane keeps its d / 128 float4 columns in registers and issues all of a
+// row's loads at once (the generic loop below is the fallback).
+template <int NV4>
+__global__ void embed_bwd_tok_vec_kernel(const float* __restrict__ dx, const int32_t* __restrict__ off,
+                                         const int32_t* __restrict__ rows, float* __restrict__ dtok,
+                                         int V, int d, int row0, int M, int acc) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int warps = blockDim.x / 32, lane = threadIdx.x & 31;
+  for (int v = blockIdx.x * warps + threadIdx.x / 32; v < V; v += gridDim.x * warps) {
+    const int b = off[v], e = off[v + 1];
+    float4 a[NV4];
+#pragma unroll
+    for (int c = 0; c < NV4; ++c) a[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int r = b; r < e; ++r) {
+      const int m = rows[r] - row0;  // this micro-batch's rows only
+      if ((unsigned)m >= (unsigned)M) continue;
+      const float4* src = reinterpret_cast<const float4*>(dx + (size_t)m * d);
+      float4 t[NV4];
+#pragma unroll
+      for (int c = 0; c < NV4; ++c) t[c] = src[lane + 32 * c];
+#pragma unroll
+      for (int c = 0; c < NV4; ++c) {
+        a[c].x += t[c].x;
+        a[c].y += t[c].y;
+        a[c].z += t[c].z;
+        a[c].w += t[c].w;
+      }
+    }
+    float4* out = reinterpret_cast<float4*>(dtok + (size_t)v * d);
+#pragma unroll
+    for (int c = 0; c < NV4; ++c) {
+      float4 o = a[c];
+      if (acc) {
+        const float4 p = out[lane + 32 * c];
+        o = make_float4(p.x + o.x, p.y + o.y, p.z + o.z, p.w + o.w);
+      }
+      out[lane + 32 * c] = o;
+    }
+  }
+}
 __global__ void embed_bwd_tok_kernel(const float* __restrict__ dx, const int32_t* __restrict__ off,
                                      const int32_t* __restrict__ rows, float* __restrict__ dtok,
                                      int V, int d, int row0, int M, int acc) {
@@ -62,10 +103,46 @@ __global__ void embed_bwd_tok_kernel(const float* __restrict__ dx, const int32_t
     }
   }
 }
+// dpos[s] = sum over the batch's rows m = s, s + S, ... in ascending m; with
+// d % 4 == 0 a thread owns a float4 of a position and has four rows' loads in
+// flight (the per-element sum order is unchanged)
 __global__ void embed_bwd_pos_kernel(const float* __restrict__ dx, float* __restrict__ dpos,
                                      int M, int S, int d, int acc) {
   pdl_launch_dependents();
   pdl_wait();
+  if (d % 4 == 0) {
+    const int d4 = d / 4;
+    const size_t total4 = (size_t)S * d4;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total4;
+         i += (size_t)gridDim.x * blockDim.x) {
+      const int s = (int)(i / d4), j4 = (int)(i % d4);
+      const float4* src = reinterpret_cast<const float4*>(dx) + j4;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+      int m = s;
+      for (; m + 3 * S < M; m += 4 * S) {
+        const float4 t0 = src[(size_t)m * d4], t1 = src[(size_t)(m + S) * d4];
+        const float4 t2 = src[(size_t)(m + 2 * S) * d4], t3 = src[(size_t)(m + 3 * S) * d4];
+        a.x = (((a.x + t0.x) + t1.x) + t2.x) + t3.x;
+        a.y = (((a.y + t0.y) + t1.y) + t2.y) + t3.y;
+        a.z = (((a.z + t0.z) + t1.z) + t2.z) + t3.z;
+        a.w = (((a.w + t0.w) + t1.w) + t2.w) + t3.w;
+      }
+      for (; m < M; m += S) {
+        const float4 t = src[(size_t)m * d4];
+        a.x += t.x;
+        a.y += t.y;
+        a.z += t.z;
+        a.w += t.w;
+      }
+      float4* o = reinterpret_cast<float4*>(dpos) + i;
+      if (acc) {
+        const float4 p = *o;
+        a = make_float4(p.x + a.x, p.y + a.y, p.z + a.z, p.w + a.w);
+      }
+      *o = a;
+    }
+    return;
+  }
   const size_t total = (size_t)S * d;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
@@ -78,8 +155,20 @@ __global__ void embed_bwd_pos_kernel(const float* __restrict__ dx, float* __rest
 
 void embed_bwd(const float* dx, const int32_t* csr_off, const int32_t* csr_rows, float* dtok,
                float* dpos, int V, int M, int S, int d, cudaStream_t st, int row0, bool acc) {
-  launch_pdl(embed_bwd_tok_kernel, std::min<int>(cdiv(V, 8), kNumSMs * 16), 256, 0, st, 
-      dx, csr_off, csr_rows, dtok, V, d, row0, M, acc ? 1 : 0);
+  const int tok_grid = std::min<int>(cdiv(V, 8), kNumSMs * 16);
+  const bool al = (reinterpret_cast<uintptr_t>(dx) & 15) == 0 && (reinterpret_cast<uintptr_t>(dtok) & 15) == 0;
+  if (al && d == 768)
+    launch_pdl(embed_bwd_tok_vec_kernel<6>, tok_grid, 256, 0, st, dx, csr_off, csr_rows, dtok, V, d,
+               row0, M, acc ? 1 : 0);
+  else if (al && d == 2048)
+    launch_pdl(embed_bwd_tok_vec_kernel<16>, tok_grid, 256, 0, st, dx, csr_off, csr_rows, dtok, V, d,
+               row0, M, acc ? 1 : 0);
+  else if (al && d == 4096)
+    launch_pdl(embed_bwd_tok_vec_kernel<32>, tok_grid, 256, 0, st, dx, csr_off, csr_rows, dtok, V, d,
+               row0, M, acc ? 1 : 0);
+  else
+    launch_pdl(embed_bwd_tok_kernel, tok_grid, 256, 0, st, dx, csr_off, csr_rows, dtok, V, d, row0, M,
+               acc ? 1 : 0);
   PH_LAUNCH_CHECK();
   launch_pdl(embed_bwd_pos_kernel, std::min<int>(cdiv((uint64_t)S * d, 256), kNumSMs * 8), 256, 0, st, 
       dx, dpos, M, S, d, acc ? 1 : 0);
