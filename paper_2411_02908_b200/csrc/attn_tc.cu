@@ -572,9 +572,12 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 template <int HD>
 __global__ void attn_bwd_prep_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dO,
                                      const float* __restrict__ lse, float* __restrict__ Lp,
-                                     float* __restrict__ Dp, int B, int S, int H, int d, int Spad) {
+                                     float* __restrict__ Dp, int B, int S, int H, int d, int Spad,
+                                     uint32_t* __restrict__ sync, int nsync) {
   pdl_launch_dependents();
   pdl_wait();
+  if (sync && blockIdx.x == 0)
+    for (int i = threadIdx.x; i < nsync; i += blockDim.x) sync[i] = 0u;
   constexpr int VPH = HD / 8;     // 16-byte vectors per head row
   constexpr int RPW = 32 / VPH;   // rows per warp instruction
   constexpr int U = 4;            // row groups in flight per lane
@@ -644,6 +647,9 @@ struct BwdArgs {
   bf16* g2;
   float* s2;
   float* dqa;
+  // fused backward's cross-CTA schedule words (zeroed by the prep kernel):
+  // sync[0] = CTA ticket, sync[1 + bh] = "head bh's first part done" flag
+  uint32_t* sync;
 };
 
 // producer, MMA, SWB softmax warps: SWB/4 warps per TMEM lane quarter, each on
@@ -1250,7 +1256,7 @@ constexpr int NRF = PHOTON_ATTN_NRF, NKF2 = PHOTON_ATTN_NKF;
 #define PHOTON_FUSED_HINTS 1
 #endif
 #ifndef PHOTON_FUSED_GRID
-#define PHOTON_FUSED_GRID 1
+#define PHOTON_FUSED_GRID 2
 #endif
 constexpr int kFusedSmem = 1024 + 2 * 32768 + (NKF2 + 1) * 16384 + NRF * (2 * 16384 + 8 * 128) + 512;
 static_assert(kFusedSmem <= 232448, "fused attention backward: shared memory");
@@ -1273,6 +1279,90 @@ __device__ __forceinline__ float4 ld_relaxed_f4(const float* p) {
                : "memory");
   return v;
 }
+
+// barrier among the fused pass's 16 softmax warps (hardware barrier 1)
+__device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, %0;" ::"n"(SWB * 32) : "memory"); }
+
+// The fused pass's work split.  A unit is one key tile of one head; its cost is
+// its number of query tiles (nt - kt).  Units are ordered head-major, each
+// head's key tiles in its walking order (odd heads descending, see desc()), and
+// logical CTA c owns the contiguous units whose cost midpoints fall in
+// [c C / G, (c+1) C / G) -- every CTA within half a unit of the mean, so all
+// SMs finish together (384 heads: 353 +- 8 tile pairs per CTA on 148 SMs instead
+// of 408 on 128).  A head cut between CTAs c and c+1 keeps one dQ summation
+// order: c walks the head's first key tiles FIRST and then raises the head's
+// flag; c+1 walks the rest LAST, after acquiring the flag, so the dQ partials
+// still arrive key tile by key tile in the head's order (bitwise the same as an
+// uncut head).  Logical ids come from a ticket taken at start, so CTA c-1 is
+// resident (or done) whenever c waits, and c-1 raises the flag before it
+// waits on anything -- no dependence on the hardware's CTA dispatch order.
+struct FusedSched {
+  int G, BH, nt;
+  int64_t Hc, C;
+  __device__ FusedSched(int g, int bh, int n)
+      : G(g), BH(bh), nt(n), Hc((int64_t)n * (n + 1) / 2), C((int64_t)bh * n * (n + 1) / 2) {}
+  // odd heads walk their key tiles in descending order: the live set of an
+  // ascending head (Q/dO tiles j..n-1 and the accumulators of dQ_{j+1..n-1})
+  // shrinks while a descending one's grows, so the L2 footprint of all heads in
+  // flight stays near half of its peak
+  __device__ bool desc(int bh) const { return PHOTON_FUSED_ALT && (bh & 1); }
+  __device__ int kt_of(int bh, int kk) const { return desc(bh) ? nt - 1 - kk : kk; }
+  __device__ int owner(int bh, int kk) const {
+    const int64_t pre = desc(bh) ? (int64_t)kk * (kk + 1) / 2 : (int64_t)kk * nt - (int64_t)kk * (kk - 1) / 2;
+    const int64_t m2 = 2 * ((int64_t)bh * Hc + pre) + (nt - kt_of(bh, kk));
+    return (int)(m2 * G / (2 * C));
+  }
+  // first global unit (bh * nt + kk) owned by CTA >= c: the unit holding cost
+  // position c C / G lies in head floor(c BH / G), so it or the next one is it
+  __device__ int64_t first_unit(int c) const {
+    if (c >= G) return (int64_t)BH * nt;
+    const int bh0 = (int)((int64_t)c * BH / G);
+    for (int bh = bh0; bh < BH && bh <= bh0 + 1; ++bh)
+      for (int kk = 0; kk < nt; ++kk)
+        if (owner(bh, kk) >= c) return (int64_t)bh * nt + kk;
+    return (int64_t)BH * nt;
+  }
+};
+
+// The segments CTA c walks, in order: the first part of its last head (if cut:
+// raises the flag), its whole heads, the rest of its first head (if cut: waits
+// for the flag).  A range inside a single head is one segment doing both.
+struct FusedSegs {
+  int hf, kf, hl, kle, n;
+  __device__ FusedSegs(const FusedSched& f, int c) {
+    const int64_t u0 = f.first_unit(c), u1 = f.first_unit(c + 1);
+    if (u1 <= u0) {
+      n = 0;
+      hf = kf = hl = kle = 0;
+      return;
+    }
+    hf = (int)(u0 / f.nt);
+    kf = (int)(u0 % f.nt);
+    hl = (int)((u1 - 1) / f.nt);
+    kle = (int)((u1 - 1) % f.nt) + 1;
+    if (hf == hl) n = 1;
+    else n = (kle < f.nt) + (kf > 0) + ((kle < f.nt ? hl : hl + 1) - (kf > 0 ? hf + 1 : hf));
+  }
+  // segment s: head bh, key-tile positions [k0, k1), wait / signal the flag
+  __device__ void get(int s, int nt, int& bh, int& k0, int& k1, bool& wait, bool& sig) const {
+    if (hf == hl) {
+      bh = hf, k0 = kf, k1 = kle, wait = kf > 0, sig = kle < nt;
+      return;
+    }
+    wait = sig = false;
+    const bool cut_last = kle < nt;
+    if (cut_last && s == 0) {
+      bh = hl, k0 = 0, k1 = kle, sig = true;
+      return;
+    }
+    if (kf > 0 && s == n - 1) {
+      bh = hf, k0 = kf, k1 = nt, wait = true;
+      return;
+    }
+    bh = (kf > 0 ? hf + 1 : hf) + s - (cut_last ? 1 : 0);
+    k0 = 0, k1 = nt;
+  }
+};
 
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_fused64_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
@@ -1308,14 +1398,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* dq_free = s_full + 5;           // dQ drained from TMEM by the softmax warps
   uint64_t* acc_empty = s_full + 6;         // dK / dV drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 7);
+  uint32_t* cta_slot = tmem_slot + 1;
 
   const int nt = (a.S + T - 1) / T;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-  // odd CTAs walk the key tiles in descending order: the live set of an
-  // ascending head (Q/dO tiles j..n-1 and the accumulators of dQ_{j+1..n-1})
-  // shrinks while a descending one's grows, so the L2 footprint of all heads in
-  // flight stays near half of its peak
-  const bool desc = PHOTON_FUSED_ALT && (blockIdx.x & 1);
+  const FusedSched fs(gridDim.x, a.BH, nt);
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < NKF2; ++i) {
@@ -1346,7 +1433,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
-  pdl_wait();  // inputs of the previous kernel visible from here
+  pdl_wait();  // inputs of the previous kernel visible from here (and the zeroed sync words)
+  if (threadIdx.x == 0) *cta_slot = atomicAdd(a.sync, 1u);
+  __syncthreads();
+  const FusedSegs segs(fs, (int)*cta_slot);
 
   if (warp == 0) {
     if (lane == 0) {  // ===== producer: K, V per key tile, the Q / dO / L / D ring =====
@@ -1355,10 +1445,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const uint64_t pol_once = PHOTON_FUSED_HINTS ? policy_evict_first() : 0;
       const uint64_t pol_keep = PHOTON_FUSED_HINTS ? policy_evict_last() : 0;
       int ti = 0, gi = 0;
-      for (int bh = blockIdx.x; bh < a.BH; bh += gridDim.x) {
+      for (int sg = 0; sg < segs.n; ++sg) {
+        int bh, k0, k1;
+        bool sw, ss;
+        segs.get(sg, nt, bh, k0, k1, sw, ss);
         const int b = bh / a.H, h = bh % a.H, row_base = b * a.S;
-        for (int kk = 0; kk < nt; ++kk, ++ti) {
-          const int kt = desc ? nt - 1 - kk : kk;
+        for (int kk = k0; kk < k1; ++kk, ++ti) {
+          const int kt = fs.kt_of(bh, kk);
           const int kb = ti % NKF2;
           mbar_wait(&k_empty[kb], ((ti / NKF2) & 1) ^ 1);
           mbar_expect_tx(&k_full[kb], KB);
@@ -1429,9 +1522,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       int ti = 0, gi = 0;
       int pend = -1, pend_st = 0, pend_t = 0, pend_kb = 0;
       bool pend_first = false, pend_last = false;
-      for (int bh = blockIdx.x; bh < a.BH; bh += gridDim.x) {
-        for (int kk = 0; kk < nt; ++kk, ++ti) {
-          const int kt = desc ? nt - 1 - kk : kk;
+      for (int sg = 0; sg < segs.n; ++sg) {
+        int bh, k0, k1;
+        bool sw, ss;
+        segs.get(sg, nt, bh, k0, k1, sw, ss);
+        for (int kk = k0; kk < k1; ++kk, ++ti) {
+          const int kt = fs.kt_of(bh, kk);
           const int kb = ti % NKF2;
           mbar_wait(&k_full[kb], (ti / NKF2) & 1);
           mbar_wait(v_full, ti & 1);
@@ -1478,6 +1574,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // tile's softmax) and where it goes
     auto emit_dq = [&](const uint32_t (&u)[GPH], int p_bh, int p_qt, int p_kt) {
       float* acc = a.dqa + (((int64_t)p_bh * nt + p_qt) * (HD / 4) + cg * (GPH / 4)) * (4 * T) + 4 * r;
+      const bool desc = fs.desc(p_bh);
       const bool first = desc ? p_kt == p_qt : p_kt == 0, fin = desc ? p_kt == 0 : p_kt == p_qt;
       if (!fin) {
 #pragma unroll
@@ -1527,10 +1624,25 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     };
     int gi = 0;
     int p_bh = 0, p_qt = 0, p_kt = 0;
-    for (int bh = blockIdx.x; bh < a.BH; bh += gridDim.x) {
+    bool pend = false;  // tile gi-1's dQ not drained yet
+    for (int sg = 0; sg < segs.n; ++sg) {
+      int bh, k0, k1;
+      bool sw, ss;
+      segs.get(sg, nt, bh, k0, k1, sw, ss);
       const int b = bh / a.H, h = bh % a.H, row_base = b * a.S;
-      for (int kk = 0; kk < nt; ++kk) {
-        const int kt = desc ? nt - 1 - kk : kk;
+      if (sw) {  // the rest of a cut head: its first part's dQ partials are in
+        if (threadIdx.x == 64) {
+          const uint32_t* f = a.sync + 1 + bh;
+          uint32_t v;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+          } while (v == 0u);
+          __threadfence();
+        }
+        softmax_bar();
+      }
+      for (int kk = k0; kk < k1; ++kk) {
+        const int kt = fs.kt_of(bh, kk);
         const int key = kt * T + r;
         const bool key_live = key < a.S;
         for (int qt = kt; qt < nt; ++qt, ++gi) {
@@ -1599,11 +1711,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(p_full);
           if (warp == 2 && lane == 0) ATTN_TRACE_P(28, gi);
-          if (gi >= 1) {
+          if (pend) {
             uint32_t dqv[GPH];
             drain_dq(gi - 1, dqv);
             emit_dq(dqv, p_bh, p_qt, p_kt);
           }
+          pend = true;
           if (warp == 2 && lane == 0) ATTN_TRACE_P(29, gi);
           if (lane == 0) ATTN_TRACE_MAX(31, gi);
           p_bh = bh;
@@ -1628,8 +1741,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           warp_colsum<GPH>(fv, a.s2 + prow);
         }
       }
+      if (ss) {  // first part of a cut head: drain its last dQ now, then raise the flag
+        if (pend) {
+          uint32_t dqv[GPH];
+          drain_dq(gi - 1, dqv);
+          emit_dq(dqv, p_bh, p_qt, p_kt);
+          pend = false;
+        }
+        __threadfence();
+        softmax_bar();
+        if (threadIdx.x == 64) {
+          __threadfence();
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.sync + 1 + bh), "r"(1u) : "memory");
+        }
+      }
     }
-    if (gi >= 1) {  // the last tile's dQ
+    if (pend) {  // the last tile's dQ
       uint32_t dqv[GPH];
       drain_dq(gi - 1, dqv);
       emit_dq(dqv, p_bh, p_qt, p_kt);
@@ -1714,7 +1841,9 @@ bool attn_tc_supported(int dh, int d) { return (dh == 64 || dh == 128) && (d % 8
 size_t attn_bwd_tc_ws_floats(int B, int S, int H, int d) {
   const size_t Spad = (size_t)(S + TQ - 1) / TQ * TQ;
   // L, D; at head dim 64 the fused pass's fp32 dQ accumulator
-  return (size_t)2 * B * H * Spad + (PHOTON_ATTN_FUSED && d == 64 * H ? (size_t)B * H * Spad * 64 : 0);
+  // (plus the schedule words: a ticket and one flag per head, 16-byte aligned)
+  return (size_t)2 * B * H * Spad +
+         (PHOTON_ATTN_FUSED && d == 64 * H ? (size_t)B * H * Spad * 64 + ((size_t)B * H + 4 + 3) / 4 * 4 : 0);
 }
 
 namespace {
@@ -1727,7 +1856,11 @@ void attn_bwd_hd(const bf16* q, const bf16* k, const bf16* v, const bf16* o, con
   if (!ws) ws = scratch(attn_bwd_tc_ws_floats(B, S, H, d));
   float* Lp = ws;
   float* Dp = Lp + (size_t)B * H * Spad;
-  launch_pdl_cls(kPdlAttn, attn_bwd_prep_kernel<HD>, std::min<int64_t>(((int64_t)B * S + 7) / 8, kNumSMs * 16), 256, 0, st, o, dO, lse, Lp, Dp, B, S, H, d, Spad);
+  const bool fused = HD == 64 && PHOTON_ATTN_FUSED;
+  uint32_t* sync = fused ? reinterpret_cast<uint32_t*>(Dp + (size_t)B * H * Spad + (size_t)B * H * Spad * 64)
+                         : nullptr;
+  const int nsync = B * H + 1;
+  launch_pdl_cls(kPdlAttn, attn_bwd_prep_kernel<HD>, std::min<int64_t>(((int64_t)B * S + 7) / 8, kNumSMs * 16), 256, 0, st, o, dO, lse, Lp, Dp, B, S, H, d, Spad, sync, nsync);
   PH_LAUNCH_CHECK();
   constexpr int TQB = HD == 64 ? 128 : 64;  // dK/dV kernel's query tile
   const CUtensorMap mq = head_map(q, rows, d), mk = head_map(k, rows, d), mv = head_map(v, rows, d),
@@ -1746,12 +1879,15 @@ void attn_bwd_hd(const bf16* q, const bf16* k, const bf16* v, const bf16* o, con
     a.s1 = sums ? sums + P : nullptr;
     a.s2 = sums ? sums + 2 * P : nullptr;
     a.dqa = Dp + (size_t)B * H * Spad;
+    a.sync = sync;
     static std::atomic<uint64_t> cfgf{0};
     set_smem_once(cfgf, attn_bwd_fused64_tc_kernel, kFusedSmem);
-    // as many CTAs as keep the waves of heads even (e.g. 384 heads: 128 x 3)
+    // PHOTON_FUSED_GRID 2: every SM, heads split between neighbouring CTAs at
+    // key-tile boundaries (FusedSched); 1: as many CTAs as keep whole heads in
+    // even waves (e.g. 384 heads: 128 x 3)
     const int waves = (B * H + kNumSMs - 1) / kNumSMs;
-    const int grid = PHOTON_FUSED_GRID ? std::min(kNumSMs, (B * H + waves - 1) / waves)
-                                       : std::min(kNumSMs, B * H);
+    const int grid = PHOTON_FUSED_GRID == 1 ? std::min(kNumSMs, (B * H + waves - 1) / waves)
+                                            : std::min(kNumSMs, B * H);
     launch_pdl_cls(kPdlAttn, attn_bwd_fused64_tc_kernel, grid, kBwdThreads, kFusedSmem, st, mq, mk, mv, mo, a);
     PH_LAUNCH_CHECK();
     return;

@@ -84,9 +84,46 @@ def test_attention_tcgen05_dh128_long():
 
 
 def test_attention_tcgen05_many_heads():
-    # B * H = 192 > 148: the fused dh-64 backward runs several heads per CTA
-    # (96 CTAs x 2), odd CTAs walking the key tiles in descending order
+    # B * H = 192 > 148: the fused dh-64 backward runs on 148 CTAs with heads cut
+    # between neighbouring CTAs at key-tile boundaries; odd heads walk their key
+    # tiles in descending order
     _run(2, 16, 256, 12, 768)
+    _run(2, 16, 640, 12, 768)
+
+
+def test_attention_tcgen05_cut_heads_bitwise():
+    # heads cut between two CTAs (B * H = 192 on 148 SMs) give bit-identical dq /
+    # dk / dv to the same heads run whole (one sequence per launch: 12 heads,
+    # no cuts; H even keeps every head's walking direction)
+    from paper_2411_02908_b200 import _capi as A
+
+    B, S, H = 16, 640, 12
+    d = 64 * H
+    g = torch.Generator(device="cuda").manual_seed(5)
+    q, k, v, dO = (torch.randn(B, S, d, device="cuda", generator=g).bfloat16() for _ in range(4))
+    err = A.photon_err()
+    ms = C.c_double()
+
+    def run(Bn, qq, kk, vv, dd):
+        o = torch.empty_like(qq)
+        lse = torch.empty(Bn * H * S, device="cuda")
+        assert A.lib().photon_debug_attention(2, Bn, S, H, d, qq.data_ptr(), kk.data_ptr(),
+                                              vv.data_ptr(), o.data_ptr(), lse.data_ptr(), None,
+                                              None, None, None, None, C.byref(ms),
+                                              C.byref(err)) == 0, err.msg
+        dq, dk, dv = torch.empty_like(qq), torch.empty_like(qq), torch.empty_like(qq)
+        assert A.lib().photon_debug_attention(2, Bn, S, H, d, qq.data_ptr(), kk.data_ptr(),
+                                              vv.data_ptr(), o.data_ptr(), lse.data_ptr(),
+                                              dd.data_ptr(), None, dq.data_ptr(), dk.data_ptr(),
+                                              dv.data_ptr(), C.byref(ms), C.byref(err)) == 0, err.msg
+        torch.cuda.synchronize()
+        return dq, dk, dv
+
+    full = run(B, q, k, v, dO)
+    for b in range(B):
+        one = run(1, *(x[b:b + 1].contiguous() for x in (q, k, v, dO)))
+        for name, x, y in zip(("dq", "dk", "dv"), full, one):
+            assert torch.equal(x[b:b + 1], y), (name, b)
 
 
 def test_attention_tcgen05_backward_deterministic():
