@@ -279,6 +279,11 @@ constexpr int NKF = 3;
 #endif
 constexpr int kFwdPre = PHOTON_FWD_PRE;  // 32-score chunks of P computed before the PV wait
 
+#ifndef PHOTON_FWD_CHUNK_MB
+#define PHOTON_FWD_CHUNK_MB 64
+#endif
+constexpr int64_t kFwdChunkBytes = (int64_t)PHOTON_FWD_CHUNK_MB << 20;
+
 template <int HD>
 __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
@@ -309,8 +314,20 @@ __global__ void __launch_bounds__(kThreads, HD == 64 ? 2 : 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(k_empty + NKF);
 
   const int nqt = (a.S + TQ - 1) / TQ;
-  const int qt = nqt - 1 - blockIdx.x;  // heavy tiles first
-  const int bh = blockIdx.y, b = bh / a.H, h = bh % a.H;
+  // dispatch order (x fastest): chunks of heads whose K / V total kFwdChunkBytes,
+  // in a chunk the heaviest query tile of every head first, then the next
+  // heaviest, ... -- the grid's last CTAs are light ones (no long tail), and a
+  // chunk's K / V stay in L2 while its tiles run (125M shape: 128 heads per
+  // chunk, 0.376 -> 0.350 ms; 1.3B heads: 64)
+  int qt, bh;
+  {
+    const int chunk = max(1, (int)(kFwdChunkBytes / ((int64_t)a.S * HD * 4)));
+    const int L = blockIdx.x + blockIdx.y * nqt, per = chunk * nqt;
+    const int c0 = L / per * chunk, r = L % per, cg = min(chunk, (int)gridDim.y - c0);
+    qt = nqt - 1 - r / cg;
+    bh = c0 + r % cg;
+  }
+  const int b = bh / a.H, h = bh % a.H;
   const int q0 = qt * TQ;
   const int row_base = b * a.S;
   const int n_kt = (q0 + TQ - 1) / TK + 1;
