@@ -406,7 +406,17 @@ void EngineT<T>::micro(const StepBatch& bt, double* loss_dev, bool backward, boo
     k::colsum<T>(logits_, M, V, part_, G(off_.head_b), stream, acc);
   }
   mm(M, d, V, logits_, V, true, W(off_.head_w), V, true, dyT_, d, TT, Epi::Store);
-  mm(d, V, M, xf_, d, false, logits_, V, false, G(off_.head_w), V, DT::F32, WG);
+  if (sizeof(T) == 2 && gemm_mode == 1 && M % 8 == 0) {
+    // K-major A for the head weight gradient: xf transposed into dq_ (free until
+    // the last block's attention backward); 4.3 -> 3.6 ms for the contraction
+    {
+      Scope sc(this, 2, 0);
+      k::transpose_bf16(reinterpret_cast<const bf16*>(xf_), M, d, reinterpret_cast<bf16*>(dq_), stream);
+    }
+    mm(d, V, M, dq_, M, true, logits_, V, false, G(off_.head_w), V, DT::F32, WG);
+  } else {
+    mm(d, V, M, xf_, d, false, logits_, V, false, G(off_.head_w), V, DT::F32, WG);
+  }
   {
     Scope sc(this, 2, 0);
     // the column sums of its output are the last block's b2 gradient

@@ -135,6 +135,8 @@ inline size_t attn_bwd_sums_floats(int B, int S, int d) { return (size_t)3 * B *
 void f64_to_f32(const double* in, float* out, uint64_t n, cudaStream_t st);
 void f32_to_f64(const float* in, double* out, uint64_t n, cudaStream_t st);
 void f32_to_bf16(const float* in, bf16* out, uint64_t n, cudaStream_t st);
+// out[c][r] = in[r][c], [rows][cols] bf16
+void transpose_bf16(const bf16* in, int rows, int cols, bf16* out, cudaStream_t st);
 
 // ---- optimizer (optim.cu, compiled without FMA contraction) ---------------------
 // global-norm clip (optim.cpp:50-57): parts -> norm, cf; bad[0] set to step+1

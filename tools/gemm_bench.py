@@ -29,7 +29,12 @@ CASES = [
     ("probe dW dxd K-major", d, d, M, 1, 1, 0, 0),
     ("probe dW w1 K-major", d, hid, M, 1, 1, 0, 0),
     ("probe fwd qkv N=3d +b", M, 3 * d, d, 1, 0, 2, 1),
+    ("probe dW head A K-major", d, V, M, 1, 0, 0, 0),
+    ("probe dW w1 A K-major", d, hid, M, 1, 0, 0, 0),
+    ("probe dW w2 A K-major", hid, d, M, 1, 0, 0, 0),
 ]
+if len(sys.argv) > 2:  # only the cases whose name contains argv[2]
+    CASES = [c for c in CASES if sys.argv[2] in c[0]]
 impl = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 tot_f, tot_t = 0.0, 0.0
 for name, m, n, k, ak, bk, epi, cb in CASES:
