@@ -30,6 +30,10 @@ CASES = [
     ("probe dW w1 K-major", d, hid, M, 1, 1, 0, 0),
     ("probe fwd qkv N=3d +b", M, 3 * d, d, 1, 0, 2, 1),
     ("probe dW head A K-major", d, V, M, 1, 0, 0, 0),
+    ("probe fwd head B K-major +b", M, V, d, 1, 1, 2, 1),
+    ("probe fwd w1 B K-major +b gelu", M, hid, d, 1, 1, 4, 1),
+    ("probe fwd qkv B K-major +b", M, d, d, 1, 1, 2, 1),
+    ("probe fwd w2 B K-major +b +resid", M, d, hid, 1, 1, 3, 0),
     ("probe dW w1 A K-major", d, hid, M, 1, 0, 0, 0),
     ("probe dW w2 A K-major", hid, d, M, 1, 0, 0, 0),
 ]
