@@ -1903,8 +1903,13 @@ void attn_bwd_hd(const bf16* q, const bf16* k, const bf16* v, const bf16* o, con
     // key-tile boundaries (FusedSched); 1: as many CTAs as keep whole heads in
     // even waves (e.g. 384 heads: 128 x 3)
     const int waves = (B * H + kNumSMs - 1) / kNumSMs;
-    const int grid = PHOTON_FUSED_GRID == 1 ? std::min(kNumSMs, (B * H + waves - 1) / waves)
-                                            : std::min(kNumSMs, B * H);
+    static const int ctas_env = [] {  // experiments: PHOTON_FUSED_CTAS caps the grid
+      const char* e = std::getenv("PHOTON_FUSED_CTAS");
+      return e ? std::atoi(e) : 0;
+    }();
+    int grid = PHOTON_FUSED_GRID == 1 ? std::min(kNumSMs, (B * H + waves - 1) / waves)
+                                      : std::min(kNumSMs, B * H);
+    if (ctas_env > 0) grid = std::min(grid, ctas_env);
     launch_pdl_cls(kPdlAttn, attn_bwd_fused64_tc_kernel, grid, kBwdThreads, kFusedSmem, st, mq, mk, mv, mo, a);
     PH_LAUNCH_CHECK();
     return;
