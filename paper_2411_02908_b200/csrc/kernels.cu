@@ -1406,13 +1406,18 @@ __global__ void __launch_bounds__(kCePipeThreads + 32, 1)
     // from l[t] in fp32 (p - 1 cancels; the bf16 copy of e would not do).  A NaN
     // logit makes s NaN and a +inf logit m = +inf and s NaN, so the reference's
     // NaN loss (tensor.cpp:569-582) is detected from (m, s).
-    float m = -INFINITY;
+    // (1) on the packed bf16 pairs (HMNMX2: the max of bf16 values is one of
+    // them, so the same m as in fp32; like fmaxf it passes over NaNs)
+    __nv_bfloat162 m2 = __floats2bfloat162_rn(-INFINITY, -INFINITY);
     for (int c = tid; c < nvec; c += kCePipeThreads) {
-      float v[8];
-      ce_unpack8(lds128(base + c * 16), v);
-      m = fmaxf(m, fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])),
-                         fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7]))));
+      const uint4 x = lds128(base + c * 16);
+      const __nv_bfloat162 a = __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&x.x),
+                                       *reinterpret_cast<const __nv_bfloat162*>(&x.y));
+      const __nv_bfloat162 b = __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&x.z),
+                                       *reinterpret_cast<const __nv_bfloat162*>(&x.w));
+      m2 = __hmax2(m2, __hmax2(a, b));
     }
+    float m = fmaxf(__low2float(m2), __high2float(m2));
     m = warp_max(m);
     if (lane == 0) red_m[warp] = m;
     named_bar_sync(1, kCePipeThreads);
