@@ -89,6 +89,8 @@ def test_attention_tcgen05_many_heads():
     # tiles in descending order
     _run(2, 16, 256, 12, 768)
     _run(2, 16, 640, 12, 768)
+    _run(2, 25, 128, 12, 768)   # 300 heads of one key tile each (no cuts possible)
+    _run(2, 5, 1000, 30, 1920)  # 150 heads on 148 CTAs: nearly every CTA boundary cuts a head
 
 
 def test_attention_tcgen05_cut_heads_bitwise():
