@@ -1272,6 +1272,9 @@ constexpr int NRF = PHOTON_ATTN_NRF, NKF2 = PHOTON_ATTN_NKF;
 #ifndef PHOTON_FUSED_HINTS
 #define PHOTON_FUSED_HINTS 1
 #endif
+#ifndef PHOTON_FUSED_EARLY_Q
+#define PHOTON_FUSED_EARLY_Q 1
+#endif
 #ifndef PHOTON_FUSED_GRID
 #define PHOTON_FUSED_GRID 2
 #endif
@@ -1522,18 +1525,33 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           mma_ts(tmem + colDV, tmem + colP + kk * 8, sw128(bo + kk * 2048, QB, 1024), IDG,
                  (!first || kk > 0) ? 1u : 0u);
         commit(pv_done);
+#if PHOTON_FUSED_EARLY_Q
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk)  // dK += dS^T Q (dS^T K-major in smem)
+          mma(tmem + colDK, sw128(ads + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+              sw128(bq + kk * 2048, QB, 1024), IDG, (!first || kk > 0) ? 1u : 0u);
+        // the stage's Q / dO / L / D are read by nothing after dK: free it before
+        // the dQ product (a stage lives ~3 tile periods; its reload is on the
+        // critical path)
+        commit(&q_empty[st]);
+        if (g > 0) mbar_wait(dq_free, (g - 1) & 1);  // the previous tile's dQ drained
+        fence_after();
+#else
         if (g > 0) mbar_wait(dq_free, (g - 1) & 1);  // the previous tile's dQ drained
         fence_after();
 #pragma unroll
         for (int kk = 0; kk < T / 16; ++kk)  // dK += dS^T Q (dS^T K-major in smem)
           mma(tmem + colDK, sw128(ads + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
               sw128(bq + kk * 2048, QB, 1024), IDG, (!first || kk > 0) ? 1u : 0u);
+#endif
 #pragma unroll
         for (int kk = 0; kk < T / 16; ++kk)  // dQ_tile = dS K (dS MN-major in smem, K MN-major)
           mma(tmem + colDQ, sw128(ads + kk * 2048, 16384, 1024), sw128(bk + kk * 2048, KB, 1024),
               IDQ, kk > 0 ? 1u : 0u);
         commit(gq_done);
+#if !PHOTON_FUSED_EARLY_Q
         commit(&q_empty[st]);
+#endif
         if (last) commit(&k_empty[kb]);  // this key tile's K no longer read
       };
       int ti = 0, gi = 0;
