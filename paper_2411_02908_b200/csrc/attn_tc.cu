@@ -1243,7 +1243,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 // (red.add), j = i reads back, adds, scales and writes the bf16 dq row and the
 // bias partials.  Same-thread same-address operations are ordered, and no other
 // CTA touches the head: deterministic, no atomics across CTAs.
-// dS^T goes to shared memory only (two 32 KB buffers, [2 query halves][128 keys]
+// dS^T goes to shared memory only (a 32 KB buffer, NDS below, [2 query halves][128 keys]
 // [64 queries] with the 128B swizzle), read as the K-major A of dK = dS^T Q and
 // as the MN-major A of dQ = dS K.  The gradient products of a tile are split
 // over two completions (pv_done: dV, which frees P^T; gq_done: dK and dQ), so
@@ -1278,7 +1278,16 @@ constexpr int NRF = PHOTON_ATTN_NRF, NKF2 = PHOTON_ATTN_NKF;
 #ifndef PHOTON_FUSED_GRID
 #define PHOTON_FUSED_GRID 2
 #endif
-constexpr int kFusedSmem = 1024 + 2 * 32768 + (NKF2 + 1) * 16384 + NRF * (2 * 16384 + 8 * 128) + 512;
+// dS^T buffers: 2 (the next tile's dS^T is stored while the previous tile's dK /
+// dQ products may still read theirs) or 1 (the store waits for them; they have
+// retired by then in the steady state).  Measured at the 125M shape: one buffer
+// 0.983-0.987 ms, two 0.995-0.996, one + a fourth Q/dO stage 0.996-0.998 (the
+// smaller shared-memory carve-out leaves more L1)
+#ifndef PHOTON_ATTN_NDS
+#define PHOTON_ATTN_NDS 1
+#endif
+constexpr int NDS = PHOTON_ATTN_NDS;
+constexpr int kFusedSmem = 1024 + NDS * 32768 + (NKF2 + 1) * 16384 + NRF * (2 * 16384 + 8 * 128) + 512;
 static_assert(kFusedSmem <= 232448, "fused attention backward: shared memory");
 
 __device__ __forceinline__ void st_relaxed_f4(float* p, float4 v) {
@@ -1396,8 +1405,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
-  uint8_t* sDS = sm;                    // dS^T [2], 32 KB each
-  uint8_t* sK = sDS + 2 * 32768;        // [NKF2]
+  uint8_t* sDS = sm;                    // dS^T [NDS], 32 KB each
+  uint8_t* sK = sDS + NDS * 32768;      // [NKF2]
   uint8_t* sV = sK + NKF2 * KB;         // [1]
   uint8_t* sQ = sV + KB;                // [NRF]
   uint8_t* sO = sQ + NRF * QB;          // [NRF] dO
@@ -1519,7 +1528,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         ATTN_TRACE_P(23, g);
         fence_after();
         const uint32_t bo = su32(sO + st * QB), bq = su32(sQ + st * QB), bk = su32(sK + kb * KB);
-        const uint32_t ads = su32(sDS + (g & 1) * 32768);
+        const uint32_t ads = su32(sDS + (NDS == 2 ? (g & 1) * 32768 : 0));
 #pragma unroll
         for (int kk = 0; kk < T / 16; ++kk)  // dV += P^T dO (P^T from TMEM)
           mma_ts(tmem + colDV, tmem + colP + kk * 8, sw128(bo + kk * 2048, QB, 1024), IDG,
@@ -1731,9 +1740,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           if (lane == 0) ATTN_TRACE_MAX(30, gi);
           // dS^T into buffer gi & 1 (its last readers, tile gi-2's dK / dQ
           // products, retired before tile gi-1 drained their dQ)
+          if (NDS == 1 && gi >= 1) {  // one buffer: the previous tile's dK / dQ products read it
+            mbar_wait(gq_done, (gi - 1) & 1);
+            fence_after();
+          }
 #pragma unroll
           for (int t = 0; t < 4; ++t)
-            sts128(ds_row + (gi & 1) * 32768 + ((((cg & 1) * 4 + t) ^ (r & 7)) << 4), dd[4 * t],
+            sts128(ds_row + (NDS == 2 ? (gi & 1) * 32768 : 0) + ((((cg & 1) * 4 + t) ^ (r & 7)) << 4), dd[4 * t],
                    dd[4 * t + 1], dd[4 * t + 2], dd[4 * t + 3]);
           // P^T is free once the previous tile's dV product retired
           if (gi >= 1) mbar_wait(pv_done, (gi - 1) & 1);
