@@ -272,8 +272,12 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, 
 // TMEM columns per CTA: S [0,128) fp32 scores, P [128,192) bf16x2, O [192,256).
 constexpr uint32_t kColS = 0, kColP = 128, kColO = 192;
 // forward K ring depth: a TMA load under the forward's traffic takes up to ~5k
-// cycles (clock64 trace), more than two tiles of softmax
-constexpr int NKF = 3;
+// cycles (clock64 trace), more than two tiles of softmax (last session: 2 stages
+// 0.353-0.361 ms, 3 0.351-0.355, 4 0.564 -- one CTA per SM at head dim 64)
+#ifndef PHOTON_FWD_NKF
+#define PHOTON_FWD_NKF 3
+#endif
+constexpr int NKF = PHOTON_FWD_NKF;
 #ifndef PHOTON_FWD_PRE
 #define PHOTON_FWD_PRE 1
 #endif
