@@ -65,14 +65,14 @@ MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 METRIC = "tokens/s/round at 1-8 B200 (125M); FedAvg aggregate GB/s vs roofline"
 
 
-NCU_STEP = os.path.join(ROOT, "profiles", "r02c_step.json")
+NCU_STEP = os.path.join(ROOT, "profiles", "r02d_step.json")
 
 
 def _gemm_ncu():
     """ncu evidence for the roofline kernel class: mean DRAM bytes (read + write)
     per tcgen05 GEMM launch over ALL 195 GEMM launches of one 125M client step,
     their algorithmic bytes, and the time-weighted tensor-pipe utilisation
-    (tools/capture_r02c.sh -> tools/step_table.py -> profiles/r02c_step.json)."""
+    (tools/capture_r02d.sh -> tools/step_table.py -> profiles/r02d_step.json)."""
     try:
         with open(NCU_STEP) as f:
             g = json.load(f)["ALL GEMMs"]
